@@ -1,0 +1,156 @@
+/*
+ * coulomb.h — C ABI of the B200-native electron–electron Coulomb collision
+ * operator: step S1 ("DSMC-Coul") of arXiv 2508.06771's operator-split PIC
+ * scheme (Table 2; Table 5 "Coulombic Collision Steps",
+ * P:299-322; §4.4).
+ *
+ * One call of coulomb_collide() = one step of S1 on a set of electrons binned
+ * in cells:  CCS1 count -> CCS2 prefix sum -> CCS3 stable bin -> random
+ * in-cell pairing (reading R1) -> CCS4 two randoms per pair ->
+ * CCS5 Takizuka–Abe binary collision -> per-cell moments
+ * (the P2C block reduction of §4.5) and global diagnostics.
+ * Everything runs in fp64 ("All runs are in double precision").
+ *
+ * Conventions
+ *  - Every pointer argument is a DEVICE pointer owned by the caller (e.g. the
+ *    storage of a torch tensor) unless documented as HOST.  The library never
+ *    allocates, frees or synchronises on the compute path; all work is
+ *    enqueued on `stream` (a cudaStream_t passed as void*; NULL = legacy
+ *    default stream).  Outputs are valid when the stream reaches that point.
+ *  - Velocities are structure-of-arrays fp64: v[c * ldv + i], c = 0,1,2
+ *    (x, y, z), i < n <= ldv.  Base pointers must be 16-byte aligned.
+ *  - cell ids are int32: 0 <= id < cells for live particles, -1 for dead
+ *    particles (SPEC "dead <=> weight 0"; reading R11).
+ *  - Return codes: CC_OK or a negative CC_E* code; no exceptions cross the ABI.
+ *    Host-side argument errors are reported before anything is enqueued.
+ *    Invalid cell ids are detected on the device: such particles are treated
+ *    as dead and a flag is raised in the workspace, returned as CC_ECELL by
+ *    cc_device_status().
+ *  - Reentrant for distinct workspaces; no global mutable state.
+ */
+#ifndef B200_COULOMB_H
+#define B200_COULOMB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CC_OK 0
+#define CC_EINVAL (-1)      /* bad argument (null/misaligned pointer, n<0, cells<1, dt<=0, step>=2^32, aliasing) */
+#define CC_EWORKSPACE (-2)  /* workspace null, misaligned (256 B) or smaller than cc_workspace_bytes() */
+#define CC_ECUDA (-3)       /* a CUDA launch failed */
+#define CC_ECELL (-4)       /* (device-detected) a cell id outside [-1, cells) was seen */
+#define CC_ECOUNT (-5)      /* n >= 2^31 or cells > CC_MAX_CELLS */
+#define CC_ENCCL (-6)       /* reserved for the multi-GPU layer */
+
+#define CC_MAX_CELLS 32768  /* binning keeps per-warp cell counters in shared memory */
+#define CC_DIAG_LEN 16
+#define CC_MOMENTS_LEN 7
+
+/* Physical parameters (HOST struct).  Defaults from cc_default_params():
+ * CODATA 2018 electron mass/charge and eps0, weight 1, cell_volume 1,
+ * ln_lambda 10 (reading R7), no per-cell arrays, flags 0.                     */
+typedef struct cc_params {
+    double mass;                  /* kg, particle mass m (m_r = m/2 for e-e, R5)          */
+    double charge;                /* C, |q|                                                */
+    double eps0;                  /* F/m                                                   */
+    double weight;                /* physical electrons per macro-particle (uniform) */
+    double cell_volume;           /* m^3, used when cell_volume_arr == NULL                */
+    const double *cell_volume_arr;/* DEVICE [cells] or NULL                                */
+    double ln_lambda;             /* Coulomb logarithm, used when ln_lambda_arr == NULL    */
+    const double *ln_lambda_arr;  /* DEVICE [cells] or NULL                                */
+    uint32_t flags;               /* reserved, must be 0                                   */
+} cc_params;
+
+void cc_default_params(cc_params *p);                         /* HOST */
+
+/* Bytes of device workspace a call with (n, cells) needs (HOST function).
+ * The workspace must be 256-byte aligned; its contents need no
+ * initialisation and are scratch between calls (except the error flag read
+ * by cc_device_status).                                                       */
+size_t cc_workspace_bytes(int64_t n, int32_t cells);
+
+/* One step of the Coulomb collision operator (Table 5, CCS1-CCS5).
+ *
+ *  v_in      [3][ldv] fp64, read only.                 cell_in [n] int32, read only.
+ *  v_out     [3][ldv] fp64, written for all n slots.   cell_out [n] int32, written.
+ *  perm_out  [n] int32 or NULL: input index of the particle at each output slot.
+ *  Output order (reading R14): cell-major; inside cell j (slots
+ *  [off_j, off_j + N_j)) the particles are in PAIR order — slots off_j+2k and
+ *  off_j+2k+1 hold pair k's first and second member, and for odd N_j slot
+ *  off_j+N_j-1 holds the particle that sat out (R2).  Dead particles follow at
+ *  [L, n) in input order (L = number of live particles).  v_out/cell_out/
+ *  perm_out must not alias the inputs.
+ *  cells     number of LOCAL cells M (1 <= M <= CC_MAX_CELLS).
+ *  cell_base global id of local cell 0 (multi-GPU cell-range sharding); the
+ *            random streams are keyed by the GLOBAL cell id, so a shard's result
+ *            equals the single-GPU result on the same particles.
+ *  dt        s, > 0.   params: HOST pointer (NULL = defaults).
+ *  seed      Philox key (64 bits).  step: < 2^32, Philox counter word (R3).
+ *  moments_out [cells][7] or NULL: {n_j [m^-3], <v_x>, <v_y>, <v_z> [m/s],
+ *            T_x, T_y, T_z [eV]} of the post-collision particles (R13).
+ *  diag_out  [16] or NULL: 0 live L, 1 dead, 2 pairs, 3 cells with odd N_j,
+ *            4-6 sum v before, 7 sum |v|^2 before, 8-10 sum v after,
+ *            11 sum |v|^2 after, 12-15 zero.  Sums are deterministic (fixed
+ *            reduction order): two calls with equal inputs give equal bytes.
+ *  workspace >= cc_workspace_bytes(n, cells) bytes, 256-byte aligned.        */
+int coulomb_collide(const double *v_in, int64_t ldv, const int32_t *cell_in,
+                    double *v_out, int32_t *cell_out, int32_t *perm_out,
+                    int64_t n, int32_t cells, uint32_t cell_base,
+                    double dt, const cc_params *params,
+                    uint64_t seed, uint64_t step,
+                    double *moments_out, double *diag_out,
+                    void *workspace, size_t workspace_bytes, void *stream);
+
+/* Synchronises `stream` and returns CC_ECELL if a previous call on this
+ * workspace saw an invalid cell id (the flag is then cleared), CC_ECUDA on a
+ * CUDA error, else CC_OK.                                                     */
+int cc_device_status(void *workspace, void *stream);
+
+const char *cc_strerror(int code);                            /* HOST */
+
+/* ---- test hooks: the same kernels as coulomb_collide, partial pipelines ---- */
+
+/* CCS1-CCS3: stable counting sort by cell.  perm_out[s] = input
+ * index at stable slot s (cell-major, input order inside a cell, dead last in
+ * input order); off_out [cells+1] = exclusive prefix sum of N_j (CCS2).      */
+int cc_bin(const int32_t *cell_in, int64_t n, int32_t cells,
+           int32_t *perm_out, int32_t *off_out,
+           void *workspace, size_t workspace_bytes, void *stream);
+
+/* Reading R1: for every pair of every cell, the two STABLE slots
+ * (off_j + pi_j(2k), off_j + pi_j(2k+1)), cell-major, k-minor, written to
+ * pair_slots_out[2*g], [2*g+1]; g runs over sum_j floor(N_j/2) pairs, at most
+ * max_pairs are written.  off: DEVICE [cells+1] as produced by cc_bin.       */
+int cc_pairs(const int32_t *off, int32_t cells, uint32_t cell_base,
+             uint64_t seed, uint64_t step,
+             int32_t *pair_slots_out, int64_t max_pairs, void *stream);
+
+/* R3: Philox4x32-10 of m counters ctr4 [m][4] with key (seed lo, seed hi). */
+int cc_philox(const uint32_t *ctr4, uint64_t seed, uint32_t *out4, int64_t m, void *stream);
+
+/* R4: AS241 PPND16 inverse normal CDF of m values. */
+int cc_ppnd16(const double *u, double *z, int64_t m, void *stream);
+
+/* CCS5: TA77 update of m explicit pairs, in place.  va, vb
+ * [3][m] SoA; C [m] per-pair variance constant (<delta^2> = C/|u|^3);
+ * u1, u2 [m] the pair's two uniforms.                                         */
+int cc_ta_pairs(double *va, double *vb, const double *C, const double *u1,
+                const double *u2, int64_t m, void *stream);
+
+/* P2C block reduction over a slot-ordered v [3][ldv] with cell
+ * offsets off [cells+1] -> out [cells][7] (same layout as moments_out).      */
+int cc_moments(const double *v, int64_t ldv, const int32_t *off, int32_t cells,
+               const cc_params *params, double *out, void *stream);
+
+/* Multi-GPU: rank-ascending sum of P gathered diagnostics vectors
+ * gathered [P][16] -> out [16] (deterministic for a given P).   */
+int cc_diag_sum_ranks(const double *gathered, int32_t nranks, double *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B200_COULOMB_H */

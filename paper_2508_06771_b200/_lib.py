@@ -1,0 +1,94 @@
+"""ctypes binding of ``lib/libcoulomb.so`` (the C ABI declared in include/coulomb.h).
+
+Argument marshalling only: every step of the operator runs in the CUDA
+kernels of ``csrc/``.  There is no CPU fallback — if the shared library is
+missing, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libcoulomb.so")
+
+CC_OK = 0
+CC_EINVAL = -1
+CC_EWORKSPACE = -2
+CC_ECUDA = -3
+CC_ECELL = -4
+CC_ECOUNT = -5
+CC_ENCCL = -6
+CC_MAX_CELLS = 32768
+CC_DIAG_LEN = 16
+CC_MOMENTS_LEN = 7
+
+# every symbol include/coulomb.h declares
+EXPORTS = ("cc_default_params", "cc_workspace_bytes", "coulomb_collide", "cc_device_status",
+           "cc_strerror", "cc_bin", "cc_pairs", "cc_philox", "cc_ppnd16", "cc_ta_pairs",
+           "cc_moments", "cc_diag_sum_ranks")
+
+
+class CCParams(C.Structure):
+    _fields_ = [("mass", C.c_double), ("charge", C.c_double), ("eps0", C.c_double),
+                ("weight", C.c_double), ("cell_volume", C.c_double),
+                ("cell_volume_arr", C.c_void_p), ("ln_lambda", C.c_double),
+                ("ln_lambda_arr", C.c_void_p), ("flags", C.c_uint32)]
+
+
+class CCError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        self.code = code
+        super().__init__(f"{what}: {strerror(code)} ({code})")
+
+
+_lib = None
+
+
+def load():
+    """Load the CUDA library (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build the CUDA extension first "
+                          "(python -c 'import __graft_entry__ as g; g.build()')")
+    L = C.CDLL(LIB_PATH)
+    vp, i64, i32, u32, u64, dbl, sz = (C.c_void_p, C.c_int64, C.c_int32, C.c_uint32, C.c_uint64,
+                                       C.c_double, C.c_size_t)
+    L.cc_default_params.argtypes = [C.POINTER(CCParams)]
+    L.cc_default_params.restype = None
+    L.cc_workspace_bytes.argtypes = [i64, i32]
+    L.cc_workspace_bytes.restype = sz
+    L.coulomb_collide.argtypes = [vp, i64, vp, vp, vp, vp, i64, i32, u32, dbl, C.POINTER(CCParams),
+                                  u64, u64, vp, vp, vp, sz, vp]
+    L.coulomb_collide.restype = C.c_int
+    L.cc_device_status.argtypes = [vp, vp]
+    L.cc_device_status.restype = C.c_int
+    L.cc_strerror.argtypes = [C.c_int]
+    L.cc_strerror.restype = C.c_char_p
+    L.cc_bin.argtypes = [vp, i64, i32, vp, vp, vp, sz, vp]
+    L.cc_bin.restype = C.c_int
+    L.cc_pairs.argtypes = [vp, i32, u32, u64, u64, vp, i64, vp]
+    L.cc_pairs.restype = C.c_int
+    L.cc_philox.argtypes = [vp, u64, vp, i64, vp]
+    L.cc_philox.restype = C.c_int
+    L.cc_ppnd16.argtypes = [vp, vp, i64, vp]
+    L.cc_ppnd16.restype = C.c_int
+    L.cc_ta_pairs.argtypes = [vp, vp, vp, vp, vp, i64, vp]
+    L.cc_ta_pairs.restype = C.c_int
+    L.cc_moments.argtypes = [vp, i64, vp, i32, C.POINTER(CCParams), vp, vp]
+    L.cc_moments.restype = C.c_int
+    L.cc_diag_sum_ranks.argtypes = [vp, i32, vp, vp]
+    L.cc_diag_sum_ranks.restype = C.c_int
+    _lib = L
+    return L
+
+
+def strerror(code: int) -> str:
+    return load().cc_strerror(code).decode()
+
+
+def check(code: int, what: str) -> None:
+    if code != CC_OK:
+        raise CCError(code, what)

@@ -1,0 +1,216 @@
+// cc_device.cuh — device building blocks of the Coulomb collision operator
+// (arXiv 2508.06771 §4.4, Table 5).  Product code: written for sm_100a from
+// the published definitions; shares nothing with oracle/.
+//
+//   philox4x32_10   CCS4 randoms, reading R3
+//   u01             two 32-bit words -> uniform on (0,1), R3
+//   ppnd16          AS241 inverse normal CDF (Wichura 1988), R4
+//   pairing (R1)    keyed in-cell permutation pi_j: sort-by-Philox-key for
+//                   N <= 64, 8-round keyed Feistel + cycle walking above
+//   ta_update       CCS5 Takizuka–Abe pair collision, R5/R8/R9
+#pragma once
+#include <cstdint>
+
+namespace cc {
+
+constexpr int kSmallCell = 64;          // R1: N <= 64 uses the sort-by-key form
+
+// ---------------------------------------------------------------- Philox4x32-10
+struct U4 { uint32_t x, y, z, w; };
+
+__device__ __forceinline__ U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1)
+{
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+        const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+        c = U4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return c;
+}
+
+// (floor((2^32 hi + lo) / 2^12) + 1/2) * 2^-52 : exact odd multiple of 2^-53.
+__device__ __forceinline__ double u01(uint32_t hi, uint32_t lo)
+{
+    const uint64_t m = ((static_cast<uint64_t>(hi) << 32) | lo) >> 12;
+    return __fma_rn(static_cast<double>(m), 0x1.0p-52, 0x1.0p-53);
+}
+
+// ---------------------------------------------------------------- AS241 PPND16
+__device__ __forceinline__ double ppnd16(double p)
+{
+    const double q = p - 0.5;
+    if (fabs(q) <= 0.425) {
+        const double r = 0.180625 - q * q;
+        const double num = (((((((2.5090809287301226727e+3 * r + 3.3430575583588128105e+4) * r +
+                                 6.7265770927008700853e+4) * r + 4.5921953931549871457e+4) * r +
+                               1.3731693765509461125e+4) * r + 1.9715909503065514427e+3) * r +
+                             1.3314166789178437745e+2) * r + 3.3871328727963666080e+0) * q;
+        const double den = (((((((5.2264952788528545610e+3 * r + 2.8729085735721942674e+4) * r +
+                                 3.9307895800092710610e+4) * r + 2.1213794301586595867e+4) * r +
+                               5.3941960214247511077e+3) * r + 6.8718700749205790830e+2) * r +
+                             4.2313330701600911252e+1) * r + 1.0);
+        return num / den;
+    }
+    double r = (q < 0.0) ? p : 1.0 - p;
+    r = sqrt(-log(r));
+    double num, den;
+    if (r <= 5.0) {
+        r -= 1.6;
+        num = (((((((7.7454501427834140764e-4 * r + 2.2723844989269184583e-2) * r +
+                    2.4178072517745061177e-1) * r + 1.2704582524523683826e+0) * r +
+                  3.6478483247632046050e+0) * r + 5.7694972214606914055e+0) * r +
+                4.6303378461565452959e+0) * r + 1.4234371107496835773e+0);
+        den = (((((((1.0507500716444168432e-9 * r + 5.4759380849953449460e-4) * r +
+                    1.5198666563616457197e-2) * r + 1.4810397642748007459e-1) * r +
+                  6.8976733498510000455e-1) * r + 1.6763848301838038494e+0) * r +
+                2.0531916266377588219e+0) * r + 1.0);
+    } else {
+        r -= 5.0;
+        num = (((((((2.0103343992922881327e-7 * r + 2.7115555687434875782e-5) * r +
+                    1.2426609473880784386e-3) * r + 2.6532189526576123093e-2) * r +
+                  2.9656057182850489123e-1) * r + 1.7848265399172913358e+0) * r +
+                5.4637849111641143699e+0) * r + 6.6579046435011037772e+0);
+        den = (((((((2.0442631033899397856e-15 * r + 1.4215117583164458887e-7) * r +
+                    1.8463183175100546818e-5) * r + 7.8686913114561325910e-4) * r +
+                  1.4875361290850614852e-2) * r + 1.3692988092273580531e-1) * r +
+                5.9983220655588793769e-1) * r + 1.0);
+    }
+    const double x = num / den;
+    return (q < 0.0) ? -x : x;
+}
+
+// ---------------------------------------------------------------- pairing (R1)
+__device__ __forceinline__ uint32_t fmix32(uint32_t h)
+{
+    h ^= h >> 16;
+    h *= 0x85EBCA6Bu;
+    h ^= h >> 13;
+    h *= 0xC2B2AE35u;
+    h ^= h >> 16;
+    return h;
+}
+
+// Parameters of the N > 64 Feistel form for a cell of N slots.
+struct Feistel {
+    uint32_t k[4];
+    uint32_t bL;     // L half: bL bits (a = 2^bL)
+    uint32_t m;      // R half: values in [0, m), m = ceil(N / a)
+    uint32_t N;
+};
+
+__device__ __forceinline__ Feistel make_feistel(uint32_t N, U4 keys)
+{
+    Feistel f;
+    f.k[0] = keys.x; f.k[1] = keys.y; f.k[2] = keys.z; f.k[3] = keys.w;
+    const uint32_t b = 32u - __clz(N - 1u);          // ceil(log2 N), N >= 2
+    f.bL = b >> 1;
+    const uint32_t a = 1u << f.bL;
+    f.m = (N + a - 1u) >> f.bL;
+    f.N = N;
+    return f;
+}
+
+__device__ __forceinline__ uint32_t feistel_E(const Feistel& f, uint32_t x)
+{
+    const uint32_t amask = (1u << f.bL) - 1u;
+    uint32_t L = x & amask, R = x >> f.bL;
+#pragma unroll
+    for (uint32_t r = 0; r < 8; ++r) {
+        const uint32_t K = f.k[r & 3u] + (r >> 2) * 0x9E3779B9u;
+        if ((r & 1u) == 0u) {
+            L ^= fmix32(R ^ K) & amask;
+        } else {
+            R += __umulhi(fmix32(L ^ K), f.m);
+            R = (R >= f.m) ? R - f.m : R;
+        }
+    }
+    return L + (R << f.bL);
+}
+
+// pi(i) for the Feistel form: cycle walking from i until the value is < N.
+__device__ __forceinline__ uint32_t feistel_pi(const Feistel& f, uint32_t i)
+{
+    uint32_t x = feistel_E(f, i);
+    while (x >= f.N) x = feistel_E(f, x);
+    return x;
+}
+
+// Sort key of stable slot s in a small cell: word (s mod 4) of
+// Philox(ctr = (s div 4, G, step, 2), key = seed).
+__device__ __forceinline__ uint32_t small_key(uint32_t s, uint32_t G, uint32_t step,
+                                              uint32_t k0, uint32_t k1)
+{
+    const U4 w = philox4x32_10(U4{s >> 2, G, step, 2u}, k0, k1);
+    const uint32_t q = s & 3u;
+    return q == 0 ? w.x : q == 1 ? w.y : q == 2 ? w.z : w.w;
+}
+
+// Warp-cooperative pi table of a small cell (N <= 64): pi_sm[q] = slot at
+// pair-order position q.  All 32 lanes must call it; the warp must be converged.
+__device__ __forceinline__ void small_cell_perm(uint32_t N, uint32_t G, uint32_t step,
+                                                uint32_t k0, uint32_t k1, int lane,
+                                                int32_t* pi_sm)
+{
+    const uint32_t s0 = static_cast<uint32_t>(lane), s1 = s0 + 32u;
+    const uint32_t r0 = (s0 < N) ? small_key(s0, G, step, k0, k1) : 0xFFFFFFFFu;
+    const uint32_t r1 = (s1 < N) ? small_key(s1, G, step, k0, k1) : 0xFFFFFFFFu;
+    uint32_t rank0 = 0, rank1 = 0;
+    for (uint32_t t = 0; t < N; ++t) {
+        const uint32_t src = (t < 32u) ? r0 : r1;
+        const uint32_t rt = __shfl_sync(0xFFFFFFFFu, src, static_cast<int>(t & 31u));
+        rank0 += (rt < r0 || (rt == r0 && t < s0)) ? 1u : 0u;
+        rank1 += (rt < r1 || (rt == r1 && t < s1)) ? 1u : 0u;
+    }
+    if (s0 < N) pi_sm[rank0] = static_cast<int32_t>(s0);
+    if (s1 < N) pi_sm[rank1] = static_cast<int32_t>(s1);
+    __syncwarp();
+}
+
+// ---------------------------------------------------------------- TA77 update
+// <delta^2> = C / |u|^3; delta = sqrt(<delta^2>) Phi^-1(u1); tan(Theta/2) = delta;
+// phi = 2 pi u2; v_a += Du/2, v_b -= Du/2.
+__device__ __forceinline__ void ta_update(double& ax, double& ay, double& az,
+                                          double& bx, double& by, double& bz,
+                                          double C, double u1, double u2)
+{
+    const double ux = ax - bx, uy = ay - by, uz = az - bz;
+    if (ux == 0.0 && uy == 0.0 && uz == 0.0) return;
+    const double usq = ux * ux + uy * uy + uz * uz;
+    const double u = sqrt(usq);
+    const double var = C / (usq * u);
+    const double delta = sqrt(var) * ppnd16(u1);
+    double sinT, omc;
+    if (fabs(delta) > 1.0) {
+        const double t = 1.0 / delta;
+        const double inv = 1.0 / (1.0 + t * t);
+        sinT = 2.0 * t * inv;
+        omc = 2.0 * inv;
+    } else {
+        const double inv = 1.0 / (1.0 + delta * delta);
+        sinT = 2.0 * delta * inv;
+        omc = 2.0 * delta * delta * inv;
+    }
+    double sphi, cphi;
+    sincospi(2.0 * u2, &sphi, &cphi);
+    double dux, duy, duz;
+    if (ux == 0.0 && uy == 0.0) {
+        dux = u * sinT * cphi;
+        duy = u * sinT * sphi;
+        duz = -uz * omc;
+    } else {
+        const double uperp = sqrt(ux * ux + uy * uy);
+        const double ip = 1.0 / uperp;
+        const double sc = sinT * cphi, ss = sinT * sphi;
+        const double A = uz * sc * ip, B = u * ss * ip;
+        dux = ux * A - uy * B - ux * omc;
+        duy = uy * A + ux * B - uy * omc;
+        duz = -uperp * sc - uz * omc;
+    }
+    ax += 0.5 * dux; ay += 0.5 * duy; az += 0.5 * duz;
+    bx -= 0.5 * dux; by -= 0.5 * duy; bz -= 0.5 * duz;
+}
+
+}  // namespace cc

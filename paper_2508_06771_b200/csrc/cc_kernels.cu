@@ -1,0 +1,988 @@
+// cc_kernels.cu — sm_100a kernels and C ABI of the e–e Coulomb collision
+// operator (arXiv 2508.06771 step S1; Table 5).
+//
+// Pipeline of one coulomb_collide() call (all on the caller's stream):
+//   k_count        CCS1: per-tile cell histograms  -> tcount[T][M+1]
+//   k_scan_tiles   CCS2, part 1: per cell, exclusive scan over tiles
+//   k_scan_cells   CCS2, part 2: off[] (cell offsets), chunk_off[], per-cell
+//                  TA constant C_j (R5/R6/R7) and Feistel keys (R1, R3)
+//   k_scatter      CCS3 as a STABLE counting sort: per-warp
+//                  sub-ranges, match.any ranks, no global atomics; writes the
+//                  particle as one 32-byte record {vx, vy, vz, (perm, cell)}
+//                  into the cell-sorted workspace array ws_v
+//   k_collide_small  N_j <= 64: one warp per cell; pi_j by sort-by-key (R1)
+//   k_collide_large  N_j > 64: cell-aligned chunks of pairs; pi_j by keyed
+//                  Feistel (R1); CCS4 Philox per pair; CCS5 TA update; output
+//                  in pair order, SoA; fused per-chunk moment partials
+//   k_copy_dead    dead particles after the live ones, input order
+//   k_finalize_cells / k_finalize_diag   deterministic reductions of the
+//                  partials -> moments_out [M][7], diag_out [16]
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+
+#include "../../include/coulomb.h"
+#include "cc_device.cuh"
+
+namespace {
+
+constexpr int kCountThreads = 256;
+constexpr int kSub = 4096;               // elements per warp sub-range in k_scatter (<= 65535)
+constexpr int kCollideThreads = 256;
+constexpr int kChunk = 1024;             // items (pairs or sitter) per k_collide_large CTA
+constexpr int kRec = 16;                 // doubles per moment record
+constexpr int kCellSum = 8;
+constexpr int kScatterSmemBudget = 96 * 1024;
+
+// ------------------------------------------------------------------ layout
+struct Layout {
+    int W = 1, tile = kSub, T = 0;
+    int64_t max_chunks = 0;
+    size_t o_err = 0, o_tcount = 0, o_cnt = 0, o_off = 0, o_chunk = 0, o_C = 0, o_keys = 0;
+    size_t o_small = 0, o_recs = 0, o_cellsum = 0, o_wsv = 0, total = 0;
+};
+
+size_t align256(size_t x) { return (x + 255u) & ~static_cast<size_t>(255u); }
+
+int scatter_warps(int32_t M)
+{
+    int W = kScatterSmemBudget / (2 * (M + 2));
+    if (W > 8) W = 8;
+    if (W < 1) W = 1;
+    return W;
+}
+
+Layout make_layout(int64_t n, int32_t M)
+{
+    Layout L;
+    L.W = scatter_warps(M);
+    L.tile = L.W * kSub;
+    L.T = static_cast<int>((n + L.tile - 1) / L.tile);
+    L.max_chunks = (n + M) / 2 / kChunk + M + 1;
+    size_t o = 0;
+    L.o_err = o;      o = align256(o + 64 * sizeof(int32_t));
+    L.o_tcount = o;   o = align256(o + static_cast<size_t>(L.T > 0 ? L.T : 1) * (M + 1) * sizeof(int32_t));
+    L.o_cnt = o;      o = align256(o + static_cast<size_t>(M + 1) * sizeof(int32_t));
+    L.o_off = o;      o = align256(o + static_cast<size_t>(M + 1) * sizeof(int32_t));
+    L.o_chunk = o;    o = align256(o + static_cast<size_t>(M + 1) * sizeof(int32_t));
+    L.o_C = o;        o = align256(o + static_cast<size_t>(M) * sizeof(double));
+    L.o_keys = o;     o = align256(o + static_cast<size_t>(M) * sizeof(cc::U4));
+    L.o_small = o;    o = align256(o + static_cast<size_t>(M) * kRec * sizeof(double));
+    L.o_recs = o;     o = align256(o + static_cast<size_t>(L.max_chunks) * kRec * sizeof(double));
+    L.o_cellsum = o;  o = align256(o + static_cast<size_t>(M) * kCellSum * sizeof(double));
+    L.o_wsv = o;      o = align256(o + static_cast<size_t>(n > 0 ? n : 1) * 4 * sizeof(double));
+    L.total = o;
+    return L;
+}
+
+template <typename T>
+T* at(void* base, size_t off) { return reinterpret_cast<T*>(static_cast<char*>(base) + off); }
+
+// ------------------------------------------------------------------ 256-bit global access
+__device__ __forceinline__ void ld256(const double* p, double& a, double& b, double& c, double& d)
+{
+    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+        : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+
+__device__ __forceinline__ void st256(double* p, double a, double b, double c, double d)
+{
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
+                 : "memory");
+}
+
+__device__ __forceinline__ double pack_pc(int32_t perm, int32_t cell)
+{
+    return __longlong_as_double((static_cast<long long>(static_cast<uint32_t>(cell)) << 32) |
+                                static_cast<uint32_t>(perm));
+}
+
+__device__ __forceinline__ int32_t unpack_perm(double w)
+{
+    return static_cast<int32_t>(static_cast<uint32_t>(__double_as_longlong(w)));
+}
+
+// ------------------------------------------------------------------ CCS1: count
+__global__ void __launch_bounds__(kCountThreads)
+k_count(const int32_t* __restrict__ cell, int n, int M, int tile, int32_t* __restrict__ tcount,
+        int32_t* __restrict__ err)
+{
+    extern __shared__ int32_t hist[];   // [M+1], bin M = dead or invalid
+    for (int i = threadIdx.x; i <= M; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const int64_t start = static_cast<int64_t>(blockIdx.x) * tile;
+    const int64_t end = min(start + tile, static_cast<int64_t>(n));
+    int bad = 0;
+    for (int64_t i = start + threadIdx.x; i < end; i += blockDim.x) {
+        const int32_t c = __ldg(cell + i);
+        const bool live = (c >= 0) && (c < M);
+        bad |= (!live && c != -1);
+        atomicAdd(&hist[live ? c : M], 1);
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(err, 1);
+    int32_t* row = tcount + static_cast<int64_t>(blockIdx.x) * (M + 1);
+    for (int i = threadIdx.x; i <= M; i += blockDim.x) row[i] = hist[i];
+}
+
+// ------------------------------------------------------------------ CCS2 part 1
+// grid: ceil((M+1)/32) CTAs of 32x8 threads; lane = bin, warp row = tile range.
+__global__ void __launch_bounds__(256)
+k_scan_tiles(int32_t* __restrict__ tcount, int T, int M1, int32_t* __restrict__ cnt)
+{
+    __shared__ int32_t part[8][33];
+    const int lane = threadIdx.x, wy = threadIdx.y;
+    const int c = blockIdx.x * 32 + lane;
+    const int per = (T + 7) / 8;
+    const int t0 = wy * per, t1 = min(t0 + per, T);
+    int32_t s = 0;
+    if (c < M1)
+        for (int t = t0; t < t1; ++t) s += tcount[static_cast<int64_t>(t) * M1 + c];
+    part[wy][lane] = s;
+    __syncthreads();
+    int32_t pre = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+        const int32_t x = part[w][lane];
+        pre += (w < wy) ? x : 0;
+        tot += x;
+    }
+    if (c < M1) {
+        int32_t run = pre;
+        for (int t = t0; t < t1; ++t) {
+            int32_t* p = tcount + static_cast<int64_t>(t) * M1 + c;
+            const int32_t x = *p;
+            *p = run;
+            run += x;
+        }
+        if (wy == 0) cnt[c] = tot;
+    }
+}
+
+// ------------------------------------------------------------------ CCS2 part 2
+struct CellConst {
+    double K;            // e^4 dt / (8 pi eps0^2 m_r^2)
+    double weight;
+    double volume;
+    const double* volume_arr;
+    double ln_lambda;
+    const double* ln_lambda_arr;
+};
+
+__device__ __forceinline__ int32_t n_chunks(int32_t N)
+{
+    if (N <= cc::kSmallCell) return 0;
+    const int32_t items = (N + 1) / 2;
+    return (items + kChunk - 1) / kChunk;
+}
+
+// single CTA of 1024 threads
+__global__ void __launch_bounds__(1024)
+k_scan_cells(const int32_t* __restrict__ cnt, int M, int32_t* __restrict__ off,
+             int32_t* __restrict__ chunk_off, double* __restrict__ Cj, cc::U4* __restrict__ keys,
+             CellConst cc_, uint32_t cell_base, uint32_t step, uint32_t s0, uint32_t s1)
+{
+    __shared__ int32_t wsum_a[32], wsum_b[32];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int per = (M + nt - 1) / nt;
+    const int j0 = min(tid * per, M), j1 = min(j0 + per, M);
+    int32_t a = 0, b = 0;
+    for (int j = j0; j < j1; ++j) { a += cnt[j]; b += n_chunks(cnt[j]); }
+    // block exclusive scan of (a, b)
+    const int lane = tid & 31, wid = tid >> 5;
+    int32_t ia = a, ib = b;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int32_t xa = __shfl_up_sync(0xFFFFFFFFu, ia, d);
+        const int32_t xb = __shfl_up_sync(0xFFFFFFFFu, ib, d);
+        if (lane >= d) { ia += xa; ib += xb; }
+    }
+    if (lane == 31) { wsum_a[wid] = ia; wsum_b[wid] = ib; }
+    __syncthreads();
+    if (wid == 0) {
+        int32_t va = (lane < nt / 32) ? wsum_a[lane] : 0;
+        int32_t vb = (lane < nt / 32) ? wsum_b[lane] : 0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int32_t xa = __shfl_up_sync(0xFFFFFFFFu, va, d);
+            const int32_t xb = __shfl_up_sync(0xFFFFFFFFu, vb, d);
+            if (lane >= d) { va += xa; vb += xb; }
+        }
+        wsum_a[lane] = va;
+        wsum_b[lane] = vb;
+    }
+    __syncthreads();
+    int32_t ra = ia - a + (wid > 0 ? wsum_a[wid - 1] : 0);
+    int32_t rb = ib - b + (wid > 0 ? wsum_b[wid - 1] : 0);
+    for (int j = j0; j < j1; ++j) {
+        const int32_t N = cnt[j];
+        off[j] = ra;
+        chunk_off[j] = rb;
+        ra += N;
+        rb += n_chunks(N);
+        const double V = cc_.volume_arr ? cc_.volume_arr[j] : cc_.volume;
+        const double lnL = cc_.ln_lambda_arr ? cc_.ln_lambda_arr[j] : cc_.ln_lambda;
+        const double nj = static_cast<double>(N) * cc_.weight / V;
+        Cj[j] = fmax(cc_.K * nj * lnL, 0.0);
+        keys[j] = cc::philox4x32_10(cc::U4{0u, cell_base + static_cast<uint32_t>(j), step, 1u}, s0, s1);
+    }
+    if (tid == nt - 1) { off[M] = ra; chunk_off[M] = rb; }
+}
+
+// ------------------------------------------------------------------ CCS3: stable scatter
+// Tile = W warps x kSub elements; warp w owns the contiguous sub-range w of the
+// tile, so "input order" = (tile, warp, step, lane).  Per-warp 16-bit counters
+// give each element its rank among equal-cell predecessors.
+__global__ void __launch_bounds__(256)
+k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__ cell, int n, int M,
+          int W, const int32_t* __restrict__ tbase, const int32_t* __restrict__ off,
+          double* __restrict__ wsv)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int M1 = M + 1;
+    int32_t* base = reinterpret_cast<int32_t*>(smem);                       // [M1]
+    uint16_t* wcnt = reinterpret_cast<uint16_t*>(smem + sizeof(int32_t) * M1);  // [W][M1]
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < W * M1; i += blockDim.x) wcnt[i] = 0;
+    __syncthreads();
+
+    const int64_t s0 = static_cast<int64_t>(blockIdx.x) * W * kSub + static_cast<int64_t>(w) * kSub;
+    const int64_t s1 = min(s0 + kSub, static_cast<int64_t>(n));
+    uint16_t* my = wcnt + w * M1;
+    const uint32_t lt = (1u << lane) - 1u;
+
+    if (w < W) {
+        for (int64_t i0 = s0; i0 < s1; i0 += 32) {
+            const int64_t i = i0 + lane;
+            const bool valid = i < s1;
+            const int32_t c = valid ? __ldg(cell + i) : 0;
+            const int32_t b = (c >= 0 && c < M) ? c : M;
+            const int32_t key = valid ? b : -1 - lane;
+            const uint32_t peers = __match_any_sync(0xFFFFFFFFu, key);
+            if (valid && lane == __ffs(peers) - 1) my[b] = static_cast<uint16_t>(my[b] + __popc(peers));
+        }
+    }
+    __syncthreads();
+    const int32_t* trow = tbase + static_cast<int64_t>(blockIdx.x) * M1;
+    for (int c = threadIdx.x; c < M1; c += blockDim.x) {
+        uint32_t run = 0;
+        for (int ww = 0; ww < W; ++ww) {
+            const uint32_t x = wcnt[ww * M1 + c];
+            wcnt[ww * M1 + c] = static_cast<uint16_t>(run);
+            run += x;
+        }
+        base[c] = off[c] + trow[c];           // off[M] = L: dead slots follow the live ones
+    }
+    __syncthreads();
+    if (w < W) {
+        for (int64_t i0 = s0; i0 < s1; i0 += 32) {
+            const int64_t i = i0 + lane;
+            const bool valid = i < s1;
+            const int32_t c = valid ? __ldg(cell + i) : 0;
+            const int32_t b = (c >= 0 && c < M) ? c : M;
+            const int32_t key = valid ? b : -1 - lane;
+            const uint32_t peers = __match_any_sync(0xFFFFFFFFu, key);
+            int32_t dest = 0;
+            if (valid) dest = base[b] + my[b] + __popc(peers & lt);
+            __syncwarp();
+            if (valid && lane == __ffs(peers) - 1) my[b] = static_cast<uint16_t>(my[b] + __popc(peers));
+            if (valid) {
+                double vx = 0.0, vy = 0.0, vz = 0.0;
+                if (v) { vx = __ldg(v + i); vy = __ldg(v + ldv + i); vz = __ldg(v + 2 * ldv + i); }
+                st256(wsv + 4 * static_cast<int64_t>(dest), vx, vy, vz,
+                      pack_pc(static_cast<int32_t>(i), b < M ? b : -1));
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ CCS4 + CCS5 items
+struct CollideArgs {
+    const double* wsv;
+    const int32_t* cnt;
+    const int32_t* off;
+    const int32_t* chunk_off;
+    const double* Cj;
+    const cc::U4* keys;
+    double* v_out;
+    int64_t ldv;
+    int32_t* cell_out;
+    int32_t* perm_out;
+    double* recs;
+    double* small_recs;
+    int M;
+    uint32_t cell_base, step, s0, s1;
+};
+
+// Moment accumulator: [0..2] sum (v - ref) post, [3..5] sum (v - ref)^2 post,
+// [6..8] sum v pre, [9] sum |v|^2 pre, [10..12] sum v post, [13] sum |v|^2 post,
+// [14] count.
+struct Acc {
+    double a[15];
+    __device__ void zero()
+    {
+#pragma unroll
+        for (int q = 0; q < 15; ++q) a[q] = 0.0;
+    }
+    __device__ void add(double px, double py, double pz, double x, double y, double z,
+                        double rx, double ry, double rz)
+    {
+        const double dx = x - rx, dy = y - ry, dz = z - rz;
+        a[0] += dx; a[1] += dy; a[2] += dz;
+        a[3] += dx * dx; a[4] += dy * dy; a[5] += dz * dz;
+        a[6] += px; a[7] += py; a[8] += pz;
+        a[9] += px * px + py * py + pz * pz;
+        a[10] += x; a[11] += y; a[12] += z;
+        a[13] += x * x + y * y + z * z;
+        a[14] += 1.0;
+    }
+};
+
+// One item k of cell (o, N): a pair (2k+1 < N) or the odd sitter (2k = N-1).
+__device__ __forceinline__ void process_item(const CollideArgs& A, int32_t j, int32_t o, int32_t N,
+                                             uint32_t k, uint32_t sa, uint32_t sb, double C,
+                                             double rx, double ry, double rz, Acc& acc)
+{
+    const int32_t pa = o + 2 * static_cast<int32_t>(k);
+    double ax, ay, az, aw;
+    ld256(A.wsv + 4 * static_cast<int64_t>(o + static_cast<int32_t>(sa)), ax, ay, az, aw);
+    if (2 * k + 1 < static_cast<uint32_t>(N)) {
+        double bx, by, bz, bw;
+        ld256(A.wsv + 4 * static_cast<int64_t>(o + static_cast<int32_t>(sb)), bx, by, bz, bw);
+        const double pax = ax, pay = ay, paz = az, pbx = bx, pby = by, pbz = bz;
+        const cc::U4 r = cc::philox4x32_10(
+            cc::U4{k, A.cell_base + static_cast<uint32_t>(j), A.step, 0u}, A.s0, A.s1);
+        cc::ta_update(ax, ay, az, bx, by, bz, C, cc::u01(r.x, r.y), cc::u01(r.z, r.w));
+        double* vo = A.v_out;
+        vo[pa] = ax; vo[pa + 1] = bx;
+        vo[A.ldv + pa] = ay; vo[A.ldv + pa + 1] = by;
+        vo[2 * A.ldv + pa] = az; vo[2 * A.ldv + pa + 1] = bz;
+        A.cell_out[pa] = j; A.cell_out[pa + 1] = j;
+        if (A.perm_out) { A.perm_out[pa] = unpack_perm(aw); A.perm_out[pa + 1] = unpack_perm(bw); }
+        acc.add(pax, pay, paz, ax, ay, az, rx, ry, rz);
+        acc.add(pbx, pby, pbz, bx, by, bz, rx, ry, rz);
+    } else {
+        double* vo = A.v_out;
+        vo[pa] = ax; vo[A.ldv + pa] = ay; vo[2 * A.ldv + pa] = az;
+        A.cell_out[pa] = j;
+        if (A.perm_out) A.perm_out[pa] = unpack_perm(aw);
+        acc.add(ax, ay, az, ax, ay, az, rx, ry, rz);
+    }
+}
+
+__device__ __forceinline__ void warp_reduce(Acc& acc)
+{
+#pragma unroll
+    for (int q = 0; q < 15; ++q)
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) acc.a[q] += __shfl_down_sync(0xFFFFFFFFu, acc.a[q], d);
+}
+
+// N_j <= 64: one warp per cell.
+__global__ void __launch_bounds__(256)
+k_collide_small(CollideArgs A)
+{
+    __shared__ int32_t pi_sm[8][cc::kSmallCell];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int j = blockIdx.x * 8 + w;
+    if (j >= A.M) return;
+    const int32_t N = A.cnt[j];
+    if (N == 0 || N > cc::kSmallCell) return;
+    const int32_t o = A.off[j];
+    const uint32_t G = A.cell_base + static_cast<uint32_t>(j);
+    cc::small_cell_perm(static_cast<uint32_t>(N), G, A.step, A.s0, A.s1, lane, pi_sm[w]);
+    double rx, ry, rz, rw;
+    ld256(A.wsv + 4 * static_cast<int64_t>(o), rx, ry, rz, rw);
+    const double C = A.Cj[j];
+    Acc acc;
+    acc.zero();
+    const uint32_t items = static_cast<uint32_t>(N + 1) / 2;
+    const uint32_t k = static_cast<uint32_t>(lane);
+    if (k < items) {
+        const uint32_t sa = static_cast<uint32_t>(pi_sm[w][2 * k]);
+        const uint32_t sb = (2 * k + 1 < static_cast<uint32_t>(N)) ? static_cast<uint32_t>(pi_sm[w][2 * k + 1]) : 0u;
+        process_item(A, j, o, N, k, sa, sb, C, rx, ry, rz, acc);
+    }
+    warp_reduce(acc);
+    if (lane == 0) {
+        double* r = A.small_recs + static_cast<int64_t>(j) * kRec;
+#pragma unroll
+        for (int q = 0; q < 15; ++q) r[q] = acc.a[q];
+        r[15] = 0.0;
+    }
+}
+
+// N_j > 64: one CTA per cell-aligned chunk of kChunk items.
+__global__ void __launch_bounds__(kCollideThreads)
+k_collide_large(CollideArgs A)
+{
+    __shared__ int32_t s_j;
+    __shared__ double red[kCollideThreads / 32][15];
+    const int c = blockIdx.x;
+    if (threadIdx.x == 0) {
+        // last j with chunk_off[j] <= c (chunk_off is non-decreasing, chunk_off[M] = total)
+        int lo = 0, hi = A.M;   // invariant: chunk_off[lo] <= c < chunk_off[hi] when c < total
+        if (c >= A.chunk_off[A.M]) {
+            s_j = -1;
+        } else {
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (A.chunk_off[mid] <= c) lo = mid; else hi = mid;
+            }
+            s_j = lo;
+        }
+    }
+    __syncthreads();
+    const int j = s_j;
+    if (j < 0) return;
+    const int32_t N = A.cnt[j], o = A.off[j];
+    const uint32_t items = static_cast<uint32_t>(N + 1) / 2;
+    const uint32_t i0 = static_cast<uint32_t>(c - A.chunk_off[j]) * kChunk;
+    const uint32_t i1 = min(i0 + static_cast<uint32_t>(kChunk), items);
+    const cc::Feistel f = cc::make_feistel(static_cast<uint32_t>(N), A.keys[j]);
+    const double C = A.Cj[j];
+    double rx, ry, rz, rw;
+    ld256(A.wsv + 4 * static_cast<int64_t>(o), rx, ry, rz, rw);
+    Acc acc;
+    acc.zero();
+    for (uint32_t k = i0 + threadIdx.x; k < i1; k += kCollideThreads) {
+        const uint32_t sa = cc::feistel_pi(f, 2 * k);
+        const uint32_t sb = (2 * k + 1 < static_cast<uint32_t>(N)) ? cc::feistel_pi(f, 2 * k + 1) : 0u;
+        process_item(A, j, o, N, k, sa, sb, C, rx, ry, rz, acc);
+    }
+    warp_reduce(acc);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < 15; ++q) red[w][q] = acc.a[q];
+    __syncthreads();
+    if (threadIdx.x < 15) {
+        double s = 0.0;
+#pragma unroll
+        for (int ww = 0; ww < kCollideThreads / 32; ++ww) s += red[ww][threadIdx.x];
+        A.recs[static_cast<int64_t>(c) * kRec + threadIdx.x] = s;
+    }
+}
+
+// Dead (and invalid) particles: slots [L, n), copied unchanged.
+__global__ void k_copy_dead(const double* __restrict__ wsv, const int32_t* __restrict__ off, int M, int n,
+                            double* __restrict__ v_out, int64_t ldv, int32_t* __restrict__ cell_out,
+                            int32_t* __restrict__ perm_out)
+{
+    const int32_t L = off[M];
+    for (int64_t p = L + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < n;
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double x, y, z, wq;
+        ld256(wsv + 4 * p, x, y, z, wq);
+        v_out[p] = x; v_out[ldv + p] = y; v_out[2 * ldv + p] = z;
+        cell_out[p] = -1;
+        if (perm_out) perm_out[p] = unpack_perm(wq);
+    }
+}
+
+// ------------------------------------------------------------------ moments and diagnostics
+struct MomConst {
+    double weight, volume;
+    const double* volume_arr;
+    double m_over_e;
+};
+
+// moments from shifted sums: mean = ref + S1/N, T = (m/e) (S2/N - (S1/N)^2)
+__device__ __forceinline__ void moments_from_sums(const double* s, double N, double rx, double ry,
+                                                  double rz, double V, const MomConst& mc, double* o)
+{
+    const double inv = 1.0 / N;
+    const double d[3] = {s[0] * inv, s[1] * inv, s[2] * inv};
+    const double r[3] = {rx, ry, rz};
+    o[0] = N * mc.weight / V;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        o[1 + q] = r[q] + d[q];
+        o[4 + q] = mc.m_over_e * (s[3 + q] * inv - d[q] * d[q]);
+    }
+}
+
+__global__ void k_finalize_cells(const int32_t* __restrict__ cnt, const int32_t* __restrict__ off,
+                                 const int32_t* __restrict__ chunk_off, const double* __restrict__ recs,
+                                 const double* __restrict__ small_recs, const double* __restrict__ wsv,
+                                 int M, MomConst mc, double* __restrict__ moments_out,
+                                 double* __restrict__ cellsum)
+{
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= M) return;
+    const int32_t N = cnt[j];
+    double s[15];
+#pragma unroll
+    for (int q = 0; q < 15; ++q) s[q] = 0.0;
+    double rx = 0, ry = 0, rz = 0;
+    if (N > 0) {
+        double rw;
+        ld256(wsv + 4 * static_cast<int64_t>(off[j]), rx, ry, rz, rw);
+        if (N <= cc::kSmallCell) {
+#pragma unroll
+            for (int q = 0; q < 15; ++q) s[q] = small_recs[static_cast<int64_t>(j) * kRec + q];
+        } else {
+            for (int32_t c = chunk_off[j]; c < chunk_off[j + 1]; ++c)
+#pragma unroll
+                for (int q = 0; q < 15; ++q) s[q] += recs[static_cast<int64_t>(c) * kRec + q];
+        }
+    }
+    if (moments_out) {
+        double* o = moments_out + static_cast<int64_t>(j) * CC_MOMENTS_LEN;
+        if (N > 0) {
+            const double V = mc.volume_arr ? mc.volume_arr[j] : mc.volume;
+            moments_from_sums(s, static_cast<double>(N), rx, ry, rz, V, mc, o);
+        } else {
+#pragma unroll
+            for (int q = 0; q < CC_MOMENTS_LEN; ++q) o[q] = 0.0;
+        }
+    }
+    double* cs = cellsum + static_cast<int64_t>(j) * kCellSum;
+#pragma unroll
+    for (int q = 0; q < kCellSum; ++q) cs[q] = s[6 + q];
+}
+
+// single CTA of 1024 threads: fixed-order reduction over cells
+__global__ void __launch_bounds__(1024)
+k_finalize_diag(const int32_t* __restrict__ cnt, const double* __restrict__ cellsum, int M,
+                double* __restrict__ diag)
+{
+    __shared__ double red[32][12];
+    double s[12];
+#pragma unroll
+    for (int q = 0; q < 12; ++q) s[q] = 0.0;
+    for (int j = threadIdx.x; j < M; j += blockDim.x) {
+        const int32_t N = cnt[j];
+        s[0] += N;
+        s[1] += N / 2;
+        s[2] += N & 1;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s[3 + q] += cellsum[static_cast<int64_t>(j) * kCellSum + q];
+    }
+    if (threadIdx.x == 0) s[11] = cnt[M];
+#pragma unroll
+    for (int q = 0; q < 12; ++q)
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) s[q] += __shfl_down_sync(0xFFFFFFFFu, s[q], d);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < 12; ++q) red[w][q] = s[q];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t[12];
+        for (int q = 0; q < 12; ++q) t[q] = 0.0;
+        for (int ww = 0; ww < static_cast<int>(blockDim.x / 32); ++ww)
+            for (int q = 0; q < 12; ++q) t[q] += red[ww][q];
+        diag[0] = t[0];
+        diag[1] = t[11];
+        diag[2] = t[1];
+        diag[3] = t[2];
+        for (int q = 0; q < 8; ++q) diag[4 + q] = t[3 + q];
+        for (int q = 12; q < 16; ++q) diag[q] = 0.0;
+    }
+}
+
+// ------------------------------------------------------------------ test-hook kernels
+__global__ void k_extract_perm(const double* __restrict__ wsv, int n, int32_t* __restrict__ perm)
+{
+    const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (p < n) {
+        double x, y, z, w;
+        ld256(wsv + 4 * p, x, y, z, w);
+        perm[p] = unpack_perm(w);
+    }
+}
+
+// one CTA per cell; pair base = sum_{i<j} floor(N_i/2) computed in-block (test hook only)
+__global__ void __launch_bounds__(256)
+k_pairs(const int32_t* __restrict__ off, int M, uint32_t cell_base, uint32_t step, uint32_t s0,
+        uint32_t s1, int32_t* __restrict__ out, int64_t max_pairs)
+{
+    __shared__ int64_t red[8];
+    __shared__ int32_t pi_sm[cc::kSmallCell];
+    const int j = blockIdx.x;
+    int64_t part = 0;
+    for (int i = threadIdx.x; i < j; i += blockDim.x) part += (off[i + 1] - off[i]) / 2;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) part += __shfl_down_sync(0xFFFFFFFFu, part, d);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+    __syncthreads();
+    int64_t pb = 0;
+    for (int w = 0; w < 8; ++w) pb += red[w];
+    const int32_t o = off[j], N = off[j + 1] - off[j];
+    if (N < 2) return;
+    const uint32_t G = cell_base + static_cast<uint32_t>(j);
+    if (N <= cc::kSmallCell) {
+        if (threadIdx.x < 32) {
+            cc::small_cell_perm(static_cast<uint32_t>(N), G, step, s0, s1, threadIdx.x, pi_sm);
+            for (int k = threadIdx.x; k < N / 2; k += 32) {
+                const int64_t g = pb + k;
+                if (g < max_pairs) {
+                    out[2 * g] = o + pi_sm[2 * k];
+                    out[2 * g + 1] = o + pi_sm[2 * k + 1];
+                }
+            }
+        }
+        return;
+    }
+    const cc::U4 keys = cc::philox4x32_10(cc::U4{0u, G, step, 1u}, s0, s1);
+    const cc::Feistel f = cc::make_feistel(static_cast<uint32_t>(N), keys);
+    for (int k = threadIdx.x; k < N / 2; k += blockDim.x) {
+        const int64_t g = pb + k;
+        if (g < max_pairs) {
+            out[2 * g] = o + static_cast<int32_t>(cc::feistel_pi(f, 2u * k));
+            out[2 * g + 1] = o + static_cast<int32_t>(cc::feistel_pi(f, 2u * k + 1u));
+        }
+    }
+}
+
+__global__ void k_philox(const uint32_t* __restrict__ ctr, uint32_t s0, uint32_t s1,
+                         uint32_t* __restrict__ out, int64_t m)
+{
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= m) return;
+    const cc::U4 r = cc::philox4x32_10(cc::U4{ctr[4 * i], ctr[4 * i + 1], ctr[4 * i + 2], ctr[4 * i + 3]}, s0, s1);
+    out[4 * i] = r.x; out[4 * i + 1] = r.y; out[4 * i + 2] = r.z; out[4 * i + 3] = r.w;
+}
+
+__global__ void k_ppnd16(const double* __restrict__ u, double* __restrict__ z, int64_t m)
+{
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < m) z[i] = cc::ppnd16(u[i]);
+}
+
+__global__ void k_ta_pairs(double* __restrict__ va, double* __restrict__ vb, const double* __restrict__ C,
+                           const double* __restrict__ u1, const double* __restrict__ u2, int64_t m)
+{
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= m) return;
+    double ax = va[i], ay = va[m + i], az = va[2 * m + i];
+    double bx = vb[i], by = vb[m + i], bz = vb[2 * m + i];
+    cc::ta_update(ax, ay, az, bx, by, bz, C[i], u1[i], u2[i]);
+    va[i] = ax; va[m + i] = ay; va[2 * m + i] = az;
+    vb[i] = bx; vb[m + i] = by; vb[2 * m + i] = bz;
+}
+
+// P2C hook: one CTA per cell, shifted single pass (ref = first slot), fixed order.
+__global__ void __launch_bounds__(256)
+k_moments(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__ off, int M, MomConst mc,
+          double* __restrict__ out)
+{
+    __shared__ double red[8][6];
+    const int j = blockIdx.x;
+    const int32_t a = off[j], b = off[j + 1], N = b - a;
+    double* o = out + static_cast<int64_t>(j) * CC_MOMENTS_LEN;
+    if (N <= 0) {
+        if (threadIdx.x < CC_MOMENTS_LEN) o[threadIdx.x] = 0.0;
+        return;
+    }
+    const double rx = v[a], ry = v[ldv + a], rz = v[2 * ldv + a];
+    double s[6] = {0, 0, 0, 0, 0, 0};
+    for (int32_t p = a + threadIdx.x; p < b; p += blockDim.x) {
+        const double dx = v[p] - rx, dy = v[ldv + p] - ry, dz = v[2 * ldv + p] - rz;
+        s[0] += dx; s[1] += dy; s[2] += dz;
+        s[3] += dx * dx; s[4] += dy * dy; s[5] += dz * dz;
+    }
+#pragma unroll
+    for (int q = 0; q < 6; ++q)
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) s[q] += __shfl_down_sync(0xFFFFFFFFu, s[q], d);
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+        for (int q = 0; q < 6; ++q) red[threadIdx.x >> 5][q] = s[q];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t[6] = {0, 0, 0, 0, 0, 0};
+        for (int w = 0; w < 8; ++w)
+            for (int q = 0; q < 6; ++q) t[q] += red[w][q];
+        const double V = mc.volume_arr ? mc.volume_arr[j] : mc.volume;
+        moments_from_sums(t, static_cast<double>(N), rx, ry, rz, V, mc, o);
+    }
+}
+
+__global__ void k_diag_sum_ranks(const double* __restrict__ g, int P, double* __restrict__ out)
+{
+    const int q = threadIdx.x;
+    if (q >= CC_DIAG_LEN) return;
+    double s = 0.0;
+    for (int r = 0; r < P; ++r) s += g[r * CC_DIAG_LEN + q];
+    out[q] = s;
+}
+
+// ------------------------------------------------------------------ host helpers
+bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+bool overlaps(const void* a, size_t na, const void* b, size_t nb)
+{
+    if (!a || !b || na == 0 || nb == 0) return false;
+    const char* pa = static_cast<const char*>(a);
+    const char* pb = static_cast<const char*>(b);
+    return pa < pb + nb && pb < pa + na;
+}
+
+int launch_ok()
+{
+    return cudaGetLastError() == cudaSuccess ? CC_OK : CC_ECUDA;
+}
+
+int prepare_max_smem(int bytes)
+{
+    // dynamic shared memory above 48 KB needs the opt-in attribute
+    static_assert(sizeof(int) == 4, "");
+    if (cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
+        return CC_ECUDA;
+    if (cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
+        return CC_ECUDA;
+    (void)bytes;
+    return CC_OK;
+}
+
+// CCS1-CCS3 into the workspace (shared by coulomb_collide and cc_bin).
+int run_binning(const double* v_in, int64_t ldv, const int32_t* cell_in, int n, int M, const Layout& L,
+                void* ws, const CellConst& k, uint32_t cell_base, uint32_t step, uint64_t seed,
+                cudaStream_t st)
+{
+    int rc = prepare_max_smem(0);
+    if (rc) return rc;
+    int32_t* err = at<int32_t>(ws, L.o_err);
+    int32_t* tcount = at<int32_t>(ws, L.o_tcount);
+    int32_t* cnt = at<int32_t>(ws, L.o_cnt);
+    int32_t* off = at<int32_t>(ws, L.o_off);
+    int32_t* chunk_off = at<int32_t>(ws, L.o_chunk);
+    double* Cj = at<double>(ws, L.o_C);
+    cc::U4* keys = at<cc::U4>(ws, L.o_keys);
+    double* wsv = at<double>(ws, L.o_wsv);
+    const int M1 = M + 1;
+    k_count<<<L.T, kCountThreads, sizeof(int32_t) * M1, st>>>(cell_in, n, M, L.tile, tcount, err);
+    k_scan_tiles<<<(M1 + 31) / 32, dim3(32, 8), 0, st>>>(tcount, L.T, M1, cnt);
+    k_scan_cells<<<1, 1024, 0, st>>>(cnt, M, off, chunk_off, Cj, keys, k, cell_base, step,
+                                     static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
+    const size_t smem = sizeof(int32_t) * M1 + sizeof(uint16_t) * static_cast<size_t>(L.W) * M1;
+    k_scatter<<<L.T, 32 * L.W, smem, st>>>(v_in, ldv, cell_in, n, M, L.W, tcount, off, wsv);
+    return launch_ok();
+}
+
+CellConst cell_const(const cc_params& p, double dt)
+{
+    CellConst k;
+    const double e2 = p.charge * p.charge;
+    const double mr = 0.5 * p.mass;
+    k.K = e2 * e2 * dt / (8.0 * M_PI * p.eps0 * p.eps0 * mr * mr);
+    k.weight = p.weight;
+    k.volume = p.cell_volume;
+    k.volume_arr = p.cell_volume_arr;
+    k.ln_lambda = p.ln_lambda;
+    k.ln_lambda_arr = p.ln_lambda_arr;
+    return k;
+}
+
+bool finite_pos(double x) { return std::isfinite(x) && x > 0.0; }
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+void cc_default_params(cc_params* p)
+{
+    if (!p) return;
+    std::memset(p, 0, sizeof(*p));
+    p->mass = 9.1093837015e-31;
+    p->charge = 1.602176634e-19;
+    p->eps0 = 8.8541878128e-12;
+    p->weight = 1.0;
+    p->cell_volume = 1.0;
+    p->ln_lambda = 10.0;
+}
+
+size_t cc_workspace_bytes(int64_t n, int32_t cells)
+{
+    if (n < 0 || cells < 1) return 0;
+    return make_layout(n, cells).total;
+}
+
+const char* cc_strerror(int code)
+{
+    switch (code) {
+        case CC_OK: return "ok";
+        case CC_EINVAL: return "invalid argument";
+        case CC_EWORKSPACE: return "workspace too small or misaligned";
+        case CC_ECUDA: return "CUDA launch failed";
+        case CC_ECELL: return "cell id outside [-1, cells)";
+        case CC_ECOUNT: return "n >= 2^31 or cells > CC_MAX_CELLS";
+        case CC_ENCCL: return "NCCL error";
+        default: return "unknown error";
+    }
+}
+
+int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, double* v_out,
+                    int32_t* cell_out, int32_t* perm_out, int64_t n, int32_t cells, uint32_t cell_base,
+                    double dt, const cc_params* params, uint64_t seed, uint64_t step,
+                    double* moments_out, double* diag_out, void* workspace, size_t workspace_bytes,
+                    void* stream)
+{
+    cc_params p;
+    if (params) p = *params; else cc_default_params(&p);
+    if (n < 0 || cells < 1 || ldv < n || !(dt > 0.0) || step >= (1ull << 32)) return CC_EINVAL;
+    if (n >= (1ll << 31) || cells > CC_MAX_CELLS) return CC_ECOUNT;
+    if (!finite_pos(p.mass) || !finite_pos(p.charge) || !finite_pos(p.eps0) || !std::isfinite(p.weight) ||
+        p.weight < 0.0 || (!p.cell_volume_arr && !finite_pos(p.cell_volume)) ||
+        (!p.ln_lambda_arr && !std::isfinite(p.ln_lambda)) || p.flags != 0)
+        return CC_EINVAL;
+    if (!workspace || !aligned(workspace, 256)) return CC_EWORKSPACE;
+    const Layout L = make_layout(n, cells);
+    if (workspace_bytes < L.total) return CC_EWORKSPACE;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int M = cells;
+    if (n == 0) {
+        if (moments_out && cudaMemsetAsync(moments_out, 0, sizeof(double) * CC_MOMENTS_LEN * M, st) != cudaSuccess)
+            return CC_ECUDA;
+        if (diag_out && cudaMemsetAsync(diag_out, 0, sizeof(double) * CC_DIAG_LEN, st) != cudaSuccess)
+            return CC_ECUDA;
+        return CC_OK;
+    }
+    if (!v_in || !cell_in || !v_out || !cell_out) return CC_EINVAL;
+    if (!aligned(v_in, 16) || !aligned(v_out, 16) || !aligned(cell_in, 4) || !aligned(cell_out, 4))
+        return CC_EINVAL;
+    const size_t vbytes = sizeof(double) * static_cast<size_t>(2 * ldv + n);
+    if (overlaps(v_in, vbytes, v_out, vbytes) || overlaps(cell_in, 4 * n, cell_out, 4 * n) ||
+        overlaps(v_out, vbytes, cell_out, 4 * n) || (perm_out && overlaps(perm_out, 4 * n, v_out, vbytes)) ||
+        (perm_out && overlaps(perm_out, 4 * n, cell_out, 4 * n)) || overlaps(workspace, L.total, v_out, vbytes))
+        return CC_EINVAL;
+
+    const CellConst k = cell_const(p, dt);
+    const int nn = static_cast<int>(n);
+    int rc = run_binning(v_in, ldv, cell_in, nn, M, L, workspace, k, cell_base, static_cast<uint32_t>(step), seed, st);
+    if (rc) return rc;
+
+    CollideArgs A;
+    A.wsv = at<double>(workspace, L.o_wsv);
+    A.cnt = at<int32_t>(workspace, L.o_cnt);
+    A.off = at<int32_t>(workspace, L.o_off);
+    A.chunk_off = at<int32_t>(workspace, L.o_chunk);
+    A.Cj = at<double>(workspace, L.o_C);
+    A.keys = at<cc::U4>(workspace, L.o_keys);
+    A.v_out = v_out;
+    A.ldv = ldv;
+    A.cell_out = cell_out;
+    A.perm_out = perm_out;
+    A.recs = at<double>(workspace, L.o_recs);
+    A.small_recs = at<double>(workspace, L.o_small);
+    A.M = M;
+    A.cell_base = cell_base;
+    A.step = static_cast<uint32_t>(step);
+    A.s0 = static_cast<uint32_t>(seed);
+    A.s1 = static_cast<uint32_t>(seed >> 32);
+
+    k_collide_small<<<(M + 7) / 8, 256, 0, st>>>(A);
+    k_collide_large<<<static_cast<unsigned>(L.max_chunks), kCollideThreads, 0, st>>>(A);
+    k_copy_dead<<<148 * 4, 256, 0, st>>>(A.wsv, A.off, M, nn, v_out, ldv, cell_out, perm_out);
+
+    MomConst mc{p.weight, p.cell_volume, p.cell_volume_arr, p.mass / p.charge};
+    double* cellsum = at<double>(workspace, L.o_cellsum);
+    k_finalize_cells<<<(M + 255) / 256, 256, 0, st>>>(A.cnt, A.off, A.chunk_off, A.recs, A.small_recs, A.wsv, M,
+                                                      mc, moments_out, cellsum);
+    if (diag_out) k_finalize_diag<<<1, 1024, 0, st>>>(A.cnt, cellsum, M, diag_out);
+    return launch_ok();
+}
+
+int cc_device_status(void* workspace, void* stream)
+{
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return CC_ECUDA;
+    if (!workspace) return CC_EWORKSPACE;
+    int32_t err = 0;
+    if (cudaMemcpy(&err, workspace, sizeof(err), cudaMemcpyDeviceToHost) != cudaSuccess) return CC_ECUDA;
+    if (err) {
+        if (cudaMemset(workspace, 0, sizeof(err)) != cudaSuccess) return CC_ECUDA;
+        return CC_ECELL;
+    }
+    return CC_OK;
+}
+
+int cc_bin(const int32_t* cell_in, int64_t n, int32_t cells, int32_t* perm_out, int32_t* off_out,
+           void* workspace, size_t workspace_bytes, void* stream)
+{
+    if (n < 0 || cells < 1) return CC_EINVAL;
+    if (n >= (1ll << 31) || cells > CC_MAX_CELLS) return CC_ECOUNT;
+    if (!workspace || !aligned(workspace, 256)) return CC_EWORKSPACE;
+    const Layout L = make_layout(n, cells);
+    if (workspace_bytes < L.total) return CC_EWORKSPACE;
+    if (!off_out || (n > 0 && (!cell_in || !perm_out))) return CC_EINVAL;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cc_params p;
+    cc_default_params(&p);
+    const CellConst k = cell_const(p, 1.0);
+    if (n == 0) {
+        return cudaMemsetAsync(off_out, 0, sizeof(int32_t) * (cells + 1), st) == cudaSuccess ? CC_OK : CC_ECUDA;
+    }
+    // the velocity payload is irrelevant for the order: bin without one
+    const int nn = static_cast<int>(n);
+    int rc = run_binning(nullptr, 0, cell_in, nn, cells, L, workspace, k, 0, 0, 0, st);
+    if (rc) return rc;
+    k_extract_perm<<<(nn + 255) / 256, 256, 0, st>>>(at<double>(workspace, L.o_wsv), nn, perm_out);
+    if (cudaMemcpyAsync(off_out, at<int32_t>(workspace, L.o_off), sizeof(int32_t) * (cells + 1),
+                        cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return CC_ECUDA;
+    return launch_ok();
+}
+
+int cc_pairs(const int32_t* off, int32_t cells, uint32_t cell_base, uint64_t seed, uint64_t step,
+             int32_t* pair_slots_out, int64_t max_pairs, void* stream)
+{
+    if (!off || cells < 1 || step >= (1ull << 32) || max_pairs < 0) return CC_EINVAL;
+    if (max_pairs > 0 && !pair_slots_out) return CC_EINVAL;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    k_pairs<<<cells, 256, 0, st>>>(off, cells, cell_base, static_cast<uint32_t>(step), static_cast<uint32_t>(seed),
+                                   static_cast<uint32_t>(seed >> 32), pair_slots_out, max_pairs);
+    return launch_ok();
+}
+
+int cc_philox(const uint32_t* ctr4, uint64_t seed, uint32_t* out4, int64_t m, void* stream)
+{
+    if (m < 0 || (m > 0 && (!ctr4 || !out4))) return CC_EINVAL;
+    if (m == 0) return CC_OK;
+    k_philox<<<static_cast<unsigned>((m + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        ctr4, static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32), out4, m);
+    return launch_ok();
+}
+
+int cc_ppnd16(const double* u, double* z, int64_t m, void* stream)
+{
+    if (m < 0 || (m > 0 && (!u || !z))) return CC_EINVAL;
+    if (m == 0) return CC_OK;
+    k_ppnd16<<<static_cast<unsigned>((m + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(u, z, m);
+    return launch_ok();
+}
+
+int cc_ta_pairs(double* va, double* vb, const double* C, const double* u1, const double* u2, int64_t m,
+                void* stream)
+{
+    if (m < 0 || (m > 0 && (!va || !vb || !C || !u1 || !u2))) return CC_EINVAL;
+    if (m == 0) return CC_OK;
+    k_ta_pairs<<<static_cast<unsigned>((m + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(va, vb, C, u1,
+                                                                                                       u2, m);
+    return launch_ok();
+}
+
+int cc_moments(const double* v, int64_t ldv, const int32_t* off, int32_t cells, const cc_params* params,
+               double* out, void* stream)
+{
+    if (!v || !off || !out || cells < 1 || ldv < 0) return CC_EINVAL;
+    cc_params p;
+    if (params) p = *params; else cc_default_params(&p);
+    MomConst mc{p.weight, p.cell_volume, p.cell_volume_arr, p.mass / p.charge};
+    k_moments<<<cells, 256, 0, static_cast<cudaStream_t>(stream)>>>(v, ldv, off, cells, mc, out);
+    return launch_ok();
+}
+
+int cc_diag_sum_ranks(const double* gathered, int32_t nranks, double* out, void* stream)
+{
+    if (!gathered || !out || nranks < 1) return CC_EINVAL;
+    k_diag_sum_ranks<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(gathered, nranks, out);
+    return launch_ok();
+}
+
+}  // extern "C"

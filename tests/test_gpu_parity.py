@@ -1,0 +1,246 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by element.
+
+Bars (BASELINE.json north_star):
+  - binning, pairing, perm, cell ids: bit-exact
+  - velocities: |v_gpu - v_ref| <= 1e-12 * max(|v_ref|_2, v_floor) per component,
+    v_floor = 1e-3 sqrt(kT/m) (reading R15)
+  - moments: 1e-12 relative (density exact; mean vs thermal speed; T vs T)
+  - diagnostics: counts exact; sums 1e-12 of the sum of magnitudes
+"""
+import numpy as np
+import pytest
+
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2508_06771_b200 as cc  # noqa: E402
+
+DEV = torch.device("cuda:0")
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def O():
+    import oracle
+    oracle.build()
+    return oracle
+
+
+def to_dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def vel_err(v_gpu, v_ref, floor):
+    scale = np.maximum(np.linalg.norm(v_ref, axis=0), floor)
+    return np.max(np.abs(v_gpu - v_ref) / scale) if v_ref.size else 0.0
+
+
+def check_collide(O, w, step=0, moments=True):
+    p = w.params()
+    out = cc.coulomb_collide(to_dev(w.v), to_dev(w.cell), w.cells, step=step, **p)
+    torch.cuda.synchronize()
+    ref = O.coulomb_collide(w.v, w.cell, w.cells, step=step, want_pairs=False, **p)
+    assert np.array_equal(out.perm_out.cpu().numpy(), ref.perm_out)
+    assert np.array_equal(out.cell_out.cpu().numpy(), ref.cell_out)
+    err = vel_err(out.v_out.cpu().numpy(), ref.v_out, 1e-3 * W.sigma_v(2.0))
+    assert err <= TOL, err
+    if moments:
+        check_moments(out.moments.cpu().numpy(), ref.moments, w)
+    check_diag(out.diag.cpu().numpy(), ref.diag, ref.v_out)
+    return out, ref, err
+
+
+def check_moments(m, r, w):
+    assert np.array_equal(m[:, 0] == 0, r[:, 0] == 0)
+    nz = r[:, 0] > 0
+    assert np.all(np.abs(m[nz, 0] - r[nz, 0]) <= 1e-15 * r[nz, 0])
+    sig = W.sigma_v(2.0)
+    assert np.max(np.abs(m[nz, 1:4] - r[nz, 1:4])) <= TOL * max(sig, np.abs(r[nz, 1:4]).max())
+    T = r[nz, 4:7]
+    assert np.all(np.abs(m[nz, 4:7] - T) <= TOL * np.maximum(T, 1e-6) + 1e-300)
+
+
+def check_diag(d, r, v_ref):
+    assert np.array_equal(d[[0, 1, 2, 3]], r[[0, 1, 2, 3]])
+    sabs = np.abs(v_ref).sum(axis=1)
+    for q in range(3):
+        assert abs(d[4 + q] - r[4 + q]) <= TOL * sabs[q] + 1e-300
+        assert abs(d[8 + q] - r[8 + q]) <= TOL * sabs[q] + 1e-300
+    assert abs(d[7] - r[7]) <= TOL * r[7]
+    assert abs(d[11] - r[11]) <= TOL * r[11]
+
+
+# ------------------------------------------------------------------ element functions
+
+
+def test_philox_matches_oracle_and_kat(O):
+    rng = np.random.default_rng(0)
+    ctr = rng.integers(0, 2 ** 32, (4096, 4), dtype=np.uint64).astype(np.uint32)
+    ctr[0] = [0, 0, 0, 0]
+    ctr[1] = [0xFFFFFFFF] * 4
+    for seed in (0, 42, (0x299F31D0 << 32) | 0xA4093822, 0xFFFFFFFFFFFFFFFF):
+        got = cc.cc_philox(to_dev(ctr.view(np.int32)), seed).cpu().numpy().view(np.uint32)
+        key = [seed & 0xFFFFFFFF, seed >> 32]
+        for i in range(0, 4096, 97):
+            assert np.array_equal(got[i], O.philox4x32_10(ctr[i], key))
+    got = cc.cc_philox(to_dev(np.array([[0x243f6a88, 0x85a308d3, 0x13198a2e, 0x03707344]],
+                                       np.uint32).view(np.int32)),
+                       (0x299f31d0 << 32) | 0xa4093822).cpu().numpy().view(np.uint32)
+    assert [hex(x) for x in got[0]] == ["0xd16cfe09", "0x94fdcceb", "0x5001e420", "0x24126ea1"]
+
+
+def test_ppnd16_matches_oracle(O):
+    rng = np.random.default_rng(1)
+    u = np.concatenate([rng.random(20000), [2.0 ** -53, 1 - 2.0 ** -53, 1e-300, 0.075, 0.925,
+                                            np.exp(-25.0), 0.5 + 2.0 ** -53]])
+    z = cc.cc_ppnd16(to_dev(u)).cpu().numpy()
+    ref = np.array([O.ppnd16(x) for x in u])
+    assert np.all(np.abs(z - ref) <= 1e-15 * np.maximum(np.abs(ref), 1e-3))
+
+
+def test_ta_pairs_match_oracle(O):
+    rng = np.random.default_rng(2)
+    m = 5000
+    s = W.sigma_v(2.0)
+    va = rng.standard_normal((3, m)) * s
+    vb = rng.standard_normal((3, m)) * s
+    vb[:, :10] = va[:, :10]                 # identical velocities
+    vb[0:2, 10:20] = va[0:2, 10:20]         # u_perp = 0 branch
+    C = 10 ** rng.uniform(10, 17, m)
+    u1, u2 = rng.random(m), rng.random(m)
+    ga, gb = to_dev(va), to_dev(vb)
+    cc.cc_ta_pairs(ga, gb, to_dev(C), to_dev(u1), to_dev(u2))
+    ga, gb = ga.cpu().numpy(), gb.cpu().numpy()
+    for i in range(m):
+        ra, rb = O.ta_pair(va[:, i], vb[:, i], C[i], u1[i], u2[i])
+        sc = np.linalg.norm(va[:, i]) + np.linalg.norm(vb[:, i])
+        assert np.max(np.abs(ga[:, i] - ra)) <= 1e-13 * sc, i
+        assert np.max(np.abs(gb[:, i] - rb)) <= 1e-13 * sc, i
+    assert np.array_equal(ga[:, :10], va[:, :10]) and np.array_equal(gb[:, :10], vb[:, :10])
+
+
+# ------------------------------------------------------------------ binning and pairing
+
+BIN_CASES = [(0, 1, 0.0), (1, 1, 0.0), (7, 3, 0.0), (1000, 1, 0.0), (33_000, 1, 0.0),
+             (100_000, 100, 0.1), (200_003, 4096, 0.02), (70_001, 32768, 0.0),
+             (50_000, 7, 1.0), (300_000, 256, 0.0)]
+
+
+@pytest.mark.parametrize("n,M,dead", BIN_CASES)
+def test_bin_bit_exact(O, n, M, dead):
+    w = W.random_cells(n, M, seed=n + M, dead_frac=dead, skew=(M > 50))
+    perm, off = cc.cc_bin(to_dev(w.cell), M)
+    torch.cuda.synchronize()
+    rp, roff = O.stable_order(w.cell, M)
+    assert np.array_equal(off.cpu().numpy(), roff)
+    assert np.array_equal(perm.cpu().numpy(), rp)
+
+
+@pytest.mark.parametrize("n,M", [(1000, 1), (5000, 3), (20_000, 500), (100_000, 13), (3000, 3000)])
+def test_pairs_bit_exact(O, n, M):
+    w = W.random_cells(n, M, seed=7 * n + M, skew=True)
+    _, off = cc.cc_bin(to_dev(w.cell), M)
+    for step in (0, 5):
+        pairs = cc.cc_pairs(off, M, cell_base=11, seed=99, step=step).cpu().numpy()
+        ref = O.coulomb_collide(w.v, w.cell, M, cell_base=11, seed=99, step=step,
+                                dt=w.dt, weight=w.weight, cell_volume=w.cell_volume)
+        assert np.array_equal(pairs, ref.pair_slots)
+
+
+# ------------------------------------------------------------------ whole operator
+
+
+@pytest.mark.parametrize("n,M,dead,skew", [(0, 4, 0.0, False), (1, 1, 0.0, False), (2, 1, 0.0, False),
+                                           (65, 1, 0.0, False), (1000, 1, 0.0, False),
+                                           (50_000, 50, 0.05, True), (120_007, 4096, 0.01, True),
+                                           (40_000, 3000, 0.0, False), (9000, 2, 0.0, False),
+                                           (100_000, 1, 0.0, False), (20_000, 9, 1.0, False)])
+def test_collide_parity(O, n, M, dead, skew):
+    w = W.random_cells(n, M, seed=n + 3 * M, dead_frac=dead, skew=skew)
+    check_collide(O, w, step=17)
+
+
+def test_c1_chained_ten_steps(O):
+    """Config 1 (1 cell, 1,000 e-, Maxwellian 2 eV, 10 steps): each step's GPU
+    output feeds the next GPU step, same for the oracle; parity every step."""
+    w = W.c1()
+    p = w.params()
+    gv, gc = to_dev(w.v), to_dev(w.cell)
+    rv, rc = w.v, w.cell
+    errs = []
+    for s in range(10):
+        out = cc.coulomb_collide(gv, gc, 1, step=s, **p)
+        ref = O.coulomb_collide(rv, rc, 1, step=s, want_pairs=False, **p)
+        assert np.array_equal(out.perm_out.cpu().numpy(), ref.perm_out)
+        errs.append(vel_err(out.v_out.cpu().numpy(), ref.v_out, 1e-3 * W.sigma_v(2.0)))
+        gv, gc = out.v_out.clone(), out.cell_out.clone()
+        rv, rc = ref.v_out, ref.cell_out
+    assert max(errs) <= TOL, errs
+
+
+def test_c2_bimaxwellian_full(O):
+    w = W.c2()
+    check_collide(O, w, step=0)
+
+
+def test_c3_full(O):
+    w = W.c3()
+    check_collide(O, w, step=2)
+
+
+def test_determinism_bitwise(O):
+    w = W.random_cells(300_000, 1000, seed=5, skew=True, dead_frac=0.01)
+    a = cc.coulomb_collide(to_dev(w.v), to_dev(w.cell), w.cells, step=1, **w.params())
+    b = cc.coulomb_collide(to_dev(w.v), to_dev(w.cell), w.cells, step=1, **w.params())
+    for x, y in ((a.v_out, b.v_out), (a.perm_out, b.perm_out), (a.moments, b.moments), (a.diag, b.diag)):
+        assert torch.equal(x, y)
+
+
+def test_invalid_cell_ids_flagged(O):
+    w = W.random_cells(10_000, 10, seed=6)
+    cell = w.cell.copy()
+    cell[[5, 77, 9000]] = [10, -7, 123]
+    ws = cc.alloc_workspace(w.n, 10, DEV)
+    out = cc.coulomb_collide(to_dev(w.v), to_dev(cell), 10, workspace=ws, step=0, **w.params())
+    assert cc.cc_device_status(ws) == -4
+    assert cc.cc_device_status(ws) == 0          # flag cleared
+    # invalid particles are treated as dead: same as the oracle with them marked -1
+    cell2 = cell.copy()
+    cell2[[5, 77, 9000]] = -1
+    ref = O.coulomb_collide(w.v, cell2, 10, step=0, want_pairs=False, **w.params())
+    assert np.array_equal(out.perm_out.cpu().numpy(), ref.perm_out)
+    assert vel_err(out.v_out.cpu().numpy(), ref.v_out, 1.0) <= TOL
+
+
+def test_per_cell_arrays(O):
+    w = W.random_cells(30_000, 40, seed=8, skew=True)
+    rng = np.random.default_rng(8)
+    V = rng.uniform(0.5e-6, 2e-6, 40)
+    lnL = rng.uniform(5, 15, 40)
+    p = w.params()
+    out = cc.coulomb_collide(to_dev(w.v), to_dev(w.cell), 40, step=3, cell_volume_arr=to_dev(V),
+                             ln_lambda_arr=to_dev(lnL), **p)
+    ref = O.coulomb_collide(w.v, w.cell, 40, step=3, cell_volume_arr=V, ln_lambda_arr=lnL,
+                            want_pairs=False, **p)
+    assert vel_err(out.v_out.cpu().numpy(), ref.v_out, 1.0) <= TOL
+    check_moments(out.moments.cpu().numpy(), ref.moments, w)
+
+
+def test_moments_hook_matches_oracle(O):
+    w = W.random_cells(50_000, 100, seed=9, skew=True)
+    perm, off = O.stable_order(w.cell, 100)
+    vs = np.ascontiguousarray(w.v[:, perm])
+    m = cc.cc_moments(to_dev(vs), to_dev(off.astype(np.int32)), 100, weight=w.weight,
+                      cell_volume=w.cell_volume).cpu().numpy()
+    r = O.moments(vs, off, w.weight, w.cell_volume)
+    check_moments(m, r, w)
+
+
+def test_diag_sum_ranks():
+    g = torch.arange(3 * 16, dtype=torch.float64, device=DEV).reshape(3, 16)
+    assert torch.equal(cc.cc_diag_sum_ranks(g), g[0] + g[1] + g[2])
