@@ -1,0 +1,394 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 e–e Coulomb collision operator (arXiv 2508.06771, step S1).
+
+Contract (driver): ``python bench.py --gpus N --steps K --warmup W`` prints ONE
+JSON line on rank 0.  A "step" is one call of the whole hot path
+(coulomb_collide: count -> scan -> stable scatter -> pair + TA collide ->
+moments/diagnostics) on one batch of synthetic input resident in HBM.
+
+Workload (BASELINE.json configs[3], "C4"): 64 x 64 = 4096 cells x 25,000
+electrons = 1.024e8 e- per GPU, isotropic Maxwellian 2 eV, particle order
+randomly permuted (the paper stores particles unsorted) — every timed
+step bins the unsorted input from scratch ("cold").  Inputs are 2.87 GB, far
+larger than the 126 MB L2, so no flush is needed between steps.  For N > 1
+(torchrun) each rank owns a C5 shard: global cells [4096 r, 4096 (r+1)),
+its own data seed; cells never cross ranks, so the data path has no
+collective; NCCL all_gather carries only the 16-double diagnostics vector
+(summed in rank order on the device).  Weak scaling.
+
+``--impl reference`` times the CPU oracle (oracle/, as it stands) on the host
+cores instead, on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "electron-electron pair collisions/sec (TA77 Coulomb operator step, fp64)"
+UNIT = "pair-collisions/s"
+# algorithmic bytes per particle: the method must read v (24 B)
+# and the cell id (4 B) and write v (24 B) once per step
+STEP_BYTES_PER_PARTICLE = 52
+# per-stage algorithmic bytes per particle (what each kernel's contract must move once)
+STAGE_BYTES = {"count": 4, "scatter": 4 + 24 + 32, "collide": 28 + 32}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--per-cell", type=int, default=25_000)
+    ap.add_argument("--nx", type=int, default=64)
+    ap.add_argument("--ny", type=int, default=64)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-cells", type=int, default=96,
+                    help="cells of the C4 workload the CPU baseline processes per step")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload(args, rank):
+    import workloads as W
+    if rank == 0 and int(os.environ.get("WORLD_SIZE", "1")) == 1:
+        return W.c4(nx=args.nx, ny=args.ny, per_cell=args.per_cell)
+    return W.c5_rank(rank, nx=args.nx, ny=args.ny, per_cell=args.per_cell)
+
+
+def workload_name(args, world):
+    base = f"C4 2D argon discharge {args.nx}x{args.ny} cells x {args.per_cell} e-/cell, Maxwellian 2 eV"
+    if world > 1:
+        return f"C5 weak scaling: {base} per GPU, cell-range sharded over {world} GPUs"
+    return base
+
+
+# ---------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU oracle (baseline / reference arm)
+
+
+def oracle_sample(args, cells_per_step, seed_offset=4):
+    """A bounded sample of the C4 workload: the first `cells_per_step` cells
+    (25,000 e- each, Maxwellian 2 eV), randomly ordered like the full input."""
+    import workloads as W
+    w = W.c4(nx=1, ny=cells_per_step, per_cell=args.per_cell, seed_offset=seed_offset)
+    return w
+
+
+def time_oracle(args, steps, cells_per_step):
+    import oracle
+    oracle.build()
+    w = oracle_sample(args, cells_per_step)
+    p = w.params()
+    oracle.coulomb_collide(w.v[:, :2000], np.zeros(2000, np.int32), 1, want_pairs=False, **p)  # load/warm
+    t0 = time.perf_counter()
+    for s in range(steps):
+        r = oracle.coulomb_collide(w.v, w.cell, w.cells, step=s, want_pairs=False, **p)
+    dt = time.perf_counter() - t0
+    pairs = float(r.diag[2]) * steps
+    return {"value": pairs / dt, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"{cells_per_step} of {args.nx * args.ny} C4 cells ({w.n:.3g} e-, "
+                      f"{int(r.diag[2])} pairs) per step, {steps} step(s), {dt:.1f} s wall",
+            "seconds": dt}
+
+
+def time_oracle_on(w, args):
+    """The oracle as it stands, on the host cores, on the SAME resident C4 input
+    (one step; ~1e8 e- is 5-30 s of CPU work depending on the core count)."""
+    import oracle
+    oracle.build()
+    p = w.params()
+    t0 = time.perf_counter()
+    r = oracle.coulomb_collide(w.v, w.cell, w.cells, step=0, want_pairs=False, **p)
+    dt = time.perf_counter() - t0
+    return {"value": float(r.diag[2]) / dt, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"the full C4 input ({w.n:.4g} e-, {int(r.diag[2])} pairs), 1 step, {dt:.1f} s wall",
+            "seconds": dt}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    steps = max(args.steps, 1)
+    # bounded: each step processes a sample sized so the whole run stays within minutes
+    cells = max(4, min(args.cpu_cells, int(1200 / max(steps + args.warmup, 1))))
+    import oracle
+    oracle.build()
+    w = oracle_sample(args, cells)
+    p = w.params()
+    for s in range(args.warmup):
+        oracle.coulomb_collide(w.v, w.cell, w.cells, step=1000 + s, want_pairs=False, **p)
+    t0 = time.perf_counter()
+    for s in range(steps):
+        r = oracle.coulomb_collide(w.v, w.cell, w.cells, step=s, want_pairs=False, **p)
+    dt = time.perf_counter() - t0
+    pairs = float(r.diag[2]) * steps
+    value = pairs / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": workload_name(args, 1) + f" — CPU oracle on a {cells}-cell sample per step",
+                   "cells_per_step": cells, "electrons_per_step": w.n},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+                         "sample": f"{cells} of {args.nx * args.ny} C4 cells ({w.n:.3g} e-) per step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
+
+
+def run_ours(args):
+    import torch
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+
+    import paper_2508_06771_b200 as cc
+    from paper_2508_06771_b200 import _lib
+    from paper_2508_06771_b200.coulomb import CollideOut
+
+    w = workload(args, rank)
+    n, M = w.n, w.cells
+    v_host = torch.from_numpy(w.v)
+    c_host = torch.from_numpy(w.cell)
+    v = v_host.to(dev)
+    cell = c_host.to(dev)
+    p = w.params()
+    ws = cc.alloc_workspace(n, M, dev)
+    out = CollideOut(torch.empty((3, n), dtype=torch.float64, device=dev),
+                     torch.empty(n, dtype=torch.int32, device=dev),
+                     torch.empty(n, dtype=torch.int32, device=dev),
+                     torch.empty((M, 7), dtype=torch.float64, device=dev),
+                     torch.empty(16, dtype=torch.float64, device=dev))
+    gathered = torch.empty((world, 16), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def one_step(s, events=None):
+        params = dict(p)
+        params.pop("seed")
+        lib = _lib.load()
+        import ctypes as C
+        prm = cc.make_params(weight=params["weight"], cell_volume=params["cell_volume"],
+                             ln_lambda=params["ln_lambda"])
+        if events is not None:
+            arr = (C.c_void_p * len(events))(*[e.cuda_event for e in events])
+            prm.stage_events = C.cast(arr, C.POINTER(C.c_void_p))
+        rc = lib.coulomb_collide(C.c_void_p(v.data_ptr()), n, C.c_void_p(cell.data_ptr()),
+                                 C.c_void_p(out.v_out.data_ptr()), C.c_void_p(out.cell_out.data_ptr()),
+                                 C.c_void_p(out.perm_out.data_ptr()), n, M, w.cell_base, w.dt,
+                                 C.byref(prm), w.seed, s, C.c_void_p(out.moments.data_ptr()),
+                                 C.c_void_p(out.diag.data_ptr()), C.c_void_p(ws.data_ptr()), ws.numel(),
+                                 C.c_void_p(stream.cuda_stream))
+        _lib.check(rc, "coulomb_collide")
+        if world > 1:
+            import torch.distributed as dist
+            dist.all_gather_into_tensor(gathered, out.diag)
+            cc.cc_diag_sum_ranks(gathered)
+
+    # warm-up
+    for s in range(args.warmup):
+        one_step(10_000 + s)
+    torch.cuda.synchronize()
+    assert cc.cc_device_status(ws) == 0
+
+    K = args.steps
+    nst = _lib.CC_NUM_STAGES
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(nst + 1)] for _ in range(K)]
+    for row in ev:
+        for e in row:
+            e.record(stream)          # materialise the cudaEvent_t handles
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        start.record(stream)
+        for s in range(K):
+            one_step(s, ev[s])
+        stop.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms = start.elapsed_time(stop)
+    stage_ms = {name: statistics.mean(ev[s][i].elapsed_time(ev[s][i + 1]) for s in range(K))
+                for i, name in enumerate(_lib.STAGE_NAMES)}
+    pairs_local = float(out.diag[2].item())
+
+    # ---- end-to-end through the public API with host buffers (pinned)
+    v_pin = v_host.pin_memory()
+    c_pin = c_host.pin_memory()
+    vo_pin = torch.empty((3, n), dtype=torch.float64).pin_memory()
+    co_pin = torch.empty(n, dtype=torch.int32).pin_memory()
+    po_pin = torch.empty(n, dtype=torch.int32).pin_memory()
+    E = max(args.e2e_steps, 1)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for s in range(E):
+        v.copy_(v_pin, non_blocking=True)
+        cell.copy_(c_pin, non_blocking=True)
+        cc.coulomb_collide(v, cell, M, step=20_000 + s, out=out, workspace=ws, **p)
+        vo_pin.copy_(out.v_out, non_blocking=True)
+        co_pin.copy_(out.cell_out, non_blocking=True)
+        po_pin.copy_(out.perm_out, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / E
+
+    # ---- max over ranks
+    if world > 1:
+        t = torch.tensor([ms, e2e_ms, pairs_local], dtype=torch.float64, device=dev)
+        mx = t.clone()
+        dist.all_reduce(mx[:2], op=dist.ReduceOp.MAX)
+        tot = t[2:].clone()
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+        ms, e2e_ms, pairs_total = float(mx[0]), float(mx[1]), float(tot[0])
+    else:
+        pairs_total = pairs_local
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    ms_step = ms / K
+    value = pairs_total / (ms_step * 1e-3)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
+    dom = max(("count", "scatter", "collide"), key=lambda k: stage_ms[k])
+    achieved = STAGE_BYTES[dom] * n / (stage_ms[dom] * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(args, world), "cells_per_gpu": M, "electrons_per_gpu": n,
+                   "pairs_per_step": pairs_total, "input_order": "random permutation (cold, re-binned every step)",
+                   "l2": "inputs 2.87 GB/GPU >> 126 MB L2 (no flush needed)",
+                   "parallelism": f"cell-range shards x{world}" if world > 1 else "1 GPU"},
+        "roofline": {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": None,
+                     "algorithmic_bytes_per_particle": STAGE_BYTES[dom], "peak_source": peak_src},
+        "stages_ms": stage_ms,
+        "step_hbm": {"algorithmic_bytes_per_particle": STEP_BYTES_PER_PARTICLE,
+                     "achieved_gbs": STEP_BYTES_PER_PARTICLE * n * world / (ms_step * 1e-3) / 1e9 / world,
+                     "frac": STEP_BYTES_PER_PARTICLE * n / (ms_step * 1e-3) / 1e9 / hbm_peak},
+        "e2e": {"value": pairs_total / (e2e_ms * 1e-3), "unit": UNIT,
+                "h2d_bytes_per_step": int(v_host.numel() * 8 + c_host.numel() * 4),
+                "d2h_bytes_per_step": int(n * 24 + n * 8), "ms_per_step": e2e_ms},
+        "gpu_launches": 9 * K + (K if world > 1 else 0),
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = time_oracle_on(w, args)
+        except Exception as e:  # the baseline must never kill the GPU number
+            line["cpu_baseline"] = {"error": repr(e)}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

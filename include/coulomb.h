@@ -63,7 +63,14 @@ typedef struct cc_params {
     double ln_lambda;             /* Coulomb logarithm, used when ln_lambda_arr == NULL    */
     const double *ln_lambda_arr;  /* DEVICE [cells] or NULL                                */
     uint32_t flags;               /* reserved, must be 0                                   */
+    void *const *stage_events;    /* HOST array of CC_NUM_STAGES+1 cudaEvent_t, or NULL.
+                                     When set, coulomb_collide records event i on `stream`
+                                     before stage i and event CC_NUM_STAGES after the last
+                                     (stages: 0 count, 1 scan, 2 scatter, 3 collide,
+                                     4 finalize) — used by bench.py for per-kernel timing. */
 } cc_params;
+
+#define CC_NUM_STAGES 5
 
 void cc_default_params(cc_params *p);                         /* HOST */
 

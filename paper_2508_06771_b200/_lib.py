@@ -22,6 +22,8 @@ CC_ENCCL = -6
 CC_MAX_CELLS = 32768
 CC_DIAG_LEN = 16
 CC_MOMENTS_LEN = 7
+CC_NUM_STAGES = 5
+STAGE_NAMES = ("count", "scan", "scatter", "collide", "finalize")
 
 # every symbol include/coulomb.h declares
 EXPORTS = ("cc_default_params", "cc_workspace_bytes", "coulomb_collide", "cc_device_status",
@@ -33,7 +35,8 @@ class CCParams(C.Structure):
     _fields_ = [("mass", C.c_double), ("charge", C.c_double), ("eps0", C.c_double),
                 ("weight", C.c_double), ("cell_volume", C.c_double),
                 ("cell_volume_arr", C.c_void_p), ("ln_lambda", C.c_double),
-                ("ln_lambda_arr", C.c_void_p), ("flags", C.c_uint32)]
+                ("ln_lambda_arr", C.c_void_p), ("flags", C.c_uint32),
+                ("stage_events", C.POINTER(C.c_void_p))]
 
 
 class CCError(RuntimeError):

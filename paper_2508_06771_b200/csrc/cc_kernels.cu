@@ -33,6 +33,7 @@ constexpr int kSub = 4096;               // elements per warp sub-range in k_sca
 constexpr int kCollideThreads = 256;
 constexpr int kChunk = 1024;             // items (pairs or sitter) per k_collide_large CTA
 constexpr int kRec = 16;                 // doubles per moment record
+constexpr int kSmallRec = 20;            // small-cell record: kRec + the shift (the cell's exact mean)
 constexpr int kCellSum = 8;
 constexpr int kScatterSmemBudget = 96 * 1024;
 
@@ -69,7 +70,7 @@ Layout make_layout(int64_t n, int32_t M)
     L.o_chunk = o;    o = align256(o + static_cast<size_t>(M + 1) * sizeof(int32_t));
     L.o_C = o;        o = align256(o + static_cast<size_t>(M) * sizeof(double));
     L.o_keys = o;     o = align256(o + static_cast<size_t>(M) * sizeof(cc::U4));
-    L.o_small = o;    o = align256(o + static_cast<size_t>(M) * kRec * sizeof(double));
+    L.o_small = o;    o = align256(o + static_cast<size_t>(M) * kSmallRec * sizeof(double));
     L.o_recs = o;     o = align256(o + static_cast<size_t>(L.max_chunks) * kRec * sizeof(double));
     L.o_cellsum = o;  o = align256(o + static_cast<size_t>(M) * kCellSum * sizeof(double));
     L.o_wsv = o;      o = align256(o + static_cast<size_t>(n > 0 ? n : 1) * 4 * sizeof(double));
@@ -379,7 +380,8 @@ __device__ __forceinline__ void warp_reduce(Acc& acc)
         for (int d = 16; d > 0; d >>= 1) acc.a[q] += __shfl_down_sync(0xFFFFFFFFu, acc.a[q], d);
 }
 
-// N_j <= 64: one warp per cell.
+// N_j <= 64: one warp per cell.  The warp holds the whole cell, so its moment
+// record is an exact two-pass one: the shift is the cell's post-collision mean.
 __global__ void __launch_bounds__(256)
 k_collide_small(CollideArgs A)
 {
@@ -392,8 +394,6 @@ k_collide_small(CollideArgs A)
     const int32_t o = A.off[j];
     const uint32_t G = A.cell_base + static_cast<uint32_t>(j);
     cc::small_cell_perm(static_cast<uint32_t>(N), G, A.step, A.s0, A.s1, lane, pi_sm[w]);
-    double rx, ry, rz, rw;
-    ld256(A.wsv + 4 * static_cast<int64_t>(o), rx, ry, rz, rw);
     const double C = A.Cj[j];
     Acc acc;
     acc.zero();
@@ -402,14 +402,33 @@ k_collide_small(CollideArgs A)
     if (k < items) {
         const uint32_t sa = static_cast<uint32_t>(pi_sm[w][2 * k]);
         const uint32_t sb = (2 * k + 1 < static_cast<uint32_t>(N)) ? static_cast<uint32_t>(pi_sm[w][2 * k + 1]) : 0u;
-        process_item(A, j, o, N, k, sa, sb, C, rx, ry, rz, acc);
+        process_item(A, j, o, N, k, sa, sb, C, 0.0, 0.0, 0.0, acc);
     }
     warp_reduce(acc);
-    if (lane == 0) {
-        double* r = A.small_recs + static_cast<int64_t>(j) * kRec;
+    // pass 2: sums of squares about the exact mean (values re-read from v_out, L1/L2 hot)
+    const double inv = 1.0 / static_cast<double>(N);
+    const double mx = __shfl_sync(0xFFFFFFFFu, acc.a[10], 0) * inv;
+    const double my = __shfl_sync(0xFFFFFFFFu, acc.a[11], 0) * inv;
+    const double mz = __shfl_sync(0xFFFFFFFFu, acc.a[12], 0) * inv;
+    __syncwarp();
+    double q[6] = {0, 0, 0, 0, 0, 0};
+    for (int32_t t = lane; t < N; t += 32) {
+        const double dx = A.v_out[o + t] - mx, dy = A.v_out[A.ldv + o + t] - my, dz = A.v_out[2 * A.ldv + o + t] - mz;
+        q[0] += dx; q[1] += dy; q[2] += dz;
+        q[3] += dx * dx; q[4] += dy * dy; q[5] += dz * dz;
+    }
 #pragma unroll
-        for (int q = 0; q < 15; ++q) r[q] = acc.a[q];
+    for (int c = 0; c < 6; ++c)
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) q[c] += __shfl_down_sync(0xFFFFFFFFu, q[c], d);
+    if (lane == 0) {
+        double* r = A.small_recs + static_cast<int64_t>(j) * kSmallRec;
+#pragma unroll
+        for (int c = 0; c < 6; ++c) r[c] = q[c];
+#pragma unroll
+        for (int c = 6; c < 15; ++c) r[c] = acc.a[c];
         r[15] = 0.0;
+        r[16] = mx; r[17] = my; r[18] = mz; r[19] = 0.0;
     }
 }
 
@@ -517,12 +536,14 @@ __global__ void k_finalize_cells(const int32_t* __restrict__ cnt, const int32_t*
     for (int q = 0; q < 15; ++q) s[q] = 0.0;
     double rx = 0, ry = 0, rz = 0;
     if (N > 0) {
-        double rw;
-        ld256(wsv + 4 * static_cast<int64_t>(off[j]), rx, ry, rz, rw);
         if (N <= cc::kSmallCell) {
+            const double* r = small_recs + static_cast<int64_t>(j) * kSmallRec;
 #pragma unroll
-            for (int q = 0; q < 15; ++q) s[q] = small_recs[static_cast<int64_t>(j) * kRec + q];
+            for (int q = 0; q < 15; ++q) s[q] = r[q];
+            rx = r[16]; ry = r[17]; rz = r[18];
         } else {
+            double rw;
+            ld256(wsv + 4 * static_cast<int64_t>(off[j]), rx, ry, rz, rw);
             for (int32_t c = chunk_off[j]; c < chunk_off[j + 1]; ++c)
 #pragma unroll
                 for (int q = 0; q < 15; ++q) s[q] += recs[static_cast<int64_t>(c) * kRec + q];
@@ -740,9 +761,14 @@ int prepare_max_smem(int bytes)
 }
 
 // CCS1-CCS3 into the workspace (shared by coulomb_collide and cc_bin).
+void mark(void* const* ev, int i, cudaStream_t st)
+{
+    if (ev && ev[i]) cudaEventRecord(static_cast<cudaEvent_t>(ev[i]), st);
+}
+
 int run_binning(const double* v_in, int64_t ldv, const int32_t* cell_in, int n, int M, const Layout& L,
                 void* ws, const CellConst& k, uint32_t cell_base, uint32_t step, uint64_t seed,
-                cudaStream_t st)
+                cudaStream_t st, void* const* ev = nullptr)
 {
     int rc = prepare_max_smem(0);
     if (rc) return rc;
@@ -755,11 +781,14 @@ int run_binning(const double* v_in, int64_t ldv, const int32_t* cell_in, int n, 
     cc::U4* keys = at<cc::U4>(ws, L.o_keys);
     double* wsv = at<double>(ws, L.o_wsv);
     const int M1 = M + 1;
+    mark(ev, 0, st);
     k_count<<<L.T, kCountThreads, sizeof(int32_t) * M1, st>>>(cell_in, n, M, L.tile, tcount, err);
+    mark(ev, 1, st);
     k_scan_tiles<<<(M1 + 31) / 32, dim3(32, 8), 0, st>>>(tcount, L.T, M1, cnt);
     k_scan_cells<<<1, 1024, 0, st>>>(cnt, M, off, chunk_off, Cj, keys, k, cell_base, step,
                                      static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
     const size_t smem = sizeof(int32_t) * M1 + sizeof(uint16_t) * static_cast<size_t>(L.W) * M1;
+    mark(ev, 2, st);
     k_scatter<<<L.T, 32 * L.W, smem, st>>>(v_in, ldv, cell_in, n, M, L.W, tcount, off, wsv);
     return launch_ok();
 }
@@ -854,7 +883,9 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
 
     const CellConst k = cell_const(p, dt);
     const int nn = static_cast<int>(n);
-    int rc = run_binning(v_in, ldv, cell_in, nn, M, L, workspace, k, cell_base, static_cast<uint32_t>(step), seed, st);
+    void* const* ev = p.stage_events;
+    int rc = run_binning(v_in, ldv, cell_in, nn, M, L, workspace, k, cell_base, static_cast<uint32_t>(step), seed,
+                         st, ev);
     if (rc) return rc;
 
     CollideArgs A;
@@ -876,15 +907,18 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     A.s0 = static_cast<uint32_t>(seed);
     A.s1 = static_cast<uint32_t>(seed >> 32);
 
+    mark(ev, 3, st);
     k_collide_small<<<(M + 7) / 8, 256, 0, st>>>(A);
     k_collide_large<<<static_cast<unsigned>(L.max_chunks), kCollideThreads, 0, st>>>(A);
     k_copy_dead<<<148 * 4, 256, 0, st>>>(A.wsv, A.off, M, nn, v_out, ldv, cell_out, perm_out);
 
     MomConst mc{p.weight, p.cell_volume, p.cell_volume_arr, p.mass / p.charge};
     double* cellsum = at<double>(workspace, L.o_cellsum);
+    mark(ev, 4, st);
     k_finalize_cells<<<(M + 255) / 256, 256, 0, st>>>(A.cnt, A.off, A.chunk_off, A.recs, A.small_recs, A.wsv, M,
                                                       mc, moments_out, cellsum);
     if (diag_out) k_finalize_diag<<<1, 1024, 0, st>>>(A.cnt, cellsum, M, diag_out);
+    mark(ev, 5, st);
     return launch_ok();
 }
 
