@@ -29,12 +29,15 @@
 namespace {
 
 constexpr int kCountThreads = 256;
-constexpr int kSub = 4096;               // elements per warp sub-range in k_scatter (<= 65535)
+constexpr int kSub = 8192;               // elements per warp sub-range in k_scatter (<= 65535)
+constexpr int kScatterUnrollA = 16;      // cell loads in flight per lane, counting pass
+constexpr int kScatterUnrollB = 8;       // (cell, v) loads in flight per lane, scatter pass
 constexpr int kCollideThreads = 256;
 constexpr int kChunk = 1024;             // items (pairs or sitter) per k_collide_large CTA
-constexpr int kRec = 16;                 // doubles per moment record
-constexpr int kSmallRec = 20;            // small-cell record: kRec + the shift (the cell's exact mean)
-constexpr int kCellSum = 8;
+constexpr int kRec = 8;                  // doubles per chunk moment record: S1' (3), S2' (3), pad
+constexpr int kSmallRec = 12;            // small-cell record: S1', S2', shift (3), pad
+constexpr int kCellSum = 4;              // per-cell post-collision raw sums: v (3), |v|^2
+constexpr int kTileSum = 4;              // per-tile pre-collision raw sums: v (3), |v|^2
 constexpr int kScatterSmemBudget = 96 * 1024;
 
 // ------------------------------------------------------------------ layout
@@ -42,7 +45,7 @@ struct Layout {
     int W = 1, tile = kSub, T = 0;
     int64_t max_chunks = 0;
     size_t o_err = 0, o_tcount = 0, o_cnt = 0, o_off = 0, o_chunk = 0, o_C = 0, o_keys = 0;
-    size_t o_small = 0, o_recs = 0, o_cellsum = 0, o_wsv = 0, total = 0;
+    size_t o_small = 0, o_recs = 0, o_cellsum = 0, o_tilesum = 0, o_wsv = 0, total = 0;
 };
 
 size_t align256(size_t x) { return (x + 255u) & ~static_cast<size_t>(255u); }
@@ -73,6 +76,7 @@ Layout make_layout(int64_t n, int32_t M)
     L.o_small = o;    o = align256(o + static_cast<size_t>(M) * kSmallRec * sizeof(double));
     L.o_recs = o;     o = align256(o + static_cast<size_t>(L.max_chunks) * kRec * sizeof(double));
     L.o_cellsum = o;  o = align256(o + static_cast<size_t>(M) * kCellSum * sizeof(double));
+    L.o_tilesum = o;  o = align256(o + static_cast<size_t>(L.T > 0 ? L.T : 1) * kTileSum * sizeof(double));
     L.o_wsv = o;      o = align256(o + static_cast<size_t>(n > 0 ? n : 1) * 4 * sizeof(double));
     L.total = o;
     return L;
@@ -128,30 +132,51 @@ k_count(const int32_t* __restrict__ cell, int n, int M, int tile, int32_t* __res
 }
 
 // ------------------------------------------------------------------ CCS2 part 1
-// grid: ceil((M+1)/32) CTAs of 32x8 threads; lane = bin, warp row = tile range.
-__global__ void __launch_bounds__(256)
+// grid: ceil((M+1)/32) CTAs of 32x16 threads; lane = bin, warp row = tile range.
+// Loads are issued 8 at a time (independent addresses) to keep DRAM busy.
+constexpr int kScanRows = 16;
+__global__ void __launch_bounds__(32 * kScanRows)
 k_scan_tiles(int32_t* __restrict__ tcount, int T, int M1, int32_t* __restrict__ cnt)
 {
-    __shared__ int32_t part[8][33];
+    __shared__ int32_t part[kScanRows][33];
     const int lane = threadIdx.x, wy = threadIdx.y;
     const int c = blockIdx.x * 32 + lane;
-    const int per = (T + 7) / 8;
-    const int t0 = wy * per, t1 = min(t0 + per, T);
+    const int per = (T + kScanRows - 1) / kScanRows;
+    const int t0 = min(wy * per, T), t1 = min(t0 + per, T);
+    const bool ok = c < M1;
     int32_t s = 0;
-    if (c < M1)
-        for (int t = t0; t < t1; ++t) s += tcount[static_cast<int64_t>(t) * M1 + c];
+    int t = t0;
+    for (; t + 8 <= t1; t += 8) {
+        int32_t x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = ok ? tcount[static_cast<int64_t>(t + u) * M1 + c] : 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += x[u];
+    }
+    for (; t < t1; ++t) s += ok ? tcount[static_cast<int64_t>(t) * M1 + c] : 0;
     part[wy][lane] = s;
     __syncthreads();
     int32_t pre = 0, tot = 0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) {
+    for (int w = 0; w < kScanRows; ++w) {
         const int32_t x = part[w][lane];
         pre += (w < wy) ? x : 0;
         tot += x;
     }
-    if (c < M1) {
+    if (ok) {
         int32_t run = pre;
-        for (int t = t0; t < t1; ++t) {
+        t = t0;
+        for (; t + 8 <= t1; t += 8) {
+            int32_t x[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) x[u] = tcount[static_cast<int64_t>(t + u) * M1 + c];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                tcount[static_cast<int64_t>(t + u) * M1 + c] = run;
+                run += x[u];
+            }
+        }
+        for (; t < t1; ++t) {
             int32_t* p = tcount + static_cast<int64_t>(t) * M1 + c;
             const int32_t x = *p;
             *p = run;
@@ -234,13 +259,16 @@ k_scan_cells(const int32_t* __restrict__ cnt, int M, int32_t* __restrict__ off,
 // ------------------------------------------------------------------ CCS3: stable scatter
 // Tile = W warps x kSub elements; warp w owns the contiguous sub-range w of the
 // tile, so "input order" = (tile, warp, step, lane).  Per-warp 16-bit counters
-// give each element its rank among equal-cell predecessors.
+// give each element its rank among equal-cell predecessors.  Loads are issued
+// in batches (kScatterUnrollA / B per lane) so each warp keeps several KB in
+// flight.  The pass also produces the tile's pre-collision sums (diagnostics).
 __global__ void __launch_bounds__(256)
 k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__ cell, int n, int M,
           int W, const int32_t* __restrict__ tbase, const int32_t* __restrict__ off,
-          double* __restrict__ wsv)
+          double* __restrict__ wsv, double* __restrict__ tilesum)
 {
     extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ double red[8][kTileSum];
     const int M1 = M + 1;
     int32_t* base = reinterpret_cast<int32_t*>(smem);                       // [M1]
     uint16_t* wcnt = reinterpret_cast<uint16_t*>(smem + sizeof(int32_t) * M1);  // [W][M1]
@@ -253,15 +281,22 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
     uint16_t* my = wcnt + w * M1;
     const uint32_t lt = (1u << lane) - 1u;
 
-    if (w < W) {
-        for (int64_t i0 = s0; i0 < s1; i0 += 32) {
-            const int64_t i = i0 + lane;
+    // pass A: per-warp counts of the sub-range
+    for (int64_t i0 = s0; i0 < s1; i0 += 32 * kScatterUnrollA) {
+        int32_t key[kScatterUnrollA];
+#pragma unroll
+        for (int u = 0; u < kScatterUnrollA; ++u) {
+            const int64_t i = i0 + 32 * u + lane;
             const bool valid = i < s1;
             const int32_t c = valid ? __ldg(cell + i) : 0;
-            const int32_t b = (c >= 0 && c < M) ? c : M;
-            const int32_t key = valid ? b : -1 - lane;
-            const uint32_t peers = __match_any_sync(0xFFFFFFFFu, key);
-            if (valid && lane == __ffs(peers) - 1) my[b] = static_cast<uint16_t>(my[b] + __popc(peers));
+            key[u] = !valid ? -1 - lane : ((c >= 0 && c < M) ? c : M);
+        }
+#pragma unroll
+        for (int u = 0; u < kScatterUnrollA; ++u) {
+            const uint32_t peers = __match_any_sync(0xFFFFFFFFu, key[u]);
+            if (key[u] >= 0 && lane == __ffs(peers) - 1)
+                my[key[u]] = static_cast<uint16_t>(my[key[u]] + __popc(peers));
+            __syncwarp();
         }
     }
     __syncthreads();
@@ -276,25 +311,54 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
         base[c] = off[c] + trow[c];           // off[M] = L: dead slots follow the live ones
     }
     __syncthreads();
-    if (w < W) {
-        for (int64_t i0 = s0; i0 < s1; i0 += 32) {
-            const int64_t i = i0 + lane;
+
+    // pass B: ranks, destinations, 32-byte records
+    double sx = 0.0, sy = 0.0, sz = 0.0, se = 0.0;
+    for (int64_t i0 = s0; i0 < s1; i0 += 32 * kScatterUnrollB) {
+        int32_t key[kScatterUnrollB];
+        double x[kScatterUnrollB], y[kScatterUnrollB], z[kScatterUnrollB];
+#pragma unroll
+        for (int u = 0; u < kScatterUnrollB; ++u) {
+            const int64_t i = i0 + 32 * u + lane;
             const bool valid = i < s1;
             const int32_t c = valid ? __ldg(cell + i) : 0;
-            const int32_t b = (c >= 0 && c < M) ? c : M;
-            const int32_t key = valid ? b : -1 - lane;
-            const uint32_t peers = __match_any_sync(0xFFFFFFFFu, key);
+            key[u] = !valid ? -1 - lane : ((c >= 0 && c < M) ? c : M);
+            x[u] = y[u] = z[u] = 0.0;
+            if (valid && v) { x[u] = __ldg(v + i); y[u] = __ldg(v + ldv + i); z[u] = __ldg(v + 2 * ldv + i); }
+        }
+#pragma unroll
+        for (int u = 0; u < kScatterUnrollB; ++u) {
+            const int32_t b = key[u];
+            const uint32_t peers = __match_any_sync(0xFFFFFFFFu, b);
             int32_t dest = 0;
-            if (valid) dest = base[b] + my[b] + __popc(peers & lt);
+            if (b >= 0) dest = base[b] + my[b] + __popc(peers & lt);
             __syncwarp();
-            if (valid && lane == __ffs(peers) - 1) my[b] = static_cast<uint16_t>(my[b] + __popc(peers));
-            if (valid) {
-                double vx = 0.0, vy = 0.0, vz = 0.0;
-                if (v) { vx = __ldg(v + i); vy = __ldg(v + ldv + i); vz = __ldg(v + 2 * ldv + i); }
-                st256(wsv + 4 * static_cast<int64_t>(dest), vx, vy, vz,
+            if (b >= 0 && lane == __ffs(peers) - 1) my[b] = static_cast<uint16_t>(my[b] + __popc(peers));
+            __syncwarp();
+            if (b >= 0) {
+                const int64_t i = i0 + 32 * u + lane;
+                st256(wsv + 4 * static_cast<int64_t>(dest), x[u], y[u], z[u],
                       pack_pc(static_cast<int32_t>(i), b < M ? b : -1));
+                if (b < M) {
+                    sx += x[u]; sy += y[u]; sz += z[u];
+                    se += x[u] * x[u] + y[u] * y[u] + z[u] * z[u];
+                }
             }
         }
+    }
+    double t4[kTileSum] = {sx, sy, sz, se};
+#pragma unroll
+    for (int q = 0; q < kTileSum; ++q)
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) t4[q] += __shfl_down_sync(0xFFFFFFFFu, t4[q], d);
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < kTileSum; ++q) red[w][q] = t4[q];
+    __syncthreads();
+    if (threadIdx.x < kTileSum) {
+        double a = 0.0;
+        for (int ww = 0; ww < W; ++ww) a += red[ww][threadIdx.x];
+        tilesum[static_cast<int64_t>(blockIdx.x) * kTileSum + threadIdx.x] = a;
     }
 }
 
@@ -316,68 +380,68 @@ struct CollideArgs {
     uint32_t cell_base, step, s0, s1;
 };
 
-// Moment accumulator: [0..2] sum (v - ref) post, [3..5] sum (v - ref)^2 post,
-// [6..8] sum v pre, [9] sum |v|^2 pre, [10..12] sum v post, [13] sum |v|^2 post,
-// [14] count.
+// Post-collision moment accumulator about a per-cell shift r:
+// [0..2] sum (v - r), [3..5] sum (v - r)^2.
 struct Acc {
-    double a[15];
+    double a[6];
     __device__ void zero()
     {
 #pragma unroll
-        for (int q = 0; q < 15; ++q) a[q] = 0.0;
+        for (int q = 0; q < 6; ++q) a[q] = 0.0;
     }
-    __device__ void add(double px, double py, double pz, double x, double y, double z,
-                        double rx, double ry, double rz)
+    __device__ void add(double x, double y, double z, double rx, double ry, double rz)
     {
         const double dx = x - rx, dy = y - ry, dz = z - rz;
         a[0] += dx; a[1] += dy; a[2] += dz;
-        a[3] += dx * dx; a[4] += dy * dy; a[5] += dz * dz;
-        a[6] += px; a[7] += py; a[8] += pz;
-        a[9] += px * px + py * py + pz * pz;
-        a[10] += x; a[11] += y; a[12] += z;
-        a[13] += x * x + y * y + z * z;
-        a[14] += 1.0;
+        a[3] = fma(dx, dx, a[3]); a[4] = fma(dy, dy, a[4]); a[5] = fma(dz, dz, a[5]);
     }
 };
 
-// One item k of cell (o, N): a pair (2k+1 < N) or the odd sitter (2k = N-1).
-__device__ __forceinline__ void process_item(const CollideArgs& A, int32_t j, int32_t o, int32_t N,
-                                             uint32_t k, uint32_t sa, uint32_t sb, double C,
-                                             double rx, double ry, double rz, Acc& acc)
+struct Rec {
+    double x, y, z, w;     // w = (perm, cell) bit pattern
+};
+
+__device__ __forceinline__ Rec ld_rec(const double* p)
+{
+    Rec r;
+    ld256(p, r.x, r.y, r.z, r.w);
+    return r;
+}
+
+// One item k of cell (j, o, N): a pair (2k+1 < N) with records a, b, or the
+// odd sitter (2k = N-1) with record a.  CCS4: one Philox call per pair,
+// ctr = (k, G, step, 0).  CCS5: TA77.  Output in pair order, SoA.
+__device__ __forceinline__ void collide_item(const CollideArgs& A, int32_t j, int32_t o, int32_t N, uint32_t k,
+                                             Rec a, Rec b, double C, double rx, double ry, double rz, Acc& acc)
 {
     const int32_t pa = o + 2 * static_cast<int32_t>(k);
-    double ax, ay, az, aw;
-    ld256(A.wsv + 4 * static_cast<int64_t>(o + static_cast<int32_t>(sa)), ax, ay, az, aw);
+    double* vo = A.v_out;
     if (2 * k + 1 < static_cast<uint32_t>(N)) {
-        double bx, by, bz, bw;
-        ld256(A.wsv + 4 * static_cast<int64_t>(o + static_cast<int32_t>(sb)), bx, by, bz, bw);
-        const double pax = ax, pay = ay, paz = az, pbx = bx, pby = by, pbz = bz;
         const cc::U4 r = cc::philox4x32_10(
             cc::U4{k, A.cell_base + static_cast<uint32_t>(j), A.step, 0u}, A.s0, A.s1);
-        cc::ta_update(ax, ay, az, bx, by, bz, C, cc::u01(r.x, r.y), cc::u01(r.z, r.w));
-        double* vo = A.v_out;
-        vo[pa] = ax; vo[pa + 1] = bx;
-        vo[A.ldv + pa] = ay; vo[A.ldv + pa + 1] = by;
-        vo[2 * A.ldv + pa] = az; vo[2 * A.ldv + pa + 1] = bz;
+        cc::ta_update(a.x, a.y, a.z, b.x, b.y, b.z, C, cc::u01(r.x, r.y), cc::u01(r.z, r.w));
+        vo[pa] = a.x; vo[pa + 1] = b.x;
+        vo[A.ldv + pa] = a.y; vo[A.ldv + pa + 1] = b.y;
+        vo[2 * A.ldv + pa] = a.z; vo[2 * A.ldv + pa + 1] = b.z;
         A.cell_out[pa] = j; A.cell_out[pa + 1] = j;
-        if (A.perm_out) { A.perm_out[pa] = unpack_perm(aw); A.perm_out[pa + 1] = unpack_perm(bw); }
-        acc.add(pax, pay, paz, ax, ay, az, rx, ry, rz);
-        acc.add(pbx, pby, pbz, bx, by, bz, rx, ry, rz);
+        if (A.perm_out) { A.perm_out[pa] = unpack_perm(a.w); A.perm_out[pa + 1] = unpack_perm(b.w); }
+        acc.add(a.x, a.y, a.z, rx, ry, rz);
+        acc.add(b.x, b.y, b.z, rx, ry, rz);
     } else {
-        double* vo = A.v_out;
-        vo[pa] = ax; vo[A.ldv + pa] = ay; vo[2 * A.ldv + pa] = az;
+        vo[pa] = a.x; vo[A.ldv + pa] = a.y; vo[2 * A.ldv + pa] = a.z;
         A.cell_out[pa] = j;
-        if (A.perm_out) A.perm_out[pa] = unpack_perm(aw);
-        acc.add(ax, ay, az, ax, ay, az, rx, ry, rz);
+        if (A.perm_out) A.perm_out[pa] = unpack_perm(a.w);
+        acc.add(a.x, a.y, a.z, rx, ry, rz);
     }
 }
 
-__device__ __forceinline__ void warp_reduce(Acc& acc)
+template <int NV>
+__device__ __forceinline__ void warp_reduce(double (&a)[NV])
 {
 #pragma unroll
-    for (int q = 0; q < 15; ++q)
+    for (int q = 0; q < NV; ++q)
 #pragma unroll
-        for (int d = 16; d > 0; d >>= 1) acc.a[q] += __shfl_down_sync(0xFFFFFFFFu, acc.a[q], d);
+        for (int d = 16; d > 0; d >>= 1) a[q] += __shfl_down_sync(0xFFFFFFFFu, a[q], d);
 }
 
 // N_j <= 64: one warp per cell.  The warp holds the whole cell, so its moment
@@ -400,47 +464,60 @@ k_collide_small(CollideArgs A)
     const uint32_t items = static_cast<uint32_t>(N + 1) / 2;
     const uint32_t k = static_cast<uint32_t>(lane);
     if (k < items) {
-        const uint32_t sa = static_cast<uint32_t>(pi_sm[w][2 * k]);
-        const uint32_t sb = (2 * k + 1 < static_cast<uint32_t>(N)) ? static_cast<uint32_t>(pi_sm[w][2 * k + 1]) : 0u;
-        process_item(A, j, o, N, k, sa, sb, C, 0.0, 0.0, 0.0, acc);
+        const Rec ra = ld_rec(A.wsv + 4 * static_cast<int64_t>(o + pi_sm[w][2 * k]));
+        Rec rb = ra;
+        if (2 * k + 1 < static_cast<uint32_t>(N)) rb = ld_rec(A.wsv + 4 * static_cast<int64_t>(o + pi_sm[w][2 * k + 1]));
+        collide_item(A, j, o, N, k, ra, rb, C, 0.0, 0.0, 0.0, acc);
     }
-    warp_reduce(acc);
-    // pass 2: sums of squares about the exact mean (values re-read from v_out, L1/L2 hot)
+    warp_reduce(acc.a);
+    // pass 2: sums about the exact mean (values re-read from v_out, L1/L2 hot)
     const double inv = 1.0 / static_cast<double>(N);
-    const double mx = __shfl_sync(0xFFFFFFFFu, acc.a[10], 0) * inv;
-    const double my = __shfl_sync(0xFFFFFFFFu, acc.a[11], 0) * inv;
-    const double mz = __shfl_sync(0xFFFFFFFFu, acc.a[12], 0) * inv;
+    const double mx = __shfl_sync(0xFFFFFFFFu, acc.a[0], 0) * inv;
+    const double my = __shfl_sync(0xFFFFFFFFu, acc.a[1], 0) * inv;
+    const double mz = __shfl_sync(0xFFFFFFFFu, acc.a[2], 0) * inv;
     __syncwarp();
-    double q[6] = {0, 0, 0, 0, 0, 0};
-    for (int32_t t = lane; t < N; t += 32) {
-        const double dx = A.v_out[o + t] - mx, dy = A.v_out[A.ldv + o + t] - my, dz = A.v_out[2 * A.ldv + o + t] - mz;
-        q[0] += dx; q[1] += dy; q[2] += dz;
-        q[3] += dx * dx; q[4] += dy * dy; q[5] += dz * dz;
-    }
-#pragma unroll
-    for (int c = 0; c < 6; ++c)
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) q[c] += __shfl_down_sync(0xFFFFFFFFu, q[c], d);
+    Acc q;
+    q.zero();
+    for (int32_t t = lane; t < N; t += 32)
+        q.add(A.v_out[o + t], A.v_out[A.ldv + o + t], A.v_out[2 * A.ldv + o + t], mx, my, mz);
+    warp_reduce(q.a);
     if (lane == 0) {
         double* r = A.small_recs + static_cast<int64_t>(j) * kSmallRec;
 #pragma unroll
-        for (int c = 0; c < 6; ++c) r[c] = q[c];
-#pragma unroll
-        for (int c = 6; c < 15; ++c) r[c] = acc.a[c];
-        r[15] = 0.0;
-        r[16] = mx; r[17] = my; r[18] = mz; r[19] = 0.0;
+        for (int c = 0; c < 6; ++c) r[c] = q.a[c];
+        r[6] = mx; r[7] = my; r[8] = mz;
+        r[9] = r[10] = r[11] = 0.0;
     }
 }
 
-// N_j > 64: one CTA per cell-aligned chunk of kChunk items.
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
+{
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem_src) : "memory");
+}
+
+__device__ __forceinline__ void cp_async_wait_all()
+{
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+}
+
+// N_j > 64: one CTA per cell-aligned chunk of kChunk items, two phases:
+//  1. every thread computes pi_j(2k), pi_j(2k+1) (keyed Feistel, R1) for its
+//     items and issues cp.async gathers of both 32-byte records into shared
+//     memory — the whole chunk's 64 KB of gathers are in flight at once;
+//  2. every thread runs CCS4 + CCS5 on its items out of shared memory and
+//     writes the pair-ordered output (coalesced), accumulating moments.
+constexpr int kItemsPerThread = kChunk / kCollideThreads;
+constexpr size_t kCollideSmem = 2ull * kChunk * 4 * sizeof(double);
+
 __global__ void __launch_bounds__(kCollideThreads)
 k_collide_large(CollideArgs A)
 {
+    extern __shared__ __align__(16) double stage[];       // [2][kChunk][4]
     __shared__ int32_t s_j;
-    __shared__ double red[kCollideThreads / 32][15];
+    __shared__ double red[kCollideThreads / 32][6];
     const int c = blockIdx.x;
     if (threadIdx.x == 0) {
-        // last j with chunk_off[j] <= c (chunk_off is non-decreasing, chunk_off[M] = total)
         int lo = 0, hi = A.M;   // invariant: chunk_off[lo] <= c < chunk_off[hi] when c < total
         if (c >= A.chunk_off[A.M]) {
             s_j = -1;
@@ -459,27 +536,56 @@ k_collide_large(CollideArgs A)
     const uint32_t items = static_cast<uint32_t>(N + 1) / 2;
     const uint32_t i0 = static_cast<uint32_t>(c - A.chunk_off[j]) * kChunk;
     const uint32_t i1 = min(i0 + static_cast<uint32_t>(kChunk), items);
-    const cc::Feistel f = cc::make_feistel(static_cast<uint32_t>(N), A.keys[j]);
-    const double C = A.Cj[j];
+    const double* cellv = A.wsv + 4 * static_cast<int64_t>(o);
+    {
+        const cc::Feistel f = cc::make_feistel(static_cast<uint32_t>(N), A.keys[j]);
+#pragma unroll
+        for (int q = 0; q < kItemsPerThread; ++q) {
+            const uint32_t k = i0 + threadIdx.x + q * kCollideThreads;
+            if (k < i1) {
+                const uint32_t e = k - i0;
+                const double* ga = cellv + 4 * static_cast<int64_t>(cc::feistel_pi(f, 2 * k));
+                cp_async16(stage + 4 * e, ga);
+                cp_async16(stage + 4 * e + 2, ga + 2);
+                if (2 * k + 1 < static_cast<uint32_t>(N)) {
+                    const double* gb = cellv + 4 * static_cast<int64_t>(cc::feistel_pi(f, 2 * k + 1));
+                    cp_async16(stage + 4 * (kChunk + e), gb);
+                    cp_async16(stage + 4 * (kChunk + e) + 2, gb + 2);
+                }
+            }
+        }
+    }
     double rx, ry, rz, rw;
-    ld256(A.wsv + 4 * static_cast<int64_t>(o), rx, ry, rz, rw);
+    ld256(cellv, rx, ry, rz, rw);          // shift: pre-collision v of the cell's first stable slot
+    const double C = A.Cj[j];
+    cp_async_wait_all();
+    __syncthreads();
     Acc acc;
     acc.zero();
-    for (uint32_t k = i0 + threadIdx.x; k < i1; k += kCollideThreads) {
-        const uint32_t sa = cc::feistel_pi(f, 2 * k);
-        const uint32_t sb = (2 * k + 1 < static_cast<uint32_t>(N)) ? cc::feistel_pi(f, 2 * k + 1) : 0u;
-        process_item(A, j, o, N, k, sa, sb, C, rx, ry, rz, acc);
+#pragma unroll 1
+    for (int q = 0; q < kItemsPerThread; ++q) {
+        const uint32_t k = i0 + threadIdx.x + q * kCollideThreads;
+        if (k < i1) {
+            const uint32_t e = k - i0;
+            const double2 a01 = *reinterpret_cast<const double2*>(stage + 4 * e);
+            const double2 a23 = *reinterpret_cast<const double2*>(stage + 4 * e + 2);
+            const double2 b01 = *reinterpret_cast<const double2*>(stage + 4 * (kChunk + e));
+            const double2 b23 = *reinterpret_cast<const double2*>(stage + 4 * (kChunk + e) + 2);
+            collide_item(A, j, o, N, k, Rec{a01.x, a01.y, a23.x, a23.y}, Rec{b01.x, b01.y, b23.x, b23.y}, C,
+                         rx, ry, rz, acc);
+        }
     }
-    warp_reduce(acc);
+    warp_reduce(acc.a);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if (lane == 0)
 #pragma unroll
-        for (int q = 0; q < 15; ++q) red[w][q] = acc.a[q];
+        for (int q = 0; q < 6; ++q) red[w][q] = acc.a[q];
     __syncthreads();
-    if (threadIdx.x < 15) {
+    if (threadIdx.x < kRec) {
         double s = 0.0;
+        if (threadIdx.x < 6)
 #pragma unroll
-        for (int ww = 0; ww < kCollideThreads / 32; ++ww) s += red[ww][threadIdx.x];
+            for (int ww = 0; ww < kCollideThreads / 32; ++ww) s += red[ww][threadIdx.x];
         A.recs[static_cast<int64_t>(c) * kRec + threadIdx.x] = s;
     }
 }
@@ -531,22 +637,20 @@ __global__ void k_finalize_cells(const int32_t* __restrict__ cnt, const int32_t*
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= M) return;
     const int32_t N = cnt[j];
-    double s[15];
-#pragma unroll
-    for (int q = 0; q < 15; ++q) s[q] = 0.0;
+    double s[6] = {0, 0, 0, 0, 0, 0};
     double rx = 0, ry = 0, rz = 0;
     if (N > 0) {
         if (N <= cc::kSmallCell) {
             const double* r = small_recs + static_cast<int64_t>(j) * kSmallRec;
 #pragma unroll
-            for (int q = 0; q < 15; ++q) s[q] = r[q];
-            rx = r[16]; ry = r[17]; rz = r[18];
+            for (int q = 0; q < 6; ++q) s[q] = r[q];
+            rx = r[6]; ry = r[7]; rz = r[8];
         } else {
             double rw;
             ld256(wsv + 4 * static_cast<int64_t>(off[j]), rx, ry, rz, rw);
             for (int32_t c = chunk_off[j]; c < chunk_off[j + 1]; ++c)
 #pragma unroll
-                for (int q = 0; q < 15; ++q) s[q] += recs[static_cast<int64_t>(c) * kRec + q];
+                for (int q = 0; q < 6; ++q) s[q] += recs[static_cast<int64_t>(c) * kRec + q];
         }
     }
     if (moments_out) {
@@ -559,15 +663,23 @@ __global__ void k_finalize_cells(const int32_t* __restrict__ cnt, const int32_t*
             for (int q = 0; q < CC_MOMENTS_LEN; ++q) o[q] = 0.0;
         }
     }
+    // raw post-collision sums: sum v = N r + S1', sum v^2 = S2' + 2 r S1' + N r^2
+    const double Nd = static_cast<double>(N);
+    const double r[3] = {rx, ry, rz};
     double* cs = cellsum + static_cast<int64_t>(j) * kCellSum;
+    double e = 0.0;
 #pragma unroll
-    for (int q = 0; q < kCellSum; ++q) cs[q] = s[6 + q];
+    for (int q = 0; q < 3; ++q) {
+        cs[q] = fma(Nd, r[q], s[q]);
+        e += s[3 + q] + 2.0 * r[q] * s[q] + Nd * r[q] * r[q];
+    }
+    cs[3] = e;
 }
 
-// single CTA of 1024 threads: fixed-order reduction over cells
+// single CTA of 1024 threads: fixed-order reductions over cells and tiles
 __global__ void __launch_bounds__(1024)
 k_finalize_diag(const int32_t* __restrict__ cnt, const double* __restrict__ cellsum, int M,
-                double* __restrict__ diag)
+                const double* __restrict__ tilesum, int T, double* __restrict__ diag)
 {
     __shared__ double red[32][12];
     double s[12];
@@ -579,8 +691,11 @@ k_finalize_diag(const int32_t* __restrict__ cnt, const double* __restrict__ cell
         s[1] += N / 2;
         s[2] += N & 1;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) s[3 + q] += cellsum[static_cast<int64_t>(j) * kCellSum + q];
+        for (int q = 0; q < 4; ++q) s[7 + q] += cellsum[static_cast<int64_t>(j) * kCellSum + q];
     }
+    for (int t = threadIdx.x; t < T; t += blockDim.x)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) s[3 + q] += tilesum[static_cast<int64_t>(t) * kTileSum + q];
     if (threadIdx.x == 0) s[11] = cnt[M];
 #pragma unroll
     for (int q = 0; q < 12; ++q)
@@ -756,6 +871,9 @@ int prepare_max_smem(int bytes)
         return CC_ECUDA;
     if (cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
         return CC_ECUDA;
+    if (cudaFuncSetAttribute(k_collide_large, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(kCollideSmem)) != cudaSuccess)
+        return CC_ECUDA;
     (void)bytes;
     return CC_OK;
 }
@@ -784,12 +902,13 @@ int run_binning(const double* v_in, int64_t ldv, const int32_t* cell_in, int n, 
     mark(ev, 0, st);
     k_count<<<L.T, kCountThreads, sizeof(int32_t) * M1, st>>>(cell_in, n, M, L.tile, tcount, err);
     mark(ev, 1, st);
-    k_scan_tiles<<<(M1 + 31) / 32, dim3(32, 8), 0, st>>>(tcount, L.T, M1, cnt);
+    k_scan_tiles<<<(M1 + 31) / 32, dim3(32, kScanRows), 0, st>>>(tcount, L.T, M1, cnt);
     k_scan_cells<<<1, 1024, 0, st>>>(cnt, M, off, chunk_off, Cj, keys, k, cell_base, step,
                                      static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
     const size_t smem = sizeof(int32_t) * M1 + sizeof(uint16_t) * static_cast<size_t>(L.W) * M1;
     mark(ev, 2, st);
-    k_scatter<<<L.T, 32 * L.W, smem, st>>>(v_in, ldv, cell_in, n, M, L.W, tcount, off, wsv);
+    k_scatter<<<L.T, 32 * L.W, smem, st>>>(v_in, ldv, cell_in, n, M, L.W, tcount, off, wsv,
+                                           at<double>(ws, L.o_tilesum));
     return launch_ok();
 }
 
@@ -909,7 +1028,7 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
 
     mark(ev, 3, st);
     k_collide_small<<<(M + 7) / 8, 256, 0, st>>>(A);
-    k_collide_large<<<static_cast<unsigned>(L.max_chunks), kCollideThreads, 0, st>>>(A);
+    k_collide_large<<<static_cast<unsigned>(L.max_chunks), kCollideThreads, kCollideSmem, st>>>(A);
     k_copy_dead<<<148 * 4, 256, 0, st>>>(A.wsv, A.off, M, nn, v_out, ldv, cell_out, perm_out);
 
     MomConst mc{p.weight, p.cell_volume, p.cell_volume_arr, p.mass / p.charge};
@@ -917,7 +1036,8 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     mark(ev, 4, st);
     k_finalize_cells<<<(M + 255) / 256, 256, 0, st>>>(A.cnt, A.off, A.chunk_off, A.recs, A.small_recs, A.wsv, M,
                                                       mc, moments_out, cellsum);
-    if (diag_out) k_finalize_diag<<<1, 1024, 0, st>>>(A.cnt, cellsum, M, diag_out);
+    if (diag_out)
+        k_finalize_diag<<<1, 1024, 0, st>>>(A.cnt, cellsum, M, at<double>(workspace, L.o_tilesum), L.T, diag_out);
     mark(ev, 5, st);
     return launch_ok();
 }
