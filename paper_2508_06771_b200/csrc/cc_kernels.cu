@@ -863,22 +863,19 @@ int launch_ok()
     return cudaGetLastError() == cudaSuccess ? CC_OK : CC_ECUDA;
 }
 
-int prepare_max_smem(int bytes)
+// Opt a kernel into `bytes` of dynamic shared memory (above the 48 KB default).
+template <typename K>
+int want_smem(K kernel, size_t bytes)
 {
-    // dynamic shared memory above 48 KB needs the opt-in attribute
-    static_assert(sizeof(int) == 4, "");
-    if (cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
+    if (bytes <= 48 * 1024) return CC_OK;
+    if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)) !=
+        cudaSuccess) {
+        cudaGetLastError();
         return CC_ECUDA;
-    if (cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
-        return CC_ECUDA;
-    if (cudaFuncSetAttribute(k_collide_large, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(kCollideSmem)) != cudaSuccess)
-        return CC_ECUDA;
-    (void)bytes;
+    }
     return CC_OK;
 }
 
-// CCS1-CCS3 into the workspace (shared by coulomb_collide and cc_bin).
 void mark(void* const* ev, int i, cudaStream_t st)
 {
     if (ev && ev[i]) cudaEventRecord(static_cast<cudaEvent_t>(ev[i]), st);
@@ -888,8 +885,6 @@ int run_binning(const double* v_in, int64_t ldv, const int32_t* cell_in, int n, 
                 void* ws, const CellConst& k, uint32_t cell_base, uint32_t step, uint64_t seed,
                 cudaStream_t st, void* const* ev = nullptr)
 {
-    int rc = prepare_max_smem(0);
-    if (rc) return rc;
     int32_t* err = at<int32_t>(ws, L.o_err);
     int32_t* tcount = at<int32_t>(ws, L.o_tcount);
     int32_t* cnt = at<int32_t>(ws, L.o_cnt);
@@ -899,13 +894,16 @@ int run_binning(const double* v_in, int64_t ldv, const int32_t* cell_in, int n, 
     cc::U4* keys = at<cc::U4>(ws, L.o_keys);
     double* wsv = at<double>(ws, L.o_wsv);
     const int M1 = M + 1;
+    const size_t smem = sizeof(int32_t) * M1 + sizeof(uint16_t) * static_cast<size_t>(L.W) * M1;
+    int rc = want_smem(k_count, sizeof(int32_t) * M1);
+    if (!rc) rc = want_smem(k_scatter, smem);
+    if (rc) return rc;
     mark(ev, 0, st);
     k_count<<<L.T, kCountThreads, sizeof(int32_t) * M1, st>>>(cell_in, n, M, L.tile, tcount, err);
     mark(ev, 1, st);
     k_scan_tiles<<<(M1 + 31) / 32, dim3(32, kScanRows), 0, st>>>(tcount, L.T, M1, cnt);
     k_scan_cells<<<1, 1024, 0, st>>>(cnt, M, off, chunk_off, Cj, keys, k, cell_base, step,
                                      static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
-    const size_t smem = sizeof(int32_t) * M1 + sizeof(uint16_t) * static_cast<size_t>(L.W) * M1;
     mark(ev, 2, st);
     k_scatter<<<L.T, 32 * L.W, smem, st>>>(v_in, ldv, cell_in, n, M, L.W, tcount, off, wsv,
                                            at<double>(ws, L.o_tilesum));
@@ -971,6 +969,7 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
                     double* moments_out, double* diag_out, void* workspace, size_t workspace_bytes,
                     void* stream)
 {
+    cudaGetLastError();   // launch errors below are ours, not a stale earlier one
     cc_params p;
     if (params) p = *params; else cc_default_params(&p);
     if (n < 0 || cells < 1 || ldv < n || !(dt > 0.0) || step >= (1ull << 32)) return CC_EINVAL;
@@ -1027,6 +1026,8 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     A.s1 = static_cast<uint32_t>(seed >> 32);
 
     mark(ev, 3, st);
+    rc = want_smem(k_collide_large, kCollideSmem);
+    if (rc) return rc;
     k_collide_small<<<(M + 7) / 8, 256, 0, st>>>(A);
     k_collide_large<<<static_cast<unsigned>(L.max_chunks), kCollideThreads, kCollideSmem, st>>>(A);
     k_copy_dead<<<148 * 4, 256, 0, st>>>(A.wsv, A.off, M, nn, v_out, ldv, cell_out, perm_out);
@@ -1059,6 +1060,7 @@ int cc_device_status(void* workspace, void* stream)
 int cc_bin(const int32_t* cell_in, int64_t n, int32_t cells, int32_t* perm_out, int32_t* off_out,
            void* workspace, size_t workspace_bytes, void* stream)
 {
+    cudaGetLastError();   // launch errors below are ours, not a stale earlier one
     if (n < 0 || cells < 1) return CC_EINVAL;
     if (n >= (1ll << 31) || cells > CC_MAX_CELLS) return CC_ECOUNT;
     if (!workspace || !aligned(workspace, 256)) return CC_EWORKSPACE;
@@ -1086,6 +1088,7 @@ int cc_bin(const int32_t* cell_in, int64_t n, int32_t cells, int32_t* perm_out, 
 int cc_pairs(const int32_t* off, int32_t cells, uint32_t cell_base, uint64_t seed, uint64_t step,
              int32_t* pair_slots_out, int64_t max_pairs, void* stream)
 {
+    cudaGetLastError();   // launch errors below are ours, not a stale earlier one
     if (!off || cells < 1 || step >= (1ull << 32) || max_pairs < 0) return CC_EINVAL;
     if (max_pairs > 0 && !pair_slots_out) return CC_EINVAL;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1096,6 +1099,7 @@ int cc_pairs(const int32_t* off, int32_t cells, uint32_t cell_base, uint64_t see
 
 int cc_philox(const uint32_t* ctr4, uint64_t seed, uint32_t* out4, int64_t m, void* stream)
 {
+    cudaGetLastError();   // launch errors below are ours, not a stale earlier one
     if (m < 0 || (m > 0 && (!ctr4 || !out4))) return CC_EINVAL;
     if (m == 0) return CC_OK;
     k_philox<<<static_cast<unsigned>((m + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
@@ -1105,6 +1109,7 @@ int cc_philox(const uint32_t* ctr4, uint64_t seed, uint32_t* out4, int64_t m, vo
 
 int cc_ppnd16(const double* u, double* z, int64_t m, void* stream)
 {
+    cudaGetLastError();   // launch errors below are ours, not a stale earlier one
     if (m < 0 || (m > 0 && (!u || !z))) return CC_EINVAL;
     if (m == 0) return CC_OK;
     k_ppnd16<<<static_cast<unsigned>((m + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(u, z, m);
@@ -1114,6 +1119,7 @@ int cc_ppnd16(const double* u, double* z, int64_t m, void* stream)
 int cc_ta_pairs(double* va, double* vb, const double* C, const double* u1, const double* u2, int64_t m,
                 void* stream)
 {
+    cudaGetLastError();   // launch errors below are ours, not a stale earlier one
     if (m < 0 || (m > 0 && (!va || !vb || !C || !u1 || !u2))) return CC_EINVAL;
     if (m == 0) return CC_OK;
     k_ta_pairs<<<static_cast<unsigned>((m + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(va, vb, C, u1,
@@ -1124,6 +1130,7 @@ int cc_ta_pairs(double* va, double* vb, const double* C, const double* u1, const
 int cc_moments(const double* v, int64_t ldv, const int32_t* off, int32_t cells, const cc_params* params,
                double* out, void* stream)
 {
+    cudaGetLastError();   // launch errors below are ours, not a stale earlier one
     if (!v || !off || !out || cells < 1 || ldv < 0) return CC_EINVAL;
     cc_params p;
     if (params) p = *params; else cc_default_params(&p);
@@ -1134,6 +1141,7 @@ int cc_moments(const double* v, int64_t ldv, const int32_t* off, int32_t cells, 
 
 int cc_diag_sum_ranks(const double* gathered, int32_t nranks, double* out, void* stream)
 {
+    cudaGetLastError();   // launch errors below are ours, not a stale earlier one
     if (!gathered || !out || nranks < 1) return CC_EINVAL;
     k_diag_sum_ranks<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(gathered, nranks, out);
     return launch_ok();
