@@ -38,24 +38,56 @@ __device__ __forceinline__ double u01(uint32_t hi, uint32_t lo)
     return __fma_rn(static_cast<double>(m), 0x1.0p-52, 0x1.0p-53);
 }
 
+// ---------------------------------------------------------------- fast fp64 reciprocal / rsqrt
+// MUFU approximations refined by two Newton steps: a few ulp, far inside the
+// 1e-12 parity bar, at ~6 instructions instead of the ~20 of IEEE div / sqrt.
+__device__ __forceinline__ double rcp_nr(double x)
+{
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+
+__device__ __forceinline__ double rsqrt_nr(double x)
+{
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double h = 0.5 * x;
+    double e = fma(-h * y, y, 0.5);
+    y = fma(y, e, y);
+    e = fma(-h * y, y, 0.5);
+    return fma(y, e, y);
+}
+
 // ---------------------------------------------------------------- AS241 PPND16
-__device__ __forceinline__ double ppnd16(double p)
+// Split into the central region (|u - 1/2| <= 0.425, ~85% of draws) and the
+// tails, so a kernel can evaluate the tails of a whole warp's items together.
+__device__ __forceinline__ bool ppnd16_is_central(double p) { return fabs(p - 0.5) <= 0.425; }
+
+__device__ __forceinline__ double ppnd16_central(double p)
 {
     const double q = p - 0.5;
-    if (fabs(q) <= 0.425) {
-        const double r = 0.180625 - q * q;
-        const double num = (((((((2.5090809287301226727e+3 * r + 3.3430575583588128105e+4) * r +
-                                 6.7265770927008700853e+4) * r + 4.5921953931549871457e+4) * r +
-                               1.3731693765509461125e+4) * r + 1.9715909503065514427e+3) * r +
-                             1.3314166789178437745e+2) * r + 3.3871328727963666080e+0) * q;
-        const double den = (((((((5.2264952788528545610e+3 * r + 2.8729085735721942674e+4) * r +
-                                 3.9307895800092710610e+4) * r + 2.1213794301586595867e+4) * r +
-                               5.3941960214247511077e+3) * r + 6.8718700749205790830e+2) * r +
-                             4.2313330701600911252e+1) * r + 1.0);
-        return num / den;
-    }
-    double r = (q < 0.0) ? p : 1.0 - p;
-    r = sqrt(-log(r));
+    const double r = 0.180625 - q * q;
+    const double num = (((((((2.5090809287301226727e+3 * r + 3.3430575583588128105e+4) * r +
+                             6.7265770927008700853e+4) * r + 4.5921953931549871457e+4) * r +
+                           1.3731693765509461125e+4) * r + 1.9715909503065514427e+3) * r +
+                         1.3314166789178437745e+2) * r + 3.3871328727963666080e+0) * q;
+    const double den = (((((((5.2264952788528545610e+3 * r + 2.8729085735721942674e+4) * r +
+                             3.9307895800092710610e+4) * r + 2.1213794301586595867e+4) * r +
+                           5.3941960214247511077e+3) * r + 6.8718700749205790830e+2) * r +
+                         4.2313330701600911252e+1) * r + 1.0);
+    return num * rcp_nr(den);
+}
+
+// Tail argument: the smaller tail mass min(p, 1-p), negative for p < 1/2.
+__device__ __forceinline__ double ppnd16_tail_arg(double p) { return (p < 0.5) ? -p : 1.0 - p; }
+
+__device__ __forceinline__ double ppnd16_tail(double targ)
+{
+    double r = sqrt(-log(fabs(targ)));
     double num, den;
     if (r <= 5.0) {
         r -= 1.6;
@@ -78,8 +110,13 @@ __device__ __forceinline__ double ppnd16(double p)
                   1.4875361290850614852e-2) * r + 1.3692988092273580531e-1) * r +
                 5.9983220655588793769e-1) * r + 1.0);
     }
-    const double x = num / den;
-    return (q < 0.0) ? -x : x;
+    const double x = num * rcp_nr(den);
+    return (targ < 0.0) ? -x : x;
+}
+
+__device__ __forceinline__ double ppnd16(double p)
+{
+    return ppnd16_is_central(p) ? ppnd16_central(p) : ppnd16_tail(ppnd16_tail_arg(p));
 }
 
 // ---------------------------------------------------------------- pairing (R1)
@@ -170,29 +207,27 @@ __device__ __forceinline__ void small_cell_perm(uint32_t N, uint32_t G, uint32_t
 }
 
 // ---------------------------------------------------------------- TA77 update
-// <delta^2> = C / |u|^3; delta = sqrt(<delta^2>) Phi^-1(u1); tan(Theta/2) = delta;
-// phi = 2 pi u2; v_a += Du/2, v_b -= Du/2.
-__device__ __forceinline__ void ta_update(double& ax, double& ay, double& az,
-                                          double& bx, double& by, double& bz,
-                                          double C, double u1, double u2)
+// <delta^2> = C / |u|^3; delta = sqrt(<delta^2>) z with z = Phi^-1(u1);
+// tan(Theta/2) = delta; phi = 2 pi u2; v_a += Du/2, v_b -= Du/2.
+// sin(Theta) = 2 delta/(1+delta^2), 1-cos(Theta) = 2 delta^2/(1+delta^2) with
+// |delta| clamped at 1e150 (then 1-cos = 2 exactly and sin(Theta) < 1e-149:
+// the algebraically equal limit of R9's t = 1/delta form, no NaN).
+__device__ __forceinline__ void ta_update_z(double& ax, double& ay, double& az,
+                                            double& bx, double& by, double& bz,
+                                            double C, double z, double u2)
 {
     const double ux = ax - bx, uy = ay - by, uz = az - bz;
     if (ux == 0.0 && uy == 0.0 && uz == 0.0) return;
-    const double usq = ux * ux + uy * uy + uz * uz;
-    const double u = sqrt(usq);
-    const double var = C / (usq * u);
-    const double delta = sqrt(var) * ppnd16(u1);
-    double sinT, omc;
-    if (fabs(delta) > 1.0) {
-        const double t = 1.0 / delta;
-        const double inv = 1.0 / (1.0 + t * t);
-        sinT = 2.0 * t * inv;
-        omc = 2.0 * inv;
-    } else {
-        const double inv = 1.0 / (1.0 + delta * delta);
-        sinT = 2.0 * delta * inv;
-        omc = 2.0 * delta * delta * inv;
-    }
+    const double usq = fma(ux, ux, fma(uy, uy, uz * uz));
+    const double rs = rsqrt_nr(usq);                 // 1/|u|
+    const double u = usq * rs;
+    const double var = C * (rs * rs) * rs;           // <delta^2>
+    const double delta = sqrt(var) * z;
+    const double dd = fmin(fabs(delta), 1e150);
+    const double d2 = dd * dd;
+    const double inv = rcp_nr(1.0 + d2);
+    const double sinT = 2.0 * copysign(dd, delta) * inv;
+    const double omc = 2.0 * d2 * inv;
     double sphi, cphi;
     sincospi(2.0 * u2, &sphi, &cphi);
     double dux, duy, duz;
@@ -201,16 +236,24 @@ __device__ __forceinline__ void ta_update(double& ax, double& ay, double& az,
         duy = u * sinT * sphi;
         duz = -uz * omc;
     } else {
-        const double uperp = sqrt(ux * ux + uy * uy);
-        const double ip = 1.0 / uperp;
+        const double up2 = fma(ux, ux, uy * uy);
+        const double ip = rsqrt_nr(up2);             // 1/u_perp
+        const double uperp = up2 * ip;
         const double sc = sinT * cphi, ss = sinT * sphi;
         const double A = uz * sc * ip, B = u * ss * ip;
         dux = ux * A - uy * B - ux * omc;
         duy = uy * A + ux * B - uy * omc;
         duz = -uperp * sc - uz * omc;
     }
-    ax += 0.5 * dux; ay += 0.5 * duy; az += 0.5 * duz;
-    bx -= 0.5 * dux; by -= 0.5 * duy; bz -= 0.5 * duz;
+    ax = fma(0.5, dux, ax); ay = fma(0.5, duy, ay); az = fma(0.5, duz, az);
+    bx = fma(-0.5, dux, bx); by = fma(-0.5, duy, by); bz = fma(-0.5, duz, bz);
+}
+
+__device__ __forceinline__ void ta_update(double& ax, double& ay, double& az,
+                                          double& bx, double& by, double& bz,
+                                          double C, double u1, double u2)
+{
+    ta_update_z(ax, ay, az, bx, by, bz, C, ppnd16(u1), u2);
 }
 
 }  // namespace cc

@@ -29,23 +29,24 @@
 namespace {
 
 constexpr int kCountThreads = 256;
-constexpr int kSub = 8192;               // elements per warp sub-range in k_scatter (<= 65535)
+constexpr int kSub = 4096;               // elements per warp sub-range in k_scatter
 constexpr int kScatterUnrollA = 16;      // cell loads in flight per lane, counting pass
 constexpr int kScatterUnrollB = 8;       // (cell, v) loads in flight per lane, scatter pass
 constexpr int kCollideThreads = 256;
 constexpr int kChunk = 1024;             // items (pairs or sitter) per k_collide_large CTA
-constexpr int kRec = 8;                  // doubles per chunk moment record: S1' (3), S2' (3), pad
-constexpr int kSmallRec = 12;            // small-cell record: S1', S2', shift (3), pad
-constexpr int kCellSum = 4;              // per-cell post-collision raw sums: v (3), |v|^2
-constexpr int kTileSum = 4;              // per-tile pre-collision raw sums: v (3), |v|^2
-constexpr int kScatterSmemBudget = 96 * 1024;
+constexpr int kRec = 12;                 // chunk moment record: S1' (3), S2' (3), pre sum v (3), pre sum |v|^2, pad
+constexpr int kSmallRec = 16;            // small-cell record: as kRec + the shift (the cell's exact mean)
+constexpr int kCellSum = 8;              // per-cell raw sums: pre v (3), pre |v|^2, post v (3), post |v|^2
+constexpr int kScatterSmemBudget = 96 * 1024;   // per-warp counters of one CTA
+constexpr int kMaxScatterWarps = 12;
+static_assert(kMaxScatterWarps * kSub <= 65536, "per-warp 16-bit cell counters must hold a whole tile");
 
 // ------------------------------------------------------------------ layout
 struct Layout {
     int W = 1, tile = kSub, T = 0;
     int64_t max_chunks = 0;
     size_t o_err = 0, o_tcount = 0, o_cnt = 0, o_off = 0, o_chunk = 0, o_C = 0, o_keys = 0;
-    size_t o_small = 0, o_recs = 0, o_cellsum = 0, o_tilesum = 0, o_wsv = 0, total = 0;
+    size_t o_small = 0, o_recs = 0, o_cellsum = 0, o_ref = 0, o_wsv = 0, total = 0;
 };
 
 size_t align256(size_t x) { return (x + 255u) & ~static_cast<size_t>(255u); }
@@ -53,7 +54,7 @@ size_t align256(size_t x) { return (x + 255u) & ~static_cast<size_t>(255u); }
 int scatter_warps(int32_t M)
 {
     int W = kScatterSmemBudget / (2 * (M + 2));
-    if (W > 8) W = 8;
+    if (W > kMaxScatterWarps) W = kMaxScatterWarps;
     if (W < 1) W = 1;
     return W;
 }
@@ -76,7 +77,7 @@ Layout make_layout(int64_t n, int32_t M)
     L.o_small = o;    o = align256(o + static_cast<size_t>(M) * kSmallRec * sizeof(double));
     L.o_recs = o;     o = align256(o + static_cast<size_t>(L.max_chunks) * kRec * sizeof(double));
     L.o_cellsum = o;  o = align256(o + static_cast<size_t>(M) * kCellSum * sizeof(double));
-    L.o_tilesum = o;  o = align256(o + static_cast<size_t>(L.T > 0 ? L.T : 1) * kTileSum * sizeof(double));
+    L.o_ref = o;      o = align256(o + static_cast<size_t>(M) * 4 * sizeof(double));
     L.o_wsv = o;      o = align256(o + static_cast<size_t>(n > 0 ? n : 1) * 4 * sizeof(double));
     L.total = o;
     return L;
@@ -110,23 +111,38 @@ __device__ __forceinline__ int32_t unpack_perm(double w)
 }
 
 // ------------------------------------------------------------------ CCS1: count
+// flags[0]: sticky invalid-id flag; flags[1]: "input not cell-sorted" (cleared
+// by the host before each call).  Sorted means live ids non-decreasing in input
+// order with every dead/invalid particle after the last live one; then the
+// stable order is the identity and k_scatter is skipped.
 __global__ void __launch_bounds__(kCountThreads)
 k_count(const int32_t* __restrict__ cell, int n, int M, int tile, int32_t* __restrict__ tcount,
-        int32_t* __restrict__ err)
+        int32_t* __restrict__ flags)
 {
     extern __shared__ int32_t hist[];   // [M+1], bin M = dead or invalid
     for (int i = threadIdx.x; i <= M; i += blockDim.x) hist[i] = 0;
     __syncthreads();
     const int64_t start = static_cast<int64_t>(blockIdx.x) * tile;
     const int64_t end = min(start + tile, static_cast<int64_t>(n));
-    int bad = 0;
+    int bad = 0, unsorted = 0;
     for (int64_t i = start + threadIdx.x; i < end; i += blockDim.x) {
         const int32_t c = __ldg(cell + i);
         const bool live = (c >= 0) && (c < M);
         bad |= (!live && c != -1);
-        atomicAdd(&hist[live ? c : M], 1);
+        const int32_t key = live ? c : M;
+        if (i > 0) {
+            const int32_t cp = __ldg(cell + i - 1);
+            const int32_t kp = (cp >= 0 && cp < M) ? cp : M;
+            unsorted |= (key < kp);
+        }
+        atomicAdd(&hist[key], 1);
     }
-    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(err, 1);
+    const int any_bad = __syncthreads_or(bad);
+    const int any_unsorted = __syncthreads_or(unsorted);
+    if (threadIdx.x == 0) {
+        if (any_bad) atomicOr(flags, 1);
+        if (any_unsorted) atomicOr(flags + 1, 1);
+    }
     int32_t* row = tcount + static_cast<int64_t>(blockIdx.x) * (M + 1);
     for (int i = threadIdx.x; i <= M; i += blockDim.x) row[i] = hist[i];
 }
@@ -259,26 +275,35 @@ k_scan_cells(const int32_t* __restrict__ cnt, int M, int32_t* __restrict__ off,
 // ------------------------------------------------------------------ CCS3: stable scatter
 // Tile = W warps x kSub elements; warp w owns the contiguous sub-range w of the
 // tile, so "input order" = (tile, warp, step, lane).  Per-warp 16-bit counters
-// give each element its rank among equal-cell predecessors.  Loads are issued
-// in batches (kScatterUnrollA / B per lane) so each warp keeps several KB in
-// flight.  The pass also produces the tile's pre-collision sums (diagnostics).
-__global__ void __launch_bounds__(256)
+// (two per 32-bit word) give each element its rank among equal-cell
+// predecessors: the leader of each match.any group advances its cell's counter
+// with one shared-memory atomic and broadcasts the old value to the group, so
+// successive groups never wait on each other.  Loads are issued in batches
+// (kScatterUnrollA / B per lane) to keep several KB per warp in flight.
+__device__ __forceinline__ uint32_t warp_counter_add(uint32_t* words, int32_t b, uint32_t add)
+{
+    const uint32_t sh = (static_cast<uint32_t>(b) & 1u) << 4;
+    return (atomicAdd(words + (b >> 1), add << sh) >> sh) & 0xFFFFu;
+}
+
+__global__ void __launch_bounds__(32 * kMaxScatterWarps)
 k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__ cell, int n, int M,
           int W, const int32_t* __restrict__ tbase, const int32_t* __restrict__ off,
-          double* __restrict__ wsv, double* __restrict__ tilesum)
+          double* __restrict__ wsv, const int32_t* __restrict__ flags)
 {
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ double red[8][kTileSum];
+    if (flags && flags[1] == 0) return;   // input already cell-sorted: the stable order is the identity
     const int M1 = M + 1;
+    const int MW = (M1 + 1) / 2;           // 32-bit words per warp row
     int32_t* base = reinterpret_cast<int32_t*>(smem);                       // [M1]
-    uint16_t* wcnt = reinterpret_cast<uint16_t*>(smem + sizeof(int32_t) * M1);  // [W][M1]
+    uint32_t* wcnt = reinterpret_cast<uint32_t*>(smem + sizeof(int32_t) * M1);  // [W][MW] packed u16 pairs
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int i = threadIdx.x; i < W * M1; i += blockDim.x) wcnt[i] = 0;
+    for (int i = threadIdx.x; i < W * MW; i += blockDim.x) wcnt[i] = 0u;
     __syncthreads();
 
     const int64_t s0 = static_cast<int64_t>(blockIdx.x) * W * kSub + static_cast<int64_t>(w) * kSub;
     const int64_t s1 = min(s0 + kSub, static_cast<int64_t>(n));
-    uint16_t* my = wcnt + w * M1;
+    uint32_t* my = wcnt + w * MW;
     const uint32_t lt = (1u << lane) - 1u;
 
     // pass A: per-warp counts of the sub-range
@@ -295,17 +320,21 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
         for (int u = 0; u < kScatterUnrollA; ++u) {
             const uint32_t peers = __match_any_sync(0xFFFFFFFFu, key[u]);
             if (key[u] >= 0 && lane == __ffs(peers) - 1)
-                my[key[u]] = static_cast<uint16_t>(my[key[u]] + __popc(peers));
-            __syncwarp();
+                atomicAdd(my + (key[u] >> 1), static_cast<uint32_t>(__popc(peers)) << ((key[u] & 1) << 4));
         }
     }
     __syncthreads();
+    // exclusive scan over warps per cell; CTA base = cell offset + tile offset
     const int32_t* trow = tbase + static_cast<int64_t>(blockIdx.x) * M1;
     for (int c = threadIdx.x; c < M1; c += blockDim.x) {
+        const uint32_t sh = (static_cast<uint32_t>(c) & 1u) << 4;
         uint32_t run = 0;
         for (int ww = 0; ww < W; ++ww) {
-            const uint32_t x = wcnt[ww * M1 + c];
-            wcnt[ww * M1 + c] = static_cast<uint16_t>(run);
+            uint32_t* wd = wcnt + ww * MW + (c >> 1);
+            const uint32_t x = (*wd >> sh) & 0xFFFFu;
+            // the two halves of a word belong to cells c and c^1, handled by
+            // different threads: update only our half with an atomic
+            atomicAdd(wd, (run - x) << sh);    // half := run (mod 2^16, no carry: run, x < 2^16)
             run += x;
         }
         base[c] = off[c] + trow[c];           // off[M] = L: dead slots follow the live ones
@@ -313,7 +342,6 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
     __syncthreads();
 
     // pass B: ranks, destinations, 32-byte records
-    double sx = 0.0, sy = 0.0, sz = 0.0, se = 0.0;
     for (int64_t i0 = s0; i0 < s1; i0 += 32 * kScatterUnrollB) {
         int32_t key[kScatterUnrollB];
         double x[kScatterUnrollB], y[kScatterUnrollB], z[kScatterUnrollB];
@@ -330,70 +358,60 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
         for (int u = 0; u < kScatterUnrollB; ++u) {
             const int32_t b = key[u];
             const uint32_t peers = __match_any_sync(0xFFFFFFFFu, b);
-            int32_t dest = 0;
-            if (b >= 0) dest = base[b] + my[b] + __popc(peers & lt);
-            __syncwarp();
-            if (b >= 0 && lane == __ffs(peers) - 1) my[b] = static_cast<uint16_t>(my[b] + __popc(peers));
-            __syncwarp();
+            const int leader = __ffs(peers) - 1;
+            uint32_t old = 0;
+            if (b >= 0 && lane == leader) old = warp_counter_add(my, b, static_cast<uint32_t>(__popc(peers)));
+            old = __shfl_sync(0xFFFFFFFFu, old, leader);
             if (b >= 0) {
+                const int32_t dest = base[b] + static_cast<int32_t>(old) + __popc(peers & lt);
                 const int64_t i = i0 + 32 * u + lane;
                 st256(wsv + 4 * static_cast<int64_t>(dest), x[u], y[u], z[u],
                       pack_pc(static_cast<int32_t>(i), b < M ? b : -1));
-                if (b < M) {
-                    sx += x[u]; sy += y[u]; sz += z[u];
-                    se += x[u] * x[u] + y[u] * y[u] + z[u] * z[u];
-                }
             }
         }
-    }
-    double t4[kTileSum] = {sx, sy, sz, se};
-#pragma unroll
-    for (int q = 0; q < kTileSum; ++q)
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) t4[q] += __shfl_down_sync(0xFFFFFFFFu, t4[q], d);
-    if (lane == 0)
-#pragma unroll
-        for (int q = 0; q < kTileSum; ++q) red[w][q] = t4[q];
-    __syncthreads();
-    if (threadIdx.x < kTileSum) {
-        double a = 0.0;
-        for (int ww = 0; ww < W; ++ww) a += red[ww][threadIdx.x];
-        tilesum[static_cast<int64_t>(blockIdx.x) * kTileSum + threadIdx.x] = a;
     }
 }
 
 // ------------------------------------------------------------------ CCS4 + CCS5 items
 struct CollideArgs {
-    const double* wsv;
+    const double* wsv;          // cell-sorted 32-byte records (cold input)
+    const double* v_in;         // the caller's SoA input (read directly when it is already sorted)
+    int64_t ldv;                // row stride of v_in and v_out
+    const int32_t* flags;       // flags[1] == 0: input cell-sorted
     const int32_t* cnt;
     const int32_t* off;
     const int32_t* chunk_off;
     const double* Cj;
     const cc::U4* keys;
     double* v_out;
-    int64_t ldv;
     int32_t* cell_out;
     int32_t* perm_out;
     double* recs;
     double* small_recs;
+    double* cellref;            // [M][4] shift of large cells (pre-collision v of the first slot)
     int M;
     uint32_t cell_base, step, s0, s1;
 };
 
-// Post-collision moment accumulator about a per-cell shift r:
-// [0..2] sum (v - r), [3..5] sum (v - r)^2.
+// Moment accumulator: [0..2] sum (v - r) post, [3..5] sum (v - r)^2 post,
+// [6..8] sum v pre, [9] sum |v|^2 pre.
 struct Acc {
-    double a[6];
+    double a[10];
     __device__ void zero()
     {
 #pragma unroll
-        for (int q = 0; q < 6; ++q) a[q] = 0.0;
+        for (int q = 0; q < 10; ++q) a[q] = 0.0;
     }
-    __device__ void add(double x, double y, double z, double rx, double ry, double rz)
+    __device__ void post(double x, double y, double z, double rx, double ry, double rz)
     {
         const double dx = x - rx, dy = y - ry, dz = z - rz;
         a[0] += dx; a[1] += dy; a[2] += dz;
         a[3] = fma(dx, dx, a[3]); a[4] = fma(dy, dy, a[4]); a[5] = fma(dz, dz, a[5]);
+    }
+    __device__ void pre(double x, double y, double z)
+    {
+        a[6] += x; a[7] += y; a[8] += z;
+        a[9] = fma(x, x, fma(y, y, fma(z, z, a[9])));
     }
 };
 
@@ -401,38 +419,35 @@ struct Rec {
     double x, y, z, w;     // w = (perm, cell) bit pattern
 };
 
-__device__ __forceinline__ Rec ld_rec(const double* p)
+// Stable slot s of the current call: a 32-byte record of ws_v (cold) or the
+// caller's SoA input at index s (sorted input: slot = input index).
+__device__ __forceinline__ Rec load_slot(const CollideArgs& A, bool sorted, int64_t s)
 {
     Rec r;
-    ld256(p, r.x, r.y, r.z, r.w);
+    if (sorted) {
+        r.x = A.v_in[s]; r.y = A.v_in[A.ldv + s]; r.z = A.v_in[2 * A.ldv + s];
+        r.w = pack_pc(static_cast<int32_t>(s), 0);
+    } else {
+        ld256(A.wsv + 4 * s, r.x, r.y, r.z, r.w);
+    }
     return r;
 }
 
-// One item k of cell (j, o, N): a pair (2k+1 < N) with records a, b, or the
-// odd sitter (2k = N-1) with record a.  CCS4: one Philox call per pair,
-// ctr = (k, G, step, 0).  CCS5: TA77.  Output in pair order, SoA.
-__device__ __forceinline__ void collide_item(const CollideArgs& A, int32_t j, int32_t o, int32_t N, uint32_t k,
-                                             Rec a, Rec b, double C, double rx, double ry, double rz, Acc& acc)
+__device__ __forceinline__ void write_out(const CollideArgs& A, int32_t p, int32_t j, const Rec& r)
 {
-    const int32_t pa = o + 2 * static_cast<int32_t>(k);
-    double* vo = A.v_out;
-    if (2 * k + 1 < static_cast<uint32_t>(N)) {
-        const cc::U4 r = cc::philox4x32_10(
-            cc::U4{k, A.cell_base + static_cast<uint32_t>(j), A.step, 0u}, A.s0, A.s1);
-        cc::ta_update(a.x, a.y, a.z, b.x, b.y, b.z, C, cc::u01(r.x, r.y), cc::u01(r.z, r.w));
-        vo[pa] = a.x; vo[pa + 1] = b.x;
-        vo[A.ldv + pa] = a.y; vo[A.ldv + pa + 1] = b.y;
-        vo[2 * A.ldv + pa] = a.z; vo[2 * A.ldv + pa + 1] = b.z;
-        A.cell_out[pa] = j; A.cell_out[pa + 1] = j;
-        if (A.perm_out) { A.perm_out[pa] = unpack_perm(a.w); A.perm_out[pa + 1] = unpack_perm(b.w); }
-        acc.add(a.x, a.y, a.z, rx, ry, rz);
-        acc.add(b.x, b.y, b.z, rx, ry, rz);
-    } else {
-        vo[pa] = a.x; vo[A.ldv + pa] = a.y; vo[2 * A.ldv + pa] = a.z;
-        A.cell_out[pa] = j;
-        if (A.perm_out) A.perm_out[pa] = unpack_perm(a.w);
-        acc.add(a.x, a.y, a.z, rx, ry, rz);
-    }
+    A.v_out[p] = r.x;
+    A.v_out[A.ldv + p] = r.y;
+    A.v_out[2 * A.ldv + p] = r.z;
+    A.cell_out[p] = j;
+    if (A.perm_out) A.perm_out[p] = unpack_perm(r.w);
+}
+
+// CCS4: one Philox call per pair, ctr = (k, G, step, 0) -> (u1, u2) (R3).
+__device__ __forceinline__ void pair_uniforms(const CollideArgs& A, int32_t j, uint32_t k, double& u1, double& u2)
+{
+    const cc::U4 r = cc::philox4x32_10(cc::U4{k, A.cell_base + static_cast<uint32_t>(j), A.step, 0u}, A.s0, A.s1);
+    u1 = cc::u01(r.x, r.y);
+    u2 = cc::u01(r.z, r.w);
 }
 
 template <int NV>
@@ -444,8 +459,8 @@ __device__ __forceinline__ void warp_reduce(double (&a)[NV])
         for (int d = 16; d > 0; d >>= 1) a[q] += __shfl_down_sync(0xFFFFFFFFu, a[q], d);
 }
 
-// N_j <= 64: one warp per cell.  The warp holds the whole cell, so its moment
-// record is an exact two-pass one: the shift is the cell's post-collision mean.
+// N_j <= 64: one warp per cell; item k = lane.  The warp holds the whole cell,
+// so its moment record is an exact two-pass one about the post-collision mean.
 __global__ void __launch_bounds__(256)
 k_collide_small(CollideArgs A)
 {
@@ -455,6 +470,7 @@ k_collide_small(CollideArgs A)
     if (j >= A.M) return;
     const int32_t N = A.cnt[j];
     if (N == 0 || N > cc::kSmallCell) return;
+    const bool sorted = A.flags[1] == 0;
     const int32_t o = A.off[j];
     const uint32_t G = A.cell_base + static_cast<uint32_t>(j);
     cc::small_cell_perm(static_cast<uint32_t>(N), G, A.step, A.s0, A.s1, lane, pi_sm[w]);
@@ -464,10 +480,20 @@ k_collide_small(CollideArgs A)
     const uint32_t items = static_cast<uint32_t>(N + 1) / 2;
     const uint32_t k = static_cast<uint32_t>(lane);
     if (k < items) {
-        const Rec ra = ld_rec(A.wsv + 4 * static_cast<int64_t>(o + pi_sm[w][2 * k]));
-        Rec rb = ra;
-        if (2 * k + 1 < static_cast<uint32_t>(N)) rb = ld_rec(A.wsv + 4 * static_cast<int64_t>(o + pi_sm[w][2 * k + 1]));
-        collide_item(A, j, o, N, k, ra, rb, C, 0.0, 0.0, 0.0, acc);
+        const int32_t pa = o + 2 * static_cast<int32_t>(k);
+        Rec a = load_slot(A, sorted, o + pi_sm[w][2 * k]);
+        acc.pre(a.x, a.y, a.z);
+        if (2 * k + 1 < static_cast<uint32_t>(N)) {
+            Rec b = load_slot(A, sorted, o + pi_sm[w][2 * k + 1]);
+            acc.pre(b.x, b.y, b.z);
+            double u1, u2;
+            pair_uniforms(A, j, k, u1, u2);
+            cc::ta_update(a.x, a.y, a.z, b.x, b.y, b.z, C, u1, u2);
+            write_out(A, pa + 1, j, b);
+            acc.post(b.x, b.y, b.z, 0.0, 0.0, 0.0);
+        }
+        write_out(A, pa, j, a);
+        acc.post(a.x, a.y, a.z, 0.0, 0.0, 0.0);
     }
     warp_reduce(acc.a);
     // pass 2: sums about the exact mean (values re-read from v_out, L1/L2 hot)
@@ -479,14 +505,16 @@ k_collide_small(CollideArgs A)
     Acc q;
     q.zero();
     for (int32_t t = lane; t < N; t += 32)
-        q.add(A.v_out[o + t], A.v_out[A.ldv + o + t], A.v_out[2 * A.ldv + o + t], mx, my, mz);
+        q.post(A.v_out[o + t], A.v_out[A.ldv + o + t], A.v_out[2 * A.ldv + o + t], mx, my, mz);
     warp_reduce(q.a);
     if (lane == 0) {
         double* r = A.small_recs + static_cast<int64_t>(j) * kSmallRec;
 #pragma unroll
         for (int c = 0; c < 6; ++c) r[c] = q.a[c];
-        r[6] = mx; r[7] = my; r[8] = mz;
-        r[9] = r[10] = r[11] = 0.0;
+#pragma unroll
+        for (int c = 6; c < 10; ++c) r[c] = acc.a[c];
+        r[10] = mx; r[11] = my; r[12] = mz;
+        r[13] = r[14] = r[15] = 0.0;
     }
 }
 
@@ -496,26 +524,52 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem_src) : "memory");
 }
 
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src)
+{
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem_src) : "memory");
+}
+
 __device__ __forceinline__ void cp_async_wait_all()
 {
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
 }
 
+// Gather stable slot s into a 32-byte shared-memory record.
+__device__ __forceinline__ void stage_slot(const CollideArgs& A, bool sorted, int64_t s, double* dst)
+{
+    if (sorted) {
+        cp_async8(dst, A.v_in + s);
+        cp_async8(dst + 1, A.v_in + A.ldv + s);
+        cp_async8(dst + 2, A.v_in + 2 * A.ldv + s);
+        dst[3] = pack_pc(static_cast<int32_t>(s), 0);
+    } else {
+        const double* g = A.wsv + 4 * s;
+        cp_async16(dst, g);
+        cp_async16(dst + 2, g + 2);
+    }
+}
+
 // N_j > 64: one CTA per cell-aligned chunk of kChunk items, two phases:
 //  1. every thread computes pi_j(2k), pi_j(2k+1) (keyed Feistel, R1) for its
-//     items and issues cp.async gathers of both 32-byte records into shared
-//     memory — the whole chunk's 64 KB of gathers are in flight at once;
-//  2. every thread runs CCS4 + CCS5 on its items out of shared memory and
-//     writes the pair-ordered output (coalesced), accumulating moments.
+//     items and issues cp.async gathers of both records into shared memory —
+//     the whole chunk's 64 KB of gathers are in flight at once;
+//  2. items are processed two per thread per round: Philox (CCS4), the central
+//     AS241 branch in place and the tail branch (~15% of draws) compacted
+//     across the warp and evaluated once per 32 tails, then TA (CCS5), and the
+//     pair-ordered, coalesced SoA output plus the moment partials.
 constexpr int kItemsPerThread = kChunk / kCollideThreads;
+constexpr int kItemsPerRound = 2;
+constexpr int kTailQueue = 32 * kItemsPerRound;
 constexpr size_t kCollideSmem = 2ull * kChunk * 4 * sizeof(double);
 
-__global__ void __launch_bounds__(kCollideThreads)
+__global__ void __launch_bounds__(kCollideThreads, 3)
 k_collide_large(CollideArgs A)
 {
     extern __shared__ __align__(16) double stage[];       // [2][kChunk][4]
     __shared__ int32_t s_j;
-    __shared__ double red[kCollideThreads / 32][6];
+    __shared__ double tailq[kCollideThreads / 32][kTailQueue];
+    __shared__ double red[kCollideThreads / 32][10];
     const int c = blockIdx.x;
     if (threadIdx.x == 0) {
         int lo = 0, hi = A.M;   // invariant: chunk_off[lo] <= c < chunk_off[hi] when c < total
@@ -532,11 +586,11 @@ k_collide_large(CollideArgs A)
     __syncthreads();
     const int j = s_j;
     if (j < 0) return;
+    const bool sorted = A.flags[1] == 0;
     const int32_t N = A.cnt[j], o = A.off[j];
     const uint32_t items = static_cast<uint32_t>(N + 1) / 2;
     const uint32_t i0 = static_cast<uint32_t>(c - A.chunk_off[j]) * kChunk;
     const uint32_t i1 = min(i0 + static_cast<uint32_t>(kChunk), items);
-    const double* cellv = A.wsv + 4 * static_cast<int64_t>(o);
     {
         const cc::Feistel f = cc::make_feistel(static_cast<uint32_t>(N), A.keys[j]);
 #pragma unroll
@@ -544,65 +598,99 @@ k_collide_large(CollideArgs A)
             const uint32_t k = i0 + threadIdx.x + q * kCollideThreads;
             if (k < i1) {
                 const uint32_t e = k - i0;
-                const double* ga = cellv + 4 * static_cast<int64_t>(cc::feistel_pi(f, 2 * k));
-                cp_async16(stage + 4 * e, ga);
-                cp_async16(stage + 4 * e + 2, ga + 2);
-                if (2 * k + 1 < static_cast<uint32_t>(N)) {
-                    const double* gb = cellv + 4 * static_cast<int64_t>(cc::feistel_pi(f, 2 * k + 1));
-                    cp_async16(stage + 4 * (kChunk + e), gb);
-                    cp_async16(stage + 4 * (kChunk + e) + 2, gb + 2);
-                }
+                stage_slot(A, sorted, o + static_cast<int64_t>(cc::feistel_pi(f, 2 * k)), stage + 4 * e);
+                if (2 * k + 1 < static_cast<uint32_t>(N))
+                    stage_slot(A, sorted, o + static_cast<int64_t>(cc::feistel_pi(f, 2 * k + 1)),
+                               stage + 4 * (kChunk + e));
             }
         }
     }
-    double rx, ry, rz, rw;
-    ld256(cellv, rx, ry, rz, rw);          // shift: pre-collision v of the cell's first stable slot
+    // shift for the moment partials: pre-collision v of the cell's first stable slot
+    const Rec ref = load_slot(A, sorted, o);
+    if (i0 == 0 && threadIdx.x == 0) {
+        double* cr = A.cellref + 4 * static_cast<int64_t>(j);
+        cr[0] = ref.x; cr[1] = ref.y; cr[2] = ref.z; cr[3] = 0.0;
+    }
     const double C = A.Cj[j];
     cp_async_wait_all();
     __syncthreads();
+
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t lt = (1u << lane) - 1u;
+    double* q_w = tailq[w];
     Acc acc;
     acc.zero();
 #pragma unroll 1
-    for (int q = 0; q < kItemsPerThread; ++q) {
-        const uint32_t k = i0 + threadIdx.x + q * kCollideThreads;
-        if (k < i1) {
-            const uint32_t e = k - i0;
-            const double2 a01 = *reinterpret_cast<const double2*>(stage + 4 * e);
-            const double2 a23 = *reinterpret_cast<const double2*>(stage + 4 * e + 2);
-            const double2 b01 = *reinterpret_cast<const double2*>(stage + 4 * (kChunk + e));
-            const double2 b23 = *reinterpret_cast<const double2*>(stage + 4 * (kChunk + e) + 2);
-            collide_item(A, j, o, N, k, Rec{a01.x, a01.y, a23.x, a23.y}, Rec{b01.x, b01.y, b23.x, b23.y}, C,
-                         rx, ry, rz, acc);
+    for (int h = 0; h < kItemsPerThread; h += kItemsPerRound) {
+        double z[kItemsPerRound], u2[kItemsPerRound];
+        int tpos[kItemsPerRound];
+        int qn = 0;
+#pragma unroll
+        for (int t = 0; t < kItemsPerRound; ++t) {
+            const uint32_t k = i0 + threadIdx.x + (h + t) * kCollideThreads;
+            const bool pair = (k < i1) && (2 * k + 1 < static_cast<uint32_t>(N));
+            double u1 = 0.5;
+            u2[t] = 0.0;
+            if (pair) pair_uniforms(A, j, k, u1, u2[t]);
+            const bool tail = pair && !cc::ppnd16_is_central(u1);
+            z[t] = cc::ppnd16_central(tail ? 0.5 : u1);
+            const uint32_t tm = __ballot_sync(0xFFFFFFFFu, tail);
+            tpos[t] = tail ? qn + __popc(tm & lt) : -1;
+            if (tail) q_w[tpos[t]] = cc::ppnd16_tail_arg(u1);
+            qn += __popc(tm);
         }
+        __syncwarp();
+        for (int e = lane; e < qn; e += 32) q_w[e] = cc::ppnd16_tail(q_w[e]);
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < kItemsPerRound; ++t) {
+            const uint32_t k = i0 + threadIdx.x + (h + t) * kCollideThreads;
+            if (k < i1) {
+                const uint32_t e = k - i0;
+                const int32_t pa = o + 2 * static_cast<int32_t>(k);
+                const double2 a01 = *reinterpret_cast<const double2*>(stage + 4 * e);
+                const double2 a23 = *reinterpret_cast<const double2*>(stage + 4 * e + 2);
+                Rec a{a01.x, a01.y, a23.x, a23.y};
+                acc.pre(a.x, a.y, a.z);
+                if (2 * k + 1 < static_cast<uint32_t>(N)) {
+                    const double2 b01 = *reinterpret_cast<const double2*>(stage + 4 * (kChunk + e));
+                    const double2 b23 = *reinterpret_cast<const double2*>(stage + 4 * (kChunk + e) + 2);
+                    Rec b{b01.x, b01.y, b23.x, b23.y};
+                    acc.pre(b.x, b.y, b.z);
+                    const double zz = (tpos[t] >= 0) ? q_w[tpos[t]] : z[t];
+                    cc::ta_update_z(a.x, a.y, a.z, b.x, b.y, b.z, C, zz, u2[t]);
+                    write_out(A, pa + 1, j, b);
+                    acc.post(b.x, b.y, b.z, ref.x, ref.y, ref.z);
+                }
+                write_out(A, pa, j, a);
+                acc.post(a.x, a.y, a.z, ref.x, ref.y, ref.z);
+            }
+        }
+        __syncwarp();
     }
     warp_reduce(acc.a);
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if (lane == 0)
 #pragma unroll
-        for (int q = 0; q < 6; ++q) red[w][q] = acc.a[q];
+        for (int q = 0; q < 10; ++q) red[w][q] = acc.a[q];
     __syncthreads();
     if (threadIdx.x < kRec) {
-        double s = 0.0;
-        if (threadIdx.x < 6)
+        double sum = 0.0;
+        if (threadIdx.x < 10)
 #pragma unroll
-            for (int ww = 0; ww < kCollideThreads / 32; ++ww) s += red[ww][threadIdx.x];
-        A.recs[static_cast<int64_t>(c) * kRec + threadIdx.x] = s;
+            for (int ww = 0; ww < kCollideThreads / 32; ++ww) sum += red[ww][threadIdx.x];
+        A.recs[static_cast<int64_t>(c) * kRec + threadIdx.x] = sum;
     }
 }
 
 // Dead (and invalid) particles: slots [L, n), copied unchanged.
-__global__ void k_copy_dead(const double* __restrict__ wsv, const int32_t* __restrict__ off, int M, int n,
-                            double* __restrict__ v_out, int64_t ldv, int32_t* __restrict__ cell_out,
-                            int32_t* __restrict__ perm_out)
+__global__ void k_copy_dead(CollideArgs A, int n)
 {
-    const int32_t L = off[M];
+    const int32_t L = A.off[A.M];
+    const bool sorted = A.flags[1] == 0;
     for (int64_t p = L + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < n;
          p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        double x, y, z, wq;
-        ld256(wsv + 4 * p, x, y, z, wq);
-        v_out[p] = x; v_out[ldv + p] = y; v_out[2 * ldv + p] = z;
-        cell_out[p] = -1;
-        if (perm_out) perm_out[p] = unpack_perm(wq);
+        const Rec r = load_slot(A, sorted, p);
+        write_out(A, static_cast<int32_t>(p), -1, r);
     }
 }
 
@@ -628,29 +716,30 @@ __device__ __forceinline__ void moments_from_sums(const double* s, double N, dou
     }
 }
 
-__global__ void k_finalize_cells(const int32_t* __restrict__ cnt, const int32_t* __restrict__ off,
-                                 const int32_t* __restrict__ chunk_off, const double* __restrict__ recs,
-                                 const double* __restrict__ small_recs, const double* __restrict__ wsv,
-                                 int M, MomConst mc, double* __restrict__ moments_out,
-                                 double* __restrict__ cellsum)
+__global__ void k_finalize_cells(const int32_t* __restrict__ cnt, const int32_t* __restrict__ chunk_off,
+                                 const double* __restrict__ recs, const double* __restrict__ small_recs,
+                                 const double* __restrict__ cellref, int M, MomConst mc,
+                                 double* __restrict__ moments_out, double* __restrict__ cellsum)
 {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= M) return;
     const int32_t N = cnt[j];
-    double s[6] = {0, 0, 0, 0, 0, 0};
+    double s[10];
+#pragma unroll
+    for (int q = 0; q < 10; ++q) s[q] = 0.0;
     double rx = 0, ry = 0, rz = 0;
     if (N > 0) {
         if (N <= cc::kSmallCell) {
             const double* r = small_recs + static_cast<int64_t>(j) * kSmallRec;
 #pragma unroll
-            for (int q = 0; q < 6; ++q) s[q] = r[q];
-            rx = r[6]; ry = r[7]; rz = r[8];
+            for (int q = 0; q < 10; ++q) s[q] = r[q];
+            rx = r[10]; ry = r[11]; rz = r[12];
         } else {
-            double rw;
-            ld256(wsv + 4 * static_cast<int64_t>(off[j]), rx, ry, rz, rw);
+            const double* cr = cellref + 4 * static_cast<int64_t>(j);
+            rx = cr[0]; ry = cr[1]; rz = cr[2];
             for (int32_t c = chunk_off[j]; c < chunk_off[j + 1]; ++c)
 #pragma unroll
-                for (int q = 0; q < 6; ++q) s[q] += recs[static_cast<int64_t>(c) * kRec + q];
+                for (int q = 0; q < 10; ++q) s[q] += recs[static_cast<int64_t>(c) * kRec + q];
         }
     }
     if (moments_out) {
@@ -667,19 +756,21 @@ __global__ void k_finalize_cells(const int32_t* __restrict__ cnt, const int32_t*
     const double Nd = static_cast<double>(N);
     const double r[3] = {rx, ry, rz};
     double* cs = cellsum + static_cast<int64_t>(j) * kCellSum;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) cs[q] = s[6 + q];
     double e = 0.0;
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-        cs[q] = fma(Nd, r[q], s[q]);
+        cs[4 + q] = fma(Nd, r[q], s[q]);
         e += s[3 + q] + 2.0 * r[q] * s[q] + Nd * r[q] * r[q];
     }
-    cs[3] = e;
+    cs[7] = e;
 }
 
-// single CTA of 1024 threads: fixed-order reductions over cells and tiles
+// single CTA of 1024 threads: fixed-order reductions over cells
 __global__ void __launch_bounds__(1024)
 k_finalize_diag(const int32_t* __restrict__ cnt, const double* __restrict__ cellsum, int M,
-                const double* __restrict__ tilesum, int T, double* __restrict__ diag)
+                double* __restrict__ diag)
 {
     __shared__ double red[32][12];
     double s[12];
@@ -691,11 +782,8 @@ k_finalize_diag(const int32_t* __restrict__ cnt, const double* __restrict__ cell
         s[1] += N / 2;
         s[2] += N & 1;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) s[7 + q] += cellsum[static_cast<int64_t>(j) * kCellSum + q];
+        for (int q = 0; q < 8; ++q) s[3 + q] += cellsum[static_cast<int64_t>(j) * kCellSum + q];
     }
-    for (int t = threadIdx.x; t < T; t += blockDim.x)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) s[3 + q] += tilesum[static_cast<int64_t>(t) * kTileSum + q];
     if (threadIdx.x == 0) s[11] = cnt[M];
 #pragma unroll
     for (int q = 0; q < 12; ++q)
@@ -883,9 +971,10 @@ void mark(void* const* ev, int i, cudaStream_t st)
 
 int run_binning(const double* v_in, int64_t ldv, const int32_t* cell_in, int n, int M, const Layout& L,
                 void* ws, const CellConst& k, uint32_t cell_base, uint32_t step, uint64_t seed,
-                cudaStream_t st, void* const* ev = nullptr)
+                cudaStream_t st, void* const* ev, bool allow_sorted_skip)
 {
     int32_t* err = at<int32_t>(ws, L.o_err);
+    if (cudaMemsetAsync(err + 1, 0, sizeof(int32_t), st) != cudaSuccess) return CC_ECUDA;   // "unsorted" flag
     int32_t* tcount = at<int32_t>(ws, L.o_tcount);
     int32_t* cnt = at<int32_t>(ws, L.o_cnt);
     int32_t* off = at<int32_t>(ws, L.o_off);
@@ -894,7 +983,7 @@ int run_binning(const double* v_in, int64_t ldv, const int32_t* cell_in, int n, 
     cc::U4* keys = at<cc::U4>(ws, L.o_keys);
     double* wsv = at<double>(ws, L.o_wsv);
     const int M1 = M + 1;
-    const size_t smem = sizeof(int32_t) * M1 + sizeof(uint16_t) * static_cast<size_t>(L.W) * M1;
+    const size_t smem = sizeof(int32_t) * M1 + sizeof(uint32_t) * static_cast<size_t>(L.W) * ((M1 + 1) / 2);
     int rc = want_smem(k_count, sizeof(int32_t) * M1);
     if (!rc) rc = want_smem(k_scatter, smem);
     if (rc) return rc;
@@ -906,7 +995,7 @@ int run_binning(const double* v_in, int64_t ldv, const int32_t* cell_in, int n, 
                                      static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
     mark(ev, 2, st);
     k_scatter<<<L.T, 32 * L.W, smem, st>>>(v_in, ldv, cell_in, n, M, L.W, tcount, off, wsv,
-                                           at<double>(ws, L.o_tilesum));
+                                           allow_sorted_skip ? err : nullptr);
     return launch_ok();
 }
 
@@ -1003,11 +1092,14 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     const int nn = static_cast<int>(n);
     void* const* ev = p.stage_events;
     int rc = run_binning(v_in, ldv, cell_in, nn, M, L, workspace, k, cell_base, static_cast<uint32_t>(step), seed,
-                         st, ev);
+                         st, ev, true);
     if (rc) return rc;
 
     CollideArgs A;
     A.wsv = at<double>(workspace, L.o_wsv);
+    A.v_in = v_in;
+    A.flags = at<int32_t>(workspace, L.o_err);
+    A.cellref = at<double>(workspace, L.o_ref);
     A.cnt = at<int32_t>(workspace, L.o_cnt);
     A.off = at<int32_t>(workspace, L.o_off);
     A.chunk_off = at<int32_t>(workspace, L.o_chunk);
@@ -1030,15 +1122,14 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     if (rc) return rc;
     k_collide_small<<<(M + 7) / 8, 256, 0, st>>>(A);
     k_collide_large<<<static_cast<unsigned>(L.max_chunks), kCollideThreads, kCollideSmem, st>>>(A);
-    k_copy_dead<<<148 * 4, 256, 0, st>>>(A.wsv, A.off, M, nn, v_out, ldv, cell_out, perm_out);
+    k_copy_dead<<<148 * 4, 256, 0, st>>>(A, nn);
 
     MomConst mc{p.weight, p.cell_volume, p.cell_volume_arr, p.mass / p.charge};
     double* cellsum = at<double>(workspace, L.o_cellsum);
     mark(ev, 4, st);
-    k_finalize_cells<<<(M + 255) / 256, 256, 0, st>>>(A.cnt, A.off, A.chunk_off, A.recs, A.small_recs, A.wsv, M,
-                                                      mc, moments_out, cellsum);
-    if (diag_out)
-        k_finalize_diag<<<1, 1024, 0, st>>>(A.cnt, cellsum, M, at<double>(workspace, L.o_tilesum), L.T, diag_out);
+    k_finalize_cells<<<(M + 255) / 256, 256, 0, st>>>(A.cnt, A.chunk_off, A.recs, A.small_recs, A.cellref, M, mc,
+                                                      moments_out, cellsum);
+    if (diag_out) k_finalize_diag<<<1, 1024, 0, st>>>(A.cnt, cellsum, M, diag_out);
     mark(ev, 5, st);
     return launch_ok();
 }
@@ -1076,7 +1167,7 @@ int cc_bin(const int32_t* cell_in, int64_t n, int32_t cells, int32_t* perm_out, 
     }
     // the velocity payload is irrelevant for the order: bin without one
     const int nn = static_cast<int>(n);
-    int rc = run_binning(nullptr, 0, cell_in, nn, cells, L, workspace, k, 0, 0, 0, st);
+    int rc = run_binning(nullptr, 0, cell_in, nn, cells, L, workspace, k, 0, 0, 0, st, nullptr, false);
     if (rc) return rc;
     k_extract_perm<<<(nn + 255) / 256, 256, 0, st>>>(at<double>(workspace, L.o_wsv), nn, perm_out);
     if (cudaMemcpyAsync(off_out, at<int32_t>(workspace, L.o_off), sizeof(int32_t) * (cells + 1),

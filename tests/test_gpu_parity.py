@@ -172,6 +172,23 @@ def test_collide_parity(O, n, M, dead, skew):
     check_collide(O, w, step=17)
 
 
+@pytest.mark.parametrize("n,M,dead", [(50_000, 64, 0.0), (80_000, 300, 0.05), (10_000, 5000, 0.1)])
+def test_sorted_input_fast_path(O, n, M, dead):
+    """Cell-sorted input (dead last): k_scatter is skipped and the collide reads
+    the caller's SoA input directly; results must equal the oracle's."""
+    w = W.random_cells(n, M, seed=n + M + 1, dead_frac=dead, skew=True)
+    key = np.where(w.cell < 0, M, w.cell)
+    order = np.argsort(key, kind="stable")
+    w.v = np.ascontiguousarray(w.v[:, order])
+    w.cell = np.ascontiguousarray(w.cell[order])
+    check_collide(O, w, step=4)
+    # one element out of order: the full binning path runs instead
+    if n > 10:
+        w.cell = w.cell.copy()
+        w.cell[[1, n // 2]] = w.cell[[n // 2, 1]]
+        check_collide(O, w, step=4)
+
+
 def test_c1_chained_ten_steps(O):
     """Config 1 (1 cell, 1,000 e-, Maxwellian 2 eV, 10 steps): each step's GPU
     output feeds the next GPU step, same for the oracle; parity every step."""

@@ -15,3 +15,10 @@ for w in $WHAT; do
     full) timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_collide_large|k_scatter|k_count|k_scan" -s 4 -c 4 -o gpurun_out/${TAG}_prof python bench.py --steps 1 --warmup 1 --no-cpu-baseline --e2e-steps 1 > gpurun_out/${TAG}_prof.log 2>&1; echo full rc=$? ;;
   esac
 done
+# extra targets
+for w in $WHAT; do
+  case $w in
+    prof_scatter) timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_scatter" -s 1 -c 1 -o gpurun_out/${TAG}_scatter python bench.py --steps 1 --warmup 1 --no-cpu-baseline --e2e-steps 1 > gpurun_out/${TAG}_scatter.log 2>&1; echo prof_scatter rc=$? ;;
+    prof_collide) timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_collide_large" -s 1 -c 1 -o gpurun_out/${TAG}_collide python bench.py --steps 1 --warmup 1 --no-cpu-baseline --e2e-steps 1 > gpurun_out/${TAG}_collide.log 2>&1; echo prof_collide rc=$? ;;
+  esac
+done
