@@ -153,6 +153,18 @@ int cc_ta_pairs(double *va, double *vb, const double *C, const double *u1,
 int cc_moments(const double *v, int64_t ldv, const int32_t *off, int32_t cells,
                const cc_params *params, double *out, void *stream);
 
+/* Multi-GPU migration: out[p] = in[idx[p]] for p < m, for the
+ * velocities [3][ldv] -> [3][ldo] and the cell ids; live cell ids are shifted
+ * by -cell_shift (global -> local), dead (-1) stay -1.  No aliasing.         */
+int cc_gather(const double *v, int64_t ldv, const int32_t *cell, const int32_t *idx, int64_t m,
+              int32_t cell_shift, double *v_out, int64_t ldo, int32_t *cell_out, void *stream);
+
+/* Multi-GPU: owner rank of each particle's global cell under the contiguous
+ * cell-range split bounds [P+1] (DEVICE, bounds[r] = first cell of rank r);
+ * -1 for dead or out-of-range ids.                                           */
+int cc_owner(const int32_t *cell, int64_t n, const int32_t *bounds, int32_t nranks,
+             int32_t *owner_out, void *stream);
+
 /* Multi-GPU: rank-ascending sum of P gathered diagnostics vectors
  * gathered [P][16] -> out [16] (deterministic for a given P).   */
 int cc_diag_sum_ranks(const double *gathered, int32_t nranks, double *out, void *stream);

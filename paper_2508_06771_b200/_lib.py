@@ -28,7 +28,7 @@ STAGE_NAMES = ("count", "scan", "scatter", "collide", "finalize")
 # every symbol include/coulomb.h declares
 EXPORTS = ("cc_default_params", "cc_workspace_bytes", "coulomb_collide", "cc_device_status",
            "cc_strerror", "cc_bin", "cc_pairs", "cc_philox", "cc_ppnd16", "cc_ta_pairs",
-           "cc_moments", "cc_diag_sum_ranks")
+           "cc_moments", "cc_gather", "cc_owner", "cc_diag_sum_ranks")
 
 
 class CCParams(C.Structure):
@@ -82,6 +82,10 @@ def load():
     L.cc_ta_pairs.restype = C.c_int
     L.cc_moments.argtypes = [vp, i64, vp, i32, C.POINTER(CCParams), vp, vp]
     L.cc_moments.restype = C.c_int
+    L.cc_gather.argtypes = [vp, i64, vp, vp, i64, i32, vp, i64, vp, vp]
+    L.cc_gather.restype = C.c_int
+    L.cc_owner.argtypes = [vp, i64, vp, i32, vp, vp]
+    L.cc_owner.restype = C.c_int
     L.cc_diag_sum_ranks.argtypes = [vp, i32, vp, vp]
     L.cc_diag_sum_ranks.restype = C.c_int
     _lib = L

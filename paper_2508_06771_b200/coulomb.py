@@ -240,6 +240,33 @@ def cc_moments(v: torch.Tensor, off: torch.Tensor, cells: int, **params) -> torc
     return out
 
 
+def cc_gather(v: torch.Tensor, cell: torch.Tensor, idx: torch.Tensor, cell_shift: int = 0):
+    """(v[:, idx], cell[idx] - cell_shift (dead stay -1)) on the device (migration pack)."""
+    dev = cell.device
+    ldv = _soa(v, "v", dev)
+    _need(cell, "cell", torch.int32, dev)
+    _need(idx, "idx", torch.int32, dev)
+    m = idx.numel()
+    vo = torch.empty((3, m), dtype=torch.float64, device=dev)
+    co = torch.empty(m, dtype=torch.int32, device=dev)
+    rc = _lib.load().cc_gather(_ptr(v), max(ldv, 1), _ptr(cell), _ptr(idx.contiguous()), m, cell_shift,
+                               _ptr(vo), max(m, 1), _ptr(co), C.c_void_p(_stream(dev)))
+    check(rc, "cc_gather")
+    return vo, co
+
+
+def cc_owner(cell_global: torch.Tensor, bounds) -> torch.Tensor:
+    """Owner rank of each particle's global cell (-1 dead / out of range)."""
+    dev = cell_global.device
+    _need(cell_global, "cell", torch.int32, dev)
+    b = torch.as_tensor(list(bounds), dtype=torch.int32, device=dev)
+    out = torch.empty_like(cell_global)
+    rc = _lib.load().cc_owner(_ptr(cell_global), cell_global.numel(), _ptr(b), b.numel() - 1, _ptr(out),
+                              C.c_void_p(_stream(dev)))
+    check(rc, "cc_owner")
+    return out
+
+
 def cc_diag_sum_ranks(gathered: torch.Tensor) -> torch.Tensor:
     dev = gathered.device
     _need(gathered, "gathered", torch.float64, dev)

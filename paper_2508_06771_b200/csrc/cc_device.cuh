@@ -67,19 +67,36 @@ __device__ __forceinline__ double rsqrt_nr(double x)
 // tails, so a kernel can evaluate the tails of a whole warp's items together.
 __device__ __forceinline__ bool ppnd16_is_central(double p) { return fabs(p - 0.5) <= 0.425; }
 
+// AS241 coefficients (Wichura 1988, PPND16), highest degree first, in constant
+// memory so polynomial evaluation reads them as uniform operands.
+__constant__ double kAS241[6][8] = {
+    {2.5090809287301226727e+3, 3.3430575583588128105e+4, 6.7265770927008700853e+4, 4.5921953931549871457e+4,
+     1.3731693765509461125e+4, 1.9715909503065514427e+3, 1.3314166789178437745e+2, 3.3871328727963666080e+0},
+    {5.2264952788528545610e+3, 2.8729085735721942674e+4, 3.9307895800092710610e+4, 2.1213794301586595867e+4,
+     5.3941960214247511077e+3, 6.8718700749205790830e+2, 4.2313330701600911252e+1, 1.0},
+    {7.7454501427834140764e-4, 2.2723844989269184583e-2, 2.4178072517745061177e-1, 1.2704582524523683826e+0,
+     3.6478483247632046050e+0, 5.7694972214606914055e+0, 4.6303378461565452959e+0, 1.4234371107496835773e+0},
+    {1.0507500716444168432e-9, 5.4759380849953449460e-4, 1.5198666563616457197e-2, 1.4810397642748007459e-1,
+     6.8976733498510000455e-1, 1.6763848301838038494e+0, 2.0531916266377588219e+0, 1.0},
+    {2.0103343992922881327e-7, 2.7115555687434875782e-5, 1.2426609473880784386e-3, 2.6532189526576123093e-2,
+     2.9656057182850489123e-1, 1.7848265399172913358e+0, 5.4637849111641143699e+0, 6.6579046435011037772e+0},
+    {2.0442631033899397856e-15, 1.4215117583164458887e-7, 1.8463183175100546818e-5, 7.8686913114561325910e-4,
+     1.4875361290850614852e-2, 1.3692988092273580531e-1, 5.9983220655588793769e-1, 1.0}};
+
+// Horner evaluation of the degree-7 polynomial kAS241[row] at r.
+__device__ __forceinline__ double as241_poly(int row, double r)
+{
+    double s = kAS241[row][0];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) s = s * r + kAS241[row][i];
+    return s;
+}
+
 __device__ __forceinline__ double ppnd16_central(double p)
 {
     const double q = p - 0.5;
     const double r = 0.180625 - q * q;
-    const double num = (((((((2.5090809287301226727e+3 * r + 3.3430575583588128105e+4) * r +
-                             6.7265770927008700853e+4) * r + 4.5921953931549871457e+4) * r +
-                           1.3731693765509461125e+4) * r + 1.9715909503065514427e+3) * r +
-                         1.3314166789178437745e+2) * r + 3.3871328727963666080e+0) * q;
-    const double den = (((((((5.2264952788528545610e+3 * r + 2.8729085735721942674e+4) * r +
-                             3.9307895800092710610e+4) * r + 2.1213794301586595867e+4) * r +
-                           5.3941960214247511077e+3) * r + 6.8718700749205790830e+2) * r +
-                         4.2313330701600911252e+1) * r + 1.0);
-    return num * rcp_nr(den);
+    return as241_poly(0, r) * q * rcp_nr(as241_poly(1, r));
 }
 
 // Tail argument: the smaller tail mass min(p, 1-p), negative for p < 1/2.
@@ -88,29 +105,10 @@ __device__ __forceinline__ double ppnd16_tail_arg(double p) { return (p < 0.5) ?
 __device__ __forceinline__ double ppnd16_tail(double targ)
 {
     double r = sqrt(-log(fabs(targ)));
-    double num, den;
-    if (r <= 5.0) {
-        r -= 1.6;
-        num = (((((((7.7454501427834140764e-4 * r + 2.2723844989269184583e-2) * r +
-                    2.4178072517745061177e-1) * r + 1.2704582524523683826e+0) * r +
-                  3.6478483247632046050e+0) * r + 5.7694972214606914055e+0) * r +
-                4.6303378461565452959e+0) * r + 1.4234371107496835773e+0);
-        den = (((((((1.0507500716444168432e-9 * r + 5.4759380849953449460e-4) * r +
-                    1.5198666563616457197e-2) * r + 1.4810397642748007459e-1) * r +
-                  6.8976733498510000455e-1) * r + 1.6763848301838038494e+0) * r +
-                2.0531916266377588219e+0) * r + 1.0);
-    } else {
-        r -= 5.0;
-        num = (((((((2.0103343992922881327e-7 * r + 2.7115555687434875782e-5) * r +
-                    1.2426609473880784386e-3) * r + 2.6532189526576123093e-2) * r +
-                  2.9656057182850489123e-1) * r + 1.7848265399172913358e+0) * r +
-                5.4637849111641143699e+0) * r + 6.6579046435011037772e+0);
-        den = (((((((2.0442631033899397856e-15 * r + 1.4215117583164458887e-7) * r +
-                    1.8463183175100546818e-5) * r + 7.8686913114561325910e-4) * r +
-                  1.4875361290850614852e-2) * r + 1.3692988092273580531e-1) * r +
-                5.9983220655588793769e-1) * r + 1.0);
-    }
-    const double x = num * rcp_nr(den);
+    const bool near = r <= 5.0;
+    r -= near ? 1.6 : 5.0;
+    const int row = near ? 2 : 4;
+    const double x = as241_poly(row, r) * rcp_nr(as241_poly(row + 1, r));
     return (targ < 0.0) ? -x : x;
 }
 

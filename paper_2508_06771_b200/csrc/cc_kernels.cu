@@ -21,6 +21,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <algorithm>
 #include <cstring>
 
 #include "../../include/coulomb.h"
@@ -286,18 +287,49 @@ __device__ __forceinline__ uint32_t warp_counter_add(uint32_t* words, int32_t b,
     return (atomicAdd(words + (b >> 1), add << sh) >> sh) & 0xFFFFu;
 }
 
+template <bool HAS_V>
+__device__ __forceinline__ void load_batch(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__ cell,
+                                           int64_t i, double& x, double& y, double& z, int32_t& c)
+{
+    c = __ldg(cell + i);
+    if (HAS_V) { x = __ldg(v + i); y = __ldg(v + ldv + i); z = __ldg(v + 2 * ldv + i); }
+    else { x = y = z = 0.0; }
+}
+
+template <bool HAS_V>
 __global__ void __launch_bounds__(32 * kMaxScatterWarps)
 k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__ cell, int n, int M,
           int W, const int32_t* __restrict__ tbase, const int32_t* __restrict__ off,
           double* __restrict__ wsv, const int32_t* __restrict__ flags)
 {
     extern __shared__ __align__(16) unsigned char smem[];
-    if (flags && flags[1] == 0) return;   // input already cell-sorted: the stable order is the identity
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (flags && flags[1] == 0) {
+        // input already cell-sorted: the stable order is the identity, so the
+        // records are written in place (a streaming SoA -> 32-byte-record pack)
+        const int64_t t0 = static_cast<int64_t>(blockIdx.x) * W * kSub;
+        const int64_t t1 = min(t0 + static_cast<int64_t>(W) * kSub, static_cast<int64_t>(n));
+        for (int64_t i0 = t0 + static_cast<int64_t>(w) * 32 * kScatterUnrollB; i0 < t1;
+             i0 += static_cast<int64_t>(W) * 32 * kScatterUnrollB) {
+            double x[kScatterUnrollB], y[kScatterUnrollB], z[kScatterUnrollB];
+            int32_t c[kScatterUnrollB];
+#pragma unroll
+            for (int u = 0; u < kScatterUnrollB; ++u)
+                load_batch<HAS_V>(v, ldv, cell, min(i0 + 32 * u + lane, t1 - 1), x[u], y[u], z[u], c[u]);
+#pragma unroll
+            for (int u = 0; u < kScatterUnrollB; ++u) {
+                const int64_t i = i0 + 32 * u + lane;
+                if (i < t1)
+                    st256(wsv + 4 * i, x[u], y[u], z[u],
+                          pack_pc(static_cast<int32_t>(i), (c[u] >= 0 && c[u] < M) ? c[u] : -1));
+            }
+        }
+        return;
+    }
     const int M1 = M + 1;
     const int MW = (M1 + 1) / 2;           // 32-bit words per warp row
     int32_t* base = reinterpret_cast<int32_t*>(smem);                       // [M1]
     uint32_t* wcnt = reinterpret_cast<uint32_t*>(smem + sizeof(int32_t) * M1);  // [W][MW] packed u16 pairs
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < W * MW; i += blockDim.x) wcnt[i] = 0u;
     __syncthreads();
 
@@ -306,15 +338,14 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
     uint32_t* my = wcnt + w * MW;
     const uint32_t lt = (1u << lane) - 1u;
 
-    // pass A: per-warp counts of the sub-range
+    // pass A: per-warp counts of the sub-range (loads batched, branch-free)
     for (int64_t i0 = s0; i0 < s1; i0 += 32 * kScatterUnrollA) {
         int32_t key[kScatterUnrollA];
 #pragma unroll
         for (int u = 0; u < kScatterUnrollA; ++u) {
             const int64_t i = i0 + 32 * u + lane;
-            const bool valid = i < s1;
-            const int32_t c = valid ? __ldg(cell + i) : 0;
-            key[u] = !valid ? -1 - lane : ((c >= 0 && c < M) ? c : M);
+            const int32_t c = __ldg(cell + min(i, s1 - 1));
+            key[u] = (i >= s1) ? -1 - lane : ((c >= 0 && c < M) ? c : M);
         }
 #pragma unroll
         for (int u = 0; u < kScatterUnrollA; ++u) {
@@ -341,29 +372,29 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
     }
     __syncthreads();
 
-    // pass B: ranks, destinations, 32-byte records
+    // pass B: ranks, destinations, 32-byte records (loads batched, branch-free)
     for (int64_t i0 = s0; i0 < s1; i0 += 32 * kScatterUnrollB) {
         int32_t key[kScatterUnrollB];
         double x[kScatterUnrollB], y[kScatterUnrollB], z[kScatterUnrollB];
 #pragma unroll
         for (int u = 0; u < kScatterUnrollB; ++u) {
             const int64_t i = i0 + 32 * u + lane;
-            const bool valid = i < s1;
-            const int32_t c = valid ? __ldg(cell + i) : 0;
-            key[u] = !valid ? -1 - lane : ((c >= 0 && c < M) ? c : M);
-            x[u] = y[u] = z[u] = 0.0;
-            if (valid && v) { x[u] = __ldg(v + i); y[u] = __ldg(v + ldv + i); z[u] = __ldg(v + 2 * ldv + i); }
+            int32_t c;
+            load_batch<HAS_V>(v, ldv, cell, min(i, s1 - 1), x[u], y[u], z[u], c);
+            key[u] = (i >= s1) ? -1 - lane : ((c >= 0 && c < M) ? c : M);
         }
+        uint32_t peers[kScatterUnrollB];
+#pragma unroll
+        for (int u = 0; u < kScatterUnrollB; ++u) peers[u] = __match_any_sync(0xFFFFFFFFu, key[u]);
 #pragma unroll
         for (int u = 0; u < kScatterUnrollB; ++u) {
             const int32_t b = key[u];
-            const uint32_t peers = __match_any_sync(0xFFFFFFFFu, b);
-            const int leader = __ffs(peers) - 1;
+            const int leader = __ffs(peers[u]) - 1;
             uint32_t old = 0;
-            if (b >= 0 && lane == leader) old = warp_counter_add(my, b, static_cast<uint32_t>(__popc(peers)));
+            if (b >= 0 && lane == leader) old = warp_counter_add(my, b, static_cast<uint32_t>(__popc(peers[u])));
             old = __shfl_sync(0xFFFFFFFFu, old, leader);
             if (b >= 0) {
-                const int32_t dest = base[b] + static_cast<int32_t>(old) + __popc(peers & lt);
+                const int32_t dest = base[b] + static_cast<int32_t>(old) + __popc(peers[u] & lt);
                 const int64_t i = i0 + 32 * u + lane;
                 st256(wsv + 4 * static_cast<int64_t>(dest), x[u], y[u], z[u],
                       pack_pc(static_cast<int32_t>(i), b < M ? b : -1));
@@ -375,9 +406,7 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
 // ------------------------------------------------------------------ CCS4 + CCS5 items
 struct CollideArgs {
     const double* wsv;          // cell-sorted 32-byte records (cold input)
-    const double* v_in;         // the caller's SoA input (read directly when it is already sorted)
-    int64_t ldv;                // row stride of v_in and v_out
-    const int32_t* flags;       // flags[1] == 0: input cell-sorted
+    int64_t ldv;                // row stride of v_out
     const int32_t* cnt;
     const int32_t* off;
     const int32_t* chunk_off;
@@ -419,17 +448,11 @@ struct Rec {
     double x, y, z, w;     // w = (perm, cell) bit pattern
 };
 
-// Stable slot s of the current call: a 32-byte record of ws_v (cold) or the
-// caller's SoA input at index s (sorted input: slot = input index).
-__device__ __forceinline__ Rec load_slot(const CollideArgs& A, bool sorted, int64_t s)
+// Stable slot s of the current call: its 32-byte record in ws_v.
+__device__ __forceinline__ Rec load_slot(const CollideArgs& A, int64_t s)
 {
     Rec r;
-    if (sorted) {
-        r.x = A.v_in[s]; r.y = A.v_in[A.ldv + s]; r.z = A.v_in[2 * A.ldv + s];
-        r.w = pack_pc(static_cast<int32_t>(s), 0);
-    } else {
-        ld256(A.wsv + 4 * s, r.x, r.y, r.z, r.w);
-    }
+    ld256(A.wsv + 4 * s, r.x, r.y, r.z, r.w);
     return r;
 }
 
@@ -470,7 +493,6 @@ k_collide_small(CollideArgs A)
     if (j >= A.M) return;
     const int32_t N = A.cnt[j];
     if (N == 0 || N > cc::kSmallCell) return;
-    const bool sorted = A.flags[1] == 0;
     const int32_t o = A.off[j];
     const uint32_t G = A.cell_base + static_cast<uint32_t>(j);
     cc::small_cell_perm(static_cast<uint32_t>(N), G, A.step, A.s0, A.s1, lane, pi_sm[w]);
@@ -481,10 +503,10 @@ k_collide_small(CollideArgs A)
     const uint32_t k = static_cast<uint32_t>(lane);
     if (k < items) {
         const int32_t pa = o + 2 * static_cast<int32_t>(k);
-        Rec a = load_slot(A, sorted, o + pi_sm[w][2 * k]);
+        Rec a = load_slot(A, o + pi_sm[w][2 * k]);
         acc.pre(a.x, a.y, a.z);
         if (2 * k + 1 < static_cast<uint32_t>(N)) {
-            Rec b = load_slot(A, sorted, o + pi_sm[w][2 * k + 1]);
+            Rec b = load_slot(A, o + pi_sm[w][2 * k + 1]);
             acc.pre(b.x, b.y, b.z);
             double u1, u2;
             pair_uniforms(A, j, k, u1, u2);
@@ -524,30 +546,17 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem_src) : "memory");
 }
 
-__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src)
-{
-    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem_src) : "memory");
-}
-
 __device__ __forceinline__ void cp_async_wait_all()
 {
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
 }
 
-// Gather stable slot s into a 32-byte shared-memory record.
-__device__ __forceinline__ void stage_slot(const CollideArgs& A, bool sorted, int64_t s, double* dst)
+// Gather stable slot s's 32-byte record into shared memory.
+__device__ __forceinline__ void stage_slot(const CollideArgs& A, int64_t s, double* dst)
 {
-    if (sorted) {
-        cp_async8(dst, A.v_in + s);
-        cp_async8(dst + 1, A.v_in + A.ldv + s);
-        cp_async8(dst + 2, A.v_in + 2 * A.ldv + s);
-        dst[3] = pack_pc(static_cast<int32_t>(s), 0);
-    } else {
-        const double* g = A.wsv + 4 * s;
-        cp_async16(dst, g);
-        cp_async16(dst + 2, g + 2);
-    }
+    const double* g = A.wsv + 4 * s;
+    cp_async16(dst, g);
+    cp_async16(dst + 2, g + 2);
 }
 
 // N_j > 64: one CTA per cell-aligned chunk of kChunk items, two phases:
@@ -559,7 +568,7 @@ __device__ __forceinline__ void stage_slot(const CollideArgs& A, bool sorted, in
 //     across the warp and evaluated once per 32 tails, then TA (CCS5), and the
 //     pair-ordered, coalesced SoA output plus the moment partials.
 constexpr int kItemsPerThread = kChunk / kCollideThreads;
-constexpr int kItemsPerRound = 2;
+constexpr int kItemsPerRound = 4;
 constexpr int kTailQueue = 32 * kItemsPerRound;
 constexpr size_t kCollideSmem = 2ull * kChunk * 4 * sizeof(double);
 
@@ -586,7 +595,6 @@ k_collide_large(CollideArgs A)
     __syncthreads();
     const int j = s_j;
     if (j < 0) return;
-    const bool sorted = A.flags[1] == 0;
     const int32_t N = A.cnt[j], o = A.off[j];
     const uint32_t items = static_cast<uint32_t>(N + 1) / 2;
     const uint32_t i0 = static_cast<uint32_t>(c - A.chunk_off[j]) * kChunk;
@@ -598,15 +606,15 @@ k_collide_large(CollideArgs A)
             const uint32_t k = i0 + threadIdx.x + q * kCollideThreads;
             if (k < i1) {
                 const uint32_t e = k - i0;
-                stage_slot(A, sorted, o + static_cast<int64_t>(cc::feistel_pi(f, 2 * k)), stage + 4 * e);
+                stage_slot(A, o + static_cast<int64_t>(cc::feistel_pi(f, 2 * k)), stage + 4 * e);
                 if (2 * k + 1 < static_cast<uint32_t>(N))
-                    stage_slot(A, sorted, o + static_cast<int64_t>(cc::feistel_pi(f, 2 * k + 1)),
+                    stage_slot(A, o + static_cast<int64_t>(cc::feistel_pi(f, 2 * k + 1)),
                                stage + 4 * (kChunk + e));
             }
         }
     }
     // shift for the moment partials: pre-collision v of the cell's first stable slot
-    const Rec ref = load_slot(A, sorted, o);
+    const Rec ref = load_slot(A, o);
     if (i0 == 0 && threadIdx.x == 0) {
         double* cr = A.cellref + 4 * static_cast<int64_t>(j);
         cr[0] = ref.x; cr[1] = ref.y; cr[2] = ref.z; cr[3] = 0.0;
@@ -686,10 +694,9 @@ k_collide_large(CollideArgs A)
 __global__ void k_copy_dead(CollideArgs A, int n)
 {
     const int32_t L = A.off[A.M];
-    const bool sorted = A.flags[1] == 0;
     for (int64_t p = L + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < n;
          p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const Rec r = load_slot(A, sorted, p);
+        const Rec r = load_slot(A, p);
         write_out(A, static_cast<int32_t>(p), -1, r);
     }
 }
@@ -926,6 +933,40 @@ k_moments(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
     }
 }
 
+__global__ void k_gather(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__ cell,
+                         const int32_t* __restrict__ idx, int64_t m, int32_t shift, double* __restrict__ vo,
+                         int64_t ldo, int32_t* __restrict__ co)
+{
+    for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < m;
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = idx[p];
+        vo[p] = v[i];
+        vo[ldo + p] = v[ldv + i];
+        vo[2 * ldo + p] = v[2 * ldv + i];
+        const int32_t c = cell[i];
+        co[p] = (c >= 0) ? c - shift : -1;
+    }
+}
+
+__global__ void k_owner(const int32_t* __restrict__ cell, int64_t n, const int32_t* __restrict__ bounds, int P,
+                        int32_t* __restrict__ owner)
+{
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int32_t c = cell[i];
+        int32_t r = -1;
+        if (c >= bounds[0] && c < bounds[P]) {
+            int lo = 0, hi = P;       // bounds[lo] <= c < bounds[hi]
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (bounds[mid] <= c) lo = mid; else hi = mid;
+            }
+            r = lo;
+        }
+        owner[i] = r;
+    }
+}
+
 __global__ void k_diag_sum_ranks(const double* __restrict__ g, int P, double* __restrict__ out)
 {
     const int q = threadIdx.x;
@@ -985,7 +1026,8 @@ int run_binning(const double* v_in, int64_t ldv, const int32_t* cell_in, int n, 
     const int M1 = M + 1;
     const size_t smem = sizeof(int32_t) * M1 + sizeof(uint32_t) * static_cast<size_t>(L.W) * ((M1 + 1) / 2);
     int rc = want_smem(k_count, sizeof(int32_t) * M1);
-    if (!rc) rc = want_smem(k_scatter, smem);
+    if (!rc) rc = want_smem(k_scatter<true>, smem);
+    if (!rc) rc = want_smem(k_scatter<false>, smem);
     if (rc) return rc;
     mark(ev, 0, st);
     k_count<<<L.T, kCountThreads, sizeof(int32_t) * M1, st>>>(cell_in, n, M, L.tile, tcount, err);
@@ -994,8 +1036,12 @@ int run_binning(const double* v_in, int64_t ldv, const int32_t* cell_in, int n, 
     k_scan_cells<<<1, 1024, 0, st>>>(cnt, M, off, chunk_off, Cj, keys, k, cell_base, step,
                                      static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
     mark(ev, 2, st);
-    k_scatter<<<L.T, 32 * L.W, smem, st>>>(v_in, ldv, cell_in, n, M, L.W, tcount, off, wsv,
-                                           allow_sorted_skip ? err : nullptr);
+    if (v_in)
+        k_scatter<true><<<L.T, 32 * L.W, smem, st>>>(v_in, ldv, cell_in, n, M, L.W, tcount, off, wsv,
+                                                     allow_sorted_skip ? err : nullptr);
+    else
+        k_scatter<false><<<L.T, 32 * L.W, smem, st>>>(nullptr, 0, cell_in, n, M, L.W, tcount, off, wsv,
+                                                      allow_sorted_skip ? err : nullptr);
     return launch_ok();
 }
 
@@ -1097,8 +1143,6 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
 
     CollideArgs A;
     A.wsv = at<double>(workspace, L.o_wsv);
-    A.v_in = v_in;
-    A.flags = at<int32_t>(workspace, L.o_err);
     A.cellref = at<double>(workspace, L.o_ref);
     A.cnt = at<int32_t>(workspace, L.o_cnt);
     A.off = at<int32_t>(workspace, L.o_off);
@@ -1227,6 +1271,30 @@ int cc_moments(const double* v, int64_t ldv, const int32_t* off, int32_t cells, 
     if (params) p = *params; else cc_default_params(&p);
     MomConst mc{p.weight, p.cell_volume, p.cell_volume_arr, p.mass / p.charge};
     k_moments<<<cells, 256, 0, static_cast<cudaStream_t>(stream)>>>(v, ldv, off, cells, mc, out);
+    return launch_ok();
+}
+
+int cc_gather(const double* v, int64_t ldv, const int32_t* cell, const int32_t* idx, int64_t m, int32_t cell_shift,
+              double* v_out, int64_t ldo, int32_t* cell_out, void* stream)
+{
+    cudaGetLastError();   // launch errors below are ours, not a stale earlier one
+    if (m < 0 || ldo < m) return CC_EINVAL;
+    if (m == 0) return CC_OK;
+    if (!v || !cell || !idx || !v_out || !cell_out) return CC_EINVAL;
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>((m + 255) / 256, 148 * 16));
+    k_gather<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(v, ldv, cell, idx, m, cell_shift, v_out, ldo,
+                                                                   cell_out);
+    return launch_ok();
+}
+
+int cc_owner(const int32_t* cell, int64_t n, const int32_t* bounds, int32_t nranks, int32_t* owner_out, void* stream)
+{
+    cudaGetLastError();   // launch errors below are ours, not a stale earlier one
+    if (n < 0 || nranks < 1) return CC_EINVAL;
+    if (n == 0) return CC_OK;
+    if (!cell || !bounds || !owner_out) return CC_EINVAL;
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 16));
+    k_owner<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(cell, n, bounds, nranks, owner_out);
     return launch_ok();
 }
 

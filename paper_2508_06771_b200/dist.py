@@ -1,0 +1,143 @@
+"""Multi-GPU layer: cell-range sharding, diagnostics reduction, particle migration.
+
+SURVEY §8(e).  Cells never interact in this operator ("we only consider
+collisions between two particles in the same grid cell"), so the
+global grid is split into contiguous cell ranges, one per rank, and every
+particle lives on the rank that owns its cell.  ``coulomb_collide`` then runs
+locally with ``cell_base`` = the rank's first global cell: the random streams
+are keyed by the global cell id, so each shard reproduces the single-GPU
+result on the same particles (the hard form of the paper's "nearly identical
+regardless of how many MPI processes").  Unlike the paper's
+replicated-grid scheme (one O(M) MPI_AllReduce per step) the data
+path has no collective; NCCL carries only
+
+  * the 16-double diagnostics vector: all_gather + a rank-ascending sum on the
+    device (deterministic for a given world size), and
+  * particle migration when a pusher moves particles across shard boundaries:
+    a stable partition by owner rank (the binning kernels with key = owner),
+    an all_to_all of the counts, and an all_to_all of the packed particles;
+    arrivals are appended in source-rank order, so results stay deterministic.
+
+The communication/plan logic here is device-agnostic (it runs on CPU tensors
+with the gloo backend in the tests); the per-particle work (partition, pack,
+ordered sum) is done by the CUDA kernels behind ``ops`` — the tests inject
+CPU stand-ins for those, the product path always uses the CUDA ones.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, Optional
+
+import torch
+import torch.distributed as dist
+
+
+def shard_cells(global_cells: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous balanced cell range of `rank`: (cell_base, local_cells)."""
+    if world < 1 or not (0 <= rank < world) or global_cells < world:
+        raise ValueError("need 0 <= rank < world <= global_cells")
+    q, r = divmod(global_cells, world)
+    base = rank * q + min(rank, r)
+    return base, q + (1 if rank < r else 0)
+
+
+def owner_bounds(global_cells: int, world: int) -> list[int]:
+    """bounds[r] = first global cell of rank r; bounds[world] = global_cells."""
+    return [shard_cells(global_cells, world, r)[0] for r in range(world)] + [global_cells]
+
+
+@dataclass
+class DistOps:
+    """Per-particle kernels the layer needs (CUDA by default)."""
+    partition: Callable   # (key int32 [n], nkeys) -> (perm int32 [n], off int32 [nkeys+1]), stable
+    gather: Callable      # (v [3][n], cell [n], perm [n], cell_shift) -> (v [3][n], cell [n]) permuted
+    sum_ranks: Callable   # (gathered [P][16]) -> [16] rank-ascending sum
+    owner: Callable       # (cell_global int32 [n], bounds list) -> owner rank int32 [n]; dead (-1) -> -1
+
+
+def cuda_ops() -> DistOps:
+    from . import coulomb as cc
+
+    def partition(key, nkeys):
+        return cc.cc_bin(key, nkeys)
+
+    def gather(v, cell, perm, cell_shift):
+        return cc.cc_gather(v, cell, perm, cell_shift)
+
+    def owner(cell_global, bounds):
+        return cc.cc_owner(cell_global, bounds)
+
+    return DistOps(partition=partition, gather=gather, sum_ranks=cc.cc_diag_sum_ranks, owner=owner)
+
+
+def reduce_diag(diag: torch.Tensor, ops: DistOps, group=None) -> torch.Tensor:
+    """All-gather every rank's 16-double diagnostics and sum them in rank order."""
+    world = dist.get_world_size(group)
+    flat = torch.empty(world * diag.numel(), dtype=diag.dtype, device=diag.device)
+    dist.all_gather_into_tensor(flat, diag.contiguous().view(-1), group=group)
+    return ops.sum_ranks(flat.view(world, diag.numel()))
+
+
+@dataclass
+class Migrated:
+    v: torch.Tensor        # [3][n_new] fp64
+    cell: torch.Tensor     # [n_new] int32, LOCAL cell ids of the receiving rank (-1 dead)
+    sent: list             # particles sent to each rank (incl. self)
+    received: list         # particles received from each rank (incl. self)
+
+
+def migrate(v: torch.Tensor, cell_global: torch.Tensor, global_cells: int, ops: DistOps,
+            group=None, keep_dead: bool = False) -> Migrated:
+    """Move every particle to the rank owning its (global) cell.
+
+    1. owner rank of every particle (dead particles: dropped unless keep_dead,
+       then they stay on this rank);
+    2. stable partition by owner (key = owner rank; the binning kernels);
+    3. all_to_all of the per-destination counts;
+    4. pack (gather in partition order) and all_to_all of velocities and cells;
+    5. arrivals concatenated in source-rank order; global -> local cell ids.
+    """
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    bounds = owner_bounds(global_cells, world)
+    dev = v.device
+    own = ops.owner(cell_global, bounds)
+    # dead particles: key `world` (dropped) or own rank (kept)
+    key = torch.where(own < 0, torch.full_like(own, rank if keep_dead else world), own)
+    perm, off = ops.partition(key.to(torch.int32), world + 1)
+    off_l = [int(x) for x in off.cpu().tolist()]
+    send = [off_l[r + 1] - off_l[r] for r in range(world)]
+    n_send = off_l[world]
+    send_t = torch.tensor(send, dtype=torch.int64, device=dev)
+    recv_t = torch.empty(world, dtype=torch.int64, device=dev)
+    dist.all_to_all_single(recv_t, send_t, group=group)
+    recv = [int(x) for x in recv_t.cpu().tolist()]
+    pv, pc = ops.gather(v, cell_global, perm[:n_send], 0)
+    n_recv = sum(recv)
+    rv = torch.empty((3, n_recv), dtype=v.dtype, device=dev)
+    for c in range(3):
+        dist.all_to_all_single(rv[c], pv[c].contiguous(), output_split_sizes=recv, input_split_sizes=send,
+                               group=group)
+    rc = torch.empty(n_recv, dtype=torch.int32, device=dev)
+    dist.all_to_all_single(rc, pc.contiguous(), output_split_sizes=recv, input_split_sizes=send, group=group)
+    base = bounds[rank]
+    ident = torch.arange(n_recv, dtype=torch.int32, device=dev)
+    lv, lc = ops.gather(rv, rc, ident, base)
+    return Migrated(lv, lc, send, recv)
+
+
+def init_from_env(backend: Optional[str] = None):
+    """torchrun environment -> (rank, world, local_rank), process group initialised."""
+    import os
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        if backend is None:
+            backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    return rank, world, local
