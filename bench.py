@@ -220,11 +220,11 @@ def run_reference(args):
 
 def run_ours(args):
     import torch
-    rank, world, local = dist_env()
+    from paper_2508_06771_b200 import dist as ccd
+    rank, world, local = ccd.init_from_env("nccl")
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist_ops = ccd.cuda_ops()
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
 
@@ -245,7 +245,6 @@ def run_ours(args):
                      torch.empty(n, dtype=torch.int32, device=dev),
                      torch.empty((M, 7), dtype=torch.float64, device=dev),
                      torch.empty(16, dtype=torch.float64, device=dev))
-    gathered = torch.empty((world, 16), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     def one_step(s, events=None):
@@ -266,9 +265,7 @@ def run_ours(args):
                                  C.c_void_p(stream.cuda_stream))
         _lib.check(rc, "coulomb_collide")
         if world > 1:
-            import torch.distributed as dist
-            dist.all_gather_into_tensor(gathered, out.diag)
-            cc.cc_diag_sum_ranks(gathered)
+            ccd.reduce_diag(out.diag, dist_ops)      # NCCL all_gather + rank-ordered device sum
 
     # warm-up
     for s in range(args.warmup):

@@ -281,10 +281,22 @@ k_scan_cells(const int32_t* __restrict__ cnt, int M, int32_t* __restrict__ off,
 // with one shared-memory atomic and broadcasts the old value to the group, so
 // successive groups never wait on each other.  Loads are issued in batches
 // (kScatterUnrollA / B per lane) to keep several KB per warp in flight.
-__device__ __forceinline__ uint32_t warp_counter_add(uint32_t* words, int32_t b, uint32_t add)
+// Predicated shared-memory atomics (no branch, so a batch of them issues
+// back to back; same-address atomics of one warp execute in program order).
+__device__ __forceinline__ uint32_t atom_add_if(bool pred, uint32_t* addr, uint32_t val)
 {
-    const uint32_t sh = (static_cast<uint32_t>(b) & 1u) << 4;
-    return (atomicAdd(words + (b >> 1), add << sh) >> sh) & 0xFFFFu;
+    uint32_t old = 0;
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(addr));
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p atom.shared.add.u32 %0, [%1], %3;\n\t}"
+                 : "+r"(old) : "r"(a), "r"(static_cast<unsigned>(pred)), "r"(val) : "memory");
+    return old;
+}
+
+__device__ __forceinline__ void red_add_if(bool pred, uint32_t* addr, uint32_t val)
+{
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(addr));
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p red.shared.add.u32 [%0], %2;\n\t}"
+                 :: "r"(a), "r"(static_cast<unsigned>(pred)), "r"(val) : "memory");
 }
 
 template <bool HAS_V>
@@ -347,11 +359,14 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
             const int32_t c = __ldg(cell + min(i, s1 - 1));
             key[u] = (i >= s1) ? -1 - lane : ((c >= 0 && c < M) ? c : M);
         }
+        uint32_t peers[kScatterUnrollA];
+#pragma unroll
+        for (int u = 0; u < kScatterUnrollA; ++u) peers[u] = __match_any_sync(0xFFFFFFFFu, key[u]);
 #pragma unroll
         for (int u = 0; u < kScatterUnrollA; ++u) {
-            const uint32_t peers = __match_any_sync(0xFFFFFFFFu, key[u]);
-            if (key[u] >= 0 && lane == __ffs(peers) - 1)
-                atomicAdd(my + (key[u] >> 1), static_cast<uint32_t>(__popc(peers)) << ((key[u] & 1) << 4));
+            const int32_t b = max(key[u], 0);
+            red_add_if(key[u] >= 0 && lane == __ffs(peers[u]) - 1, my + (b >> 1),
+                       static_cast<uint32_t>(__popc(peers[u])) << ((b & 1) << 4));
         }
     }
     __syncthreads();
@@ -383,18 +398,22 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
             load_batch<HAS_V>(v, ldv, cell, min(i, s1 - 1), x[u], y[u], z[u], c);
             key[u] = (i >= s1) ? -1 - lane : ((c >= 0 && c < M) ? c : M);
         }
-        uint32_t peers[kScatterUnrollB];
+        uint32_t peers[kScatterUnrollB], old[kScatterUnrollB];
 #pragma unroll
         for (int u = 0; u < kScatterUnrollB; ++u) peers[u] = __match_any_sync(0xFFFFFFFFu, key[u]);
 #pragma unroll
         for (int u = 0; u < kScatterUnrollB; ++u) {
+            const int32_t b = max(key[u], 0);
+            old[u] = atom_add_if(key[u] >= 0 && lane == __ffs(peers[u]) - 1, my + (b >> 1),
+                                 static_cast<uint32_t>(__popc(peers[u])) << ((b & 1) << 4));
+        }
+#pragma unroll
+        for (int u = 0; u < kScatterUnrollB; ++u) {
             const int32_t b = key[u];
-            const int leader = __ffs(peers[u]) - 1;
-            uint32_t old = 0;
-            if (b >= 0 && lane == leader) old = warp_counter_add(my, b, static_cast<uint32_t>(__popc(peers[u])));
-            old = __shfl_sync(0xFFFFFFFFu, old, leader);
+            const uint32_t o = __shfl_sync(0xFFFFFFFFu, (old[u] >> ((max(b, 0) & 1) << 4)) & 0xFFFFu,
+                                           __ffs(peers[u]) - 1);
             if (b >= 0) {
-                const int32_t dest = base[b] + static_cast<int32_t>(old) + __popc(peers[u] & lt);
+                const int32_t dest = base[b] + static_cast<int32_t>(o) + __popc(peers[u] & lt);
                 const int64_t i = i0 + 32 * u + lane;
                 st256(wsv + 4 * static_cast<int64_t>(dest), x[u], y[u], z[u],
                       pack_pc(static_cast<int32_t>(i), b < M ? b : -1));

@@ -1,0 +1,72 @@
+"""GPU tests of the multi-GPU layer's CUDA kernels (cc_owner, cc_gather, the
+rank-ordered diag sum) and of migrate()/reduce_diag() through a 1-rank NCCL
+group (a real NCCL communicator on the one GPU a gpurun box gives us)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import torch.distributed as dist  # noqa: E402
+
+import paper_2508_06771_b200 as cc  # noqa: E402
+from paper_2508_06771_b200 import dist as ccd  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def test_owner_matches_searchsorted():
+    rng = np.random.default_rng(1)
+    bounds = [0, 4096, 8192, 12288, 16384]
+    cell = rng.integers(-2, 17000, 100_000).astype(np.int32)
+    got = cc.cc_owner(torch.from_numpy(cell).to(DEV), bounds).cpu().numpy()
+    b = np.asarray(bounds)
+    exp = np.searchsorted(b, cell, side="right") - 1
+    exp[(cell < 0) | (cell >= b[-1])] = -1
+    assert np.array_equal(got, exp)
+
+
+def test_gather_matches_numpy():
+    rng = np.random.default_rng(2)
+    n = 50_000
+    v = rng.standard_normal((3, n))
+    cell = rng.integers(-1, 100, n).astype(np.int32)
+    idx = rng.permutation(n)[: n // 2].astype(np.int32)
+    gv, gc = cc.cc_gather(torch.from_numpy(v).to(DEV), torch.from_numpy(cell).to(DEV),
+                          torch.from_numpy(idx).to(DEV), 10)
+    assert np.array_equal(gv.cpu().numpy(), v[:, idx])
+    c = cell[idx]
+    assert np.array_equal(gc.cpu().numpy(), np.where(c >= 0, c - 10, -1))
+
+
+@pytest.fixture(scope="module")
+def nccl1():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=DEV)
+    yield
+    dist.destroy_process_group()
+
+
+def test_reduce_diag_and_migrate_one_rank(nccl1):
+    ops = ccd.cuda_ops()
+    d = torch.arange(16, dtype=torch.float64, device=DEV)
+    assert torch.equal(ccd.reduce_diag(d, ops), d)
+    rng = np.random.default_rng(3)
+    n = 20_000
+    v = rng.standard_normal((3, n))
+    cell = rng.integers(-1, 64, n).astype(np.int32)
+    m = ccd.migrate(torch.from_numpy(v).to(DEV), torch.from_numpy(cell).to(DEV), 64, ops)
+    live = cell >= 0
+    assert np.array_equal(m.v.cpu().numpy(), v[:, live])
+    assert np.array_equal(m.cell.cpu().numpy(), cell[live])
+    assert m.sent == [int(live.sum())] and m.received == [int(live.sum())]
