@@ -6,10 +6,10 @@
 //   k_scan_tiles   CCS2, part 1: per cell, exclusive scan over tiles
 //   k_scan_cells   CCS2, part 2: off[] (cell offsets), chunk_off[], per-cell
 //                  TA constant C_j (R5/R6/R7) and Feistel keys (R1, R3)
-//   k_scatter      CCS3 as a STABLE counting sort: per-warp
-//                  sub-ranges, match.any ranks, no global atomics; writes the
-//                  particle as one 32-byte record {vx, vy, vz, (perm, cell)}
-//                  into the cell-sorted workspace array ws_v
+//   k_rank         CCS3 as a STABLE counting sort, part 1: per-warp
+//                  sub-ranges, match.any ranks, no global atomics -> dest[i]
+//   k_move         CCS3 part 2: streams each particle into its 32-byte record
+//                  {vx, vy, vz, perm} at dest[i] of the cell-sorted array ws_v
 //   k_collide_small  N_j <= 64: one warp per cell; pi_j by sort-by-key (R1)
 //   k_collide_large  N_j > 64: cell-aligned chunks of pairs; pi_j by keyed
 //                  Feistel (R1); CCS4 Philox per pair; CCS5 TA update; output
@@ -30,14 +30,17 @@
 namespace {
 
 constexpr int kCountThreads = 256;
-constexpr int kSub = 4096;               // elements per warp sub-range in k_scatter
-constexpr int kScatterUnrollA = 16;      // cell loads in flight per lane, counting pass
-constexpr int kScatterUnrollB = 8;       // (cell, v) loads in flight per lane, scatter pass
+constexpr int kSub = 4096;               // elements per warp sub-range in k_rank
+constexpr int kRankUnroll = 16;          // cell loads in flight per lane in k_rank
+constexpr int kMoveBlocks = 148 * 8;     // k_move: fixed grid (deterministic per-block sums)
+constexpr int kMoveThreads = 256;
+constexpr int kMoveUnroll = 4;
 constexpr int kCollideThreads = 256;
 constexpr int kChunk = 1024;             // items (pairs or sitter) per k_collide_large CTA
-constexpr int kRec = 12;                 // chunk moment record: S1' (3), S2' (3), pre sum v (3), pre sum |v|^2, pad
-constexpr int kSmallRec = 16;            // small-cell record: as kRec + the shift (the cell's exact mean)
-constexpr int kCellSum = 8;              // per-cell raw sums: pre v (3), pre |v|^2, post v (3), post |v|^2
+constexpr int kRec = 8;                  // chunk moment record: S1' (3), S2' (3), pad
+constexpr int kSmallRec = 12;            // small-cell record: S1', S2' about the exact mean, the mean (3), pad
+constexpr int kCellSum = 4;              // per-cell raw post-collision sums: v (3), |v|^2
+constexpr int kTileSum = 4;              // per-tile raw pre-collision sums of live particles: v (3), |v|^2
 constexpr int kScatterSmemBudget = 96 * 1024;   // per-warp counters of one CTA
 constexpr int kMaxScatterWarps = 12;
 static_assert(kMaxScatterWarps * kSub <= 65536, "per-warp 16-bit cell counters must hold a whole tile");
@@ -47,7 +50,7 @@ struct Layout {
     int W = 1, tile = kSub, T = 0;
     int64_t max_chunks = 0;
     size_t o_err = 0, o_tcount = 0, o_cnt = 0, o_off = 0, o_chunk = 0, o_C = 0, o_keys = 0;
-    size_t o_small = 0, o_recs = 0, o_cellsum = 0, o_ref = 0, o_wsv = 0, total = 0;
+    size_t o_small = 0, o_recs = 0, o_cellsum = 0, o_ref = 0, o_tilesum = 0, o_chunkcell = 0, o_dest = 0, o_wsv = 0, total = 0;
 };
 
 size_t align256(size_t x) { return (x + 255u) & ~static_cast<size_t>(255u); }
@@ -79,6 +82,9 @@ Layout make_layout(int64_t n, int32_t M)
     L.o_recs = o;     o = align256(o + static_cast<size_t>(L.max_chunks) * kRec * sizeof(double));
     L.o_cellsum = o;  o = align256(o + static_cast<size_t>(M) * kCellSum * sizeof(double));
     L.o_ref = o;      o = align256(o + static_cast<size_t>(M) * 4 * sizeof(double));
+    L.o_tilesum = o;  o = align256(o + static_cast<size_t>(kMoveBlocks) * kTileSum * sizeof(double));
+    L.o_dest = o;     o = align256(o + static_cast<size_t>(n > 0 ? n : 1) * sizeof(int32_t));
+    L.o_chunkcell = o; o = align256(o + static_cast<size_t>(L.max_chunks) * sizeof(int32_t));
     L.o_wsv = o;      o = align256(o + static_cast<size_t>(n > 0 ? n : 1) * 4 * sizeof(double));
     L.total = o;
     return L;
@@ -115,7 +121,7 @@ __device__ __forceinline__ int32_t unpack_perm(double w)
 // flags[0]: sticky invalid-id flag; flags[1]: "input not cell-sorted" (cleared
 // by the host before each call).  Sorted means live ids non-decreasing in input
 // order with every dead/invalid particle after the last live one; then the
-// stable order is the identity and k_scatter is skipped.
+// stable order is the identity: k_rank is skipped and k_move copies in place.
 __global__ void __launch_bounds__(kCountThreads)
 k_count(const int32_t* __restrict__ cell, int n, int M, int tile, int32_t* __restrict__ tcount,
         int32_t* __restrict__ flags)
@@ -223,7 +229,8 @@ __device__ __forceinline__ int32_t n_chunks(int32_t N)
 // single CTA of 1024 threads
 __global__ void __launch_bounds__(1024)
 k_scan_cells(const int32_t* __restrict__ cnt, int M, int32_t* __restrict__ off,
-             int32_t* __restrict__ chunk_off, double* __restrict__ Cj, cc::U4* __restrict__ keys,
+             int32_t* __restrict__ chunk_off, int32_t* __restrict__ chunk_cell, double* __restrict__ Cj,
+             cc::U4* __restrict__ keys,
              CellConst cc_, uint32_t cell_base, uint32_t step, uint32_t s0, uint32_t s1)
 {
     __shared__ int32_t wsum_a[32], wsum_b[32];
@@ -263,6 +270,7 @@ k_scan_cells(const int32_t* __restrict__ cnt, int M, int32_t* __restrict__ off,
         off[j] = ra;
         chunk_off[j] = rb;
         ra += N;
+        for (int32_t q = 0; q < n_chunks(N); ++q) chunk_cell[rb + q] = j;
         rb += n_chunks(N);
         const double V = cc_.volume_arr ? cc_.volume_arr[j] : cc_.volume;
         const double lnL = cc_.ln_lambda_arr ? cc_.ln_lambda_arr[j] : cc_.ln_lambda;
@@ -299,45 +307,18 @@ __device__ __forceinline__ void red_add_if(bool pred, uint32_t* addr, uint32_t v
                  :: "r"(a), "r"(static_cast<unsigned>(pred)), "r"(val) : "memory");
 }
 
-template <bool HAS_V>
-__device__ __forceinline__ void load_batch(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__ cell,
-                                           int64_t i, double& x, double& y, double& z, int32_t& c)
-{
-    c = __ldg(cell + i);
-    if (HAS_V) { x = __ldg(v + i); y = __ldg(v + ldv + i); z = __ldg(v + 2 * ldv + i); }
-    else { x = y = z = 0.0; }
-}
-
-template <bool HAS_V>
+// Rank kernel: dest[i] = the stable slot of particle i (cell-major, input
+// order inside a cell, dead/invalid after the live ones).  Only cell ids are
+// touched here (4 B/particle, read twice); the 32-byte records are written by
+// the streaming k_move, so this latency-bound pass keeps little data in flight
+// per element and can run many warps.
 __global__ void __launch_bounds__(32 * kMaxScatterWarps)
-k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__ cell, int n, int M,
-          int W, const int32_t* __restrict__ tbase, const int32_t* __restrict__ off,
-          double* __restrict__ wsv, const int32_t* __restrict__ flags)
+k_rank(const int32_t* __restrict__ cell, int n, int M, int W, const int32_t* __restrict__ tbase,
+       const int32_t* __restrict__ off, int32_t* __restrict__ dest, const int32_t* __restrict__ flags)
 {
     extern __shared__ __align__(16) unsigned char smem[];
+    if (flags && flags[1] == 0) return;   // input already cell-sorted: dest = identity (k_move)
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    if (flags && flags[1] == 0) {
-        // input already cell-sorted: the stable order is the identity, so the
-        // records are written in place (a streaming SoA -> 32-byte-record pack)
-        const int64_t t0 = static_cast<int64_t>(blockIdx.x) * W * kSub;
-        const int64_t t1 = min(t0 + static_cast<int64_t>(W) * kSub, static_cast<int64_t>(n));
-        for (int64_t i0 = t0 + static_cast<int64_t>(w) * 32 * kScatterUnrollB; i0 < t1;
-             i0 += static_cast<int64_t>(W) * 32 * kScatterUnrollB) {
-            double x[kScatterUnrollB], y[kScatterUnrollB], z[kScatterUnrollB];
-            int32_t c[kScatterUnrollB];
-#pragma unroll
-            for (int u = 0; u < kScatterUnrollB; ++u)
-                load_batch<HAS_V>(v, ldv, cell, min(i0 + 32 * u + lane, t1 - 1), x[u], y[u], z[u], c[u]);
-#pragma unroll
-            for (int u = 0; u < kScatterUnrollB; ++u) {
-                const int64_t i = i0 + 32 * u + lane;
-                if (i < t1)
-                    st256(wsv + 4 * i, x[u], y[u], z[u],
-                          pack_pc(static_cast<int32_t>(i), (c[u] >= 0 && c[u] < M) ? c[u] : -1));
-            }
-        }
-        return;
-    }
     const int M1 = M + 1;
     const int MW = (M1 + 1) / 2;           // 32-bit words per warp row
     int32_t* base = reinterpret_cast<int32_t*>(smem);                       // [M1]
@@ -351,19 +332,19 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
     const uint32_t lt = (1u << lane) - 1u;
 
     // pass A: per-warp counts of the sub-range (loads batched, branch-free)
-    for (int64_t i0 = s0; i0 < s1; i0 += 32 * kScatterUnrollA) {
-        int32_t key[kScatterUnrollA];
+    for (int64_t i0 = s0; i0 < s1; i0 += 32 * kRankUnroll) {
+        int32_t key[kRankUnroll];
 #pragma unroll
-        for (int u = 0; u < kScatterUnrollA; ++u) {
+        for (int u = 0; u < kRankUnroll; ++u) {
             const int64_t i = i0 + 32 * u + lane;
             const int32_t c = __ldg(cell + min(i, s1 - 1));
             key[u] = (i >= s1) ? -1 - lane : ((c >= 0 && c < M) ? c : M);
         }
-        uint32_t peers[kScatterUnrollA];
+        uint32_t peers[kRankUnroll];
 #pragma unroll
-        for (int u = 0; u < kScatterUnrollA; ++u) peers[u] = __match_any_sync(0xFFFFFFFFu, key[u]);
+        for (int u = 0; u < kRankUnroll; ++u) peers[u] = __match_any_sync(0xFFFFFFFFu, key[u]);
 #pragma unroll
-        for (int u = 0; u < kScatterUnrollA; ++u) {
+        for (int u = 0; u < kRankUnroll; ++u) {
             const int32_t b = max(key[u], 0);
             red_add_if(key[u] >= 0 && lane == __ffs(peers[u]) - 1, my + (b >> 1),
                        static_cast<uint32_t>(__popc(peers[u])) << ((b & 1) << 4));
@@ -387,38 +368,87 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
     }
     __syncthreads();
 
-    // pass B: ranks, destinations, 32-byte records (loads batched, branch-free)
-    for (int64_t i0 = s0; i0 < s1; i0 += 32 * kScatterUnrollB) {
-        int32_t key[kScatterUnrollB];
-        double x[kScatterUnrollB], y[kScatterUnrollB], z[kScatterUnrollB];
+    // pass B: ranks -> destinations
+    for (int64_t i0 = s0; i0 < s1; i0 += 32 * kRankUnroll) {
+        int32_t key[kRankUnroll];
 #pragma unroll
-        for (int u = 0; u < kScatterUnrollB; ++u) {
+        for (int u = 0; u < kRankUnroll; ++u) {
             const int64_t i = i0 + 32 * u + lane;
-            int32_t c;
-            load_batch<HAS_V>(v, ldv, cell, min(i, s1 - 1), x[u], y[u], z[u], c);
+            const int32_t c = __ldg(cell + min(i, s1 - 1));
             key[u] = (i >= s1) ? -1 - lane : ((c >= 0 && c < M) ? c : M);
         }
-        uint32_t peers[kScatterUnrollB], old[kScatterUnrollB];
+        uint32_t peers[kRankUnroll], old[kRankUnroll];
 #pragma unroll
-        for (int u = 0; u < kScatterUnrollB; ++u) peers[u] = __match_any_sync(0xFFFFFFFFu, key[u]);
+        for (int u = 0; u < kRankUnroll; ++u) peers[u] = __match_any_sync(0xFFFFFFFFu, key[u]);
 #pragma unroll
-        for (int u = 0; u < kScatterUnrollB; ++u) {
+        for (int u = 0; u < kRankUnroll; ++u) {
             const int32_t b = max(key[u], 0);
             old[u] = atom_add_if(key[u] >= 0 && lane == __ffs(peers[u]) - 1, my + (b >> 1),
                                  static_cast<uint32_t>(__popc(peers[u])) << ((b & 1) << 4));
         }
 #pragma unroll
-        for (int u = 0; u < kScatterUnrollB; ++u) {
+        for (int u = 0; u < kRankUnroll; ++u) {
             const int32_t b = key[u];
             const uint32_t o = __shfl_sync(0xFFFFFFFFu, (old[u] >> ((max(b, 0) & 1) << 4)) & 0xFFFFu,
                                            __ffs(peers[u]) - 1);
-            if (b >= 0) {
-                const int32_t dest = base[b] + static_cast<int32_t>(o) + __popc(peers[u] & lt);
-                const int64_t i = i0 + 32 * u + lane;
-                st256(wsv + 4 * static_cast<int64_t>(dest), x[u], y[u], z[u],
-                      pack_pc(static_cast<int32_t>(i), b < M ? b : -1));
+            const int64_t i = i0 + 32 * u + lane;
+            if (b >= 0) dest[i] = base[b] + static_cast<int32_t>(o) + __popc(peers[u] & lt);
+        }
+    }
+}
+
+// Move kernel: streams the particles into their 32-byte records
+// ws_v[dest[i]] = {vx, vy, vz, perm = i}; identity when the input is sorted.
+// Fixed grid-stride partition, so the per-block pre-collision sums of the live
+// particles (dest < L) are deterministic.
+
+template <bool HAS_V>
+__global__ void __launch_bounds__(kMoveThreads)
+k_move(const double* __restrict__ v, int64_t ldv, int n, const int32_t* __restrict__ dest,
+       const int32_t* __restrict__ off, int M, double* __restrict__ wsv, const int32_t* __restrict__ flags,
+       double* __restrict__ blocksum)
+{
+    __shared__ double red[kMoveThreads / 32][kTileSum];
+    const bool sorted = flags && flags[1] == 0;
+    const int32_t L = off[M];
+    double pre[kTileSum] = {0.0, 0.0, 0.0, 0.0};
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * kMoveThreads * kMoveUnroll;
+    for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * kMoveThreads * kMoveUnroll + threadIdx.x; i0 < n;
+         i0 += stride) {
+        double x[kMoveUnroll], y[kMoveUnroll], z[kMoveUnroll];
+        int32_t d[kMoveUnroll];
+#pragma unroll
+        for (int u = 0; u < kMoveUnroll; ++u) {
+            const int64_t i = min(i0 + static_cast<int64_t>(u) * kMoveThreads, static_cast<int64_t>(n) - 1);
+            d[u] = sorted ? static_cast<int32_t>(i) : __ldg(dest + i);
+            if (HAS_V) { x[u] = __ldg(v + i); y[u] = __ldg(v + ldv + i); z[u] = __ldg(v + 2 * ldv + i); }
+            else { x[u] = y[u] = z[u] = 0.0; }
+        }
+#pragma unroll
+        for (int u = 0; u < kMoveUnroll; ++u) {
+            const int64_t i = i0 + static_cast<int64_t>(u) * kMoveThreads;
+            if (i < n) {
+                st256(wsv + 4 * static_cast<int64_t>(d[u]), x[u], y[u], z[u], pack_pc(static_cast<int32_t>(i), 0));
+                if (d[u] < L) {
+                    pre[0] += x[u]; pre[1] += y[u]; pre[2] += z[u];
+                    pre[3] = fma(x[u], x[u], fma(y[u], y[u], fma(z[u], z[u], pre[3])));
+                }
             }
         }
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < kTileSum; ++q)
+#pragma unroll
+        for (int dd = 16; dd > 0; dd >>= 1) pre[q] += __shfl_down_sync(0xFFFFFFFFu, pre[q], dd);
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < kTileSum; ++q) red[w][q] = pre[q];
+    __syncthreads();
+    if (threadIdx.x < kTileSum && blocksum) {
+        double a = 0.0;
+        for (int ww = 0; ww < kMoveThreads / 32; ++ww) a += red[ww][threadIdx.x];
+        blocksum[static_cast<int64_t>(blockIdx.x) * kTileSum + threadIdx.x] = a;
     }
 }
 
@@ -429,6 +459,7 @@ struct CollideArgs {
     const int32_t* cnt;
     const int32_t* off;
     const int32_t* chunk_off;
+    const int32_t* chunk_cell;  // [max_chunks] cell of each chunk (valid below chunk_off[M])
     const double* Cj;
     const cc::U4* keys;
     double* v_out;
@@ -441,25 +472,21 @@ struct CollideArgs {
     uint32_t cell_base, step, s0, s1;
 };
 
-// Moment accumulator: [0..2] sum (v - r) post, [3..5] sum (v - r)^2 post,
-// [6..8] sum v pre, [9] sum |v|^2 pre.
+// Post-collision moment accumulator about a per-cell shift r:
+// [0..2] sum (v - r), [3..5] sum (v - r)^2.  (Pre-collision sums come from
+// k_move, which holds every particle in registers anyway.)
 struct Acc {
-    double a[10];
+    double a[6];
     __device__ void zero()
     {
 #pragma unroll
-        for (int q = 0; q < 10; ++q) a[q] = 0.0;
+        for (int q = 0; q < 6; ++q) a[q] = 0.0;
     }
     __device__ void post(double x, double y, double z, double rx, double ry, double rz)
     {
         const double dx = x - rx, dy = y - ry, dz = z - rz;
         a[0] += dx; a[1] += dy; a[2] += dz;
         a[3] = fma(dx, dx, a[3]); a[4] = fma(dy, dy, a[4]); a[5] = fma(dz, dz, a[5]);
-    }
-    __device__ void pre(double x, double y, double z)
-    {
-        a[6] += x; a[7] += y; a[8] += z;
-        a[9] = fma(x, x, fma(y, y, fma(z, z, a[9])));
     }
 };
 
@@ -523,10 +550,8 @@ k_collide_small(CollideArgs A)
     if (k < items) {
         const int32_t pa = o + 2 * static_cast<int32_t>(k);
         Rec a = load_slot(A, o + pi_sm[w][2 * k]);
-        acc.pre(a.x, a.y, a.z);
         if (2 * k + 1 < static_cast<uint32_t>(N)) {
             Rec b = load_slot(A, o + pi_sm[w][2 * k + 1]);
-            acc.pre(b.x, b.y, b.z);
             double u1, u2;
             pair_uniforms(A, j, k, u1, u2);
             cc::ta_update(a.x, a.y, a.z, b.x, b.y, b.z, C, u1, u2);
@@ -552,10 +577,8 @@ k_collide_small(CollideArgs A)
         double* r = A.small_recs + static_cast<int64_t>(j) * kSmallRec;
 #pragma unroll
         for (int c = 0; c < 6; ++c) r[c] = q.a[c];
-#pragma unroll
-        for (int c = 6; c < 10; ++c) r[c] = acc.a[c];
-        r[10] = mx; r[11] = my; r[12] = mz;
-        r[13] = r[14] = r[15] = 0.0;
+        r[6] = mx; r[7] = my; r[8] = mz;
+        r[9] = r[10] = r[11] = 0.0;
     }
 }
 
@@ -595,25 +618,11 @@ __global__ void __launch_bounds__(kCollideThreads, 3)
 k_collide_large(CollideArgs A)
 {
     extern __shared__ __align__(16) double stage[];       // [2][kChunk][4]
-    __shared__ int32_t s_j;
     __shared__ double tailq[kCollideThreads / 32][kTailQueue];
-    __shared__ double red[kCollideThreads / 32][10];
+    __shared__ double red[kCollideThreads / 32][6];
     const int c = blockIdx.x;
-    if (threadIdx.x == 0) {
-        int lo = 0, hi = A.M;   // invariant: chunk_off[lo] <= c < chunk_off[hi] when c < total
-        if (c >= A.chunk_off[A.M]) {
-            s_j = -1;
-        } else {
-            while (hi - lo > 1) {
-                const int mid = (lo + hi) >> 1;
-                if (A.chunk_off[mid] <= c) lo = mid; else hi = mid;
-            }
-            s_j = lo;
-        }
-    }
-    __syncthreads();
-    const int j = s_j;
-    if (j < 0) return;
+    if (c >= A.chunk_off[A.M]) return;      // grid is an upper bound on the chunk count
+    const int j = A.chunk_cell[c];
     const int32_t N = A.cnt[j], o = A.off[j];
     const uint32_t items = static_cast<uint32_t>(N + 1) / 2;
     const uint32_t i0 = static_cast<uint32_t>(c - A.chunk_off[j]) * kChunk;
@@ -678,12 +687,10 @@ k_collide_large(CollideArgs A)
                 const double2 a01 = *reinterpret_cast<const double2*>(stage + 4 * e);
                 const double2 a23 = *reinterpret_cast<const double2*>(stage + 4 * e + 2);
                 Rec a{a01.x, a01.y, a23.x, a23.y};
-                acc.pre(a.x, a.y, a.z);
                 if (2 * k + 1 < static_cast<uint32_t>(N)) {
                     const double2 b01 = *reinterpret_cast<const double2*>(stage + 4 * (kChunk + e));
                     const double2 b23 = *reinterpret_cast<const double2*>(stage + 4 * (kChunk + e) + 2);
                     Rec b{b01.x, b01.y, b23.x, b23.y};
-                    acc.pre(b.x, b.y, b.z);
                     const double zz = (tpos[t] >= 0) ? q_w[tpos[t]] : z[t];
                     cc::ta_update_z(a.x, a.y, a.z, b.x, b.y, b.z, C, zz, u2[t]);
                     write_out(A, pa + 1, j, b);
@@ -698,11 +705,11 @@ k_collide_large(CollideArgs A)
     warp_reduce(acc.a);
     if (lane == 0)
 #pragma unroll
-        for (int q = 0; q < 10; ++q) red[w][q] = acc.a[q];
+        for (int q = 0; q < 6; ++q) red[w][q] = acc.a[q];
     __syncthreads();
     if (threadIdx.x < kRec) {
         double sum = 0.0;
-        if (threadIdx.x < 10)
+        if (threadIdx.x < 6)
 #pragma unroll
             for (int ww = 0; ww < kCollideThreads / 32; ++ww) sum += red[ww][threadIdx.x];
         A.recs[static_cast<int64_t>(c) * kRec + threadIdx.x] = sum;
@@ -750,22 +757,20 @@ __global__ void k_finalize_cells(const int32_t* __restrict__ cnt, const int32_t*
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= M) return;
     const int32_t N = cnt[j];
-    double s[10];
-#pragma unroll
-    for (int q = 0; q < 10; ++q) s[q] = 0.0;
+    double s[6] = {0, 0, 0, 0, 0, 0};
     double rx = 0, ry = 0, rz = 0;
     if (N > 0) {
         if (N <= cc::kSmallCell) {
             const double* r = small_recs + static_cast<int64_t>(j) * kSmallRec;
 #pragma unroll
-            for (int q = 0; q < 10; ++q) s[q] = r[q];
-            rx = r[10]; ry = r[11]; rz = r[12];
+            for (int q = 0; q < 6; ++q) s[q] = r[q];
+            rx = r[6]; ry = r[7]; rz = r[8];
         } else {
             const double* cr = cellref + 4 * static_cast<int64_t>(j);
             rx = cr[0]; ry = cr[1]; rz = cr[2];
             for (int32_t c = chunk_off[j]; c < chunk_off[j + 1]; ++c)
 #pragma unroll
-                for (int q = 0; q < 10; ++q) s[q] += recs[static_cast<int64_t>(c) * kRec + q];
+                for (int q = 0; q < 6; ++q) s[q] += recs[static_cast<int64_t>(c) * kRec + q];
         }
     }
     if (moments_out) {
@@ -782,21 +787,19 @@ __global__ void k_finalize_cells(const int32_t* __restrict__ cnt, const int32_t*
     const double Nd = static_cast<double>(N);
     const double r[3] = {rx, ry, rz};
     double* cs = cellsum + static_cast<int64_t>(j) * kCellSum;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) cs[q] = s[6 + q];
     double e = 0.0;
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-        cs[4 + q] = fma(Nd, r[q], s[q]);
+        cs[q] = fma(Nd, r[q], s[q]);
         e += s[3 + q] + 2.0 * r[q] * s[q] + Nd * r[q] * r[q];
     }
-    cs[7] = e;
+    cs[3] = e;
 }
 
-// single CTA of 1024 threads: fixed-order reductions over cells
+// single CTA of 1024 threads: fixed-order reductions over cells and tiles
 __global__ void __launch_bounds__(1024)
 k_finalize_diag(const int32_t* __restrict__ cnt, const double* __restrict__ cellsum, int M,
-                double* __restrict__ diag)
+                const double* __restrict__ tilesum, int T, double* __restrict__ diag)
 {
     __shared__ double red[32][12];
     double s[12];
@@ -808,8 +811,11 @@ k_finalize_diag(const int32_t* __restrict__ cnt, const double* __restrict__ cell
         s[1] += N / 2;
         s[2] += N & 1;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) s[3 + q] += cellsum[static_cast<int64_t>(j) * kCellSum + q];
+        for (int q = 0; q < 4; ++q) s[7 + q] += cellsum[static_cast<int64_t>(j) * kCellSum + q];
     }
+    for (int t = threadIdx.x; t < T; t += blockDim.x)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) s[3 + q] += tilesum[static_cast<int64_t>(t) * kTileSum + q];
     if (threadIdx.x == 0) s[11] = cnt[M];
 #pragma unroll
     for (int q = 0; q < 12; ++q)
@@ -1045,22 +1051,24 @@ int run_binning(const double* v_in, int64_t ldv, const int32_t* cell_in, int n, 
     const int M1 = M + 1;
     const size_t smem = sizeof(int32_t) * M1 + sizeof(uint32_t) * static_cast<size_t>(L.W) * ((M1 + 1) / 2);
     int rc = want_smem(k_count, sizeof(int32_t) * M1);
-    if (!rc) rc = want_smem(k_scatter<true>, smem);
-    if (!rc) rc = want_smem(k_scatter<false>, smem);
+    if (!rc) rc = want_smem(k_rank, smem);
     if (rc) return rc;
+    int32_t* dest = at<int32_t>(ws, L.o_dest);
+    const int32_t* skip = allow_sorted_skip ? err : nullptr;
     mark(ev, 0, st);
     k_count<<<L.T, kCountThreads, sizeof(int32_t) * M1, st>>>(cell_in, n, M, L.tile, tcount, err);
     mark(ev, 1, st);
     k_scan_tiles<<<(M1 + 31) / 32, dim3(32, kScanRows), 0, st>>>(tcount, L.T, M1, cnt);
-    k_scan_cells<<<1, 1024, 0, st>>>(cnt, M, off, chunk_off, Cj, keys, k, cell_base, step,
+    k_scan_cells<<<1, 1024, 0, st>>>(cnt, M, off, chunk_off, at<int32_t>(ws, L.o_chunkcell), Cj, keys, k,
+                                     cell_base, step,
                                      static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
     mark(ev, 2, st);
+    k_rank<<<L.T, 32 * L.W, smem, st>>>(cell_in, n, M, L.W, tcount, off, dest, skip);
     if (v_in)
-        k_scatter<true><<<L.T, 32 * L.W, smem, st>>>(v_in, ldv, cell_in, n, M, L.W, tcount, off, wsv,
-                                                     allow_sorted_skip ? err : nullptr);
+        k_move<true><<<kMoveBlocks, kMoveThreads, 0, st>>>(v_in, ldv, n, dest, off, M, wsv, skip,
+                                                           at<double>(ws, L.o_tilesum));
     else
-        k_scatter<false><<<L.T, 32 * L.W, smem, st>>>(nullptr, 0, cell_in, n, M, L.W, tcount, off, wsv,
-                                                      allow_sorted_skip ? err : nullptr);
+        k_move<false><<<kMoveBlocks, kMoveThreads, 0, st>>>(nullptr, 0, n, dest, off, M, wsv, skip, nullptr);
     return launch_ok();
 }
 
@@ -1166,6 +1174,7 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     A.cnt = at<int32_t>(workspace, L.o_cnt);
     A.off = at<int32_t>(workspace, L.o_off);
     A.chunk_off = at<int32_t>(workspace, L.o_chunk);
+    A.chunk_cell = at<int32_t>(workspace, L.o_chunkcell);
     A.Cj = at<double>(workspace, L.o_C);
     A.keys = at<cc::U4>(workspace, L.o_keys);
     A.v_out = v_out;
@@ -1192,7 +1201,9 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     mark(ev, 4, st);
     k_finalize_cells<<<(M + 255) / 256, 256, 0, st>>>(A.cnt, A.chunk_off, A.recs, A.small_recs, A.cellref, M, mc,
                                                       moments_out, cellsum);
-    if (diag_out) k_finalize_diag<<<1, 1024, 0, st>>>(A.cnt, cellsum, M, diag_out);
+    if (diag_out)
+        k_finalize_diag<<<1, 1024, 0, st>>>(A.cnt, cellsum, M, at<double>(workspace, L.o_tilesum), kMoveBlocks,
+                                            diag_out);
     mark(ev, 5, st);
     return launch_ok();
 }
