@@ -6,10 +6,10 @@
 //   k_scan_tiles   CCS2, part 1: per cell, exclusive scan over tiles
 //   k_scan_cells   CCS2, part 2: off[] (cell offsets), chunk_off[], per-cell
 //                  TA constant C_j (R5/R6/R7) and Feistel keys (R1, R3)
-//   k_rank         CCS3 as a STABLE counting sort, part 1: per-warp
-//                  sub-ranges, match.any ranks, no global atomics -> dest[i]
-//   k_move         CCS3 part 2: streams each particle into its 32-byte record
-//                  {vx, vy, vz, perm} at dest[i] of the cell-sorted array ws_v
+//   k_scatter      CCS3 as a STABLE counting sort: per-warp
+//                  sub-ranges, match.any ranks, no global atomics; writes the
+//                  particle as one 32-byte record {vx, vy, vz, (perm, cell)}
+//                  into the cell-sorted workspace array ws_v
 //   k_collide_small  N_j <= 64: one warp per cell; pi_j by sort-by-key (R1)
 //   k_collide_large  N_j > 64: cell-aligned chunks of pairs; pi_j by keyed
 //                  Feistel (R1); CCS4 Philox per pair; CCS5 TA update; output
@@ -30,11 +30,9 @@
 namespace {
 
 constexpr int kCountThreads = 256;
-constexpr int kSub = 4096;               // elements per warp sub-range in k_rank
-constexpr int kRankUnroll = 16;          // cell loads in flight per lane in k_rank
-constexpr int kMoveBlocks = 148 * 8;     // k_move: fixed grid (deterministic per-block sums)
-constexpr int kMoveThreads = 256;
-constexpr int kMoveUnroll = 4;
+constexpr int kSub = 4096;               // elements per warp sub-range in k_scatter
+constexpr int kScatterUnrollA = 16;      // cell loads in flight per lane, counting pass
+constexpr int kScatterUnrollB = 6;       // (cell, v) loads in flight per lane, scatter pass
 constexpr int kCollideThreads = 256;
 constexpr int kChunk = 1024;             // items (pairs or sitter) per k_collide_large CTA
 constexpr int kRec = 8;                  // chunk moment record: S1' (3), S2' (3), pad
@@ -50,7 +48,7 @@ struct Layout {
     int W = 1, tile = kSub, T = 0;
     int64_t max_chunks = 0;
     size_t o_err = 0, o_tcount = 0, o_cnt = 0, o_off = 0, o_chunk = 0, o_C = 0, o_keys = 0;
-    size_t o_small = 0, o_recs = 0, o_cellsum = 0, o_ref = 0, o_tilesum = 0, o_chunkcell = 0, o_dest = 0, o_wsv = 0, total = 0;
+    size_t o_small = 0, o_recs = 0, o_cellsum = 0, o_ref = 0, o_tilesum = 0, o_chunkcell = 0, o_wsv = 0, total = 0;
 };
 
 size_t align256(size_t x) { return (x + 255u) & ~static_cast<size_t>(255u); }
@@ -82,8 +80,7 @@ Layout make_layout(int64_t n, int32_t M)
     L.o_recs = o;     o = align256(o + static_cast<size_t>(L.max_chunks) * kRec * sizeof(double));
     L.o_cellsum = o;  o = align256(o + static_cast<size_t>(M) * kCellSum * sizeof(double));
     L.o_ref = o;      o = align256(o + static_cast<size_t>(M) * 4 * sizeof(double));
-    L.o_tilesum = o;  o = align256(o + static_cast<size_t>(kMoveBlocks) * kTileSum * sizeof(double));
-    L.o_dest = o;     o = align256(o + static_cast<size_t>(n > 0 ? n : 1) * sizeof(int32_t));
+    L.o_tilesum = o;  o = align256(o + static_cast<size_t>(L.T > 0 ? L.T : 1) * kTileSum * sizeof(double));
     L.o_chunkcell = o; o = align256(o + static_cast<size_t>(L.max_chunks) * sizeof(int32_t));
     L.o_wsv = o;      o = align256(o + static_cast<size_t>(n > 0 ? n : 1) * 4 * sizeof(double));
     L.total = o;
@@ -121,7 +118,7 @@ __device__ __forceinline__ int32_t unpack_perm(double w)
 // flags[0]: sticky invalid-id flag; flags[1]: "input not cell-sorted" (cleared
 // by the host before each call).  Sorted means live ids non-decreasing in input
 // order with every dead/invalid particle after the last live one; then the
-// stable order is the identity: k_rank is skipped and k_move copies in place.
+// stable order is the identity and k_scatter packs the records in place.
 __global__ void __launch_bounds__(kCountThreads)
 k_count(const int32_t* __restrict__ cell, int n, int M, int tile, int32_t* __restrict__ tcount,
         int32_t* __restrict__ flags)
@@ -307,18 +304,75 @@ __device__ __forceinline__ void red_add_if(bool pred, uint32_t* addr, uint32_t v
                  :: "r"(a), "r"(static_cast<unsigned>(pred)), "r"(val) : "memory");
 }
 
-// Rank kernel: dest[i] = the stable slot of particle i (cell-major, input
-// order inside a cell, dead/invalid after the live ones).  Only cell ids are
-// touched here (4 B/particle, read twice); the 32-byte records are written by
-// the streaming k_move, so this latency-bound pass keeps little data in flight
-// per element and can run many warps.
-__global__ void __launch_bounds__(32 * kMaxScatterWarps)
-k_rank(const int32_t* __restrict__ cell, int n, int M, int W, const int32_t* __restrict__ tbase,
-       const int32_t* __restrict__ off, int32_t* __restrict__ dest, const int32_t* __restrict__ flags)
+__device__ __forceinline__ void tile_pre_add(double (&pre)[kTileSum], double x, double y, double z)
+{
+    pre[0] += x; pre[1] += y; pre[2] += z;
+    pre[3] = fma(x, x, fma(y, y, fma(z, z, pre[3])));
+}
+
+// fixed-order block reduction of the per-thread pre-collision sums -> tilesum[tile]
+__device__ __forceinline__ void tile_pre_store(double (&pre)[kTileSum], double* tilesum, int W)
+{
+    __shared__ double red[kMaxScatterWarps][kTileSum];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < kTileSum; ++q)
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) pre[q] += __shfl_down_sync(0xFFFFFFFFu, pre[q], d);
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < kTileSum; ++q) red[w][q] = pre[q];
+    __syncthreads();
+    if (threadIdx.x < kTileSum) {
+        double a = 0.0;
+        for (int ww = 0; ww < W; ++ww) a += red[ww][threadIdx.x];
+        if (tilesum) tilesum[static_cast<int64_t>(blockIdx.x) * kTileSum + threadIdx.x] = a;
+    }
+}
+
+template <bool HAS_V>
+__device__ __forceinline__ void load_batch(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__ cell,
+                                           int64_t i, double& x, double& y, double& z, int32_t& c)
+{
+    c = __ldg(cell + i);
+    if (HAS_V) { x = __ldg(v + i); y = __ldg(v + ldv + i); z = __ldg(v + 2 * ldv + i); }
+    else { x = y = z = 0.0; }
+}
+
+template <bool HAS_V>
+__global__ void __launch_bounds__(32 * kMaxScatterWarps, 2)
+k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__ cell, int n, int M,
+          int W, const int32_t* __restrict__ tbase, const int32_t* __restrict__ off,
+          double* __restrict__ wsv, const int32_t* __restrict__ flags, double* __restrict__ tilesum)
 {
     extern __shared__ __align__(16) unsigned char smem[];
-    if (flags && flags[1] == 0) return;   // input already cell-sorted: dest = identity (k_move)
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double pre[kTileSum] = {0.0, 0.0, 0.0, 0.0};      // pre-collision sums of the tile's live particles
+    if (flags && flags[1] == 0) {
+        // input already cell-sorted: the stable order is the identity, so the
+        // records are written in place (a streaming SoA -> 32-byte-record pack)
+        const int64_t t0 = static_cast<int64_t>(blockIdx.x) * W * kSub;
+        const int64_t t1 = min(t0 + static_cast<int64_t>(W) * kSub, static_cast<int64_t>(n));
+        for (int64_t i0 = t0 + static_cast<int64_t>(w) * 32 * kScatterUnrollB; i0 < t1;
+             i0 += static_cast<int64_t>(W) * 32 * kScatterUnrollB) {
+            double x[kScatterUnrollB], y[kScatterUnrollB], z[kScatterUnrollB];
+            int32_t c[kScatterUnrollB];
+#pragma unroll
+            for (int u = 0; u < kScatterUnrollB; ++u)
+                load_batch<HAS_V>(v, ldv, cell, min(i0 + 32 * u + lane, t1 - 1), x[u], y[u], z[u], c[u]);
+#pragma unroll
+            for (int u = 0; u < kScatterUnrollB; ++u) {
+                const int64_t i = i0 + 32 * u + lane;
+                const bool live = c[u] >= 0 && c[u] < M;
+                if (i < t1) {
+                    st256(wsv + 4 * i, x[u], y[u], z[u], pack_pc(static_cast<int32_t>(i), live ? c[u] : -1));
+                    if (live) tile_pre_add(pre, x[u], y[u], z[u]);
+                }
+            }
+        }
+        tile_pre_store(pre, tilesum, W);
+        return;
+    }
     const int M1 = M + 1;
     const int MW = (M1 + 1) / 2;           // 32-bit words per warp row
     int32_t* base = reinterpret_cast<int32_t*>(smem);                       // [M1]
@@ -332,19 +386,19 @@ k_rank(const int32_t* __restrict__ cell, int n, int M, int W, const int32_t* __r
     const uint32_t lt = (1u << lane) - 1u;
 
     // pass A: per-warp counts of the sub-range (loads batched, branch-free)
-    for (int64_t i0 = s0; i0 < s1; i0 += 32 * kRankUnroll) {
-        int32_t key[kRankUnroll];
+    for (int64_t i0 = s0; i0 < s1; i0 += 32 * kScatterUnrollA) {
+        int32_t key[kScatterUnrollA];
 #pragma unroll
-        for (int u = 0; u < kRankUnroll; ++u) {
+        for (int u = 0; u < kScatterUnrollA; ++u) {
             const int64_t i = i0 + 32 * u + lane;
             const int32_t c = __ldg(cell + min(i, s1 - 1));
             key[u] = (i >= s1) ? -1 - lane : ((c >= 0 && c < M) ? c : M);
         }
-        uint32_t peers[kRankUnroll];
+        uint32_t peers[kScatterUnrollA];
 #pragma unroll
-        for (int u = 0; u < kRankUnroll; ++u) peers[u] = __match_any_sync(0xFFFFFFFFu, key[u]);
+        for (int u = 0; u < kScatterUnrollA; ++u) peers[u] = __match_any_sync(0xFFFFFFFFu, key[u]);
 #pragma unroll
-        for (int u = 0; u < kRankUnroll; ++u) {
+        for (int u = 0; u < kScatterUnrollA; ++u) {
             const int32_t b = max(key[u], 0);
             red_add_if(key[u] >= 0 && lane == __ffs(peers[u]) - 1, my + (b >> 1),
                        static_cast<uint32_t>(__popc(peers[u])) << ((b & 1) << 4));
@@ -368,88 +422,41 @@ k_rank(const int32_t* __restrict__ cell, int n, int M, int W, const int32_t* __r
     }
     __syncthreads();
 
-    // pass B: ranks -> destinations
-    for (int64_t i0 = s0; i0 < s1; i0 += 32 * kRankUnroll) {
-        int32_t key[kRankUnroll];
+    // pass B: ranks, destinations, 32-byte records (loads batched, branch-free)
+    for (int64_t i0 = s0; i0 < s1; i0 += 32 * kScatterUnrollB) {
+        int32_t key[kScatterUnrollB];
+        double x[kScatterUnrollB], y[kScatterUnrollB], z[kScatterUnrollB];
 #pragma unroll
-        for (int u = 0; u < kRankUnroll; ++u) {
+        for (int u = 0; u < kScatterUnrollB; ++u) {
             const int64_t i = i0 + 32 * u + lane;
-            const int32_t c = __ldg(cell + min(i, s1 - 1));
+            int32_t c;
+            load_batch<HAS_V>(v, ldv, cell, min(i, s1 - 1), x[u], y[u], z[u], c);
             key[u] = (i >= s1) ? -1 - lane : ((c >= 0 && c < M) ? c : M);
         }
-        uint32_t peers[kRankUnroll], old[kRankUnroll];
+        uint32_t peers[kScatterUnrollB], old[kScatterUnrollB];
 #pragma unroll
-        for (int u = 0; u < kRankUnroll; ++u) peers[u] = __match_any_sync(0xFFFFFFFFu, key[u]);
+        for (int u = 0; u < kScatterUnrollB; ++u) peers[u] = __match_any_sync(0xFFFFFFFFu, key[u]);
 #pragma unroll
-        for (int u = 0; u < kRankUnroll; ++u) {
+        for (int u = 0; u < kScatterUnrollB; ++u) {
             const int32_t b = max(key[u], 0);
             old[u] = atom_add_if(key[u] >= 0 && lane == __ffs(peers[u]) - 1, my + (b >> 1),
                                  static_cast<uint32_t>(__popc(peers[u])) << ((b & 1) << 4));
         }
 #pragma unroll
-        for (int u = 0; u < kRankUnroll; ++u) {
+        for (int u = 0; u < kScatterUnrollB; ++u) {
             const int32_t b = key[u];
             const uint32_t o = __shfl_sync(0xFFFFFFFFu, (old[u] >> ((max(b, 0) & 1) << 4)) & 0xFFFFu,
                                            __ffs(peers[u]) - 1);
-            const int64_t i = i0 + 32 * u + lane;
-            if (b >= 0) dest[i] = base[b] + static_cast<int32_t>(o) + __popc(peers[u] & lt);
-        }
-    }
-}
-
-// Move kernel: streams the particles into their 32-byte records
-// ws_v[dest[i]] = {vx, vy, vz, perm = i}; identity when the input is sorted.
-// Fixed grid-stride partition, so the per-block pre-collision sums of the live
-// particles (dest < L) are deterministic.
-
-template <bool HAS_V>
-__global__ void __launch_bounds__(kMoveThreads)
-k_move(const double* __restrict__ v, int64_t ldv, int n, const int32_t* __restrict__ dest,
-       const int32_t* __restrict__ off, int M, double* __restrict__ wsv, const int32_t* __restrict__ flags,
-       double* __restrict__ blocksum)
-{
-    __shared__ double red[kMoveThreads / 32][kTileSum];
-    const bool sorted = flags && flags[1] == 0;
-    const int32_t L = off[M];
-    double pre[kTileSum] = {0.0, 0.0, 0.0, 0.0};
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * kMoveThreads * kMoveUnroll;
-    for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * kMoveThreads * kMoveUnroll + threadIdx.x; i0 < n;
-         i0 += stride) {
-        double x[kMoveUnroll], y[kMoveUnroll], z[kMoveUnroll];
-        int32_t d[kMoveUnroll];
-#pragma unroll
-        for (int u = 0; u < kMoveUnroll; ++u) {
-            const int64_t i = min(i0 + static_cast<int64_t>(u) * kMoveThreads, static_cast<int64_t>(n) - 1);
-            d[u] = sorted ? static_cast<int32_t>(i) : __ldg(dest + i);
-            if (HAS_V) { x[u] = __ldg(v + i); y[u] = __ldg(v + ldv + i); z[u] = __ldg(v + 2 * ldv + i); }
-            else { x[u] = y[u] = z[u] = 0.0; }
-        }
-#pragma unroll
-        for (int u = 0; u < kMoveUnroll; ++u) {
-            const int64_t i = i0 + static_cast<int64_t>(u) * kMoveThreads;
-            if (i < n) {
-                st256(wsv + 4 * static_cast<int64_t>(d[u]), x[u], y[u], z[u], pack_pc(static_cast<int32_t>(i), 0));
-                if (d[u] < L) {
-                    pre[0] += x[u]; pre[1] += y[u]; pre[2] += z[u];
-                    pre[3] = fma(x[u], x[u], fma(y[u], y[u], fma(z[u], z[u], pre[3])));
-                }
+            if (b >= 0) {
+                const int32_t dest = base[b] + static_cast<int32_t>(o) + __popc(peers[u] & lt);
+                const int64_t i = i0 + 32 * u + lane;
+                st256(wsv + 4 * static_cast<int64_t>(dest), x[u], y[u], z[u],
+                      pack_pc(static_cast<int32_t>(i), b < M ? b : -1));
+                if (b < M) tile_pre_add(pre, x[u], y[u], z[u]);
             }
         }
     }
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-    for (int q = 0; q < kTileSum; ++q)
-#pragma unroll
-        for (int dd = 16; dd > 0; dd >>= 1) pre[q] += __shfl_down_sync(0xFFFFFFFFu, pre[q], dd);
-    if (lane == 0)
-#pragma unroll
-        for (int q = 0; q < kTileSum; ++q) red[w][q] = pre[q];
-    __syncthreads();
-    if (threadIdx.x < kTileSum && blocksum) {
-        double a = 0.0;
-        for (int ww = 0; ww < kMoveThreads / 32; ++ww) a += red[ww][threadIdx.x];
-        blocksum[static_cast<int64_t>(blockIdx.x) * kTileSum + threadIdx.x] = a;
-    }
+    tile_pre_store(pre, tilesum, W);
 }
 
 // ------------------------------------------------------------------ CCS4 + CCS5 items
@@ -474,7 +481,7 @@ struct CollideArgs {
 
 // Post-collision moment accumulator about a per-cell shift r:
 // [0..2] sum (v - r), [3..5] sum (v - r)^2.  (Pre-collision sums come from
-// k_move, which holds every particle in registers anyway.)
+// k_scatter, which holds every particle in registers anyway.)
 struct Acc {
     double a[6];
     __device__ void zero()
@@ -1051,9 +1058,9 @@ int run_binning(const double* v_in, int64_t ldv, const int32_t* cell_in, int n, 
     const int M1 = M + 1;
     const size_t smem = sizeof(int32_t) * M1 + sizeof(uint32_t) * static_cast<size_t>(L.W) * ((M1 + 1) / 2);
     int rc = want_smem(k_count, sizeof(int32_t) * M1);
-    if (!rc) rc = want_smem(k_rank, smem);
+    if (!rc) rc = want_smem(k_scatter<true>, smem);
+    if (!rc) rc = want_smem(k_scatter<false>, smem);
     if (rc) return rc;
-    int32_t* dest = at<int32_t>(ws, L.o_dest);
     const int32_t* skip = allow_sorted_skip ? err : nullptr;
     mark(ev, 0, st);
     k_count<<<L.T, kCountThreads, sizeof(int32_t) * M1, st>>>(cell_in, n, M, L.tile, tcount, err);
@@ -1063,12 +1070,12 @@ int run_binning(const double* v_in, int64_t ldv, const int32_t* cell_in, int n, 
                                      cell_base, step,
                                      static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
     mark(ev, 2, st);
-    k_rank<<<L.T, 32 * L.W, smem, st>>>(cell_in, n, M, L.W, tcount, off, dest, skip);
     if (v_in)
-        k_move<true><<<kMoveBlocks, kMoveThreads, 0, st>>>(v_in, ldv, n, dest, off, M, wsv, skip,
-                                                           at<double>(ws, L.o_tilesum));
+        k_scatter<true><<<L.T, 32 * L.W, smem, st>>>(v_in, ldv, cell_in, n, M, L.W, tcount, off, wsv, skip,
+                                                     at<double>(ws, L.o_tilesum));
     else
-        k_move<false><<<kMoveBlocks, kMoveThreads, 0, st>>>(nullptr, 0, n, dest, off, M, wsv, skip, nullptr);
+        k_scatter<false><<<L.T, 32 * L.W, smem, st>>>(nullptr, 0, cell_in, n, M, L.W, tcount, off, wsv, skip,
+                                                      nullptr);
     return launch_ok();
 }
 
@@ -1202,8 +1209,7 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     k_finalize_cells<<<(M + 255) / 256, 256, 0, st>>>(A.cnt, A.chunk_off, A.recs, A.small_recs, A.cellref, M, mc,
                                                       moments_out, cellsum);
     if (diag_out)
-        k_finalize_diag<<<1, 1024, 0, st>>>(A.cnt, cellsum, M, at<double>(workspace, L.o_tilesum), kMoveBlocks,
-                                            diag_out);
+        k_finalize_diag<<<1, 1024, 0, st>>>(A.cnt, cellsum, M, at<double>(workspace, L.o_tilesum), L.T, diag_out);
     mark(ev, 5, st);
     return launch_ok();
 }
