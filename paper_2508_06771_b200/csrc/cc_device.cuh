@@ -204,6 +204,37 @@ __device__ __forceinline__ void small_cell_perm(uint32_t N, uint32_t G, uint32_t
     __syncwarp();
 }
 
+// ---------------------------------------------------------------- sin / cos of 2 pi u
+// phi = 2 pi u2 (R4): u in (0,1) is reduced exactly to a quadrant q and
+// r = 4u - q in [-1/2, 1/2]; x = r pi/2; sin/cos on [-pi/4, pi/4] by the
+// classic minimax kernels (FDLIBM __kernel_sin/__kernel_cos coefficients).
+__constant__ double kSinCos[12] = {
+    -1.66666666666666324348e-01, 8.33333333332248946124e-03, -1.98412698298579493134e-04,
+    2.75573137070700676789e-06, -2.50507602534068634195e-08, 1.58969099521155010221e-10,
+    4.16666666666666019037e-02, -1.38888888888741095749e-03, 2.48015872894767294178e-05,
+    -2.75573143513906633035e-07, 2.08757232129817482790e-09, -1.13596475577881948265e-11};
+
+__device__ __forceinline__ void sincos2pi(double u, double* sn, double* cs)
+{
+    const double t = 4.0 * u;
+    const double q = rint(t);
+    const double x = (t - q) * 1.5707963267948966192;   // pi/2
+    const double z = x * x;
+    double ps = kSinCos[5], pc = kSinCos[11];
+#pragma unroll
+    for (int i = 4; i >= 0; --i) {
+        ps = fma(ps, z, kSinCos[i]);
+        pc = fma(pc, z, kSinCos[6 + i]);
+    }
+    const double s = fma(x * z, ps, x);
+    const double c = fma(z * z, pc, fma(-0.5, z, 1.0));
+    const int qi = static_cast<int>(q) & 3;
+    const double ss = (qi & 1) ? c : s;
+    const double cc_ = (qi & 1) ? s : c;
+    *sn = (qi & 2) ? -ss : ss;
+    *cs = ((qi + 1) & 2) ? -cc_ : cc_;
+}
+
 // ---------------------------------------------------------------- TA77 update
 // <delta^2> = C / |u|^3; delta = sqrt(<delta^2>) z with z = Phi^-1(u1);
 // tan(Theta/2) = delta; phi = 2 pi u2; v_a += Du/2, v_b -= Du/2.
@@ -227,7 +258,7 @@ __device__ __forceinline__ void ta_update_z(double& ax, double& ay, double& az,
     const double sinT = 2.0 * copysign(dd, delta) * inv;
     const double omc = 2.0 * d2 * inv;
     double sphi, cphi;
-    sincospi(2.0 * u2, &sphi, &cphi);
+    sincos2pi(u2, &sphi, &cphi);
     double dux, duy, duz;
     if (ux == 0.0 && uy == 0.0) {
         dux = u * sinT * cphi;

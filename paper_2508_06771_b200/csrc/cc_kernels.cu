@@ -22,6 +22,7 @@
 #include <cmath>
 #include <cstdint>
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/coulomb.h"
@@ -476,6 +477,8 @@ struct CollideArgs {
     double* small_recs;
     double* cellref;            // [M][4] shift of large cells (pre-collision v of the first slot)
     int M;
+    int pf_dist;                // k_collide_large: L2-prefetch the slice share of chunk c + pf_dist
+    int pair_vec;               // outputs aligned for 16-byte (v) / 8-byte (cell, perm) pair stores
     uint32_t cell_base, step, s0, s1;
 };
 
@@ -516,6 +519,23 @@ __device__ __forceinline__ void write_out(const CollideArgs& A, int32_t p, int32
     A.v_out[2 * A.ldv + p] = r.z;
     A.cell_out[p] = j;
     if (A.perm_out) A.perm_out[p] = unpack_perm(r.w);
+}
+
+// Both members of pair k: slots pa, pa+1 of every output row.  With an even
+// pa and aligned outputs this is one 16-byte store per velocity row and one
+// 8-byte store for the cell ids and for perm.
+__device__ __forceinline__ void write_pair_out(const CollideArgs& A, int32_t pa, int32_t j, const Rec& a, const Rec& b)
+{
+    if (A.pair_vec && (pa & 1) == 0) {
+        *reinterpret_cast<double2*>(A.v_out + pa) = make_double2(a.x, b.x);
+        *reinterpret_cast<double2*>(A.v_out + A.ldv + pa) = make_double2(a.y, b.y);
+        *reinterpret_cast<double2*>(A.v_out + 2 * A.ldv + pa) = make_double2(a.z, b.z);
+        *reinterpret_cast<int2*>(A.cell_out + pa) = make_int2(j, j);
+        if (A.perm_out) *reinterpret_cast<int2*>(A.perm_out + pa) = make_int2(unpack_perm(a.w), unpack_perm(b.w));
+    } else {
+        write_out(A, pa, j, a);
+        write_out(A, pa + 1, j, b);
+    }
 }
 
 // CCS4: one Philox call per pair, ctr = (k, G, step, 0) -> (u1, u2) (R3).
@@ -630,6 +650,24 @@ k_collide_large(CollideArgs A)
     const int c = blockIdx.x;
     if (c >= A.chunk_off[A.M]) return;      // grid is an upper bound on the chunk count
     const int j = A.chunk_cell[c];
+    if (A.pf_dist > 0 && threadIdx.x < 4) {
+        // Every chunk gathers from its whole cell slice at random; prefetch a later
+        // chunk's share of its cell slice into L2 with sequential bulk requests so
+        // the gathers hit L2 instead of issuing random 32-byte DRAM reads.
+        const int c2 = c + A.pf_dist;
+        if (c2 < A.chunk_off[A.M]) {
+            const int j2 = A.chunk_cell[c2];
+            const int64_t N2 = A.cnt[j2], nch = A.chunk_off[j2 + 1] - A.chunk_off[j2], q = c2 - A.chunk_off[j2];
+            const int64_t r0 = A.off[j2] + q * N2 / nch, r1 = A.off[j2] + (q + 1) * N2 / nch;
+            const int64_t per = (r1 - r0 + 3) / 4;
+            const int64_t a = r0 + threadIdx.x * per, b = min(r1, a + per);
+            if (b > a) {
+                const double* g = A.wsv + 4 * a;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g),
+                             "r"(static_cast<unsigned>((b - a) * 32)) : "memory");
+            }
+        }
+    }
     const int32_t N = A.cnt[j], o = A.off[j];
     const uint32_t items = static_cast<uint32_t>(N + 1) / 2;
     const uint32_t i0 = static_cast<uint32_t>(c - A.chunk_off[j]) * kChunk;
@@ -700,10 +738,11 @@ k_collide_large(CollideArgs A)
                     Rec b{b01.x, b01.y, b23.x, b23.y};
                     const double zz = (tpos[t] >= 0) ? q_w[tpos[t]] : z[t];
                     cc::ta_update_z(a.x, a.y, a.z, b.x, b.y, b.z, C, zz, u2[t]);
-                    write_out(A, pa + 1, j, b);
+                    write_pair_out(A, pa, j, a, b);
                     acc.post(b.x, b.y, b.z, ref.x, ref.y, ref.z);
+                } else {
+                    write_out(A, pa, j, a);
                 }
-                write_out(A, pa, j, a);
                 acc.post(a.x, a.y, a.z, ref.x, ref.y, ref.z);
             }
         }
@@ -1095,6 +1134,16 @@ CellConst cell_const(const cc_params& p, double dt)
 
 bool finite_pos(double x) { return std::isfinite(x) && x > 0.0; }
 
+// L2 prefetch distance of k_collide_large in chunks (tuning knob; env CC_PREFETCH_DIST).
+int prefetch_distance()
+{
+    static const int d = [] {
+        const char* e = std::getenv("CC_PREFETCH_DIST");
+        return e ? std::atoi(e) : 0;
+    }();
+    return d;
+}
+
 }  // namespace
 
 // ====================================================================== C ABI
@@ -1195,6 +1244,8 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     A.step = static_cast<uint32_t>(step);
     A.s0 = static_cast<uint32_t>(seed);
     A.s1 = static_cast<uint32_t>(seed >> 32);
+    A.pf_dist = prefetch_distance();
+    A.pair_vec = aligned(v_out, 16) && (ldv % 2 == 0) && aligned(cell_out, 8) && (!perm_out || aligned(perm_out, 8));
 
     mark(ev, 3, st);
     rc = want_smem(k_collide_large, kCollideSmem);
