@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--nx", type=int, default=64)
     ap.add_argument("--ny", type=int, default=64)
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--drift", type=float, default=0.02, help="fraction of electrons changing cell per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-cells", type=int, default=96,
                     help="cells of the C4 workload the CPU baseline processes per step")
@@ -218,10 +219,31 @@ def run_reference(args):
 # ---------------------------------------------------------------- GPU arm
 
 
+def drift_cells(cell, nx, ny, frac, gen):
+    """Stand-in pusher (workload generation, not the operator): each live
+    particle moves to a random von-Neumann neighbour cell of the periodic
+    nx x ny grid with probability `frac` (SURVEY §8(e)/(f2) stand-in drift)."""
+    import torch
+    live = cell >= 0
+    r = torch.rand(cell.numel(), generator=gen, device=cell.device)
+    mv = (r < frac) & live
+    d = torch.clamp((r * (4.0 / frac)).to(torch.int32), max=3)
+    cx = torch.remainder(cell, nx)
+    cy = torch.div(cell, nx, rounding_mode="floor")
+    cx = torch.where(mv & (d == 0), torch.remainder(cx + 1, nx), cx)
+    cx = torch.where(mv & (d == 1), torch.remainder(cx - 1, nx), cx)
+    cy = torch.where(mv & (d == 2), torch.remainder(cy + 1, ny), cy)
+    cy = torch.where(mv & (d == 3), torch.remainder(cy - 1, ny), cy)
+    cell.copy_(torch.where(live, cy * nx + cx, cell))
+
+
 def run_ours(args):
+    import ctypes as C
+
     import torch
     from paper_2508_06771_b200 import dist as ccd
     rank, world, local = ccd.init_from_env("nccl")
+    dist = None
     if world > 1:
         import torch.distributed as dist
         dist_ops = ccd.cuda_ops()
@@ -240,118 +262,105 @@ def run_ours(args):
     cell = c_host.to(dev)
     p = w.params()
     ws = cc.alloc_workspace(n, M, dev)
-    out = CollideOut(torch.empty((3, n), dtype=torch.float64, device=dev),
-                     torch.empty(n, dtype=torch.int32, device=dev),
-                     torch.empty(n, dtype=torch.int32, device=dev),
-                     torch.empty((M, 7), dtype=torch.float64, device=dev),
-                     torch.empty(16, dtype=torch.float64, device=dev))
-    stream = torch.cuda.current_stream(dev)
 
-    def one_step(s, events=None):
-        params = dict(p)
-        params.pop("seed")
-        lib = _lib.load()
-        import ctypes as C
-        prm = cc.make_params(weight=params["weight"], cell_volume=params["cell_volume"],
-                             ln_lambda=params["ln_lambda"])
+    def new_out():
+        return CollideOut(torch.empty((3, n), dtype=torch.float64, device=dev),
+                          torch.empty(n, dtype=torch.int32, device=dev),
+                          torch.empty(n, dtype=torch.int32, device=dev),
+                          torch.empty((M, 7), dtype=torch.float64, device=dev),
+                          torch.empty(16, dtype=torch.float64, device=dev))
+
+    bufs = [new_out(), new_out()]
+    stream = torch.cuda.current_stream(dev)
+    nst = _lib.CC_NUM_STAGES
+    lib = _lib.load()
+
+    def call(src_v, src_cell, dst, step, events=None):
+        prm = cc.make_params(weight=p["weight"], cell_volume=p["cell_volume"], ln_lambda=p["ln_lambda"])
         if events is not None:
-            arr = (C.c_void_p * len(events))(*[e.cuda_event for e in events])
+            arr = (C.c_void_p * (nst + 1))(*[e.cuda_event for e in events])
             prm.stage_events = C.cast(arr, C.POINTER(C.c_void_p))
-        rc = lib.coulomb_collide(C.c_void_p(v.data_ptr()), n, C.c_void_p(cell.data_ptr()),
-                                 C.c_void_p(out.v_out.data_ptr()), C.c_void_p(out.cell_out.data_ptr()),
-                                 C.c_void_p(out.perm_out.data_ptr()), n, M, w.cell_base, w.dt,
-                                 C.byref(prm), w.seed, s, C.c_void_p(out.moments.data_ptr()),
-                                 C.c_void_p(out.diag.data_ptr()), C.c_void_p(ws.data_ptr()), ws.numel(),
-                                 C.c_void_p(stream.cuda_stream))
+        rc = lib.coulomb_collide(C.c_void_p(src_v.data_ptr()), n, C.c_void_p(src_cell.data_ptr()),
+                                 C.c_void_p(dst.v_out.data_ptr()), C.c_void_p(dst.cell_out.data_ptr()),
+                                 C.c_void_p(dst.perm_out.data_ptr()), n, M, w.cell_base, w.dt, C.byref(prm),
+                                 w.seed, step, C.c_void_p(dst.moments.data_ptr()), C.c_void_p(dst.diag.data_ptr()),
+                                 C.c_void_p(ws.data_ptr()), ws.numel(), C.c_void_p(stream.cuda_stream))
         _lib.check(rc, "coulomb_collide")
         if world > 1:
-            ccd.reduce_diag(out.diag, dist_ops)      # NCCL all_gather + rank-ordered device sum
+            ccd.reduce_diag(dst.diag, dist_ops)      # NCCL all_gather + rank-ordered device sum
 
-    # warm-up
-    for s in range(args.warmup):
-        one_step(10_000 + s)
-    torch.cuda.synchronize()
-    assert cc.cc_device_status(ws) == 0
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
 
-    K = args.steps
-    nst = _lib.CC_NUM_STAGES
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(nst + 1)] for _ in range(K)]
-    for row in ev:
-        for e in row:
-            e.record(stream)          # materialise the cudaEvent_t handles
-    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        start.record(stream)
-        for s in range(K):
-            one_step(s, ev[s])
-        stop.record(stream)
+    def run_mode(mode, K, W, step0, sampler=None):
+        """K timed operator calls after W untimed ones.  cold: the same randomly
+        ordered input every step; warm: each step consumes the previous step's
+        (cell-sorted) output; steady: warm + the stand-in drift between steps
+        (the drift runs outside the operator's events)."""
+        cur = (v, cell)
+        for s in range(W):
+            dst = bufs[s % 2]
+            call(*cur, dst, step0 + s)
+            if mode != "cold":
+                if mode == "steady":
+                    drift_cells(dst.cell_out, args.nx, args.ny, args.drift, gen)
+                cur = (dst.v_out, dst.cell_out)
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(nst + 1)] for _ in range(K)]
+        for row in ev:
+            for e in row:
+                e.record(stream)          # materialise the cudaEvent_t handles
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ms = start.elapsed_time(stop)
-    stage_ms = {name: statistics.mean(ev[s][i].elapsed_time(ev[s][i + 1]) for s in range(K))
-                for i, name in enumerate(_lib.STAGE_NAMES)}
-    pairs_local = float(out.diag[2].item())
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        if sampler:
+            sampler.__enter__()
+        t0.record(stream)
+        for s in range(K):
+            dst = bufs[(W + s) % 2]
+            call(*cur, dst, step0 + W + s, ev[s])
+            if mode != "cold":
+                if mode == "steady":
+                    drift_cells(dst.cell_out, args.nx, args.ny, args.drift, gen)
+                cur = (dst.v_out, dst.cell_out)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        if sampler:
+            sampler.__exit__()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        op_ms = statistics.mean(ev[s][0].elapsed_time(ev[s][nst]) for s in range(K))
+        stages = {name: statistics.mean(ev[s][i].elapsed_time(ev[s][i + 1]) for s in range(K))
+                  for i, name in enumerate(_lib.STAGE_NAMES)}
+        assert cc.cc_device_status(ws) == 0
+        return {"ms": op_ms, "wall_ms": t0.elapsed_time(t1) / K, "stages": stages,
+                "pairs": float(bufs[(W + K - 1) % 2].diag[2].item())}
 
-    # ---- warm: chained steps, each step's (cell-sorted) output is the next input
-    out2 = CollideOut(torch.empty_like(out.v_out), torch.empty_like(out.cell_out), torch.empty_like(out.perm_out),
-                      torch.empty_like(out.moments), torch.empty_like(out.diag))
-    cc.coulomb_collide(v, cell, M, step=30_000, out=out2, workspace=ws, **p)
-    bufs = [out2, out]
-    for s in range(2):
-        src, dst = bufs[s % 2], bufs[(s + 1) % 2]
-        cc.coulomb_collide(src.v_out, src.cell_out, M, step=30_001 + s, out=dst, workspace=ws, **p)
-    wev = [[torch.cuda.Event(enable_timing=True) for _ in range(nst + 1)] for _ in range(K)]
-    for row in wev:
-        for e in row:
-            e.record(stream)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    w0.record(stream)
-    for s in range(K):
-        src, dst = bufs[s % 2], bufs[(s + 1) % 2]
-        import ctypes as C
-        prm = cc.make_params(weight=p["weight"], cell_volume=p["cell_volume"], ln_lambda=p["ln_lambda"])
-        arr = (C.c_void_p * (nst + 1))(*[e.cuda_event for e in wev[s]])
-        prm.stage_events = C.cast(arr, C.POINTER(C.c_void_p))
-        rc = _lib.load().coulomb_collide(
-            C.c_void_p(src.v_out.data_ptr()), n, C.c_void_p(src.cell_out.data_ptr()),
-            C.c_void_p(dst.v_out.data_ptr()), C.c_void_p(dst.cell_out.data_ptr()),
-            C.c_void_p(dst.perm_out.data_ptr()), n, M, w.cell_base, w.dt, C.byref(prm), w.seed, 40_000 + s,
-            C.c_void_p(dst.moments.data_ptr()), C.c_void_p(dst.diag.data_ptr()), C.c_void_p(ws.data_ptr()),
-            ws.numel(), C.c_void_p(stream.cuda_stream))
-        _lib.check(rc, "coulomb_collide")
-    w1.record(stream)
-    torch.cuda.synchronize()
-    warm_ms = w0.elapsed_time(w1) / K
-    warm_stage_ms = {name: statistics.mean(wev[s][i].elapsed_time(wev[s][i + 1]) for s in range(K))
-                     for i, name in enumerate(_lib.STAGE_NAMES)}
-    del out2, bufs
+    K, W = args.steps, args.warmup
+    clk = ClockSampler(local)
+    res = {"steady": run_mode("steady", K, W, 0, clk),
+           "cold": run_mode("cold", K, W, 100_000),
+           "warm": run_mode("warm", K, W, 200_000)}
 
-    # ---- end-to-end through the public API with host buffers (pinned)
+    # ---- end-to-end through the public API with host buffers (pinned), cold input
     v_pin = v_host.pin_memory()
     c_pin = c_host.pin_memory()
     vo_pin = torch.empty((3, n), dtype=torch.float64).pin_memory()
     co_pin = torch.empty(n, dtype=torch.int32).pin_memory()
     po_pin = torch.empty(n, dtype=torch.int32).pin_memory()
     E = max(args.e2e_steps, 1)
+    out = bufs[0]
     torch.cuda.synchronize()
-    if world > 1:
+    if dist is not None:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for s in range(E):
         v.copy_(v_pin, non_blocking=True)
         cell.copy_(c_pin, non_blocking=True)
-        cc.coulomb_collide(v, cell, M, step=20_000 + s, out=out, workspace=ws, **p)
+        cc.coulomb_collide(v, cell, M, step=300_000 + s, out=out, workspace=ws, **p)
         vo_pin.copy_(out.v_out, non_blocking=True)
         co_pin.copy_(out.cell_out, non_blocking=True)
         po_pin.copy_(out.perm_out, non_blocking=True)
@@ -359,23 +368,24 @@ def run_ours(args):
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / E
 
-    # ---- max over ranks
-    if world > 1:
-        t = torch.tensor([ms, e2e_ms, warm_ms * K, pairs_local], dtype=torch.float64, device=dev)
-        mx = t.clone()
-        dist.all_reduce(mx[:3], op=dist.ReduceOp.MAX)
-        tot = t[3:].clone()
+    # ---- max over ranks (times), sum over ranks (pairs)
+    names = ["steady", "cold", "warm"]
+    if dist is not None:
+        t = torch.tensor([res[k]["ms"] for k in names] + [e2e_ms] + [res[k]["pairs"] for k in names],
+                         dtype=torch.float64, device=dev)
+        mx = t[:4].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        tot = t[4:].clone()
         dist.all_reduce(tot, op=dist.ReduceOp.SUM)
-        ms, e2e_ms, warm_ms, pairs_total = float(mx[0]), float(mx[1]), float(mx[2]) / K, float(tot[0])
-    else:
-        pairs_total = pairs_local
+        for i, k in enumerate(names):
+            res[k]["ms"] = float(mx[i])
+            res[k]["pairs"] = float(tot[i])
+        e2e_ms = float(mx[3])
     if rank != 0:
-        if world > 1:
+        if dist is not None:
             dist.destroy_process_group()
         return
 
-    ms_step = ms / K
-    value = pairs_total / (ms_step * 1e-3)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -383,30 +393,42 @@ def run_ours(args):
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
-    dom = max(("count", "scatter", "collide"), key=lambda k: stage_ms[k])
-    achieved = STAGE_BYTES[dom] * n / (stage_ms[dom] * 1e-3) / 1e9
+
+    def roofline(r):
+        st = r["stages"]
+        dom = max(("count", "scatter", "collide"), key=lambda k: st[k])
+        achieved = STAGE_BYTES[dom] * n / (st[dom] * 1e-3) / 1e9
+        return {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": None, "algorithmic_bytes_per_particle": STAGE_BYTES[dom],
+                "peak_source": peak_src}
+
+    def summary(r):
+        return {"value": r["pairs"] / (r["ms"] * 1e-3), "ms_per_step": r["ms"], "wall_ms_per_step": r["wall_ms"],
+                "stages_ms": r["stages"], "roofline": roofline(r),
+                "step_hbm_frac": STEP_BYTES_PER_PARTICLE * n * world / (r["ms"] * 1e-3) / 1e9 / world / hbm_peak}
+
+    head = res["steady"]
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "metric": METRIC, "value": head["pairs"] / (head["ms"] * 1e-3), "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": W, "ms_per_step": head["ms"], "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_name(args, world), "cells_per_gpu": M, "electrons_per_gpu": n,
-                   "pairs_per_step": pairs_total, "input_order": "random permutation (cold, re-binned every step)",
+        "config": {"workload": workload_name(args, world) + f"; steady-state PIC: each step consumes the previous "
+                   f"step's output after a stand-in drift moves {100 * args.drift:g}% of the electrons to a "
+                   f"neighbour cell (first step: randomly ordered input)",
+                   "cells_per_gpu": M, "electrons_per_gpu": n, "pairs_per_step": head["pairs"],
                    "l2": "inputs 2.87 GB/GPU >> 126 MB L2 (no flush needed)",
+                   "timing": "CUDA events around each operator call (drift excluded), mean of K",
                    "parallelism": f"cell-range shards x{world}" if world > 1 else "1 GPU"},
-        "roofline": {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": None,
-                     "algorithmic_bytes_per_particle": STAGE_BYTES[dom], "peak_source": peak_src},
-        "stages_ms": stage_ms,
+        "roofline": roofline(head),
+        "stages_ms": head["stages"],
         "step_hbm": {"algorithmic_bytes_per_particle": STEP_BYTES_PER_PARTICLE,
-                     "achieved_gbs": STEP_BYTES_PER_PARTICLE * n * world / (ms_step * 1e-3) / 1e9 / world,
-                     "frac": STEP_BYTES_PER_PARTICLE * n / (ms_step * 1e-3) / 1e9 / hbm_peak},
-        "e2e": {"value": pairs_total / (e2e_ms * 1e-3), "unit": UNIT,
+                     "frac": STEP_BYTES_PER_PARTICLE * n / (head["ms"] * 1e-3) / 1e9 / hbm_peak},
+        "cold": dict(summary(res["cold"]), what="every step bins the same randomly ordered input"),
+        "warm": dict(summary(res["warm"]), what="chained steps, no drift (input already cell-sorted)"),
+        "e2e": {"value": res["cold"]["pairs"] / (e2e_ms * 1e-3), "unit": UNIT,
                 "h2d_bytes_per_step": int(v_host.numel() * 8 + c_host.numel() * 4),
-                "d2h_bytes_per_step": int(n * 24 + n * 8), "ms_per_step": e2e_ms},
-        "warm": {"what": "chained steps: each step's cell-sorted output is the next input "
-                         "(sortedness detected on device, binning scatter skipped)",
-                 "value": pairs_total / (warm_ms * 1e-3), "ms_per_step": warm_ms, "stages_ms": warm_stage_ms,
-                 "step_hbm_frac": STEP_BYTES_PER_PARTICLE * n / (warm_ms * 1e-3) / 1e9 / hbm_peak},
+                "d2h_bytes_per_step": int(n * 24 + n * 8), "ms_per_step": e2e_ms,
+                "what": "coulomb_collide with host buffers: pinned H2D of v and cell ids, D2H of v, cell, perm"},
         "gpu_launches": 9 * K + (K if world > 1 else 0),
         "clocks": clk.summary(),
     }
@@ -416,7 +438,7 @@ def run_ours(args):
         except Exception as e:  # the baseline must never kill the GPU number
             line["cpu_baseline"] = {"error": repr(e)}
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist is not None:
         dist.destroy_process_group()
 
 
