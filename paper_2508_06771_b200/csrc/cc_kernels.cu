@@ -35,7 +35,7 @@ constexpr int kSub = 4096;               // elements per warp sub-range in k_sca
 constexpr int kScatterUnrollA = 16;      // cell loads in flight per lane, counting pass
 constexpr int kScatterUnrollB = 6;       // (cell, v) loads in flight per lane, scatter pass
 constexpr int kCollideThreads = 256;
-constexpr int kChunk = 1024;             // items (pairs or sitter) per k_collide_large CTA
+constexpr int kChunk = 768;              // items (pairs or sitter) per k_collide_large CTA
 constexpr int kRec = 8;                  // chunk moment record: S1' (3), S2' (3), pad
 constexpr int kSmallRec = 12;            // small-cell record: S1', S2' about the exact mean, the mean (3), pad
 constexpr int kCellSum = 4;              // per-cell raw post-collision sums: v (3), |v|^2
@@ -637,23 +637,24 @@ __device__ __forceinline__ void stage_slot(const CollideArgs& A, int64_t s, doub
 //     across the warp and evaluated once per 32 tails, then TA (CCS5), and the
 //     pair-ordered, coalesced SoA output plus the moment partials.
 constexpr int kItemsPerThread = kChunk / kCollideThreads;
-constexpr int kItemsPerRound = 4;
-constexpr int kTailQueue = 32 * kItemsPerRound;
+constexpr int kWarpItems = 32 * kItemsPerThread;            // items of one warp per chunk
 constexpr size_t kCollideSmem = 2ull * kChunk * 4 * sizeof(double);
+static_assert(kChunk % kCollideThreads == 0, "chunk must be a whole number of thread items");
 
 __global__ void __launch_bounds__(kCollideThreads, 3)
 k_collide_large(CollideArgs A)
 {
     extern __shared__ __align__(16) double stage[];       // [2][kChunk][4]
-    __shared__ double tailq[kCollideThreads / 32][kTailQueue];
+    __shared__ double zq[kCollideThreads / 32][kWarpItems];  // normal variate z = Phi^-1(u1) per item
+    __shared__ double u2q[kCollideThreads / 32][kWarpItems]; // u2 per item
+    __shared__ int16_t tq[kCollideThreads / 32][kWarpItems]; // compacted AS241-tail items
     __shared__ double red[kCollideThreads / 32][6];
     const int c = blockIdx.x;
     if (c >= A.chunk_off[A.M]) return;      // grid is an upper bound on the chunk count
     const int j = A.chunk_cell[c];
     if (A.pf_dist > 0 && threadIdx.x < 4) {
         // Every chunk gathers from its whole cell slice at random; prefetch a later
-        // chunk's share of its cell slice into L2 with sequential bulk requests so
-        // the gathers hit L2 instead of issuing random 32-byte DRAM reads.
+        // chunk's share of its cell slice into L2 with sequential bulk requests.
         const int c2 = c + A.pf_dist;
         if (c2 < A.chunk_off[A.M]) {
             const int j2 = A.chunk_cell[c2];
@@ -672,6 +673,8 @@ k_collide_large(CollideArgs A)
     const uint32_t items = static_cast<uint32_t>(N + 1) / 2;
     const uint32_t i0 = static_cast<uint32_t>(c - A.chunk_off[j]) * kChunk;
     const uint32_t i1 = min(i0 + static_cast<uint32_t>(kChunk), items);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    // phase 1: pi_j (keyed Feistel, R1) and the cp.async gathers of both records
     {
         const cc::Feistel f = cc::make_feistel(static_cast<uint32_t>(N), A.keys[j]);
 #pragma unroll
@@ -686,6 +689,31 @@ k_collide_large(CollideArgs A)
             }
         }
     }
+    // phase 2a (overlaps the gathers): CCS4 Philox per pair and AS241; the
+    // central branch in place, the tails compacted across the warp
+    {
+        const uint32_t lt = (1u << lane) - 1u;
+        int qn = 0;
+#pragma unroll
+        for (int t = 0; t < kItemsPerThread; ++t) {
+            const uint32_t k = i0 + threadIdx.x + t * kCollideThreads;
+            const bool pair = (k < i1) && (2 * k + 1 < static_cast<uint32_t>(N));
+            double u1 = 0.5, u2 = 0.0;
+            if (pair) pair_uniforms(A, j, k, u1, u2);
+            const bool tail = pair && !cc::ppnd16_is_central(u1);
+            const int slot = t * 32 + lane;
+            zq[w][slot] = tail ? cc::ppnd16_tail_arg(u1) : cc::ppnd16_central(u1);
+            u2q[w][slot] = u2;
+            const uint32_t tm = __ballot_sync(0xFFFFFFFFu, tail);
+            if (tail) tq[w][qn + __popc(tm & lt)] = static_cast<int16_t>(slot);
+            qn += __popc(tm);
+        }
+        __syncwarp();
+        for (int e = lane; e < qn; e += 32) {
+            const int slot = tq[w][e];
+            zq[w][slot] = cc::ppnd16_tail(zq[w][slot]);
+        }
+    }
     // shift for the moment partials: pre-collision v of the cell's first stable slot
     const Rec ref = load_slot(A, o);
     if (i0 == 0 && threadIdx.x == 0) {
@@ -696,57 +724,31 @@ k_collide_large(CollideArgs A)
     cp_async_wait_all();
     __syncthreads();
 
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const uint32_t lt = (1u << lane) - 1u;
-    double* q_w = tailq[w];
+    // phase 2b: CCS5 TA update out of shared memory, pair-ordered coalesced output
     Acc acc;
     acc.zero();
 #pragma unroll 1
-    for (int h = 0; h < kItemsPerThread; h += kItemsPerRound) {
-        double z[kItemsPerRound], u2[kItemsPerRound];
-        int tpos[kItemsPerRound];
-        int qn = 0;
-#pragma unroll
-        for (int t = 0; t < kItemsPerRound; ++t) {
-            const uint32_t k = i0 + threadIdx.x + (h + t) * kCollideThreads;
-            const bool pair = (k < i1) && (2 * k + 1 < static_cast<uint32_t>(N));
-            double u1 = 0.5;
-            u2[t] = 0.0;
-            if (pair) pair_uniforms(A, j, k, u1, u2[t]);
-            const bool tail = pair && !cc::ppnd16_is_central(u1);
-            z[t] = cc::ppnd16_central(tail ? 0.5 : u1);
-            const uint32_t tm = __ballot_sync(0xFFFFFFFFu, tail);
-            tpos[t] = tail ? qn + __popc(tm & lt) : -1;
-            if (tail) q_w[tpos[t]] = cc::ppnd16_tail_arg(u1);
-            qn += __popc(tm);
-        }
-        __syncwarp();
-        for (int e = lane; e < qn; e += 32) q_w[e] = cc::ppnd16_tail(q_w[e]);
-        __syncwarp();
-#pragma unroll
-        for (int t = 0; t < kItemsPerRound; ++t) {
-            const uint32_t k = i0 + threadIdx.x + (h + t) * kCollideThreads;
-            if (k < i1) {
-                const uint32_t e = k - i0;
-                const int32_t pa = o + 2 * static_cast<int32_t>(k);
-                const double2 a01 = *reinterpret_cast<const double2*>(stage + 4 * e);
-                const double2 a23 = *reinterpret_cast<const double2*>(stage + 4 * e + 2);
-                Rec a{a01.x, a01.y, a23.x, a23.y};
-                if (2 * k + 1 < static_cast<uint32_t>(N)) {
-                    const double2 b01 = *reinterpret_cast<const double2*>(stage + 4 * (kChunk + e));
-                    const double2 b23 = *reinterpret_cast<const double2*>(stage + 4 * (kChunk + e) + 2);
-                    Rec b{b01.x, b01.y, b23.x, b23.y};
-                    const double zz = (tpos[t] >= 0) ? q_w[tpos[t]] : z[t];
-                    cc::ta_update_z(a.x, a.y, a.z, b.x, b.y, b.z, C, zz, u2[t]);
-                    write_pair_out(A, pa, j, a, b);
-                    acc.post(b.x, b.y, b.z, ref.x, ref.y, ref.z);
-                } else {
-                    write_out(A, pa, j, a);
-                }
-                acc.post(a.x, a.y, a.z, ref.x, ref.y, ref.z);
+    for (int t = 0; t < kItemsPerThread; ++t) {
+        const uint32_t k = i0 + threadIdx.x + t * kCollideThreads;
+        if (k < i1) {
+            const uint32_t e = k - i0;
+            const int32_t pa = o + 2 * static_cast<int32_t>(k);
+            const double2 a01 = *reinterpret_cast<const double2*>(stage + 4 * e);
+            const double2 a23 = *reinterpret_cast<const double2*>(stage + 4 * e + 2);
+            Rec a{a01.x, a01.y, a23.x, a23.y};
+            if (2 * k + 1 < static_cast<uint32_t>(N)) {
+                const double2 b01 = *reinterpret_cast<const double2*>(stage + 4 * (kChunk + e));
+                const double2 b23 = *reinterpret_cast<const double2*>(stage + 4 * (kChunk + e) + 2);
+                Rec b{b01.x, b01.y, b23.x, b23.y};
+                const int slot = t * 32 + lane;
+                cc::ta_update_z(a.x, a.y, a.z, b.x, b.y, b.z, C, zq[w][slot], u2q[w][slot]);
+                write_pair_out(A, pa, j, a, b);
+                acc.post(b.x, b.y, b.z, ref.x, ref.y, ref.z);
+            } else {
+                write_out(A, pa, j, a);
             }
+            acc.post(a.x, a.y, a.z, ref.x, ref.y, ref.z);
         }
-        __syncwarp();
     }
     warp_reduce(acc.a);
     if (lane == 0)
