@@ -1069,7 +1069,7 @@ int launch_ok()
 template <typename K>
 int want_smem(K kernel, size_t bytes)
 {
-    if (bytes <= 48 * 1024) return CC_OK;
+    // (static shared memory counts against the 48 KB default too, so always opt in)
     if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)) !=
         cudaSuccess) {
         cudaGetLastError();
