@@ -165,6 +165,32 @@ __device__ __forceinline__ uint32_t feistel_E(const Feistel& f, uint32_t x)
     return L + (R << f.bL);
 }
 
+// E applied to NV independent inputs in lock step (the rounds interleave, so
+// the 8-round dependency chains of different inputs hide each other's latency).
+template <int NV>
+__device__ __forceinline__ void feistel_E_multi(const Feistel& f, uint32_t (&x)[NV])
+{
+    const uint32_t amask = (1u << f.bL) - 1u;
+    uint32_t L[NV], R[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) { L[v] = x[v] & amask; R[v] = x[v] >> f.bL; }
+#pragma unroll
+    for (uint32_t r = 0; r < 8; ++r) {
+        const uint32_t K = f.k[r & 3u] + (r >> 2) * 0x9E3779B9u;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            if ((r & 1u) == 0u) {
+                L[v] ^= fmix32(R[v] ^ K) & amask;
+            } else {
+                R[v] += __umulhi(fmix32(L[v] ^ K), f.m);
+                R[v] = (R[v] >= f.m) ? R[v] - f.m : R[v];
+            }
+        }
+    }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) x[v] = L[v] + (R[v] << f.bL);
+}
+
 // pi(i) for the Feistel form: cycle walking from i until the value is < N.
 __device__ __forceinline__ uint32_t feistel_pi(const Feistel& f, uint32_t i)
 {

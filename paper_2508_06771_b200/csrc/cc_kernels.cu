@@ -674,18 +674,30 @@ k_collide_large(CollideArgs A)
     const uint32_t i0 = static_cast<uint32_t>(c - A.chunk_off[j]) * kChunk;
     const uint32_t i1 = min(i0 + static_cast<uint32_t>(kChunk), items);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    // phase 1: pi_j (keyed Feistel, R1) and the cp.async gathers of both records
+    // phase 1: pi_j (keyed Feistel, R1) for all 2 x kItemsPerThread slots of this
+    // thread in lock step, rare cycle walks afterwards, then the cp.async gathers
     {
         const cc::Feistel f = cc::make_feistel(static_cast<uint32_t>(N), A.keys[j]);
+        uint32_t x[2 * kItemsPerThread];
+#pragma unroll
+        for (int q = 0; q < kItemsPerThread; ++q) {
+            const uint32_t k = i0 + threadIdx.x + q * kCollideThreads;
+            x[2 * q] = 2 * k;
+            x[2 * q + 1] = 2 * k + 1;
+        }
+        cc::feistel_E_multi(f, x);
 #pragma unroll
         for (int q = 0; q < kItemsPerThread; ++q) {
             const uint32_t k = i0 + threadIdx.x + q * kCollideThreads;
             if (k < i1) {
                 const uint32_t e = k - i0;
-                stage_slot(A, o + static_cast<int64_t>(cc::feistel_pi(f, 2 * k)), stage + 4 * e);
-                if (2 * k + 1 < static_cast<uint32_t>(N))
-                    stage_slot(A, o + static_cast<int64_t>(cc::feistel_pi(f, 2 * k + 1)),
-                               stage + 4 * (kChunk + e));
+                uint32_t sa = x[2 * q], sb = x[2 * q + 1];
+                while (sa >= f.N) sa = cc::feistel_E(f, sa);           // cycle walking (rare)
+                stage_slot(A, o + static_cast<int64_t>(sa), stage + 4 * e);
+                if (2 * k + 1 < static_cast<uint32_t>(N)) {
+                    while (sb >= f.N) sb = cc::feistel_E(f, sb);
+                    stage_slot(A, o + static_cast<int64_t>(sb), stage + 4 * (kChunk + e));
+                }
             }
         }
     }
@@ -694,16 +706,18 @@ k_collide_large(CollideArgs A)
     {
         const uint32_t lt = (1u << lane) - 1u;
         int qn = 0;
+        double u1[kItemsPerThread], u2[kItemsPerThread];
+#pragma unroll
+        for (int t = 0; t < kItemsPerThread; ++t)      // independent Philox calls, interleaved
+            pair_uniforms(A, j, i0 + threadIdx.x + t * kCollideThreads, u1[t], u2[t]);
 #pragma unroll
         for (int t = 0; t < kItemsPerThread; ++t) {
             const uint32_t k = i0 + threadIdx.x + t * kCollideThreads;
             const bool pair = (k < i1) && (2 * k + 1 < static_cast<uint32_t>(N));
-            double u1 = 0.5, u2 = 0.0;
-            if (pair) pair_uniforms(A, j, k, u1, u2);
-            const bool tail = pair && !cc::ppnd16_is_central(u1);
+            const bool tail = pair && !cc::ppnd16_is_central(u1[t]);
             const int slot = t * 32 + lane;
-            zq[w][slot] = tail ? cc::ppnd16_tail_arg(u1) : cc::ppnd16_central(u1);
-            u2q[w][slot] = u2;
+            zq[w][slot] = tail ? cc::ppnd16_tail_arg(u1[t]) : cc::ppnd16_central(u1[t]);
+            u2q[w][slot] = u2[t];
             const uint32_t tm = __ballot_sync(0xFFFFFFFFu, tail);
             if (tail) tq[w][qn + __popc(tm & lt)] = static_cast<int16_t>(slot);
             qn += __popc(tm);
