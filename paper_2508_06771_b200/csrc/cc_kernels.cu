@@ -674,29 +674,22 @@ k_collide_large(CollideArgs A)
     const uint32_t i0 = static_cast<uint32_t>(c - A.chunk_off[j]) * kChunk;
     const uint32_t i1 = min(i0 + static_cast<uint32_t>(kChunk), items);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    // phase 1: pi_j (keyed Feistel, R1) for all 2 x kItemsPerThread slots of this
-    // thread in lock step, rare cycle walks afterwards, then the cp.async gathers
+    // phase 1: pi_j (keyed Feistel, R1) of each item's two slots in lock step
+    // (rare cycle walks afterwards), gathers issued item by item
     {
         const cc::Feistel f = cc::make_feistel(static_cast<uint32_t>(N), A.keys[j]);
-        uint32_t x[2 * kItemsPerThread];
-#pragma unroll
-        for (int q = 0; q < kItemsPerThread; ++q) {
-            const uint32_t k = i0 + threadIdx.x + q * kCollideThreads;
-            x[2 * q] = 2 * k;
-            x[2 * q + 1] = 2 * k + 1;
-        }
-        cc::feistel_E_multi(f, x);
 #pragma unroll
         for (int q = 0; q < kItemsPerThread; ++q) {
             const uint32_t k = i0 + threadIdx.x + q * kCollideThreads;
             if (k < i1) {
                 const uint32_t e = k - i0;
-                uint32_t sa = x[2 * q], sb = x[2 * q + 1];
-                while (sa >= f.N) sa = cc::feistel_E(f, sa);           // cycle walking (rare)
-                stage_slot(A, o + static_cast<int64_t>(sa), stage + 4 * e);
+                uint32_t x[2] = {2 * k, 2 * k + 1};
+                cc::feistel_E_multi(f, x);
+                while (x[0] >= f.N) x[0] = cc::feistel_E(f, x[0]);       // cycle walking (rare)
+                stage_slot(A, o + static_cast<int64_t>(x[0]), stage + 4 * e);
                 if (2 * k + 1 < static_cast<uint32_t>(N)) {
-                    while (sb >= f.N) sb = cc::feistel_E(f, sb);
-                    stage_slot(A, o + static_cast<int64_t>(sb), stage + 4 * (kChunk + e));
+                    while (x[1] >= f.N) x[1] = cc::feistel_E(f, x[1]);
+                    stage_slot(A, o + static_cast<int64_t>(x[1]), stage + 4 * (kChunk + e));
                 }
             }
         }
