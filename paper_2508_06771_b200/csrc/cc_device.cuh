@@ -129,8 +129,12 @@ __device__ __forceinline__ uint32_t fmix32(uint32_t h)
 }
 
 // Parameters of the N > 64 Feistel form for a cell of N slots.
+// Both halves stay below 2^16 (L < 2^bL <= 2^15, R < m <= 2^16), so the first
+// xor-shift of fmix32(x ^ K), (x ^ K) ^ ((x ^ K) >> 16), equals x ^ K' with the
+// per-round constant K' = K ^ (K >> 16): the rounds below are fmix32 exactly,
+// two instructions shorter.
 struct Feistel {
-    uint32_t k[4];
+    uint32_t kp[8];  // K'_r = K_r ^ (K_r >> 16), K_r = k[r mod 4] + (r div 4) * 0x9E3779B9
     uint32_t bL;     // L half: bL bits (a = 2^bL)
     uint32_t m;      // R half: values in [0, m), m = ceil(N / a)
     uint32_t N;
@@ -139,7 +143,12 @@ struct Feistel {
 __device__ __forceinline__ Feistel make_feistel(uint32_t N, U4 keys)
 {
     Feistel f;
-    f.k[0] = keys.x; f.k[1] = keys.y; f.k[2] = keys.z; f.k[3] = keys.w;
+    const uint32_t k[4] = {keys.x, keys.y, keys.z, keys.w};
+#pragma unroll
+    for (uint32_t r = 0; r < 8; ++r) {
+        const uint32_t K = k[r & 3u] + (r >> 2) * 0x9E3779B9u;
+        f.kp[r] = K ^ (K >> 16);
+    }
     const uint32_t b = 32u - __clz(N - 1u);          // ceil(log2 N), N >= 2
     f.bL = b >> 1;
     const uint32_t a = 1u << f.bL;
@@ -148,18 +157,28 @@ __device__ __forceinline__ Feistel make_feistel(uint32_t N, U4 keys)
     return f;
 }
 
+// fmix32(x ^ K) for x < 2^16, given K' = K ^ (K >> 16)
+__device__ __forceinline__ uint32_t fmix32_small(uint32_t x, uint32_t kp)
+{
+    uint32_t h = x ^ kp;
+    h *= 0x85EBCA6Bu;
+    h ^= h >> 13;
+    h *= 0xC2B2AE35u;
+    h ^= h >> 16;
+    return h;
+}
+
 __device__ __forceinline__ uint32_t feistel_E(const Feistel& f, uint32_t x)
 {
     const uint32_t amask = (1u << f.bL) - 1u;
     uint32_t L = x & amask, R = x >> f.bL;
 #pragma unroll
     for (uint32_t r = 0; r < 8; ++r) {
-        const uint32_t K = f.k[r & 3u] + (r >> 2) * 0x9E3779B9u;
         if ((r & 1u) == 0u) {
-            L ^= fmix32(R ^ K) & amask;
+            L ^= fmix32_small(R, f.kp[r]) & amask;
         } else {
-            R += __umulhi(fmix32(L ^ K), f.m);
-            R = (R >= f.m) ? R - f.m : R;
+            const uint32_t s = R + __umulhi(fmix32_small(L, f.kp[r]), f.m);
+            R = min(s, s - f.m);                     // (R + t) mod m, R + t < 2m
         }
     }
     return L + (R << f.bL);
@@ -176,14 +195,13 @@ __device__ __forceinline__ void feistel_E_multi(const Feistel& f, uint32_t (&x)[
     for (int v = 0; v < NV; ++v) { L[v] = x[v] & amask; R[v] = x[v] >> f.bL; }
 #pragma unroll
     for (uint32_t r = 0; r < 8; ++r) {
-        const uint32_t K = f.k[r & 3u] + (r >> 2) * 0x9E3779B9u;
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
             if ((r & 1u) == 0u) {
-                L[v] ^= fmix32(R[v] ^ K) & amask;
+                L[v] ^= fmix32_small(R[v], f.kp[r]) & amask;
             } else {
-                R[v] += __umulhi(fmix32(L[v] ^ K), f.m);
-                R[v] = (R[v] >= f.m) ? R[v] - f.m : R[v];
+                const uint32_t s = R[v] + __umulhi(fmix32_small(L[v], f.kp[r]), f.m);
+                R[v] = min(s, s - f.m);
             }
         }
     }
