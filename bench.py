@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--ny", type=int, default=64)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--drift", type=float, default=0.02, help="fraction of electrons changing cell per step")
+    ap.add_argument("--dist-backend", default="nccl", help="torch.distributed backend for N > 1 (nccl; gloo "
+                    "only to smoke-test the multi-rank path when fewer GPUs than ranks are available)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-cells", type=int, default=96,
                     help="cells of the C4 workload the CPU baseline processes per step")
@@ -242,11 +244,12 @@ def run_ours(args):
 
     import torch
     from paper_2508_06771_b200 import dist as ccd
-    rank, world, local = ccd.init_from_env("nccl")
+    rank, world, local = ccd.init_from_env(args.dist_backend)
     dist = None
     if world > 1:
         import torch.distributed as dist
         dist_ops = ccd.cuda_ops()
+    local = local % torch.cuda.device_count()
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
 
@@ -275,7 +278,7 @@ def run_ours(args):
     nst = _lib.CC_NUM_STAGES
     lib = _lib.load()
 
-    def call(src_v, src_cell, dst, step, events=None):
+    def call(src_v, src_cell, dst, step, events=None, post=None):
         prm = cc.make_params(weight=p["weight"], cell_volume=p["cell_volume"], ln_lambda=p["ln_lambda"])
         if events is not None:
             arr = (C.c_void_p * (nst + 1))(*[e.cuda_event for e in events])
@@ -288,6 +291,8 @@ def run_ours(args):
         _lib.check(rc, "coulomb_collide")
         if world > 1:
             ccd.reduce_diag(dst.diag, dist_ops)      # NCCL all_gather + rank-ordered device sum
+        if post is not None:
+            post.record(stream)                      # end of the step incl. the diagnostics collective
 
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
@@ -305,7 +310,7 @@ def run_ours(args):
                 if mode == "steady":
                     drift_cells(dst.cell_out, args.nx, args.ny, args.drift, gen)
                 cur = (dst.v_out, dst.cell_out)
-        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(nst + 1)] for _ in range(K)]
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(nst + 2)] for _ in range(K)]
         for row in ev:
             for e in row:
                 e.record(stream)          # materialise the cudaEvent_t handles
@@ -319,7 +324,7 @@ def run_ours(args):
         t0.record(stream)
         for s in range(K):
             dst = bufs[(W + s) % 2]
-            call(*cur, dst, step0 + W + s, ev[s])
+            call(*cur, dst, step0 + W + s, ev[s][:nst + 1], ev[s][nst + 1])
             if mode != "cold":
                 if mode == "steady":
                     drift_cells(dst.cell_out, args.nx, args.ny, args.drift, gen)
@@ -331,7 +336,7 @@ def run_ours(args):
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
-        op_ms = statistics.mean(ev[s][0].elapsed_time(ev[s][nst]) for s in range(K))
+        op_ms = statistics.mean(ev[s][0].elapsed_time(ev[s][nst + 1]) for s in range(K))
         stages = {name: statistics.mean(ev[s][i].elapsed_time(ev[s][i + 1]) for s in range(K))
                   for i, name in enumerate(_lib.STAGE_NAMES)}
         assert cc.cc_device_status(ws) == 0

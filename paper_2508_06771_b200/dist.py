@@ -139,5 +139,7 @@ def init_from_env(backend: Optional[str] = None):
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
+            if torch.cuda.is_available():
+                torch.cuda.set_device(local % torch.cuda.device_count())
             dist.init_process_group(backend)
     return rank, world, local
