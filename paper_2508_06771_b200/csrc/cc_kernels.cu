@@ -35,7 +35,7 @@ constexpr int kSub = 4096;               // elements per warp sub-range in k_sca
 constexpr int kScatterUnrollA = 16;      // cell loads in flight per lane, counting pass
 constexpr int kScatterUnrollB = 6;       // (cell, v) loads in flight per lane, scatter pass
 constexpr int kCollideThreads = 256;
-constexpr int kChunk = 512;              // items (pairs or sitter) per k_collide_large chunk
+constexpr int kChunk = 768;              // items (pairs or sitter) per k_collide_large CTA
 constexpr int kRec = 8;                  // chunk moment record: S1' (3), S2' (3), pad
 constexpr int kSmallRec = 12;            // small-cell record: S1', S2' about the exact mean, the mean (3), pad
 constexpr int kCellSum = 4;              // per-cell raw post-collision sums: v (3), |v|^2
@@ -638,158 +638,136 @@ __device__ __forceinline__ void stage_slot(const CollideArgs& A, int64_t s, doub
 //     pair-ordered, coalesced SoA output plus the moment partials.
 constexpr int kItemsPerThread = kChunk / kCollideThreads;
 constexpr int kWarpItems = 32 * kItemsPerThread;            // items of one warp per chunk
-constexpr size_t kStageDoubles = 2ull * kChunk * 4;          // one chunk: records a and b
-constexpr size_t kCollideSmem = 2 * kStageDoubles * sizeof(double);   // double-buffered
-constexpr int kCollideCtasPerSm = 3;
+constexpr size_t kCollideSmem = 2ull * kChunk * 4 * sizeof(double);
 static_assert(kChunk % kCollideThreads == 0, "chunk must be a whole number of thread items");
 
-struct Chunk {
-    int32_t j, N, o;
-    uint32_t i0, i1;
-};
-
-__device__ __forceinline__ Chunk chunk_meta(const CollideArgs& A, int c)
+__global__ void __launch_bounds__(kCollideThreads, 3)
+k_collide_large(CollideArgs A)
 {
-    Chunk h;
-    h.j = A.chunk_cell[c];
-    h.N = A.cnt[h.j];
-    h.o = A.off[h.j];
-    const uint32_t items = static_cast<uint32_t>(h.N + 1) / 2;
-    h.i0 = static_cast<uint32_t>(c - A.chunk_off[h.j]) * kChunk;
-    h.i1 = min(h.i0 + static_cast<uint32_t>(kChunk), items);
-    return h;
-}
-
-// Phase 1 of a chunk: pi_j (keyed Feistel, R1) of each item's two slots in lock
-// step (rare cycle walks afterwards); cp.async gathers of both 32-byte records
-// into `stage`; one commit group per chunk.
-__device__ __forceinline__ void collide_phase1(const CollideArgs& A, const Chunk& h, double* stage)
-{
-    const cc::Feistel f = cc::make_feistel(static_cast<uint32_t>(h.N), A.keys[h.j]);
-#pragma unroll
-    for (int q = 0; q < kItemsPerThread; ++q) {
-        const uint32_t k = h.i0 + threadIdx.x + q * kCollideThreads;
-        if (k < h.i1) {
-            const uint32_t e = k - h.i0;
-            uint32_t x[2] = {2 * k, 2 * k + 1};
-            cc::feistel_E_multi(f, x);
-            while (x[0] >= f.N) x[0] = cc::feistel_E(f, x[0]);       // cycle walking (rare)
-            stage_slot(A, h.o + static_cast<int64_t>(x[0]), stage + 4 * e);
-            if (2 * k + 1 < static_cast<uint32_t>(h.N)) {
-                while (x[1] >= f.N) x[1] = cc::feistel_E(f, x[1]);
-                stage_slot(A, h.o + static_cast<int64_t>(x[1]), stage + 4 * (kChunk + e));
+    extern __shared__ __align__(16) double stage[];       // [2][kChunk][4]
+    __shared__ double zq[kCollideThreads / 32][kWarpItems];  // normal variate z = Phi^-1(u1) per item
+    __shared__ double u2q[kCollideThreads / 32][kWarpItems]; // u2 per item
+    __shared__ int16_t tq[kCollideThreads / 32][kWarpItems]; // compacted AS241-tail items
+    __shared__ double red[kCollideThreads / 32][6];
+    const int c = blockIdx.x;
+    if (c >= A.chunk_off[A.M]) return;      // grid is an upper bound on the chunk count
+    const int j = A.chunk_cell[c];
+    if (A.pf_dist > 0 && threadIdx.x < 4) {
+        // Every chunk gathers from its whole cell slice at random; prefetch a later
+        // chunk's share of its cell slice into L2 with sequential bulk requests.
+        const int c2 = c + A.pf_dist;
+        if (c2 < A.chunk_off[A.M]) {
+            const int j2 = A.chunk_cell[c2];
+            const int64_t N2 = A.cnt[j2], nch = A.chunk_off[j2 + 1] - A.chunk_off[j2], q = c2 - A.chunk_off[j2];
+            const int64_t r0 = A.off[j2] + q * N2 / nch, r1 = A.off[j2] + (q + 1) * N2 / nch;
+            const int64_t per = (r1 - r0 + 3) / 4;
+            const int64_t a = r0 + threadIdx.x * per, b = min(r1, a + per);
+            if (b > a) {
+                const double* g = A.wsv + 4 * a;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g),
+                             "r"(static_cast<unsigned>((b - a) * 32)) : "memory");
             }
         }
     }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-}
-
-// N_j > 64: persistent CTAs walk the cell-aligned chunks (kChunk pairs each)
-// with a two-stage software pipeline: the gathers of the next chunk (phase 1)
-// are in flight while this chunk runs CCS4 (Philox + AS241, tails compacted
-// across the warp) and CCS5 (TA77) out of shared memory and writes its
-// pair-ordered, coalesced output and moment partials.
-__global__ void __launch_bounds__(kCollideThreads, kCollideCtasPerSm)
-k_collide_large(CollideArgs A)
-{
-    extern __shared__ __align__(16) double stage[];           // [2][2][kChunk][4]
-    __shared__ double zq[kCollideThreads / 32][kWarpItems];   // z = Phi^-1(u1) per item
-    __shared__ double u2q[kCollideThreads / 32][kWarpItems];  // u2 per item
-    __shared__ int16_t tq[kCollideThreads / 32][kWarpItems];  // compacted AS241-tail items
-    __shared__ double red[kCollideThreads / 32][6];
-    const int total = A.chunk_off[A.M];
+    const int32_t N = A.cnt[j], o = A.off[j];
+    const uint32_t items = static_cast<uint32_t>(N + 1) / 2;
+    const uint32_t i0 = static_cast<uint32_t>(c - A.chunk_off[j]) * kChunk;
+    const uint32_t i1 = min(i0 + static_cast<uint32_t>(kChunk), items);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    int c = blockIdx.x;
-    if (c >= total) return;
-    Chunk h = chunk_meta(A, c);
-    collide_phase1(A, h, stage);
-    int buf = 0;
-    while (c < total) {
-        const int cn = c + gridDim.x;
-        Chunk hn = h;
-        if (cn < total) {
-            hn = chunk_meta(A, cn);
-            collide_phase1(A, hn, stage + (buf ^ 1) * kStageDoubles);
-        }
-        double* st_c = stage + buf * kStageDoubles;
-        // phase 2a: CCS4 — Philox per pair; AS241 central branch in place, tails compacted
-        {
-            const uint32_t lt = (1u << lane) - 1u;
-            int qn = 0;
-            double u1[kItemsPerThread], u2[kItemsPerThread];
+    // phase 1: pi_j (keyed Feistel, R1) of each item's two slots in lock step
+    // (rare cycle walks afterwards), gathers issued item by item
+    {
+        const cc::Feistel f = cc::make_feistel(static_cast<uint32_t>(N), A.keys[j]);
 #pragma unroll
-            for (int t = 0; t < kItemsPerThread; ++t)
-                pair_uniforms(A, h.j, h.i0 + threadIdx.x + t * kCollideThreads, u1[t], u2[t]);
-#pragma unroll
-            for (int t = 0; t < kItemsPerThread; ++t) {
-                const uint32_t k = h.i0 + threadIdx.x + t * kCollideThreads;
-                const bool pair = (k < h.i1) && (2 * k + 1 < static_cast<uint32_t>(h.N));
-                const bool tail = pair && !cc::ppnd16_is_central(u1[t]);
-                const int slot = t * 32 + lane;
-                zq[w][slot] = tail ? cc::ppnd16_tail_arg(u1[t]) : cc::ppnd16_central(u1[t]);
-                u2q[w][slot] = u2[t];
-                const uint32_t tm = __ballot_sync(0xFFFFFFFFu, tail);
-                if (tail) tq[w][qn + __popc(tm & lt)] = static_cast<int16_t>(slot);
-                qn += __popc(tm);
-            }
-            __syncwarp();
-            for (int e = lane; e < qn; e += 32) {
-                const int slot = tq[w][e];
-                zq[w][slot] = cc::ppnd16_tail(zq[w][slot]);
-            }
-        }
-        // shift for the moment partials: pre-collision v of the cell's first stable slot
-        const Rec ref = load_slot(A, h.o);
-        if (h.i0 == 0 && threadIdx.x == 0) {
-            double* cr = A.cellref + 4 * static_cast<int64_t>(h.j);
-            cr[0] = ref.x; cr[1] = ref.y; cr[2] = ref.z; cr[3] = 0.0;
-        }
-        const double C = A.Cj[h.j];
-        if (cn < total) asm volatile("cp.async.wait_group 1;" ::: "memory");   // this chunk's gathers
-        else asm volatile("cp.async.wait_group 0;" ::: "memory");
-        __syncthreads();
-        // phase 2b: CCS5 TA update out of shared memory
-        Acc acc;
-        acc.zero();
-#pragma unroll 1
-        for (int t = 0; t < kItemsPerThread; ++t) {
-            const uint32_t k = h.i0 + threadIdx.x + t * kCollideThreads;
-            if (k < h.i1) {
-                const uint32_t e = k - h.i0;
-                const int32_t pa = h.o + 2 * static_cast<int32_t>(k);
-                const double2 a01 = *reinterpret_cast<const double2*>(st_c + 4 * e);
-                const double2 a23 = *reinterpret_cast<const double2*>(st_c + 4 * e + 2);
-                Rec a{a01.x, a01.y, a23.x, a23.y};
-                if (2 * k + 1 < static_cast<uint32_t>(h.N)) {
-                    const double2 b01 = *reinterpret_cast<const double2*>(st_c + 4 * (kChunk + e));
-                    const double2 b23 = *reinterpret_cast<const double2*>(st_c + 4 * (kChunk + e) + 2);
-                    Rec b{b01.x, b01.y, b23.x, b23.y};
-                    const int slot = t * 32 + lane;
-                    cc::ta_update_z(a.x, a.y, a.z, b.x, b.y, b.z, C, zq[w][slot], u2q[w][slot]);
-                    write_pair_out(A, pa, h.j, a, b);
-                    acc.post(b.x, b.y, b.z, ref.x, ref.y, ref.z);
-                } else {
-                    write_out(A, pa, h.j, a);
+        for (int q = 0; q < kItemsPerThread; ++q) {
+            const uint32_t k = i0 + threadIdx.x + q * kCollideThreads;
+            if (k < i1) {
+                const uint32_t e = k - i0;
+                uint32_t x[2] = {2 * k, 2 * k + 1};
+                cc::feistel_E_multi(f, x);
+                while (x[0] >= f.N) x[0] = cc::feistel_E(f, x[0]);       // cycle walking (rare)
+                stage_slot(A, o + static_cast<int64_t>(x[0]), stage + 4 * e);
+                if (2 * k + 1 < static_cast<uint32_t>(N)) {
+                    while (x[1] >= f.N) x[1] = cc::feistel_E(f, x[1]);
+                    stage_slot(A, o + static_cast<int64_t>(x[1]), stage + 4 * (kChunk + e));
                 }
-                acc.post(a.x, a.y, a.z, ref.x, ref.y, ref.z);
             }
         }
-        warp_reduce(acc.a);
-        if (lane == 0)
+    }
+    // phase 2a (overlaps the gathers): CCS4 Philox per pair and AS241; the
+    // central branch in place, the tails compacted across the warp
+    {
+        const uint32_t lt = (1u << lane) - 1u;
+        int qn = 0;
+        double u1[kItemsPerThread], u2[kItemsPerThread];
 #pragma unroll
-            for (int q = 0; q < 6; ++q) red[w][q] = acc.a[q];
-        __syncthreads();
-        if (threadIdx.x < kRec) {
-            double sum = 0.0;
-            if (threadIdx.x < 6)
+        for (int t = 0; t < kItemsPerThread; ++t)      // independent Philox calls, interleaved
+            pair_uniforms(A, j, i0 + threadIdx.x + t * kCollideThreads, u1[t], u2[t]);
 #pragma unroll
-                for (int ww = 0; ww < kCollideThreads / 32; ++ww) sum += red[ww][threadIdx.x];
-            A.recs[static_cast<int64_t>(c) * kRec + threadIdx.x] = sum;
+        for (int t = 0; t < kItemsPerThread; ++t) {
+            const uint32_t k = i0 + threadIdx.x + t * kCollideThreads;
+            const bool pair = (k < i1) && (2 * k + 1 < static_cast<uint32_t>(N));
+            const bool tail = pair && !cc::ppnd16_is_central(u1[t]);
+            const int slot = t * 32 + lane;
+            zq[w][slot] = tail ? cc::ppnd16_tail_arg(u1[t]) : cc::ppnd16_central(u1[t]);
+            u2q[w][slot] = u2[t];
+            const uint32_t tm = __ballot_sync(0xFFFFFFFFu, tail);
+            if (tail) tq[w][qn + __popc(tm & lt)] = static_cast<int16_t>(slot);
+            qn += __popc(tm);
         }
-        __syncthreads();      // zq/u2q/tq/red and this stage buffer are reused next iteration
-        c = cn;
-        h = hn;
-        buf ^= 1;
+        __syncwarp();
+        for (int e = lane; e < qn; e += 32) {
+            const int slot = tq[w][e];
+            zq[w][slot] = cc::ppnd16_tail(zq[w][slot]);
+        }
+    }
+    // shift for the moment partials: pre-collision v of the cell's first stable slot
+    const Rec ref = load_slot(A, o);
+    if (i0 == 0 && threadIdx.x == 0) {
+        double* cr = A.cellref + 4 * static_cast<int64_t>(j);
+        cr[0] = ref.x; cr[1] = ref.y; cr[2] = ref.z; cr[3] = 0.0;
+    }
+    const double C = A.Cj[j];
+    cp_async_wait_all();
+    __syncthreads();
+
+    // phase 2b: CCS5 TA update out of shared memory, pair-ordered coalesced output
+    Acc acc;
+    acc.zero();
+#pragma unroll 1
+    for (int t = 0; t < kItemsPerThread; ++t) {
+        const uint32_t k = i0 + threadIdx.x + t * kCollideThreads;
+        if (k < i1) {
+            const uint32_t e = k - i0;
+            const int32_t pa = o + 2 * static_cast<int32_t>(k);
+            const double2 a01 = *reinterpret_cast<const double2*>(stage + 4 * e);
+            const double2 a23 = *reinterpret_cast<const double2*>(stage + 4 * e + 2);
+            Rec a{a01.x, a01.y, a23.x, a23.y};
+            if (2 * k + 1 < static_cast<uint32_t>(N)) {
+                const double2 b01 = *reinterpret_cast<const double2*>(stage + 4 * (kChunk + e));
+                const double2 b23 = *reinterpret_cast<const double2*>(stage + 4 * (kChunk + e) + 2);
+                Rec b{b01.x, b01.y, b23.x, b23.y};
+                const int slot = t * 32 + lane;
+                cc::ta_update_z(a.x, a.y, a.z, b.x, b.y, b.z, C, zq[w][slot], u2q[w][slot]);
+                write_pair_out(A, pa, j, a, b);
+                acc.post(b.x, b.y, b.z, ref.x, ref.y, ref.z);
+            } else {
+                write_out(A, pa, j, a);
+            }
+            acc.post(a.x, a.y, a.z, ref.x, ref.y, ref.z);
+        }
+    }
+    warp_reduce(acc.a);
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < 6; ++q) red[w][q] = acc.a[q];
+    __syncthreads();
+    if (threadIdx.x < kRec) {
+        double sum = 0.0;
+        if (threadIdx.x < 6)
+#pragma unroll
+            for (int ww = 0; ww < kCollideThreads / 32; ++ww) sum += red[ww][threadIdx.x];
+        A.recs[static_cast<int64_t>(c) * kRec + threadIdx.x] = sum;
     }
 }
 
@@ -1165,17 +1143,6 @@ CellConst cell_const(const cc_params& p, double dt)
 
 bool finite_pos(double x) { return std::isfinite(x) && x > 0.0; }
 
-// Persistent grid of k_collide_large: kCollideCtasPerSm CTAs on every SM.
-int collide_grid()
-{
-    static const int g = [] {
-        int dev = 0, sms = 148;
-        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        return sms * kCollideCtasPerSm;
-    }();
-    return g;
-}
-
 // L2 prefetch distance of k_collide_large in chunks (tuning knob; env CC_PREFETCH_DIST).
 int prefetch_distance()
 {
@@ -1293,8 +1260,7 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     rc = want_smem(k_collide_large, kCollideSmem);
     if (rc) return rc;
     k_collide_small<<<(M + 7) / 8, 256, 0, st>>>(A);
-    k_collide_large<<<static_cast<unsigned>(std::min<int64_t>(L.max_chunks, collide_grid())), kCollideThreads,
-                      kCollideSmem, st>>>(A);
+    k_collide_large<<<static_cast<unsigned>(L.max_chunks), kCollideThreads, kCollideSmem, st>>>(A);
     k_copy_dead<<<148 * 4, 256, 0, st>>>(A, nn);
 
     MomConst mc{p.weight, p.cell_volume, p.cell_volume_arr, p.mass / p.charge};
