@@ -434,7 +434,7 @@ def run_ours(args):
                 "h2d_bytes_per_step": int(v_host.numel() * 8 + c_host.numel() * 4),
                 "d2h_bytes_per_step": int(n * 24 + n * 8), "ms_per_step": e2e_ms,
                 "what": "coulomb_collide with host buffers: pinned H2D of v and cell ids, D2H of v, cell, perm"},
-        "gpu_launches": 9 * K + (K if world > 1 else 0),
+        "gpu_launches": 10 * K + (K if world > 1 else 0),
         "clocks": clk.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:

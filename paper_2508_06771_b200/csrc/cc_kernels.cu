@@ -104,6 +104,41 @@ __device__ __forceinline__ void st256(double* p, double a, double b, double c, d
                  : "memory");
 }
 
+// L2 eviction-priority policies (createpolicy) for loads/stores with cache hints.
+__device__ __forceinline__ uint64_t l2_policy_last()
+{
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+__device__ __forceinline__ uint64_t l2_policy_first()
+{
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+__device__ __forceinline__ int32_t ld_hint_i32(const int32_t* p, uint64_t pol)
+{
+    int32_t v;
+    asm("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
+__device__ __forceinline__ double ld_hint_f64(const double* p, uint64_t pol)
+{
+    double v;
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
+__device__ __forceinline__ void st256_hint(double* p, double a, double b, double c, double d, uint64_t pol)
+{
+    asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "d"(a), "d"(b), "d"(c),
+                 "d"(d), "l"(pol) : "memory");
+}
+
 __device__ __forceinline__ double pack_pc(int32_t perm, int32_t cell)
 {
     return __longlong_as_double((static_cast<long long>(static_cast<uint32_t>(cell)) << 32) |
@@ -155,7 +190,7 @@ k_count(const int32_t* __restrict__ cell, int n, int M, int tile, int32_t* __res
 // ------------------------------------------------------------------ CCS2 part 1
 // grid: ceil((M+1)/32) CTAs of 32x16 threads; lane = bin, warp row = tile range.
 // Loads are issued 8 at a time (independent addresses) to keep DRAM busy.
-constexpr int kScanRows = 16;
+constexpr int kScanRows = 32;
 __global__ void __launch_bounds__(32 * kScanRows)
 k_scan_tiles(int32_t* __restrict__ tcount, int T, int M1, int32_t* __restrict__ cnt)
 {
@@ -226,10 +261,7 @@ __device__ __forceinline__ int32_t n_chunks(int32_t N)
 
 // single CTA of 1024 threads
 __global__ void __launch_bounds__(1024)
-k_scan_cells(const int32_t* __restrict__ cnt, int M, int32_t* __restrict__ off,
-             int32_t* __restrict__ chunk_off, int32_t* __restrict__ chunk_cell, double* __restrict__ Cj,
-             cc::U4* __restrict__ keys,
-             CellConst cc_, uint32_t cell_base, uint32_t step, uint32_t s0, uint32_t s1)
+k_scan_cells(const int32_t* __restrict__ cnt, int M, int32_t* __restrict__ off, int32_t* __restrict__ chunk_off)
 {
     __shared__ int32_t wsum_a[32], wsum_b[32];
     const int tid = threadIdx.x, nt = blockDim.x;
@@ -268,15 +300,26 @@ k_scan_cells(const int32_t* __restrict__ cnt, int M, int32_t* __restrict__ off,
         off[j] = ra;
         chunk_off[j] = rb;
         ra += N;
-        for (int32_t q = 0; q < n_chunks(N); ++q) chunk_cell[rb + q] = j;
         rb += n_chunks(N);
-        const double V = cc_.volume_arr ? cc_.volume_arr[j] : cc_.volume;
-        const double lnL = cc_.ln_lambda_arr ? cc_.ln_lambda_arr[j] : cc_.ln_lambda;
-        const double nj = static_cast<double>(N) * cc_.weight / V;
-        Cj[j] = fmax(cc_.K * nj * lnL, 0.0);
-        keys[j] = cc::philox4x32_10(cc::U4{0u, cell_base + static_cast<uint32_t>(j), step, 1u}, s0, s1);
     }
     if (tid == nt - 1) { off[M] = ra; chunk_off[M] = rb; }
+}
+
+// Per-cell constants (thread per cell, many CTAs): TA constant C_j (R5-R7),
+// Feistel keys (R1, R3), and the chunk -> cell table of k_collide_large.
+__global__ void k_cell_setup(const int32_t* __restrict__ cnt, const int32_t* __restrict__ chunk_off, int M,
+                             int32_t* __restrict__ chunk_cell, double* __restrict__ Cj, cc::U4* __restrict__ keys,
+                             CellConst cc_, uint32_t cell_base, uint32_t step, uint32_t s0, uint32_t s1)
+{
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= M) return;
+    const int32_t N = cnt[j];
+    const double V = cc_.volume_arr ? cc_.volume_arr[j] : cc_.volume;
+    const double lnL = cc_.ln_lambda_arr ? cc_.ln_lambda_arr[j] : cc_.ln_lambda;
+    const double nj = static_cast<double>(N) * cc_.weight / V;
+    Cj[j] = fmax(cc_.K * nj * lnL, 0.0);
+    keys[j] = cc::philox4x32_10(cc::U4{0u, cell_base + static_cast<uint32_t>(j), step, 1u}, s0, s1);
+    for (int32_t c = chunk_off[j]; c < chunk_off[j + 1]; ++c) chunk_cell[c] = j;
 }
 
 // ------------------------------------------------------------------ CCS3: stable scatter
@@ -331,12 +374,14 @@ __device__ __forceinline__ void tile_pre_store(double (&pre)[kTileSum], double* 
     }
 }
 
+// last use of the cell ids and of v: evict-first hints keep them from pushing
+// the tile's cell ids (read twice) out of L2
 template <bool HAS_V>
 __device__ __forceinline__ void load_batch(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__ cell,
-                                           int64_t i, double& x, double& y, double& z, int32_t& c)
+                                           int64_t i, double& x, double& y, double& z, int32_t& c, uint64_t pol)
 {
-    c = __ldg(cell + i);
-    if (HAS_V) { x = __ldg(v + i); y = __ldg(v + ldv + i); z = __ldg(v + 2 * ldv + i); }
+    c = ld_hint_i32(cell + i, pol);
+    if (HAS_V) { x = ld_hint_f64(v + i, pol); y = ld_hint_f64(v + ldv + i, pol); z = ld_hint_f64(v + 2 * ldv + i, pol); }
     else { x = y = z = 0.0; }
 }
 
@@ -349,6 +394,7 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     double pre[kTileSum] = {0.0, 0.0, 0.0, 0.0};      // pre-collision sums of the tile's live particles
+    const uint64_t pol_first = l2_policy_first(), pol_last = l2_policy_last();
     if (flags && flags[1] == 0) {
         // input already cell-sorted: the stable order is the identity, so the
         // records are written in place (a streaming SoA -> 32-byte-record pack)
@@ -360,7 +406,7 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
             int32_t c[kScatterUnrollB];
 #pragma unroll
             for (int u = 0; u < kScatterUnrollB; ++u)
-                load_batch<HAS_V>(v, ldv, cell, min(i0 + 32 * u + lane, t1 - 1), x[u], y[u], z[u], c[u]);
+                load_batch<HAS_V>(v, ldv, cell, min(i0 + 32 * u + lane, t1 - 1), x[u], y[u], z[u], c[u], pol_first);
 #pragma unroll
             for (int u = 0; u < kScatterUnrollB; ++u) {
                 const int64_t i = i0 + 32 * u + lane;
@@ -392,7 +438,7 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
 #pragma unroll
         for (int u = 0; u < kScatterUnrollA; ++u) {
             const int64_t i = i0 + 32 * u + lane;
-            const int32_t c = __ldg(cell + min(i, s1 - 1));
+            const int32_t c = ld_hint_i32(cell + min(i, s1 - 1), pol_last);   // re-read in pass B
             key[u] = (i >= s1) ? -1 - lane : ((c >= 0 && c < M) ? c : M);
         }
         uint32_t peers[kScatterUnrollA];
@@ -431,7 +477,7 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
         for (int u = 0; u < kScatterUnrollB; ++u) {
             const int64_t i = i0 + 32 * u + lane;
             int32_t c;
-            load_batch<HAS_V>(v, ldv, cell, min(i, s1 - 1), x[u], y[u], z[u], c);
+            load_batch<HAS_V>(v, ldv, cell, min(i, s1 - 1), x[u], y[u], z[u], c, pol_first);
             key[u] = (i >= s1) ? -1 - lane : ((c >= 0 && c < M) ? c : M);
         }
         uint32_t peers[kScatterUnrollB], old[kScatterUnrollB];
@@ -1114,9 +1160,10 @@ int run_binning(const double* v_in, int64_t ldv, const int32_t* cell_in, int n, 
     k_count<<<L.T, kCountThreads, sizeof(int32_t) * M1, st>>>(cell_in, n, M, L.tile, tcount, err);
     mark(ev, 1, st);
     k_scan_tiles<<<(M1 + 31) / 32, dim3(32, kScanRows), 0, st>>>(tcount, L.T, M1, cnt);
-    k_scan_cells<<<1, 1024, 0, st>>>(cnt, M, off, chunk_off, at<int32_t>(ws, L.o_chunkcell), Cj, keys, k,
-                                     cell_base, step,
-                                     static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
+    k_scan_cells<<<1, 1024, 0, st>>>(cnt, M, off, chunk_off);
+    k_cell_setup<<<(M + 255) / 256, 256, 0, st>>>(cnt, chunk_off, M, at<int32_t>(ws, L.o_chunkcell), Cj, keys, k,
+                                                   cell_base, step, static_cast<uint32_t>(seed),
+                                                   static_cast<uint32_t>(seed >> 32));
     mark(ev, 2, st);
     if (v_in)
         k_scatter<true><<<L.T, 32 * L.W, smem, st>>>(v_in, ldv, cell_in, n, M, L.W, tcount, off, wsv, skip,
