@@ -22,3 +22,9 @@ for w in $WHAT; do
     prof_collide) timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_collide_large" -s 1 -c 1 -o gpurun_out/${TAG}_collide python bench.py --steps 1 --warmup 1 --no-cpu-baseline --e2e-steps 1 > gpurun_out/${TAG}_collide.log 2>&1; echo prof_collide rc=$? ;;
   esac
 done
+for w in $WHAT; do
+  case $w in
+    prof_scatter_steady) timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_scatter" -s 4 -c 1 -o gpurun_out/${TAG}_scatter_steady python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/${TAG}_scatter_steady.log 2>&1; echo prof_scatter_steady rc=$? ;;
+    prof_collide_steady) timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_collide_large" -s 4 -c 1 -o gpurun_out/${TAG}_collide_steady python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/${TAG}_collide_steady.log 2>&1; echo prof_collide_steady rc=$? ;;
+  esac
+done
