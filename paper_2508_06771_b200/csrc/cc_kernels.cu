@@ -104,41 +104,6 @@ __device__ __forceinline__ void st256(double* p, double a, double b, double c, d
                  : "memory");
 }
 
-// L2 eviction-priority policies (createpolicy) for loads/stores with cache hints.
-__device__ __forceinline__ uint64_t l2_policy_last()
-{
-    uint64_t p;
-    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-
-__device__ __forceinline__ uint64_t l2_policy_first()
-{
-    uint64_t p;
-    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-
-__device__ __forceinline__ int32_t ld_hint_i32(const int32_t* p, uint64_t pol)
-{
-    int32_t v;
-    asm("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
-    return v;
-}
-
-__device__ __forceinline__ double ld_hint_f64(const double* p, uint64_t pol)
-{
-    double v;
-    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
-    return v;
-}
-
-__device__ __forceinline__ void st256_hint(double* p, double a, double b, double c, double d, uint64_t pol)
-{
-    asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "d"(a), "d"(b), "d"(c),
-                 "d"(d), "l"(pol) : "memory");
-}
-
 __device__ __forceinline__ double pack_pc(int32_t perm, int32_t cell)
 {
     return __longlong_as_double((static_cast<long long>(static_cast<uint32_t>(cell)) << 32) |
@@ -374,14 +339,12 @@ __device__ __forceinline__ void tile_pre_store(double (&pre)[kTileSum], double* 
     }
 }
 
-// last use of the cell ids and of v: evict-first hints keep them from pushing
-// the tile's cell ids (read twice) out of L2
 template <bool HAS_V>
 __device__ __forceinline__ void load_batch(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__ cell,
-                                           int64_t i, double& x, double& y, double& z, int32_t& c, uint64_t pol)
+                                           int64_t i, double& x, double& y, double& z, int32_t& c)
 {
-    c = ld_hint_i32(cell + i, pol);
-    if (HAS_V) { x = ld_hint_f64(v + i, pol); y = ld_hint_f64(v + ldv + i, pol); z = ld_hint_f64(v + 2 * ldv + i, pol); }
+    c = __ldg(cell + i);
+    if (HAS_V) { x = __ldg(v + i); y = __ldg(v + ldv + i); z = __ldg(v + 2 * ldv + i); }
     else { x = y = z = 0.0; }
 }
 
@@ -394,7 +357,6 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     double pre[kTileSum] = {0.0, 0.0, 0.0, 0.0};      // pre-collision sums of the tile's live particles
-    const uint64_t pol_first = l2_policy_first(), pol_last = l2_policy_last();
     if (flags && flags[1] == 0) {
         // input already cell-sorted: the stable order is the identity, so the
         // records are written in place (a streaming SoA -> 32-byte-record pack)
@@ -406,7 +368,7 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
             int32_t c[kScatterUnrollB];
 #pragma unroll
             for (int u = 0; u < kScatterUnrollB; ++u)
-                load_batch<HAS_V>(v, ldv, cell, min(i0 + 32 * u + lane, t1 - 1), x[u], y[u], z[u], c[u], pol_first);
+                load_batch<HAS_V>(v, ldv, cell, min(i0 + 32 * u + lane, t1 - 1), x[u], y[u], z[u], c[u]);
 #pragma unroll
             for (int u = 0; u < kScatterUnrollB; ++u) {
                 const int64_t i = i0 + 32 * u + lane;
@@ -438,7 +400,7 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
 #pragma unroll
         for (int u = 0; u < kScatterUnrollA; ++u) {
             const int64_t i = i0 + 32 * u + lane;
-            const int32_t c = ld_hint_i32(cell + min(i, s1 - 1), pol_last);   // re-read in pass B
+            const int32_t c = __ldg(cell + min(i, s1 - 1));
             key[u] = (i >= s1) ? -1 - lane : ((c >= 0 && c < M) ? c : M);
         }
         uint32_t peers[kScatterUnrollA];
@@ -477,7 +439,7 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
         for (int u = 0; u < kScatterUnrollB; ++u) {
             const int64_t i = i0 + 32 * u + lane;
             int32_t c;
-            load_batch<HAS_V>(v, ldv, cell, min(i, s1 - 1), x[u], y[u], z[u], c, pol_first);
+            load_batch<HAS_V>(v, ldv, cell, min(i, s1 - 1), x[u], y[u], z[u], c);
             key[u] = (i >= s1) ? -1 - lane : ((c >= 0 && c < M) ? c : M);
         }
         uint32_t peers[kScatterUnrollB], old[kScatterUnrollB];
