@@ -28,6 +28,13 @@
 #include "../../include/coulomb.h"
 #include "cc_device.cuh"
 
+// Ablation switch for performance studies only (tools/ablate.sh); 0 in every
+// build of the product: bit 0 skips the TA math, bit 1 pairs slots 2k, 2k+1
+// (no Feistel), bit 2 skips CCS4 (Philox + AS241).
+#ifndef CC_ABLATE
+#define CC_ABLATE 0
+#endif
+
 namespace {
 
 constexpr int kCountThreads = 256;
@@ -692,7 +699,7 @@ k_collide_large(CollideArgs A)
             if (k < i1) {
                 const uint32_t e = k - i0;
                 uint32_t x[2] = {2 * k, 2 * k + 1};
-                cc::feistel_E_multi(f, x);
+                if (!(CC_ABLATE & 2)) cc::feistel_E_multi(f, x);
                 while (x[0] >= f.N) x[0] = cc::feistel_E(f, x[0]);       // cycle walking (rare)
                 stage_slot(A, o + static_cast<int64_t>(x[0]), stage + 4 * e);
                 if (2 * k + 1 < static_cast<uint32_t>(N)) {
@@ -709,8 +716,10 @@ k_collide_large(CollideArgs A)
         int qn = 0;
         double u1[kItemsPerThread], u2[kItemsPerThread];
 #pragma unroll
-        for (int t = 0; t < kItemsPerThread; ++t)      // independent Philox calls, interleaved
+        for (int t = 0; t < kItemsPerThread; ++t) {    // independent Philox calls, interleaved
+            if (CC_ABLATE & 4) { u1[t] = 0.3; u2[t] = 0.7; continue; }
             pair_uniforms(A, j, i0 + threadIdx.x + t * kCollideThreads, u1[t], u2[t]);
+        }
 #pragma unroll
         for (int t = 0; t < kItemsPerThread; ++t) {
             const uint32_t k = i0 + threadIdx.x + t * kCollideThreads;
@@ -742,7 +751,7 @@ k_collide_large(CollideArgs A)
     // phase 2b: CCS5 TA update out of shared memory, pair-ordered coalesced output
     Acc acc;
     acc.zero();
-#pragma unroll 1
+#pragma unroll
     for (int t = 0; t < kItemsPerThread; ++t) {
         const uint32_t k = i0 + threadIdx.x + t * kCollideThreads;
         if (k < i1) {
@@ -756,7 +765,7 @@ k_collide_large(CollideArgs A)
                 const double2 b23 = *reinterpret_cast<const double2*>(stage + 4 * (kChunk + e) + 2);
                 Rec b{b01.x, b01.y, b23.x, b23.y};
                 const int slot = t * 32 + lane;
-                cc::ta_update_z(a.x, a.y, a.z, b.x, b.y, b.z, C, zq[w][slot], u2q[w][slot]);
+                if (!(CC_ABLATE & 1)) cc::ta_update_z(a.x, a.y, a.z, b.x, b.y, b.z, C, zq[w][slot], u2q[w][slot]);
                 write_pair_out(A, pa, j, a, b);
                 acc.post(b.x, b.y, b.z, ref.x, ref.y, ref.z);
             } else {

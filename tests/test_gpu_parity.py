@@ -268,3 +268,54 @@ def test_moments_hook_matches_oracle(O):
 def test_diag_sum_ranks():
     g = torch.arange(3 * 16, dtype=torch.float64, device=DEV).reshape(3, 16)
     assert torch.equal(cc.cc_diag_sum_ranks(g), g[0] + g[1] + g[2])
+
+
+def test_steady_state_chain_with_drift(O):
+    """The bench headline's input pattern: each step consumes the previous
+    step's (cell-sorted, pair-ordered) output after a stand-in drift moved a
+    few percent of the particles to another cell; parity every step."""
+    w = W.c3(total=300_000, M=64)
+    p = w.params()
+    rng = np.random.default_rng(21)
+    gv, gc = to_dev(w.v), to_dev(w.cell)
+    rv, rc = w.v, w.cell
+    for s in range(4):
+        out = cc.coulomb_collide(gv, gc, w.cells, step=s, **p)
+        ref = O.coulomb_collide(rv, rc, w.cells, step=s, want_pairs=False, **p)
+        assert np.array_equal(out.perm_out.cpu().numpy(), ref.perm_out)
+        assert vel_err(out.v_out.cpu().numpy(), ref.v_out, 1e-3 * W.sigma_v(2.0)) <= TOL
+        check_moments(out.moments.cpu().numpy(), ref.moments, w)
+        # stand-in drift: 3% of the live particles move to a neighbouring cell
+        cell = ref.cell_out.copy()
+        mv = (rng.random(cell.size) < 0.03) & (cell >= 0)
+        cell[mv] = (cell[mv] + rng.choice([-1, 1], mv.sum())) % w.cells
+        gv, gc = out.v_out.clone(), to_dev(cell)
+        rv, rc = ref.v_out, cell
+
+
+def test_strided_rows_ldv_greater_than_n(O):
+    """[3][ldv] SoA views with ldv > n (odd and even ldv) are honoured."""
+    w = W.random_cells(10_001, 37, seed=23, skew=True)
+    for extra in (0, 3, 64):
+        ldv = w.n + extra
+        big = torch.zeros((3, ldv), dtype=torch.float64, device=DEV)
+        big[:, : w.n] = to_dev(w.v)
+        vin = big[:, : w.n]
+        vout_big = torch.full((3, ldv), 7.0, dtype=torch.float64, device=DEV)
+        out = cc.CollideOut(vout_big[:, : w.n], torch.empty(w.n, dtype=torch.int32, device=DEV),
+                            torch.empty(w.n, dtype=torch.int32, device=DEV),
+                            torch.empty((37, 7), dtype=torch.float64, device=DEV),
+                            torch.empty(16, dtype=torch.float64, device=DEV))
+        cc.coulomb_collide(vin, to_dev(w.cell), 37, step=2, out=out, **w.params())
+        ref = O.coulomb_collide(w.v, w.cell, 37, step=2, want_pairs=False, **w.params())
+        assert vel_err(vout_big[:, : w.n].cpu().numpy(), ref.v_out, 1.0) <= TOL
+        assert torch.all(vout_big[:, w.n:] == 7.0)          # padding untouched
+
+
+def test_large_cell_counts_and_max_cells(O):
+    """A cell larger than one collide chunk's worth of pairs many times over
+    (C2-like, 2e5 particles) and the CC_MAX_CELLS limit."""
+    w = W.random_cells(200_001, 1, seed=24)
+    check_collide(O, w, step=9)
+    w = W.random_cells(100_000, cc._lib.CC_MAX_CELLS, seed=25)
+    check_collide(O, w, step=1)
