@@ -1,0 +1,19 @@
+# compute-sanitizer memcheck / racecheck / synccheck on a small end-to-end case
+python -c "import __graft_entry__ as g; g.build()"
+cat > /tmp/san_case.py <<'PY'
+import sys; sys.path.insert(0, ".")
+import numpy as np, torch, workloads as W, paper_2508_06771_b200 as cc
+for (n, M, dead, skew) in [(5003, 37, 0.05, True), (40_000, 3, 0.0, False), (3000, 900, 0.1, True)]:
+    w = W.random_cells(n, M, seed=n, dead_frac=dead, skew=skew)
+    out = cc.coulomb_collide(torch.from_numpy(w.v).cuda(), torch.from_numpy(w.cell).cuda(), M, step=1, **w.params())
+    # sorted input path too
+    out2 = cc.coulomb_collide(out.v_out, out.cell_out, M, step=2, **w.params())
+    perm, off = cc.cc_bin(torch.from_numpy(w.cell).cuda(), M)
+    cc.cc_pairs(off, M)
+torch.cuda.synchronize()
+print("case ok")
+PY
+for tool in memcheck racecheck synccheck; do
+  timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python /tmp/san_case.py > gpurun_out/sanitize_$tool.log 2>&1
+  echo "$tool rc=$? $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY' gpurun_out/sanitize_$tool.log | tail -1)"
+done
