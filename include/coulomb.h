@@ -46,6 +46,17 @@ extern "C" {
 #define CC_ECOUNT (-5)      /* n >= 2^31 or cells > CC_MAX_CELLS */
 #define CC_ENCCL (-6)       /* reserved for the multi-GPU layer */
 
+/* cc_params.flags: collision-model variants (DESIGN R19-R20)
+ *  CC_ODD_TRIPLET  odd N_j >= 3: the last three particles of the pair order collide
+ *                  pairwise (1,2), (2,3), (3,1) with half the time step (TA77's rule)
+ *                  instead of one particle sitting out (R2).  Randoms: Philox(ctr =
+ *                  (q, G, step, 3)) for sub-collision q.
+ *  CC_NANBU        Nanbu (1997) cumulative scattering angle (the alternative the paper
+ *                  names) instead of TA77's Gaussian tan(Theta/2): s = 2<delta^2>,
+ *                  coth A - 1/A = exp(-s), cos chi = 1 + ln(u1 + (1-u1) e^{-2A})/A.      */
+#define CC_ODD_TRIPLET 1u
+#define CC_NANBU 2u
+
 #define CC_MAX_CELLS 32768  /* binning keeps per-warp cell counters in shared memory */
 #define CC_DIAG_LEN 16
 #define CC_MOMENTS_LEN 7
@@ -62,7 +73,7 @@ typedef struct cc_params {
     const double *cell_volume_arr;/* DEVICE [cells] or NULL                                */
     double ln_lambda;             /* Coulomb logarithm, used when ln_lambda_arr == NULL    */
     const double *ln_lambda_arr;  /* DEVICE [cells] or NULL                                */
-    uint32_t flags;               /* reserved, must be 0                                   */
+    uint32_t flags;               /* 0 (TA77, odd sitter) or CC_ODD_TRIPLET | CC_NANBU      */
     void *const *stage_events;    /* HOST array of CC_NUM_STAGES+1 cudaEvent_t, or NULL.
                                      When set, coulomb_collide records event i on `stream`
                                      before stage i and event CC_NUM_STAGES after the last
@@ -152,6 +163,13 @@ int cc_ta_pairs(double *va, double *vb, const double *C, const double *u1,
  * offsets off [cells+1] -> out [cells][7] (same layout as moments_out).      */
 int cc_moments(const double *v, int64_t ldv, const int32_t *off, int32_t cells,
                const cc_params *params, double *out, void *stream);
+
+/* NEXT f1 (R21): NRL electron-electron Coulomb logarithm from (lagged) moments:
+ * lnL_j = 23.5 - ln(n^1/2 T^-5/4) - sqrt(1e-5 + (ln T - 2)^2/16), n in cm^-3 from
+ * moments[j][0] (m^-3), T = (T_x+T_y+T_z)/3 eV from moments[j][4..6]; floored at 2.
+ * moments: DEVICE [cells][7] (coulomb_collide's moments_out); out: DEVICE [cells],
+ * usable as cc_params.ln_lambda_arr for the next step.                        */
+int cc_coulomb_log(const double *moments, int32_t cells, double *out, void *stream);
 
 /* Multi-GPU migration: out[p] = in[idx[p]] for p < m, for the
  * velocities [3][ldv] -> [3][ldo] and the cell ids; live cell ids are shifted

@@ -86,9 +86,20 @@ def lib():
             C.c_double, C.c_double, C.c_double, C.c_double,   # dt, mass, charge, eps0
             C.c_double, C.c_double, C.c_void_p,           # weight, volume, volume_arr
             C.c_double, C.c_void_p,                       # lnL, lnL_arr
-            C.c_uint64, C.c_uint64,                       # seed, step
+            C.c_uint64, C.c_uint64, C.c_uint32,           # seed, step, flags
             C.c_void_p, C.c_void_p, C.c_void_p]           # moments, diag, pair_slots
         L.or_coulomb_collide.restype = C.c_int
+        L.or_nanbu_A.argtypes = [C.c_double]
+        L.or_nanbu_A.restype = C.c_double
+        L.or_langevin.argtypes = [C.c_double]
+        L.or_langevin.restype = C.c_double
+        L.or_nanbu_pair.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_double]
+        L.or_nanbu_pair.restype = None
+        L.or_triplet.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_uint32, C.c_uint32,
+                                 C.c_uint64, C.c_uint32]
+        L.or_triplet.restype = None
+        L.or_coulomb_log.argtypes = [C.c_void_p, C.c_int32, C.c_void_p]
+        L.or_coulomb_log.restype = None
         L.or_num_threads.argtypes = []
         L.or_num_threads.restype = C.c_int
         _lib = L
@@ -204,9 +215,41 @@ class OracleResult:
     pair_slots: np.ndarray  # [pairs][2] stable slots
 
 
+ODD_TRIPLET = 1
+NANBU = 2
+
+
+def nanbu_A(s: float) -> float:
+    return lib().or_nanbu_A(s)
+
+
+def langevin(A: float) -> float:
+    return lib().or_langevin(A)
+
+
+def nanbu_pair(va, vb, Cj, u1, u2):
+    a = np.array(va, dtype=np.float64)
+    b = np.array(vb, dtype=np.float64)
+    lib().or_nanbu_pair(_ptr(a), _ptr(b), Cj, u1, u2)
+    return a, b
+
+
+def triplet(v1, v2, v3, Cj, G, step, seed, flags=0):
+    a, b, c = (np.array(x, dtype=np.float64) for x in (v1, v2, v3))
+    lib().or_triplet(_ptr(a), _ptr(b), _ptr(c), Cj, G, step, seed, flags)
+    return a, b, c
+
+
+def coulomb_log(moments):
+    m = np.ascontiguousarray(moments, dtype=np.float64)
+    out = np.zeros(m.shape[0], np.float64)
+    lib().or_coulomb_log(_ptr(m), m.shape[0], _ptr(out))
+    return out
+
+
 def coulomb_collide(v_in, cell_in, cells, *, dt, weight, cell_volume, ln_lambda=10.0,
                     cell_volume_arr=None, ln_lambda_arr=None, cell_base=0, seed=42, step=0,
-                    mass=M_E, charge=Q_E, eps0=EPS0, want_pairs=True) -> OracleResult:
+                    mass=M_E, charge=Q_E, eps0=EPS0, want_pairs=True, flags=0) -> OracleResult:
     """One call of the whole operator (Table 5 CCS1-CCS5 + moments/diagnostics)."""
     v_in = np.ascontiguousarray(v_in, dtype=np.float64)
     cell_in = np.ascontiguousarray(cell_in, dtype=np.int32)
@@ -224,7 +267,7 @@ def coulomb_collide(v_in, cell_in, cells, *, dt, weight, cell_volume, ln_lambda=
     rc = lib().or_coulomb_collide(_ptr(v_in), n, _ptr(cell_in), _ptr(v_out), _ptr(cell_out),
                                   _ptr(perm_out), n, cells, cell_base, dt, mass, charge, eps0,
                                   weight, cell_volume, _ptr(va), ln_lambda, _ptr(la),
-                                  seed, step, _ptr(mom), _ptr(diag), _ptr(pairs))
+                                  seed, step, flags, _ptr(mom), _ptr(diag), _ptr(pairs))
     if rc == -4:
         raise ValueError("invalid cell id")
     if rc != 0:

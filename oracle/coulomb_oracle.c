@@ -375,6 +375,145 @@ void or_ta_pair(double va[3], double vb[3], double C, double u1, double u2)
 }
 
 /* ------------------------------------------------------------------------ */
+/* NEXT row f1 — collision-model variants (R19-R21).                 */
+
+/* R20: Nanbu (1997) cumulative small-angle scattering, the alternative the
+ * paper names.  s = 2 <delta^2> = 2 C / |u|^3; A solves the inverse
+ * Langevin equation coth(A) - 1/A = exp(-s) (Newton iteration from Cohen's
+ * Pade start, A = 1/(1 - exp(-s)) where coth(A) = 1 in double precision);
+ * cos(chi) = 1 + ln(U1 + (1 - U1) exp(-2A)) / A  (A = 0: cos(chi) = 2 U1 - 1).   */
+/* Langevin function L(A) = coth A - 1/A and L'(A); Taylor series below
+ * A = 1/4 (8 terms, truncation < 1e-17 relative) where the closed forms cancel. */
+static const double OR_LANG_C[8] = { 1.0 / 3.0, -1.0 / 45.0, 2.0 / 945.0, -1.0 / 4725.0, 2.0 / 93555.0,
+                                     -1382.0 / 638512875.0, 4.0 / 18243225.0, -3617.0 / 162820783125.0 };
+static const double OR_LANGD_C[8] = { 1.0 / 3.0, -1.0 / 15.0, 2.0 / 189.0, -1.0 / 675.0, 2.0 / 10395.0,
+                                      -1382.0 / 58046625.0, 4.0 / 1403325.0, -3617.0 / 10854718875.0 };
+
+double or_langevin(double A)
+{
+    if (A < 0.25) {
+        double z = A * A, s = 0.0;
+        for (int i = 7; i >= 0; --i) s = s * z + OR_LANG_C[i];
+        return A * s;
+    }
+    return 1.0 / tanh(A) - 1.0 / A;
+}
+
+double or_langevin_d(double A)
+{
+    if (A < 0.25) {
+        double z = A * A, s = 0.0;
+        for (int i = 7; i >= 0; --i) s = s * z + OR_LANGD_C[i];
+        return s;
+    }
+    double sh = sinh(A);
+    return 1.0 / (A * A) - 1.0 / (sh * sh);
+}
+
+double or_nanbu_A(double s)
+{
+    if (!(s > 0.0)) return INFINITY;                 /* no scattering */
+    double x = exp(-s);                              /* <cos chi> */
+    if (x <= 0.0) return 0.0;                        /* isotropic */
+    double omx = -expm1(-s);                         /* 1 - x, accurately */
+    if (omx < 1.0 / 40.0) return 1.0 / omx;          /* A > 40: coth A = 1 in double, L = 1 - 1/A */
+    double A = x * (3.0 - x * x) / (1.0 - x * x);    /* Cohen's Pade start */
+    for (int it = 0; it < 60; ++it) {
+        double dA = (or_langevin(A) - x) / or_langevin_d(A);
+        A -= dA;
+        if (fabs(dA) <= 1e-15 * A) break;
+    }
+    return A;
+}
+
+/* Rotation of u by polar angle chi (given as sin chi and 1 - cos chi) and
+ * azimuth phi = 2 pi u2, written as TA77's component formula (R9), then the
+ * equal-mass split v_a += Du/2, v_b -= Du/2. */
+static void or_rotate_pair(double va[3], double vb[3], double sinT, double omc, double u2)
+{
+    double ux = va[0] - vb[0], uy = va[1] - vb[1], uz = va[2] - vb[2];
+    double u = sqrt(ux * ux + uy * uy + uz * uz);
+    double phi = 2.0 * M_PI * u2;
+    double cphi = cos(phi), sphi = sin(phi);
+    double dux, duy, duz;
+    if (ux == 0.0 && uy == 0.0) {
+        dux = u * sinT * cphi;
+        duy = u * sinT * sphi;
+        duz = -uz * omc;
+    } else {
+        double uperp = sqrt(ux * ux + uy * uy);
+        dux = (ux / uperp) * uz * sinT * cphi - (uy / uperp) * u * sinT * sphi - ux * omc;
+        duy = (uy / uperp) * uz * sinT * cphi + (ux / uperp) * u * sinT * sphi - uy * omc;
+        duz = -uperp * sinT * cphi - uz * omc;
+    }
+    va[0] += 0.5 * dux; va[1] += 0.5 * duy; va[2] += 0.5 * duz;
+    vb[0] -= 0.5 * dux; vb[1] -= 0.5 * duy; vb[2] -= 0.5 * duz;
+}
+
+void or_nanbu_pair(double va[3], double vb[3], double C, double u1, double u2)
+{
+    double ux = va[0] - vb[0], uy = va[1] - vb[1], uz = va[2] - vb[2];
+    if (ux == 0.0 && uy == 0.0 && uz == 0.0) return;
+    double usq = ux * ux + uy * uy + uz * uz;
+    double s = 2.0 * C / (usq * sqrt(usq));
+    double A = or_nanbu_A(s);
+    double omc;                                      /* 1 - cos(chi) */
+    if (isinf(A)) return;                            /* s = 0: no scattering */
+    if (A == 0.0) omc = 2.0 - 2.0 * u1;              /* cos chi = 2 u1 - 1 */
+    else omc = -log(u1 + (1.0 - u1) * exp(-2.0 * A)) / A;
+    if (omc > 2.0) omc = 2.0;
+    if (omc < 0.0) omc = 0.0;
+    double sinT = sqrt(omc * (2.0 - omc));
+    or_rotate_pair(va, vb, sinT, omc, u2);
+}
+
+#define OR_ODD_TRIPLET 1u
+#define OR_NANBU 2u
+
+/* one binary collision of the selected model */
+void or_collide_pair(double va[3], double vb[3], double C, double u1, double u2, uint32_t flags)
+{
+    if (flags & OR_NANBU) or_nanbu_pair(va, vb, C, u1, u2);
+    else or_ta_pair(va, vb, C, u1, u2);
+}
+
+/* R19: TA77's rule for an odd number of particles: the last three of the
+ * pair order, p1 = pi(N-3), p2 = pi(N-2), p3 = pi(N-1), collide pairwise
+ * (p1,p2), (p2,p3), (p3,p1) in that order, each with half the time step
+ * (C/2), randoms Philox(ctr = (q, G, step, 3)) for sub-collision q.            */
+void or_triplet(double v1[3], double v2[3], double v3[3], double C, uint32_t G, uint32_t step,
+                uint64_t seed, uint32_t flags)
+{
+    double *a[3] = { v1, v2, v3 }, *b[3] = { v2, v3, v1 };
+    uint32_t key[2] = { (uint32_t)seed, (uint32_t)(seed >> 32) };
+    for (uint32_t q = 0; q < 3; ++q) {
+        uint32_t ctr[4] = { q, G, step, 3u }, x[4];
+        or_philox4x32_10(ctr, key, x);
+        or_collide_pair(a[q], b[q], 0.5 * C, or_u01(x[0], x[1]), or_u01(x[2], x[3]), flags);
+    }
+}
+
+/* R21: NRL Plasma Formulary electron-electron Coulomb logarithm from lagged
+ * moments: lnL = 23.5 - ln(n_e^1/2 T^-5/4) - sqrt(1e-5 + (ln T - 2)^2 / 16),
+ * n_e in cm^-3, T = (T_x + T_y + T_z)/3 in eV; floored at 2;
+ * empty or cold cells get the floor.                                         */
+void or_coulomb_log(const double *moments, int32_t M, double *out)
+{
+    for (int32_t j = 0; j < M; ++j) {
+        const double *m = moments + 7 * (int64_t)j;
+        double n_cm = m[0] * 1e-6;
+        double T = (m[4] + m[5] + m[6]) / 3.0;
+        double l = 2.0;
+        if (n_cm > 0.0 && T > 0.0) {
+            double lt = log(T);
+            l = 23.5 - (0.5 * log(n_cm) - 1.25 * lt) - sqrt(1e-5 + (lt - 2.0) * (lt - 2.0) / 16.0);
+            if (!(l >= 2.0)) l = 2.0;
+        }
+        out[j] = l;
+    }
+}
+
+/* ------------------------------------------------------------------------ */
 /* P2C block reduction restricted to the operator's moments (P:330-342,
  * "V^j = sum_{x_l in omega_j} V_l"; T_e of P:336 with R13's constants):
  * out[j] = { n_j [m^-3], <v_x>, <v_y>, <v_z> [m/s], T_x, T_y, T_z [eV] } with
@@ -428,7 +567,7 @@ int or_coulomb_collide(const double *v_in, int64_t ldv, const int32_t *cell_in,
                        double dt, double mass, double charge, double eps0,
                        double weight, double volume, const double *volume_arr,
                        double lnL, const double *lnL_arr,
-                       uint64_t seed, uint64_t step,
+                       uint64_t seed, uint64_t step, uint32_t flags,
                        double *moments_out, double *diag_out, int64_t *pair_slots)
 {
     if (n < 0 || M < 1 || ldv < n || !(dt > 0.0)) return OR_EINVAL;
@@ -461,7 +600,9 @@ int or_coulomb_collide(const double *v_in, int64_t ldv, const int32_t *cell_in,
         or_cell_perm(N, G, (uint32_t)step, seed, pi);
         double C = or_cell_constant(N, weight, volume_arr ? volume_arr[j] : volume,
                                     lnL_arr ? lnL_arr[j] : lnL, dt, mass, charge, eps0);
-        for (int64_t k = 0; k < N / 2; ++k) {
+        int triplet = (flags & OR_ODD_TRIPLET) && N >= 3 && (N % 2 == 1);
+        int64_t npairs = triplet ? (N - 3) / 2 : N / 2;
+        for (int64_t k = 0; k < npairs; ++k) {
             int64_t sa = o + pi[2 * k];
             int64_t sb = o + pi[2 * k + 1];
             int64_t la = P[sa], lb = P[sb];
@@ -469,18 +610,31 @@ int or_coulomb_collide(const double *v_in, int64_t ldv, const int32_t *cell_in,
             double vb[3] = { v_in[lb], v_in[ldv + lb], v_in[2 * ldv + lb] };
             double u1, u2;
             or_pair_uniforms((uint32_t)k, G, (uint32_t)step, seed, &u1, &u2);
-            or_ta_pair(va, vb, C, u1, u2);
+            or_collide_pair(va, vb, C, u1, u2, flags);
             int64_t pa = o + 2 * k, pb = o + 2 * k + 1;
             for (int c = 0; c < 3; ++c) { v_out[c * ldv + pa] = va[c]; v_out[c * ldv + pb] = vb[c]; }
             perm_out[pa] = la; perm_out[pb] = lb;
             cell_out[pa] = j; cell_out[pb] = j;
-            if (pair_slots) {
+            if (pair_slots) {                       /* pi-pairs (default-mode layout) */
                 int64_t g = pair_off[j] + k;
                 pair_slots[2 * g] = sa;
                 pair_slots[2 * g + 1] = sb;
             }
         }
-        if (N % 2 == 1) {                               /* R2: one sits out */
+        if (triplet) {                                  /* R19: TA77 triplet */
+            int64_t l3[3];
+            double v3[3][3];
+            for (int q = 0; q < 3; ++q) {
+                l3[q] = P[o + pi[N - 3 + q]];
+                for (int c = 0; c < 3; ++c) v3[q][c] = v_in[c * ldv + l3[q]];
+            }
+            or_triplet(v3[0], v3[1], v3[2], C, G, (uint32_t)step, seed, flags);
+            for (int q = 0; q < 3; ++q) {
+                int64_t p = o + N - 3 + q;
+                for (int c = 0; c < 3; ++c) v_out[c * ldv + p] = v3[q][c];
+                perm_out[p] = l3[q]; cell_out[p] = j;
+            }
+        } else if (N % 2 == 1) {                        /* R2: one sits out */
             int64_t s = o + pi[N - 1];
             int64_t l = P[s], p = o + N - 1;
             for (int c = 0; c < 3; ++c) v_out[c * ldv + p] = v_in[c * ldv + l];

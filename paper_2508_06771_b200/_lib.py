@@ -23,12 +23,14 @@ CC_MAX_CELLS = 32768
 CC_DIAG_LEN = 16
 CC_MOMENTS_LEN = 7
 CC_NUM_STAGES = 5
+CC_ODD_TRIPLET = 1
+CC_NANBU = 2
 STAGE_NAMES = ("count", "scan", "scatter", "collide", "finalize")
 
 # every symbol include/coulomb.h declares
 EXPORTS = ("cc_default_params", "cc_workspace_bytes", "coulomb_collide", "cc_device_status",
            "cc_strerror", "cc_bin", "cc_pairs", "cc_philox", "cc_ppnd16", "cc_ta_pairs",
-           "cc_moments", "cc_gather", "cc_owner", "cc_diag_sum_ranks")
+           "cc_moments", "cc_coulomb_log", "cc_gather", "cc_owner", "cc_diag_sum_ranks")
 
 
 class CCParams(C.Structure):
@@ -82,6 +84,8 @@ def load():
     L.cc_ta_pairs.restype = C.c_int
     L.cc_moments.argtypes = [vp, i64, vp, i32, C.POINTER(CCParams), vp, vp]
     L.cc_moments.restype = C.c_int
+    L.cc_coulomb_log.argtypes = [vp, i32, vp, vp]
+    L.cc_coulomb_log.restype = C.c_int
     L.cc_gather.argtypes = [vp, i64, vp, vp, i64, i32, vp, i64, vp, vp]
     L.cc_gather.restype = C.c_int
     L.cc_owner.argtypes = [vp, i64, vp, i32, vp, vp]

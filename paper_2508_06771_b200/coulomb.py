@@ -48,13 +48,14 @@ def _soa(v: torch.Tensor, name: str, dev: torch.device) -> int:
 
 def make_params(*, mass=M_E, charge=Q_E, eps0=EPS0, weight=1.0, cell_volume=1.0, ln_lambda=10.0,
                 cell_volume_arr: Optional[torch.Tensor] = None,
-                ln_lambda_arr: Optional[torch.Tensor] = None) -> CCParams:
+                ln_lambda_arr: Optional[torch.Tensor] = None, flags: int = 0) -> CCParams:
     p = CCParams()
     _lib.load().cc_default_params(C.byref(p))
     p.mass, p.charge, p.eps0 = mass, charge, eps0
     p.weight, p.cell_volume, p.ln_lambda = weight, cell_volume, ln_lambda
     p.cell_volume_arr = None if cell_volume_arr is None else cell_volume_arr.data_ptr()
     p.ln_lambda_arr = None if ln_lambda_arr is None else ln_lambda_arr.data_ptr()
+    p.flags = flags
     return p
 
 
@@ -93,7 +94,7 @@ def coulomb_collide(v: torch.Tensor, cell: torch.Tensor, cells: int, *, dt: floa
                     seed: int = 42, step: int = 0, mass: float = M_E, charge: float = Q_E,
                     eps0: float = EPS0, out: Optional[CollideOut] = None,
                     workspace: Optional[torch.Tensor] = None, moments: bool = True,
-                    diag: bool = True) -> CollideOut:
+                    diag: bool = True, flags: int = 0) -> CollideOut:
     """One step of the Coulomb collision operator on CUDA tensors (see coulomb.h)."""
     dev = cell.device
     if dev.type != "cuda":
@@ -122,7 +123,8 @@ def coulomb_collide(v: torch.Tensor, cell: torch.Tensor, cells: int, *, dt: floa
             if arr.numel() != cells or not arr.is_contiguous():
                 raise ValueError(f"{nm} must be a contiguous [cells] tensor")
     p = make_params(mass=mass, charge=charge, eps0=eps0, weight=weight, cell_volume=cell_volume,
-                    ln_lambda=ln_lambda, cell_volume_arr=cell_volume_arr, ln_lambda_arr=ln_lambda_arr)
+                    ln_lambda=ln_lambda, cell_volume_arr=cell_volume_arr, ln_lambda_arr=ln_lambda_arr,
+                    flags=flags)
     rc = _lib.load().coulomb_collide(
         _ptr(v), max(ldv, n), _ptr(cell), _ptr(out.v_out), _ptr(out.cell_out), _ptr(out.perm_out),
         n, cells, cell_base, dt, C.byref(p), seed, step,
@@ -264,6 +266,17 @@ def cc_owner(cell_global: torch.Tensor, bounds) -> torch.Tensor:
     rc = _lib.load().cc_owner(_ptr(cell_global), cell_global.numel(), _ptr(b), b.numel() - 1, _ptr(out),
                               C.c_void_p(_stream(dev)))
     check(rc, "cc_owner")
+    return out
+
+
+def cc_coulomb_log(moments: torch.Tensor) -> torch.Tensor:
+    """NRL e-e Coulomb logarithm per cell from a [cells][7] moments tensor (R21)."""
+    dev = moments.device
+    _need(moments, "moments", torch.float64, dev)
+    m = moments.contiguous()
+    out = torch.empty(m.shape[0], dtype=torch.float64, device=dev)
+    rc = _lib.load().cc_coulomb_log(_ptr(m), m.shape[0], _ptr(out), C.c_void_p(_stream(dev)))
+    check(rc, "cc_coulomb_log")
     return out
 
 

@@ -279,6 +279,35 @@ __device__ __forceinline__ void sincos2pi(double u, double* sn, double* cs)
     *cs = ((qi + 1) & 2) ? -cc_ : cc_;
 }
 
+// ---------------------------------------------------------------- pair rotation
+// Rotate u = v_a - v_b by the polar angle Theta (given as sin Theta and
+// 1 - cos Theta) and azimuth phi = 2 pi u2 in TA77's component form (R9,
+// u_perp = 0 branch for u_x = u_y = 0), then v_a += Du/2, v_b -= Du/2.
+__device__ __forceinline__ void rotate_pair(double& ax, double& ay, double& az, double& bx, double& by, double& bz,
+                                            double ux, double uy, double uz, double u, double sinT, double omc,
+                                            double u2)
+{
+    double sphi, cphi;
+    sincos2pi(u2, &sphi, &cphi);
+    double dux, duy, duz;
+    if (ux == 0.0 && uy == 0.0) {
+        dux = u * sinT * cphi;
+        duy = u * sinT * sphi;
+        duz = -uz * omc;
+    } else {
+        const double up2 = fma(ux, ux, uy * uy);
+        const double ip = rsqrt_nr(up2);             // 1/u_perp
+        const double uperp = up2 * ip;
+        const double sc = sinT * cphi, ss = sinT * sphi;
+        const double A = uz * sc * ip, B = u * ss * ip;
+        dux = ux * A - uy * B - ux * omc;
+        duy = uy * A + ux * B - uy * omc;
+        duz = -uperp * sc - uz * omc;
+    }
+    ax = fma(0.5, dux, ax); ay = fma(0.5, duy, ay); az = fma(0.5, duz, az);
+    bx = fma(-0.5, dux, bx); by = fma(-0.5, duy, by); bz = fma(-0.5, duz, bz);
+}
+
 // ---------------------------------------------------------------- TA77 update
 // <delta^2> = C / |u|^3; delta = sqrt(<delta^2>) z with z = Phi^-1(u1);
 // tan(Theta/2) = delta; phi = 2 pi u2; v_a += Du/2, v_b -= Du/2.
@@ -301,25 +330,7 @@ __device__ __forceinline__ void ta_update_z(double& ax, double& ay, double& az,
     const double inv = rcp_nr(1.0 + d2);
     const double sinT = 2.0 * copysign(dd, delta) * inv;
     const double omc = 2.0 * d2 * inv;
-    double sphi, cphi;
-    sincos2pi(u2, &sphi, &cphi);
-    double dux, duy, duz;
-    if (ux == 0.0 && uy == 0.0) {
-        dux = u * sinT * cphi;
-        duy = u * sinT * sphi;
-        duz = -uz * omc;
-    } else {
-        const double up2 = fma(ux, ux, uy * uy);
-        const double ip = rsqrt_nr(up2);             // 1/u_perp
-        const double uperp = up2 * ip;
-        const double sc = sinT * cphi, ss = sinT * sphi;
-        const double A = uz * sc * ip, B = u * ss * ip;
-        dux = ux * A - uy * B - ux * omc;
-        duy = uy * A + ux * B - uy * omc;
-        duz = -uperp * sc - uz * omc;
-    }
-    ax = fma(0.5, dux, ax); ay = fma(0.5, duy, ay); az = fma(0.5, duz, az);
-    bx = fma(-0.5, dux, bx); by = fma(-0.5, duy, by); bz = fma(-0.5, duz, bz);
+    rotate_pair(ax, ay, az, bx, by, bz, ux, uy, uz, u, sinT, omc, u2);
 }
 
 __device__ __forceinline__ void ta_update(double& ax, double& ay, double& az,
@@ -327,6 +338,75 @@ __device__ __forceinline__ void ta_update(double& ax, double& ay, double& az,
                                           double C, double u1, double u2)
 {
     ta_update_z(ax, ay, az, bx, by, bz, C, ppnd16(u1), u2);
+}
+
+// ---------------------------------------------------------------- Nanbu (R20)
+// s = 2 <delta^2>; A solves coth A - 1/A = exp(-s) (inverse Langevin: Newton
+// from Cohen's Pade start; Taylor series of L and L' below A = 1/4; A = 1/(1 -
+// exp(-s)) when that exceeds 40); 1 - cos(chi) = -ln(u1 + (1-u1) e^{-2A}) / A.
+__constant__ double kLangC[8] = {1.0 / 3.0, -1.0 / 45.0, 2.0 / 945.0, -1.0 / 4725.0, 2.0 / 93555.0,
+                                 -1382.0 / 638512875.0, 4.0 / 18243225.0, -3617.0 / 162820783125.0};
+__constant__ double kLangD[8] = {1.0 / 3.0, -1.0 / 15.0, 2.0 / 189.0, -1.0 / 675.0, 2.0 / 10395.0,
+                                 -1382.0 / 58046625.0, 4.0 / 1403325.0, -3617.0 / 10854718875.0};
+
+__device__ __forceinline__ double langevin(double A, double* dL)
+{
+    if (A < 0.25) {
+        const double z = A * A;
+        double s = kLangC[7], d = kLangD[7];
+#pragma unroll
+        for (int i = 6; i >= 0; --i) { s = s * z + kLangC[i]; d = d * z + kLangD[i]; }
+        *dL = d;
+        return A * s;
+    }
+    const double sh = sinh(A);
+    *dL = 1.0 / (A * A) - 1.0 / (sh * sh);
+    return 1.0 / tanh(A) - 1.0 / A;
+}
+
+// returns A; +inf means "no scattering" (s = 0), 0 means isotropic
+__device__ __forceinline__ double nanbu_A(double s)
+{
+    if (!(s > 0.0)) return __longlong_as_double(0x7FF0000000000000ll);
+    const double x = exp(-s);
+    if (x <= 0.0) return 0.0;
+    const double omx = -expm1(-s);
+    if (omx < 1.0 / 40.0) return 1.0 / omx;
+    double A = x * (3.0 - x * x) / (1.0 - x * x);
+    for (int it = 0; it < 60; ++it) {
+        double dL;
+        const double dA = (langevin(A, &dL) - x) / dL;
+        A -= dA;
+        if (fabs(dA) <= 1e-15 * A) break;
+    }
+    return A;
+}
+
+__device__ __forceinline__ void nanbu_update(double& ax, double& ay, double& az, double& bx, double& by, double& bz,
+                                             double C, double u1, double u2)
+{
+    const double ux = ax - bx, uy = ay - by, uz = az - bz;
+    if (ux == 0.0 && uy == 0.0 && uz == 0.0) return;
+    const double usq = fma(ux, ux, fma(uy, uy, uz * uz));
+    const double u = sqrt(usq);
+    const double s = 2.0 * C / (usq * u);
+    const double A = nanbu_A(s);
+    if (isinf(A)) return;
+    double omc = (A == 0.0) ? 2.0 - 2.0 * u1 : -log(u1 + (1.0 - u1) * exp(-2.0 * A)) / A;
+    omc = fmin(fmax(omc, 0.0), 2.0);
+    const double sinT = sqrt(omc * (2.0 - omc));
+    rotate_pair(ax, ay, az, bx, by, bz, ux, uy, uz, u, sinT, omc, u2);
+}
+
+constexpr uint32_t kOddTriplet = 1u;   // CC_ODD_TRIPLET
+constexpr uint32_t kNanbu = 2u;        // CC_NANBU
+
+// one binary collision of the selected model (u1 uniform)
+__device__ __forceinline__ void collide_model(double& ax, double& ay, double& az, double& bx, double& by, double& bz,
+                                              double C, double u1, double u2, uint32_t flags)
+{
+    if (flags & kNanbu) nanbu_update(ax, ay, az, bx, by, bz, C, u1, u2);
+    else ta_update(ax, ay, az, bx, by, bz, C, u1, u2);
 }
 
 }  // namespace cc

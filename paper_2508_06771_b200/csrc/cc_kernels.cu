@@ -56,7 +56,7 @@ struct Layout {
     int W = 1, tile = kSub, T = 0;
     int64_t max_chunks = 0;
     size_t o_err = 0, o_tcount = 0, o_cnt = 0, o_off = 0, o_chunk = 0, o_C = 0, o_keys = 0;
-    size_t o_small = 0, o_recs = 0, o_cellsum = 0, o_ref = 0, o_tilesum = 0, o_chunkcell = 0, o_wsv = 0, total = 0;
+    size_t o_small = 0, o_recs = 0, o_cellsum = 0, o_ref = 0, o_tilesum = 0, o_chunkcell = 0, o_trec = 0, o_wsv = 0, total = 0;
 };
 
 size_t align256(size_t x) { return (x + 255u) & ~static_cast<size_t>(255u); }
@@ -88,6 +88,7 @@ Layout make_layout(int64_t n, int32_t M)
     L.o_recs = o;     o = align256(o + static_cast<size_t>(L.max_chunks) * kRec * sizeof(double));
     L.o_cellsum = o;  o = align256(o + static_cast<size_t>(M) * kCellSum * sizeof(double));
     L.o_ref = o;      o = align256(o + static_cast<size_t>(M) * 4 * sizeof(double));
+    L.o_trec = o;     o = align256(o + static_cast<size_t>(M) * kRec * sizeof(double));
     L.o_tilesum = o;  o = align256(o + static_cast<size_t>(L.T > 0 ? L.T : 1) * kTileSum * sizeof(double));
     L.o_chunkcell = o; o = align256(o + static_cast<size_t>(L.max_chunks) * sizeof(int32_t));
     L.o_wsv = o;      o = align256(o + static_cast<size_t>(n > 0 ? n : 1) * 4 * sizeof(double));
@@ -493,6 +494,8 @@ struct CollideArgs {
     double* cellref;            // [M][4] shift of large cells (pre-collision v of the first slot)
     int M;
     int pf_dist;                // k_collide_large: L2-prefetch the slice share of chunk c + pf_dist
+    uint32_t model;             // CC_ODD_TRIPLET | CC_NANBU (NEXT f1 collision-model variants)
+    double* trec;               // [M][kRec] triplet moment records of large odd cells (triplet mode)
     int pair_vec;               // outputs aligned for 16-byte (v) / 8-byte (cell, perm) pair stores
     uint32_t cell_base, step, s0, s1;
 };
@@ -570,6 +573,19 @@ __device__ __forceinline__ void warp_reduce(double (&a)[NV])
         for (int d = 16; d > 0; d >>= 1) a[q] += __shfl_down_sync(0xFFFFFFFFu, a[q], d);
 }
 
+// R19: TA77 odd-count triplet — (1,2), (2,3), (3,1) in order, each with C/2,
+// randoms Philox(ctr = (q, G, step, 3)) for sub-collision q; r[] in place.
+__device__ __forceinline__ void triplet_update(const CollideArgs& A, uint32_t G, double C, Rec (&r)[3])
+{
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        const cc::U4 x = cc::philox4x32_10(cc::U4{static_cast<uint32_t>(q), G, A.step, 3u}, A.s0, A.s1);
+        Rec& a = r[q];
+        Rec& b = r[(q + 1) % 3];
+        cc::collide_model(a.x, a.y, a.z, b.x, b.y, b.z, 0.5 * C, cc::u01(x.x, x.y), cc::u01(x.z, x.w), A.model);
+    }
+}
+
 // N_j <= 64: one warp per cell; item k = lane.  The warp holds the whole cell,
 // so its moment record is an exact two-pass one about the post-collision mean.
 __global__ void __launch_bounds__(256)
@@ -589,14 +605,26 @@ k_collide_small(CollideArgs A)
     acc.zero();
     const uint32_t items = static_cast<uint32_t>(N + 1) / 2;
     const uint32_t k = static_cast<uint32_t>(lane);
-    if (k < items) {
+    const bool triplet = (A.model & cc::kOddTriplet) && N >= 3 && (N & 1);
+    if (triplet && k == items - 2) {
+        // R19: the last three of the pair order collide as a TA77 triplet
+        Rec r[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) r[q] = load_slot(A, o + pi_sm[w][N - 3 + q]);
+        triplet_update(A, G, C, r);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            write_out(A, o + N - 3 + q, j, r[q]);
+            acc.post(r[q].x, r[q].y, r[q].z, 0.0, 0.0, 0.0);
+        }
+    } else if (k < items && !(triplet && k == items - 1)) {
         const int32_t pa = o + 2 * static_cast<int32_t>(k);
         Rec a = load_slot(A, o + pi_sm[w][2 * k]);
         if (2 * k + 1 < static_cast<uint32_t>(N)) {
             Rec b = load_slot(A, o + pi_sm[w][2 * k + 1]);
             double u1, u2;
             pair_uniforms(A, j, k, u1, u2);
-            cc::ta_update(a.x, a.y, a.z, b.x, b.y, b.z, C, u1, u2);
+            cc::collide_model(a.x, a.y, a.z, b.x, b.y, b.z, C, u1, u2, A.model);
             write_out(A, pa + 1, j, b);
             acc.post(b.x, b.y, b.z, 0.0, 0.0, 0.0);
         }
@@ -688,6 +716,7 @@ k_collide_large(CollideArgs A)
     const uint32_t items = static_cast<uint32_t>(N + 1) / 2;
     const uint32_t i0 = static_cast<uint32_t>(c - A.chunk_off[j]) * kChunk;
     const uint32_t i1 = min(i0 + static_cast<uint32_t>(kChunk), items);
+    const bool triplet = (A.model & cc::kOddTriplet) && (N & 1);   // N > 64 here
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     // phase 1: pi_j (keyed Feistel, R1) of each item's two slots in lock step
     // (rare cycle walks afterwards), gathers issued item by item
@@ -724,9 +753,10 @@ k_collide_large(CollideArgs A)
         for (int t = 0; t < kItemsPerThread; ++t) {
             const uint32_t k = i0 + threadIdx.x + t * kCollideThreads;
             const bool pair = (k < i1) && (2 * k + 1 < static_cast<uint32_t>(N));
-            const bool tail = pair && !cc::ppnd16_is_central(u1[t]);
+            const bool nanbu = A.model & cc::kNanbu;       // Nanbu samples from u1 itself (phase 2b)
+            const bool tail = pair && !nanbu && !cc::ppnd16_is_central(u1[t]);
             const int slot = t * 32 + lane;
-            zq[w][slot] = tail ? cc::ppnd16_tail_arg(u1[t]) : cc::ppnd16_central(u1[t]);
+            zq[w][slot] = nanbu ? u1[t] : tail ? cc::ppnd16_tail_arg(u1[t]) : cc::ppnd16_central(u1[t]);
             u2q[w][slot] = u2[t];
             const uint32_t tm = __ballot_sync(0xFFFFFFFFu, tail);
             if (tail) tq[w][qn + __popc(tm & lt)] = static_cast<int16_t>(slot);
@@ -754,7 +784,7 @@ k_collide_large(CollideArgs A)
 #pragma unroll
     for (int t = 0; t < kItemsPerThread; ++t) {
         const uint32_t k = i0 + threadIdx.x + t * kCollideThreads;
-        if (k < i1) {
+        if (k < i1 && !(triplet && k + 2 >= items)) {     // the triplet's two items: k_triplets
             const uint32_t e = k - i0;
             const int32_t pa = o + 2 * static_cast<int32_t>(k);
             const double2 a01 = *reinterpret_cast<const double2*>(stage + 4 * e);
@@ -765,7 +795,10 @@ k_collide_large(CollideArgs A)
                 const double2 b23 = *reinterpret_cast<const double2*>(stage + 4 * (kChunk + e) + 2);
                 Rec b{b01.x, b01.y, b23.x, b23.y};
                 const int slot = t * 32 + lane;
-                if (!(CC_ABLATE & 1)) cc::ta_update_z(a.x, a.y, a.z, b.x, b.y, b.z, C, zq[w][slot], u2q[w][slot]);
+                if (A.model & cc::kNanbu)
+                    cc::nanbu_update(a.x, a.y, a.z, b.x, b.y, b.z, C, zq[w][slot], u2q[w][slot]);
+                else if (!(CC_ABLATE & 1))
+                    cc::ta_update_z(a.x, a.y, a.z, b.x, b.y, b.z, C, zq[w][slot], u2q[w][slot]);
                 write_pair_out(A, pa, j, a, b);
                 acc.post(b.x, b.y, b.z, ref.x, ref.y, ref.z);
             } else {
@@ -786,6 +819,37 @@ k_collide_large(CollideArgs A)
             for (int ww = 0; ww < kCollideThreads / 32; ++ww) sum += red[ww][threadIdx.x];
         A.recs[static_cast<int64_t>(c) * kRec + threadIdx.x] = sum;
     }
+}
+
+// Triplet mode, N_j > 64 and odd: thread per cell runs R19 on the last three
+// slots of the pair order and writes their moment partials (about the cell's
+// shift) to trec[j]; every other large cell gets a zero record.
+__global__ void k_triplets(CollideArgs A)
+{
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= A.M) return;
+    const int32_t N = A.cnt[j];
+    if (N <= cc::kSmallCell) return;
+    double* tr = A.trec + static_cast<int64_t>(j) * kRec;
+    Acc acc;
+    acc.zero();
+    if (N & 1) {
+        const int32_t o = A.off[j];
+        const cc::Feistel f = cc::make_feistel(static_cast<uint32_t>(N), A.keys[j]);
+        Rec r[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) r[q] = load_slot(A, o + static_cast<int64_t>(cc::feistel_pi(f, N - 3 + q)));
+        triplet_update(A, A.cell_base + static_cast<uint32_t>(j), A.Cj[j], r);
+        const double* cr = A.cellref + 4 * static_cast<int64_t>(j);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            write_out(A, o + N - 3 + q, j, r[q]);
+            acc.post(r[q].x, r[q].y, r[q].z, cr[0], cr[1], cr[2]);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 6; ++q) tr[q] = acc.a[q];
+    tr[6] = tr[7] = 0.0;
 }
 
 // Dead (and invalid) particles: slots [L, n), copied unchanged.
@@ -823,8 +887,8 @@ __device__ __forceinline__ void moments_from_sums(const double* s, double N, dou
 
 __global__ void k_finalize_cells(const int32_t* __restrict__ cnt, const int32_t* __restrict__ chunk_off,
                                  const double* __restrict__ recs, const double* __restrict__ small_recs,
-                                 const double* __restrict__ cellref, int M, MomConst mc,
-                                 double* __restrict__ moments_out, double* __restrict__ cellsum)
+                                 const double* __restrict__ cellref, const double* __restrict__ trec, int M,
+                                 MomConst mc, double* __restrict__ moments_out, double* __restrict__ cellsum)
 {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= M) return;
@@ -843,6 +907,9 @@ __global__ void k_finalize_cells(const int32_t* __restrict__ cnt, const int32_t*
             for (int32_t c = chunk_off[j]; c < chunk_off[j + 1]; ++c)
 #pragma unroll
                 for (int q = 0; q < 6; ++q) s[q] += recs[static_cast<int64_t>(c) * kRec + q];
+            if (trec)
+#pragma unroll
+                for (int q = 0; q < 6; ++q) s[q] += trec[static_cast<int64_t>(j) * kRec + q];
         }
     }
     if (moments_out) {
@@ -1064,6 +1131,22 @@ __global__ void k_owner(const int32_t* __restrict__ cell, int64_t n, const int32
     }
 }
 
+__global__ void k_coulomb_log(const double* __restrict__ m, int M, double* __restrict__ out)
+{
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= M) return;
+    const double* r = m + static_cast<int64_t>(j) * CC_MOMENTS_LEN;
+    const double n_cm = r[0] * 1e-6;
+    const double T = (r[4] + r[5] + r[6]) / 3.0;
+    double l = 2.0;
+    if (n_cm > 0.0 && T > 0.0) {
+        const double lt = log(T);
+        l = 23.5 - (0.5 * log(n_cm) - 1.25 * lt) - sqrt(1e-5 + (lt - 2.0) * (lt - 2.0) / 16.0);
+        if (!(l >= 2.0)) l = 2.0;
+    }
+    out[j] = l;
+}
+
 __global__ void k_diag_sum_ranks(const double* __restrict__ g, int P, double* __restrict__ out)
 {
     const int q = threadIdx.x;
@@ -1221,7 +1304,7 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     if (n >= (1ll << 31) || cells > CC_MAX_CELLS) return CC_ECOUNT;
     if (!finite_pos(p.mass) || !finite_pos(p.charge) || !finite_pos(p.eps0) || !std::isfinite(p.weight) ||
         p.weight < 0.0 || (!p.cell_volume_arr && !finite_pos(p.cell_volume)) ||
-        (!p.ln_lambda_arr && !std::isfinite(p.ln_lambda)) || p.flags != 0)
+        (!p.ln_lambda_arr && !std::isfinite(p.ln_lambda)) || (p.flags & ~(CC_ODD_TRIPLET | CC_NANBU)) != 0)
         return CC_EINVAL;
     if (!workspace || !aligned(workspace, 256)) return CC_EWORKSPACE;
     const Layout L = make_layout(n, cells);
@@ -1272,6 +1355,8 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     A.s0 = static_cast<uint32_t>(seed);
     A.s1 = static_cast<uint32_t>(seed >> 32);
     A.pf_dist = prefetch_distance();
+    A.model = p.flags;
+    A.trec = at<double>(workspace, L.o_trec);
     A.pair_vec = aligned(v_out, 16) && (ldv % 2 == 0) && aligned(cell_out, 8) && (!perm_out || aligned(perm_out, 8));
 
     mark(ev, 3, st);
@@ -1279,12 +1364,14 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     if (rc) return rc;
     k_collide_small<<<(M + 7) / 8, 256, 0, st>>>(A);
     k_collide_large<<<static_cast<unsigned>(L.max_chunks), kCollideThreads, kCollideSmem, st>>>(A);
+    if (A.model & CC_ODD_TRIPLET) k_triplets<<<(M + 255) / 256, 256, 0, st>>>(A);
     k_copy_dead<<<148 * 4, 256, 0, st>>>(A, nn);
 
     MomConst mc{p.weight, p.cell_volume, p.cell_volume_arr, p.mass / p.charge};
     double* cellsum = at<double>(workspace, L.o_cellsum);
     mark(ev, 4, st);
-    k_finalize_cells<<<(M + 255) / 256, 256, 0, st>>>(A.cnt, A.chunk_off, A.recs, A.small_recs, A.cellref, M, mc,
+    k_finalize_cells<<<(M + 255) / 256, 256, 0, st>>>(A.cnt, A.chunk_off, A.recs, A.small_recs, A.cellref,
+                                                      (A.model & CC_ODD_TRIPLET) ? A.trec : nullptr, M, mc,
                                                       moments_out, cellsum);
     if (diag_out)
         k_finalize_diag<<<1, 1024, 0, st>>>(A.cnt, cellsum, M, at<double>(workspace, L.o_tilesum), L.T, diag_out);
@@ -1409,6 +1496,14 @@ int cc_owner(const int32_t* cell, int64_t n, const int32_t* bounds, int32_t nran
     if (!cell || !bounds || !owner_out) return CC_EINVAL;
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 16));
     k_owner<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(cell, n, bounds, nranks, owner_out);
+    return launch_ok();
+}
+
+int cc_coulomb_log(const double* moments, int32_t cells, double* out, void* stream)
+{
+    cudaGetLastError();   // launch errors below are ours, not a stale earlier one
+    if (!moments || !out || cells < 1) return CC_EINVAL;
+    k_coulomb_log<<<(cells + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(moments, cells, out);
     return launch_ok();
 }
 

@@ -319,3 +319,30 @@ def test_large_cell_counts_and_max_cells(O):
     check_collide(O, w, step=9)
     w = W.random_cells(100_000, cc._lib.CC_MAX_CELLS, seed=25)
     check_collide(O, w, step=1)
+
+
+@pytest.mark.parametrize("flags", [1, 2, 3])
+@pytest.mark.parametrize("n,M,skew", [(30_001, 7, False), (50_000, 600, True), (999, 1, False), (3, 1, False)])
+def test_model_variants_parity(O, flags, n, M, skew):
+    """NEXT f1: TA77 odd triplet (1), Nanbu sampler (2), both (3) vs the oracle."""
+    w = W.random_cells(n, M, seed=n + M + flags, skew=skew)
+    p = w.params()
+    out = cc.coulomb_collide(to_dev(w.v), to_dev(w.cell), M, step=5, flags=flags, **p)
+    ref = O.coulomb_collide(w.v, w.cell, M, step=5, flags=flags, want_pairs=False, **p)
+    assert np.array_equal(out.perm_out.cpu().numpy(), ref.perm_out)
+    assert vel_err(out.v_out.cpu().numpy(), ref.v_out, 1e-3 * W.sigma_v(2.0)) <= TOL
+    check_moments(out.moments.cpu().numpy(), ref.moments, w)
+    check_diag(out.diag.cpu().numpy(), ref.diag, ref.v_out)
+
+
+def test_coulomb_log_matches_oracle(O):
+    w = W.c3(total=500_000, M=64)
+    out = cc.coulomb_collide(to_dev(w.v), to_dev(w.cell), w.cells, step=0, **w.params())
+    lnl = cc.cc_coulomb_log(out.moments).cpu().numpy()
+    ref = O.coulomb_log(out.moments.cpu().numpy())
+    assert np.max(np.abs(lnl - ref)) <= 1e-13 * np.max(ref)
+    # feed it back as the per-cell Coulomb logarithm of the next step
+    out2 = cc.coulomb_collide(out.v_out, out.cell_out, w.cells, step=1, ln_lambda_arr=to_dev(ref), **w.params())
+    r2 = O.coulomb_collide(out.v_out.cpu().numpy(), out.cell_out.cpu().numpy(), w.cells, step=1,
+                           ln_lambda_arr=ref, want_pairs=False, **w.params())
+    assert vel_err(out2.v_out.cpu().numpy(), r2.v_out, 1.0) <= TOL
