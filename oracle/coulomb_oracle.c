@@ -381,7 +381,8 @@ void or_ta_pair(double va[3], double vb[3], double C, double u1, double u2)
  * paper names.  s = 2 <delta^2> = 2 C / |u|^3; A solves the inverse
  * Langevin equation coth(A) - 1/A = exp(-s) (Newton iteration from Cohen's
  * Pade start, A = 1/(1 - exp(-s)) where coth(A) = 1 in double precision);
- * cos(chi) = 1 + ln(U1 + (1 - U1) exp(-2A)) / A  (A = 0: cos(chi) = 2 U1 - 1).   */
+ * cos(chi) = 1 + ln(U1 + (1 - U1) exp(-2A)) / A  (A = 0: cos(chi) = 2 U1 - 1),
+ * evaluated as 1 - cos(chi) = -log1p((1 - U1) expm1(-2A)) / A.                */
 /* Langevin function L(A) = coth A - 1/A and L'(A); Taylor series below
  * A = 1/4 (8 terms, truncation < 1e-17 relative) where the closed forms cancel. */
 static const double OR_LANG_C[8] = { 1.0 / 3.0, -1.0 / 45.0, 2.0 / 945.0, -1.0 / 4725.0, 2.0 / 93555.0,
@@ -459,8 +460,11 @@ void or_nanbu_pair(double va[3], double vb[3], double C, double u1, double u2)
     double A = or_nanbu_A(s);
     double omc;                                      /* 1 - cos(chi) */
     if (isinf(A)) return;                            /* s = 0: no scattering */
+    /* 1 - cos chi = -ln(u1 + (1-u1) e^{-2A}) / A, written as
+     * -log1p((1-u1) expm1(-2A)) / A: the same number without the cancellation
+     * of ln(1 - tiny) for small A (A -> 0 gives the isotropic 2(1-u1)). */
     if (A == 0.0) omc = 2.0 - 2.0 * u1;              /* cos chi = 2 u1 - 1 */
-    else omc = -log(u1 + (1.0 - u1) * exp(-2.0 * A)) / A;
+    else omc = -log1p((1.0 - u1) * expm1(-2.0 * A)) / A;
     if (omc > 2.0) omc = 2.0;
     if (omc < 0.0) omc = 0.0;
     double sinT = sqrt(omc * (2.0 - omc));

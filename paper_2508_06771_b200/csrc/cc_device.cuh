@@ -392,7 +392,8 @@ __device__ __forceinline__ void nanbu_update(double& ax, double& ay, double& az,
     const double s = 2.0 * C / (usq * u);
     const double A = nanbu_A(s);
     if (isinf(A)) return;
-    double omc = (A == 0.0) ? 2.0 - 2.0 * u1 : -log(u1 + (1.0 - u1) * exp(-2.0 * A)) / A;
+    // 1 - cos chi = -ln(u1 + (1-u1) e^{-2A}) / A = -log1p((1-u1) expm1(-2A)) / A (no cancellation)
+    double omc = (A == 0.0) ? 2.0 - 2.0 * u1 : -log1p((1.0 - u1) * expm1(-2.0 * A)) / A;
     omc = fmin(fmax(omc, 0.0), 2.0);
     const double sinT = sqrt(omc * (2.0 - omc));
     rotate_pair(ax, ay, az, bx, by, bz, ux, uy, uz, u, sinT, omc, u2);
