@@ -343,7 +343,7 @@ __device__ __forceinline__ void ta_update(double& ax, double& ay, double& az,
 // ---------------------------------------------------------------- Nanbu (R20)
 // s = 2 <delta^2>; A solves coth A - 1/A = exp(-s) (inverse Langevin: Newton
 // from Cohen's Pade start; Taylor series of L and L' below A = 1/4; A = 1/(1 -
-// exp(-s)) when that exceeds 40); 1 - cos(chi) = -ln(u1 + (1-u1) e^{-2A}) / A.
+// exp(-s)) when that exceeds 40); 1 - cos(chi) = -log1p((1-u1) expm1(-2A)) / A.
 __constant__ double kLangC[8] = {1.0 / 3.0, -1.0 / 45.0, 2.0 / 945.0, -1.0 / 4725.0, 2.0 / 93555.0,
                                  -1382.0 / 638512875.0, 4.0 / 18243225.0, -3617.0 / 162820783125.0};
 __constant__ double kLangD[8] = {1.0 / 3.0, -1.0 / 15.0, 2.0 / 189.0, -1.0 / 675.0, 2.0 / 10395.0,

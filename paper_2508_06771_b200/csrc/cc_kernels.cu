@@ -684,6 +684,7 @@ constexpr int kWarpItems = 32 * kItemsPerThread;            // items of one warp
 constexpr size_t kCollideSmem = 2ull * kChunk * 4 * sizeof(double);
 static_assert(kChunk % kCollideThreads == 0, "chunk must be a whole number of thread items");
 
+template <bool NANBU>
 __global__ void __launch_bounds__(kCollideThreads, 3)
 k_collide_large(CollideArgs A)
 {
@@ -753,7 +754,7 @@ k_collide_large(CollideArgs A)
         for (int t = 0; t < kItemsPerThread; ++t) {
             const uint32_t k = i0 + threadIdx.x + t * kCollideThreads;
             const bool pair = (k < i1) && (2 * k + 1 < static_cast<uint32_t>(N));
-            const bool nanbu = A.model & cc::kNanbu;       // Nanbu samples from u1 itself (phase 2b)
+            const bool nanbu = NANBU;                       // Nanbu samples from u1 itself (phase 2b)
             const bool tail = pair && !nanbu && !cc::ppnd16_is_central(u1[t]);
             const int slot = t * 32 + lane;
             zq[w][slot] = nanbu ? u1[t] : tail ? cc::ppnd16_tail_arg(u1[t]) : cc::ppnd16_central(u1[t]);
@@ -795,7 +796,7 @@ k_collide_large(CollideArgs A)
                 const double2 b23 = *reinterpret_cast<const double2*>(stage + 4 * (kChunk + e) + 2);
                 Rec b{b01.x, b01.y, b23.x, b23.y};
                 const int slot = t * 32 + lane;
-                if (A.model & cc::kNanbu)
+                if (NANBU)
                     cc::nanbu_update(a.x, a.y, a.z, b.x, b.y, b.z, C, zq[w][slot], u2q[w][slot]);
                 else if (!(CC_ABLATE & 1))
                     cc::ta_update_z(a.x, a.y, a.z, b.x, b.y, b.z, C, zq[w][slot], u2q[w][slot]);
@@ -1360,10 +1361,14 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     A.pair_vec = aligned(v_out, 16) && (ldv % 2 == 0) && aligned(cell_out, 8) && (!perm_out || aligned(perm_out, 8));
 
     mark(ev, 3, st);
-    rc = want_smem(k_collide_large, kCollideSmem);
+    rc = want_smem(k_collide_large<false>, kCollideSmem);
+    if (!rc) rc = want_smem(k_collide_large<true>, kCollideSmem);
     if (rc) return rc;
     k_collide_small<<<(M + 7) / 8, 256, 0, st>>>(A);
-    k_collide_large<<<static_cast<unsigned>(L.max_chunks), kCollideThreads, kCollideSmem, st>>>(A);
+    if (A.model & CC_NANBU)
+        k_collide_large<true><<<static_cast<unsigned>(L.max_chunks), kCollideThreads, kCollideSmem, st>>>(A);
+    else
+        k_collide_large<false><<<static_cast<unsigned>(L.max_chunks), kCollideThreads, kCollideSmem, st>>>(A);
     if (A.model & CC_ODD_TRIPLET) k_triplets<<<(M + 255) / 256, 256, 0, st>>>(A);
     k_copy_dead<<<148 * 4, 256, 0, st>>>(A, nn);
 
