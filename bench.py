@@ -278,8 +278,11 @@ def run_ours(args):
     nst = _lib.CC_NUM_STAGES
     lib = _lib.load()
 
+    model = {"flags": 0}
+
     def call(src_v, src_cell, dst, step, events=None, post=None):
-        prm = cc.make_params(weight=p["weight"], cell_volume=p["cell_volume"], ln_lambda=p["ln_lambda"])
+        prm = cc.make_params(weight=p["weight"], cell_volume=p["cell_volume"], ln_lambda=p["ln_lambda"],
+                             flags=model["flags"])
         if events is not None:
             arr = (C.c_void_p * (nst + 1))(*[e.cuda_event for e in events])
             prm.stage_events = C.cast(arr, C.POINTER(C.c_void_p))
@@ -348,6 +351,14 @@ def run_ours(args):
     res = {"steady": run_mode("steady", K, W, 0, clk),
            "cold": run_mode("cold", K, W, 100_000),
            "warm": run_mode("warm", K, W, 200_000)}
+    # NEXT f1 collision-model variants, steady state (shorter runs)
+    variants = {}
+    for name, fl in (("odd_triplet", _lib.CC_ODD_TRIPLET), ("nanbu", _lib.CC_NANBU)):
+        model["flags"] = fl
+        r = run_mode("steady", max(3, K // 4), W, 400_000 + 1000 * fl)
+        variants[name] = {"flags": fl, "ms_per_step": r["ms"], "stages_ms": r["stages"],
+                          "value": r["pairs"] / (r["ms"] * 1e-3)}
+    model["flags"] = 0
 
     # ---- end-to-end through the public API with host buffers (pinned), cold input
     v_pin = v_host.pin_memory()
@@ -434,6 +445,7 @@ def run_ours(args):
                 "h2d_bytes_per_step": int(v_host.numel() * 8 + c_host.numel() * 4),
                 "d2h_bytes_per_step": int(n * 24 + n * 8), "ms_per_step": e2e_ms,
                 "what": "coulomb_collide with host buffers: pinned H2D of v and cell ids, D2H of v, cell, perm"},
+        "variants": variants,
         "gpu_launches": 10 * K + (K if world > 1 else 0),
         "clocks": clk.summary(),
     }
