@@ -402,12 +402,8 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
     uint32_t* my = wcnt + w * MW;
     const uint32_t lt = (1u << lane) - 1u;
 
-    // pass A: per-warp counts of the sub-range (loads batched, branch-free).
-    // A register-cached "run" cell absorbs the lanes that share it (the PIC
-    // steady state feeds nearly sorted input: most lanes of a group are in the
-    // run); only the other lanes go through match.any + shared atomics.  The
-    // run cell may change only at batch boundaries.
-    int32_t run_key = -1;
+    // pass A: per-warp counts of the sub-range (loads batched, branch-free)
+    int32_t run_key = -1;                  // register-cached run of one cell (fast path)
     uint32_t run_cnt = 0;
     for (int64_t i0 = s0; i0 < s1; i0 += 32 * kScatterUnrollA) {
         int32_t key[kScatterUnrollA];
@@ -417,35 +413,36 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
             const int32_t c = __ldg(cell + min(i, s1 - 1));
             key[u] = (i >= s1) ? -1 - lane : ((c >= 0 && c < M) ? c : M);
         }
-        const int32_t cand = __shfl_sync(0xFFFFFFFFu, key[0], 0);
-        if (cand != run_key && cand >= 0 && cand == __shfl_sync(0xFFFFFFFFu, key[0], 31)) {
-            __syncwarp();
-            if (run_key >= 0 && lane == 0) my[run_key >> 1] += run_cnt << ((run_key & 1) << 4);
-            __syncwarp();
-            run_key = cand;
-            run_cnt = 0;
-        }
-        bool any_slow = false;
-        int32_t skey[kScatterUnrollA];
+        // fast path (nearly sorted input, the PIC steady state): every 32-element
+        // group of the batch is a single cell -> count in a register
+        bool uni = true;
 #pragma unroll
-        for (int u = 0; u < kScatterUnrollA; ++u) {
-            const bool in_run = key[u] == run_key;
-            run_cnt += __popc(__ballot_sync(0xFFFFFFFFu, in_run));
-            skey[u] = in_run ? -1 - lane : key[u];
-            any_slow = any_slow || __any_sync(0xFFFFFFFFu, skey[u] >= 0);
+        for (int u = 0; u < kScatterUnrollA; ++u)
+            uni = uni && __all_sync(0xFFFFFFFFu, key[u] == __shfl_sync(0xFFFFFFFFu, key[u], 0) && key[u] >= 0);
+        if (uni) {
+            __syncwarp();                          // earlier slow-path atomics of this warp are visible
+#pragma unroll
+            for (int u = 0; u < kScatterUnrollA; ++u) {
+                if (key[u] != run_key) {
+                    __syncwarp();
+    if (run_key >= 0 && lane == 0) my[run_key >> 1] += run_cnt << ((run_key & 1) << 4);
+                    run_key = key[u];
+                    run_cnt = 0;
+                }
+                run_cnt += 32;
+            }
+            continue;
         }
-        if (!any_slow) continue;
         uint32_t peers[kScatterUnrollA];
 #pragma unroll
-        for (int u = 0; u < kScatterUnrollA; ++u) peers[u] = __match_any_sync(0xFFFFFFFFu, skey[u]);
+        for (int u = 0; u < kScatterUnrollA; ++u) peers[u] = __match_any_sync(0xFFFFFFFFu, key[u]);
 #pragma unroll
         for (int u = 0; u < kScatterUnrollA; ++u) {
-            const int32_t b = max(skey[u], 0);
-            red_add_if(skey[u] >= 0 && lane == __ffs(peers[u]) - 1, my + (b >> 1),
+            const int32_t b = max(key[u], 0);
+            red_add_if(key[u] >= 0 && lane == __ffs(peers[u]) - 1, my + (b >> 1),
                        static_cast<uint32_t>(__popc(peers[u])) << ((b & 1) << 4));
         }
     }
-    __syncwarp();
     if (run_key >= 0 && lane == 0) my[run_key >> 1] += run_cnt << ((run_key & 1) << 4);
     __syncthreads();
     // exclusive scan over warps per cell; CTA base = cell offset + tile offset
@@ -465,8 +462,7 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
     }
     __syncthreads();
 
-    // pass B: ranks, destinations, 32-byte records (loads batched, branch-free);
-    // the run cell's running offset lives in a register (same rule as pass A)
+    // pass B: ranks, destinations, 32-byte records (loads batched, branch-free)
     run_key = -1;
     uint32_t run_pos = 0;
     int32_t run_base = 0;
@@ -480,54 +476,68 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
             load_batch<HAS_V>(v, ldv, cell, min(i, s1 - 1), x[u], y[u], z[u], c);
             key[u] = (i >= s1) ? -1 - lane : ((c >= 0 && c < M) ? c : M);
         }
-        const int32_t cand = __shfl_sync(0xFFFFFFFFu, key[0], 0);
-        if (cand != run_key && cand >= 0 && cand == __shfl_sync(0xFFFFFFFFu, key[0], 31)) {
+        // fast path (nearly sorted input): every 32-element group of the batch is
+        // one cell -> slots come from a register-cached running offset
+        bool uni = true;
+#pragma unroll
+        for (int u = 0; u < kScatterUnrollB; ++u)
+            uni = uni && __all_sync(0xFFFFFFFFu, key[u] == __shfl_sync(0xFFFFFFFFu, key[u], 0) && key[u] >= 0);
+        if (uni) {
+            __syncwarp();                          // earlier slow-path atomics of this warp are visible
+#pragma unroll
+            for (int u = 0; u < kScatterUnrollB; ++u) {
+                const int32_t b = key[u];
+                if (b != run_key) {
+                    if (run_key >= 0) {                 // write the running offset back
+                        __syncwarp();
+                        if (lane == 0) {
+                            const uint32_t sh = (run_key & 1) << 4;
+                            uint32_t* wd = my + (run_key >> 1);
+                            *wd = (*wd & ~(0xFFFFu << sh)) | ((run_pos & 0xFFFFu) << sh);
+                        }
+                        __syncwarp();
+                    }
+                    run_key = b;
+                    run_pos = (my[b >> 1] >> ((b & 1) << 4)) & 0xFFFFu;
+                    run_base = base[b];
+                }
+                const int32_t dest = run_base + static_cast<int32_t>(run_pos) + lane;
+                run_pos += 32;
+                const int64_t i = i0 + 32 * u + lane;
+                st256(wsv + 4 * static_cast<int64_t>(dest), x[u], y[u], z[u],
+                      pack_pc(static_cast<int32_t>(i), b < M ? b : -1));
+                if (b < M) tile_pre_add(pre, x[u], y[u], z[u]);
+            }
+            continue;
+        }
+        if (run_key >= 0) {                             // leave the fast path: flush the cache
             __syncwarp();
-            if (run_key >= 0 && lane == 0) {        // write the cached running offset back
+            if (lane == 0) {
                 const uint32_t sh = (run_key & 1) << 4;
                 uint32_t* wd = my + (run_key >> 1);
                 *wd = (*wd & ~(0xFFFFu << sh)) | ((run_pos & 0xFFFFu) << sh);
             }
             __syncwarp();
-            run_key = cand;
-            run_pos = (my[cand >> 1] >> ((cand & 1) << 4)) & 0xFFFFu;
-            run_base = base[cand];
+            run_key = -1;
         }
-        bool any_slow = false;
-        int32_t skey[kScatterUnrollB], dest[kScatterUnrollB];
+        uint32_t peers[kScatterUnrollB], old[kScatterUnrollB];
+#pragma unroll
+        for (int u = 0; u < kScatterUnrollB; ++u) peers[u] = __match_any_sync(0xFFFFFFFFu, key[u]);
 #pragma unroll
         for (int u = 0; u < kScatterUnrollB; ++u) {
-            const bool in_run = key[u] == run_key;
-            const uint32_t m = __ballot_sync(0xFFFFFFFFu, in_run);
-            dest[u] = run_base + static_cast<int32_t>(run_pos) + __popc(m & lt);
-            run_pos += __popc(m);
-            skey[u] = in_run ? -1 - lane : key[u];
-            any_slow = any_slow || __any_sync(0xFFFFFFFFu, skey[u] >= 0);
-        }
-        if (any_slow) {
-            uint32_t peers[kScatterUnrollB], old[kScatterUnrollB];
-#pragma unroll
-            for (int u = 0; u < kScatterUnrollB; ++u) peers[u] = __match_any_sync(0xFFFFFFFFu, skey[u]);
-#pragma unroll
-            for (int u = 0; u < kScatterUnrollB; ++u) {
-                const int32_t b = max(skey[u], 0);
-                old[u] = atom_add_if(skey[u] >= 0 && lane == __ffs(peers[u]) - 1, my + (b >> 1),
-                                     static_cast<uint32_t>(__popc(peers[u])) << ((b & 1) << 4));
-            }
-#pragma unroll
-            for (int u = 0; u < kScatterUnrollB; ++u) {
-                const int32_t b = skey[u];
-                const uint32_t o = __shfl_sync(0xFFFFFFFFu, (old[u] >> ((max(b, 0) & 1) << 4)) & 0xFFFFu,
-                                               __ffs(peers[u]) - 1);
-                if (b >= 0) dest[u] = base[b] + static_cast<int32_t>(o) + __popc(peers[u] & lt);
-            }
+            const int32_t b = max(key[u], 0);
+            old[u] = atom_add_if(key[u] >= 0 && lane == __ffs(peers[u]) - 1, my + (b >> 1),
+                                 static_cast<uint32_t>(__popc(peers[u])) << ((b & 1) << 4));
         }
 #pragma unroll
         for (int u = 0; u < kScatterUnrollB; ++u) {
             const int32_t b = key[u];
+            const uint32_t o = __shfl_sync(0xFFFFFFFFu, (old[u] >> ((max(b, 0) & 1) << 4)) & 0xFFFFu,
+                                           __ffs(peers[u]) - 1);
             if (b >= 0) {
+                const int32_t dest = base[b] + static_cast<int32_t>(o) + __popc(peers[u] & lt);
                 const int64_t i = i0 + 32 * u + lane;
-                st256(wsv + 4 * static_cast<int64_t>(dest[u]), x[u], y[u], z[u],
+                st256(wsv + 4 * static_cast<int64_t>(dest), x[u], y[u], z[u],
                       pack_pc(static_cast<int32_t>(i), b < M ? b : -1));
                 if (b < M) tile_pre_add(pre, x[u], y[u], z[u]);
             }
