@@ -403,8 +403,6 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
     const uint32_t lt = (1u << lane) - 1u;
 
     // pass A: per-warp counts of the sub-range (loads batched, branch-free)
-    int32_t run_key = -1;                  // register-cached run of one cell (fast path)
-    uint32_t run_cnt = 0;
     for (int64_t i0 = s0; i0 < s1; i0 += 32 * kScatterUnrollA) {
         int32_t key[kScatterUnrollA];
 #pragma unroll
@@ -412,26 +410,6 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
             const int64_t i = i0 + 32 * u + lane;
             const int32_t c = __ldg(cell + min(i, s1 - 1));
             key[u] = (i >= s1) ? -1 - lane : ((c >= 0 && c < M) ? c : M);
-        }
-        // fast path (nearly sorted input, the PIC steady state): every 32-element
-        // group of the batch is a single cell -> count in a register
-        bool uni = true;
-#pragma unroll
-        for (int u = 0; u < kScatterUnrollA; ++u)
-            uni = uni && __all_sync(0xFFFFFFFFu, key[u] == __shfl_sync(0xFFFFFFFFu, key[u], 0) && key[u] >= 0);
-        if (uni) {
-            __syncwarp();                          // earlier slow-path atomics of this warp are visible
-#pragma unroll
-            for (int u = 0; u < kScatterUnrollA; ++u) {
-                if (key[u] != run_key) {
-                    __syncwarp();
-    if (run_key >= 0 && lane == 0) my[run_key >> 1] += run_cnt << ((run_key & 1) << 4);
-                    run_key = key[u];
-                    run_cnt = 0;
-                }
-                run_cnt += 32;
-            }
-            continue;
         }
         uint32_t peers[kScatterUnrollA];
 #pragma unroll
@@ -443,7 +421,6 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
                        static_cast<uint32_t>(__popc(peers[u])) << ((b & 1) << 4));
         }
     }
-    if (run_key >= 0 && lane == 0) my[run_key >> 1] += run_cnt << ((run_key & 1) << 4);
     __syncthreads();
     // exclusive scan over warps per cell; CTA base = cell offset + tile offset
     const int32_t* trow = tbase + static_cast<int64_t>(blockIdx.x) * M1;
@@ -463,9 +440,6 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
     __syncthreads();
 
     // pass B: ranks, destinations, 32-byte records (loads batched, branch-free)
-    run_key = -1;
-    uint32_t run_pos = 0;
-    int32_t run_base = 0;
     for (int64_t i0 = s0; i0 < s1; i0 += 32 * kScatterUnrollB) {
         int32_t key[kScatterUnrollB];
         double x[kScatterUnrollB], y[kScatterUnrollB], z[kScatterUnrollB];
@@ -475,50 +449,6 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
             int32_t c;
             load_batch<HAS_V>(v, ldv, cell, min(i, s1 - 1), x[u], y[u], z[u], c);
             key[u] = (i >= s1) ? -1 - lane : ((c >= 0 && c < M) ? c : M);
-        }
-        // fast path (nearly sorted input): every 32-element group of the batch is
-        // one cell -> slots come from a register-cached running offset
-        bool uni = true;
-#pragma unroll
-        for (int u = 0; u < kScatterUnrollB; ++u)
-            uni = uni && __all_sync(0xFFFFFFFFu, key[u] == __shfl_sync(0xFFFFFFFFu, key[u], 0) && key[u] >= 0);
-        if (uni) {
-            __syncwarp();                          // earlier slow-path atomics of this warp are visible
-#pragma unroll
-            for (int u = 0; u < kScatterUnrollB; ++u) {
-                const int32_t b = key[u];
-                if (b != run_key) {
-                    if (run_key >= 0) {                 // write the running offset back
-                        __syncwarp();
-                        if (lane == 0) {
-                            const uint32_t sh = (run_key & 1) << 4;
-                            uint32_t* wd = my + (run_key >> 1);
-                            *wd = (*wd & ~(0xFFFFu << sh)) | ((run_pos & 0xFFFFu) << sh);
-                        }
-                        __syncwarp();
-                    }
-                    run_key = b;
-                    run_pos = (my[b >> 1] >> ((b & 1) << 4)) & 0xFFFFu;
-                    run_base = base[b];
-                }
-                const int32_t dest = run_base + static_cast<int32_t>(run_pos) + lane;
-                run_pos += 32;
-                const int64_t i = i0 + 32 * u + lane;
-                st256(wsv + 4 * static_cast<int64_t>(dest), x[u], y[u], z[u],
-                      pack_pc(static_cast<int32_t>(i), b < M ? b : -1));
-                if (b < M) tile_pre_add(pre, x[u], y[u], z[u]);
-            }
-            continue;
-        }
-        if (run_key >= 0) {                             // leave the fast path: flush the cache
-            __syncwarp();
-            if (lane == 0) {
-                const uint32_t sh = (run_key & 1) << 4;
-                uint32_t* wd = my + (run_key >> 1);
-                *wd = (*wd & ~(0xFFFFu << sh)) | ((run_pos & 0xFFFFu) << sh);
-            }
-            __syncwarp();
-            run_key = -1;
         }
         uint32_t peers[kScatterUnrollB], old[kScatterUnrollB];
 #pragma unroll
