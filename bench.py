@@ -410,13 +410,23 @@ def run_ours(args):
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
 
-    def roofline(r):
+    traffic = {}
+    try:      # DRAM bytes per launch from the committed ncu capture of this config (tools/traffic_from_ncu.py)
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+    except Exception:
+        pass
+    kernel_of = {"count": "k_count", "scatter": "k_scatter", "collide": "k_collide_large"}
+
+    def roofline(r, with_traffic=False):
         st = r["stages"]
         dom = max(("count", "scatter", "collide"), key=lambda k: st[k])
         achieved = STAGE_BYTES[dom] * n / (st[dom] * 1e-3) / 1e9
+        tr = traffic.get(kernel_of[dom], {}).get("dram_bytes_per_launch") if (world == 1 and with_traffic) else None
         return {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": None, "algorithmic_bytes_per_particle": STAGE_BYTES[dom],
-                "peak_source": peak_src}
+                "frac": achieved / hbm_peak, "traffic": tr,
+                "traffic_source": "profiles/traffic.json (ncu --set full, same config)" if tr else None,
+                "algorithmic_bytes_per_launch": STAGE_BYTES[dom] * n,
+                "algorithmic_bytes_per_particle": STAGE_BYTES[dom], "peak_source": peak_src}
 
     def summary(r):
         return {"value": r["pairs"] / (r["ms"] * 1e-3), "ms_per_step": r["ms"], "wall_ms_per_step": r["wall_ms"],
@@ -435,7 +445,7 @@ def run_ours(args):
                    "l2": "inputs 2.87 GB/GPU >> 126 MB L2 (no flush needed)",
                    "timing": "CUDA events around each operator call (drift excluded), mean of K",
                    "parallelism": f"cell-range shards x{world}" if world > 1 else "1 GPU"},
-        "roofline": roofline(head),
+        "roofline": roofline(head, with_traffic=True),
         "stages_ms": head["stages"],
         "step_hbm": {"algorithmic_bytes_per_particle": STEP_BYTES_PER_PARTICLE,
                      "frac": STEP_BYTES_PER_PARTICLE * n / (head["ms"] * 1e-3) / 1e9 / hbm_peak},
