@@ -88,7 +88,12 @@ def workload_name(args, world):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks/throttle reasons sampled around the timed region.
+
+    Sampling starts before the warm-up (nvidia-smi needs ~100 ms to emit its
+    first line); `mark()` brackets the timed region and `summary()` keeps the
+    samples taken inside it (or, if the region is shorter than the sampling
+    period, the nearest ones)."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -97,24 +102,37 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.proc = None
-        self.lines = []
+        self.lines = []            # (time, line)
+        self.t0 = self.t1 = None
 
-    def __enter__(self):
+    def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
                  "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            deadline = time.time() + 5.0
+            while not self.lines and time.time() < deadline:
+                time.sleep(0.01)
         except FileNotFoundError:
             self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
-    def __exit__(self, *a):
+    def mark(self, begin: bool):
+        if begin:
+            self.t0 = time.time()
+        else:
+            self.t1 = time.time()
+            deadline = self.t1 + 0.5          # one more sample after the region
+            while self.proc and time.time() < deadline and (not self.lines or self.lines[-1][0] < self.t1):
+                time.sleep(0.01)
+
+    def stop(self):
         if self.proc:
             self.proc.terminate()
             try:
@@ -123,9 +141,15 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = self.lines
+        if self.t0 is not None and self.t1 is not None:
+            inside = [x for x in lines if self.t0 <= x[0] <= self.t1 + 0.05]
+            if not inside and lines:          # region shorter than the sampling period
+                inside = sorted(lines, key=lambda x: abs(x[0] - 0.5 * (self.t0 + self.t1)))[:2]
+            lines = inside
+        sm, mx, reasons = [], None, set()
+        for _, ln in lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 8:
                 continue
@@ -323,7 +347,7 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
         if sampler:
-            sampler.__enter__()
+            sampler.mark(True)
         t0.record(stream)
         for s in range(K):
             dst = bufs[(W + s) % 2]
@@ -335,7 +359,7 @@ def run_ours(args):
         t1.record(stream)
         torch.cuda.synchronize()
         if sampler:
-            sampler.__exit__()
+            sampler.mark(False)
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
@@ -347,10 +371,11 @@ def run_ours(args):
                 "pairs": float(bufs[(W + K - 1) % 2].diag[2].item())}
 
     K, W = args.steps, args.warmup
-    clk = ClockSampler(local)
+    clk = ClockSampler(local).start()
     res = {"steady": run_mode("steady", K, W, 0, clk),
            "cold": run_mode("cold", K, W, 100_000),
            "warm": run_mode("warm", K, W, 200_000)}
+    clk.stop()
     # NEXT f1 collision-model variants, steady state (shorter runs)
     variants = {}
     for name, fl in (("odd_triplet", _lib.CC_ODD_TRIPLET), ("nanbu", _lib.CC_NANBU)):
