@@ -88,83 +88,81 @@ def workload_name(args, world):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled around the timed region.
+    """SM clocks and clock-event (throttle) reasons sampled through NVML every
+    ~2 ms from a background thread; `mark()` brackets the timed region and
+    `summary()` keeps the samples taken inside it.  (nvidia-smi -lms could not
+    resolve a ~70 ms timed region: round-1 runs recorded 0 samples.)"""
 
-    Sampling starts before the warm-up (nvidia-smi needs ~100 ms to emit its
-    first line); `mark()` brackets the timed region and `summary()` keeps the
-    samples taken inside it (or, if the region is shorter than the sampling
-    period, the nearest ones)."""
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_s: float = 0.002):
         self.index = index
-        self.proc = None
-        self.lines = []            # (time, line)
+        self.period = period_s
+        self.samples = []          # (time, sm_mhz, reasons bitmask)
         self.t0 = self.t1 = None
+        self.max_mhz = None
+        self.err = None
+        self._stop = threading.Event()
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-            deadline = time.time() + 5.0
-            while not self.lines and time.time() < deadline:
-                time.sleep(0.01)
-        except FileNotFoundError:
-            self.proc = None
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = self.index
+            if vis:                                  # NVML indexes physical GPUs
+                ids = [x.strip() for x in vis.split(",") if x.strip()]
+                if idx < len(ids) and ids[idx].isdigit():
+                    idx = int(ids[idx])
+            self.h = N.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM))
+            self.thread = threading.Thread(target=self._run, daemon=True)
+            self.thread.start()
+        except Exception as e:                       # never let clock sampling kill the bench
+            self.err = repr(e)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append((time.time(), line.strip()))
+    def _run(self):
+        N = self.N
+        while not self._stop.is_set():
+            try:
+                sm = N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)
+                rs = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((time.time(), float(sm), int(rs)))
+            except Exception as e:
+                self.err = repr(e)
+                return
+            time.sleep(self.period)
 
     def mark(self, begin: bool):
         if begin:
             self.t0 = time.time()
         else:
             self.t1 = time.time()
-            deadline = self.t1 + 0.5          # one more sample after the region
-            while self.proc and time.time() < deadline and (not self.lines or self.lines[-1][0] < self.t1):
-                time.sleep(0.01)
 
     def stop(self):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self._stop.set()
+        if hasattr(self, "thread"):
+            self.thread.join(timeout=2)
 
     def summary(self):
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        lines = self.lines
+        s = self.samples
         if self.t0 is not None and self.t1 is not None:
-            inside = [x for x in lines if self.t0 <= x[0] <= self.t1 + 0.05]
-            if not inside and lines:          # region shorter than the sampling period
-                inside = sorted(lines, key=lambda x: abs(x[0] - 0.5 * (self.t0 + self.t1)))[:2]
-            lines = inside
-        sm, mx, reasons = [], None, set()
-        for _, ln in lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 8:
-                continue
-            try:
-                sm.append(float(f[0]))
-                mx = float(f[1])
-            except ValueError:
-                continue
-            for nm, val in zip(names, f[4:8]):
-                if val.lower().startswith("active"):
-                    reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+            s = [x for x in s if self.t0 <= x[0] <= self.t1]
+        if not s:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0,
+                    "source": "nvml", "error": self.err}
+        N = self.N
+        reasons = sorted({nm for _, _, rs in s for nm, attr in self.REASONS
+                          if hasattr(N, attr) and rs & getattr(N, attr)})
+        return {"sm_mhz": statistics.median(x[1] for x in s), "sm_min_mhz": min(x[1] for x in s),
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(s),
+                "source": "nvml, 2 ms period, timed region of the headline mode"}
 
 
 # ---------------------------------------------------------------- CPU oracle (baseline / reference arm)
