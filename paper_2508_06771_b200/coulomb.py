@@ -84,7 +84,9 @@ def alloc_workspace(n: int, cells: int, device) -> torch.Tensor:
     nbytes = cc_workspace_bytes(n, cells)
     ws = torch.empty(nbytes + 256, dtype=torch.uint8, device=device)
     pad = (-ws.data_ptr()) % 256
-    return ws[pad:pad + nbytes]
+    ws = ws[pad:pad + nbytes]
+    ws[:256].zero_()          # the device error flags (cc_device_status) start clear
+    return ws
 
 
 def coulomb_collide(v: torch.Tensor, cell: torch.Tensor, cells: int, *, dt: float,
