@@ -74,6 +74,10 @@ typedef struct cc_params {
     double ln_lambda;             /* Coulomb logarithm, used when ln_lambda_arr == NULL    */
     const double *ln_lambda_arr;  /* DEVICE [cells] or NULL                                */
     uint32_t flags;               /* 0 (TA77, odd sitter) or CC_ODD_TRIPLET | CC_NANBU      */
+    const uint32_t *step_dev;     /* DEVICE uint32 or NULL: when set, the effective step is
+                                     (step + *step_dev) mod 2^32, read on the device, so a
+                                     captured CUDA graph replays with advancing randoms
+                                     (cc_step_advance); NEXT f2 subcycled loop.           */
     void *const *stage_events;    /* HOST array of CC_NUM_STAGES+1 cudaEvent_t, or NULL.
                                      When set, coulomb_collide records event i on `stream`
                                      before stage i and event CC_NUM_STAGES after the last
@@ -186,6 +190,45 @@ int cc_owner(const int32_t *cell, int64_t n, const int32_t *bounds, int32_t nran
 /* Multi-GPU: rank-ascending sum of P gathered diagnostics vectors
  * gathered [P][16] -> out [16] (deterministic for a given P).   */
 int cc_diag_sum_ranks(const double *gathered, int32_t nranks, double *out, void *stream);
+
+/* ---- NEXT f2: the kinetic push of a subcycled PIC loop ---------- */
+
+/* Regular grid of the push (HOST struct).  Global cell id of a position:
+ * i_a = floor(x_a / d[a]) clamped to n[a]-1, G = i_0 + n[0] (i_1 + n[1] i_2)
+ * ("j = floor(x/dx)"; readings R22-R24).                         */
+typedef struct cc_grid {
+    int32_t dims;            /* 1, 2 or 3 position components in use (x, y, z) */
+    int32_t n[3];            /* global cells per axis; n[a] = 1 for a >= dims   */
+    double d[3];             /* cell size per axis [m]                          */
+    uint32_t periodic;       /* bit a set: axis a periodic (wraps by L_a = n[a] d[a]);
+                                clear: absorbing, a particle leaving [0, L_a) dies
+                                (Table 3 CS7)                    */
+} cc_grid;
+
+/* Steps S2b + S2c of Table 2 (SPEC push S:204-210) for n particles
+ * in the OUTPUT order of a coulomb_collide call:
+ *   v' = v + dt (q/m) E[cell]   (per-cell constant field; E NULL = 0)
+ *   x' = x + dt v'              (position rows a < dims; boundary per axis)
+ *   cell' = global cell of x', or -1 if absorbed.
+ *  x_in   [3][ldx_in] fp64 positions; row a of particle p is read at index
+ *         perm[p] (perm = coulomb_collide's perm_out, or NULL = p).
+ *  x_out  [3][ldx_out] fp64, written for all n (rows >= dims copied).
+ *         Must not alias x_in unless perm == NULL and the rows coincide.
+ *  v      [3][ldv] fp64, updated in place (live particles).
+ *  cell   [n] int32, in place: in = LOCAL cell of the collision call (-1 dead,
+ *         E row), out = GLOBAL cell after the push (-1 dead).
+ *  cells, cell_base  the local cell range (rows of E; global id of local 0).
+ *  E      DEVICE [3][ldE] (x, y, z rows, one column per local cell) or NULL.
+ * Bit-exact with the oracle (no FMA contraction: every product and sum is
+ * rounded as written).  Dead particles keep x and v.  CC_EINVAL on bad grid
+ * (dims not 1..3, n[a] < 1, d[a] <= 0, prod n >= 2^31) or arguments.        */
+int cc_push(const double *x_in, int64_t ldx_in, const int32_t *perm, double *x_out, int64_t ldx_out,
+            double *v, int64_t ldv, int32_t *cell, int64_t n, int32_t cells, uint32_t cell_base,
+            const cc_grid *grid, const double *E, int64_t ldE, double q_over_m, double dt, void *stream);
+
+/* Graph-friendly step counter (CUDA-graph replay of a subcycled loop):
+ * *step_dev += inc on the device (cc_params.step_dev; see coulomb_collide). */
+int cc_step_advance(uint32_t *step_dev, uint32_t inc, void *stream);
 
 #ifdef __cplusplus
 }

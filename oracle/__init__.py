@@ -100,6 +100,11 @@ def lib():
         L.or_triplet.restype = None
         L.or_coulomb_log.argtypes = [C.c_void_p, C.c_int32, C.c_void_p]
         L.or_coulomb_log.restype = None
+        L.or_push.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64,   # x_in, ldx, perm, x_out, ldo
+                              C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32,   # v, ldv, cell, n, dims
+                              C.c_void_p, C.c_void_p, C.c_uint32,                        # nc[3], d[3], periodic
+                              C.c_void_p, C.c_int64, C.c_double, C.c_double]             # E, ldE, q/m, dt
+        L.or_push.restype = None
         L.or_num_threads.argtypes = []
         L.or_num_threads.restype = C.c_int
         _lib = L
@@ -275,6 +280,27 @@ def coulomb_collide(v_in, cell_in, cells, *, dt, weight, cell_volume, ln_lambda=
     npairs = int(diag[2])
     return OracleResult(v_out, cell_out, perm_out, mom, diag,
                         pairs[:npairs].copy() if want_pairs else None)
+
+
+def push(x, v, cell, *, dims, nc, d, periodic, dt, q_over_m=-Q_E / M_E, E=None, perm=None):
+    """NEXT f2: S2b + S2c (Table 2; SPEC push S:204-210).  Returns
+    (x_out [3][n], v_out [3][n], cell_out [n] GLOBAL ids, -1 dead); inputs untouched.
+    x rows are indexed through perm (the collision call's perm_out) if given."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    v_out = np.array(v, dtype=np.float64, order="C", copy=True)
+    cell_out = np.array(cell, dtype=np.int32, copy=True)
+    n = cell_out.size
+    assert x.shape[0] == 3 and v_out.shape == (3, n)
+    x_out = np.zeros((3, n), np.float64)
+    nc3 = np.ones(3, np.int32)
+    nc3[:len(nc)] = nc
+    d3 = np.ones(3, np.float64)
+    d3[:len(d)] = d
+    pm = None if perm is None else np.ascontiguousarray(perm, dtype=np.int64)
+    Ea = None if E is None else np.ascontiguousarray(E, dtype=np.float64)
+    lib().or_push(_ptr(x), x.shape[1], _ptr(pm), _ptr(x_out), n, _ptr(v_out), n, _ptr(cell_out), n, dims,
+                  _ptr(nc3), _ptr(d3), periodic, _ptr(Ea), 0 if Ea is None else Ea.shape[1], q_over_m, dt)
+    return x_out, v_out, cell_out
 
 
 def num_threads() -> int:

@@ -698,3 +698,68 @@ int or_num_threads(void)
     return 1;
 #endif
 }
+
+/* ------------------------------------------------------------------------ */
+/* NEXT f2: the kinetic push between two collision calls.
+ * Table 2: Step S2b "E_l^c = -q grad phi(x_l^c)" (the cell-to-
+ * particle field) and Step S2c "x_l^+ = x_l^c + delta v_l^c; v_l^c + delta
+ * E_l^c" (DSMC-Push); SPEC push: "v' = v + dt (q/m) E;
+ * x' = x + dt v'" with E the per-cell constant field retrieved by cell id
+ * (S:207); boundary (Table 3 CS7): a particle leaving an
+ * absorbing axis dies; cell assignment j = floor(x/dx).  Readings
+ * R22-R24 of DESIGN.md §3: periodic axes wrap (repeated add/subtract of
+ * L = n_a d_a), i_a = floor(x_a / d_a) clamped to n_a - 1 (x just below L
+ * can divide to n_a), global cell = i_0 + n_0 (i_1 + n_1 i_2).
+ *
+ * Particle p (output order of the collision call): x_in row a at index
+ * perm[p] (perm NULL = p) -> x_out[a][p]; v[c][p] updated in place;
+ * cell[p]: in = LOCAL cell of the collision call (-1 dead), out = GLOBAL
+ * cell after the push (-1 dead).  Dead particles keep x and v.
+ * E: [3][ldE] rows x, y, z per LOCAL cell, or NULL (no field).             */
+void or_push(const double *x_in, int64_t ldx_in, const int64_t *perm, double *x_out, int64_t ldx_out,
+             double *v, int64_t ldv, int32_t *cell, int64_t n, int32_t dims, const int32_t nc[3],
+             const double d[3], uint32_t periodic, const double *E, int64_t ldE, double q_over_m, double dt)
+{
+    const double kick = dt * q_over_m;
+    for (int64_t p = 0; p < n; ++p) {
+        const int64_t src = perm ? perm[p] : p;
+        double x[3];
+        for (int a = 0; a < 3; ++a) x[a] = x_in[a * ldx_in + src];
+        const int32_t j = cell[p];
+        if (j < 0) {                                      /* dead: unchanged */
+            for (int a = 0; a < 3; ++a) x_out[a * ldx_out + p] = x[a];
+            continue;
+        }
+        /* S2b + S2c kick: v' = v + dt (q/m) E_j */
+        double vn[3];
+        for (int c = 0; c < 3; ++c) {
+            double e = E ? E[c * ldE + j] : 0.0;
+            vn[c] = v[c * ldv + p] + kick * e;
+            v[c * ldv + p] = vn[c];
+        }
+        /* S2c drift: x' = x + dt v', boundary, cell index */
+        int alive = 1;
+        int64_t G = 0, stride = 1;
+        for (int a = 0; a < 3; ++a) {
+            if (a < dims) {
+                double xa = x[a] + dt * vn[a];
+                const double L = (double)nc[a] * d[a];
+                if (periodic & (1u << a)) {
+                    while (xa < 0.0) xa = xa + L;
+                    while (xa >= L) xa = xa - L;
+                } else if (xa < 0.0 || xa >= L) {
+                    alive = 0;
+                }
+                x[a] = xa;
+                if (alive) {
+                    int64_t i = (int64_t)floor(xa / d[a]);
+                    if (i > nc[a] - 1) i = nc[a] - 1;
+                    G += i * stride;
+                }
+            }
+            stride *= nc[a];
+            x_out[a * ldx_out + p] = x[a];
+        }
+        cell[p] = alive ? (int32_t)G : -1;
+    }
+}

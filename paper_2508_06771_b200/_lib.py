@@ -30,7 +30,8 @@ STAGE_NAMES = ("count", "scan", "scatter", "collide", "finalize")
 # every symbol include/coulomb.h declares
 EXPORTS = ("cc_default_params", "cc_workspace_bytes", "coulomb_collide", "cc_device_status",
            "cc_strerror", "cc_bin", "cc_pairs", "cc_philox", "cc_ppnd16", "cc_ta_pairs",
-           "cc_moments", "cc_coulomb_log", "cc_gather", "cc_owner", "cc_diag_sum_ranks")
+           "cc_moments", "cc_coulomb_log", "cc_gather", "cc_owner", "cc_diag_sum_ranks", "cc_push",
+           "cc_step_advance")
 
 
 class CCParams(C.Structure):
@@ -38,7 +39,12 @@ class CCParams(C.Structure):
                 ("weight", C.c_double), ("cell_volume", C.c_double),
                 ("cell_volume_arr", C.c_void_p), ("ln_lambda", C.c_double),
                 ("ln_lambda_arr", C.c_void_p), ("flags", C.c_uint32),
+                ("step_dev", C.c_void_p),
                 ("stage_events", C.POINTER(C.c_void_p))]
+
+
+class CCGrid(C.Structure):
+    _fields_ = [("dims", C.c_int32), ("n", C.c_int32 * 3), ("d", C.c_double * 3), ("periodic", C.c_uint32)]
 
 
 class CCError(RuntimeError):
@@ -92,6 +98,10 @@ def load():
     L.cc_owner.restype = C.c_int
     L.cc_diag_sum_ranks.argtypes = [vp, i32, vp, vp]
     L.cc_diag_sum_ranks.restype = C.c_int
+    L.cc_push.argtypes = [vp, i64, vp, vp, i64, vp, i64, vp, i64, i32, u32, C.POINTER(CCGrid), vp, i64, dbl, dbl, vp]
+    L.cc_push.restype = C.c_int
+    L.cc_step_advance.argtypes = [vp, u32, vp]
+    L.cc_step_advance.restype = C.c_int
     _lib = L
     return L
 

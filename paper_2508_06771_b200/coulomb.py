@@ -48,7 +48,8 @@ def _soa(v: torch.Tensor, name: str, dev: torch.device) -> int:
 
 def make_params(*, mass=M_E, charge=Q_E, eps0=EPS0, weight=1.0, cell_volume=1.0, ln_lambda=10.0,
                 cell_volume_arr: Optional[torch.Tensor] = None,
-                ln_lambda_arr: Optional[torch.Tensor] = None, flags: int = 0) -> CCParams:
+                ln_lambda_arr: Optional[torch.Tensor] = None, flags: int = 0,
+                step_dev: Optional[torch.Tensor] = None) -> CCParams:
     p = CCParams()
     _lib.load().cc_default_params(C.byref(p))
     p.mass, p.charge, p.eps0 = mass, charge, eps0
@@ -56,6 +57,7 @@ def make_params(*, mass=M_E, charge=Q_E, eps0=EPS0, weight=1.0, cell_volume=1.0,
     p.cell_volume_arr = None if cell_volume_arr is None else cell_volume_arr.data_ptr()
     p.ln_lambda_arr = None if ln_lambda_arr is None else ln_lambda_arr.data_ptr()
     p.flags = flags
+    p.step_dev = None if step_dev is None else step_dev.data_ptr()
     return p
 
 
@@ -96,7 +98,7 @@ def coulomb_collide(v: torch.Tensor, cell: torch.Tensor, cells: int, *, dt: floa
                     seed: int = 42, step: int = 0, mass: float = M_E, charge: float = Q_E,
                     eps0: float = EPS0, out: Optional[CollideOut] = None,
                     workspace: Optional[torch.Tensor] = None, moments: bool = True,
-                    diag: bool = True, flags: int = 0) -> CollideOut:
+                    diag: bool = True, flags: int = 0, step_dev: Optional[torch.Tensor] = None) -> CollideOut:
     """One step of the Coulomb collision operator on CUDA tensors (see coulomb.h)."""
     dev = cell.device
     if dev.type != "cuda":
@@ -124,9 +126,11 @@ def coulomb_collide(v: torch.Tensor, cell: torch.Tensor, cells: int, *, dt: floa
             _need(arr, nm, torch.float64, dev)
             if arr.numel() != cells or not arr.is_contiguous():
                 raise ValueError(f"{nm} must be a contiguous [cells] tensor")
+    if step_dev is not None:
+        _need(step_dev, "step_dev", torch.int32, dev)
     p = make_params(mass=mass, charge=charge, eps0=eps0, weight=weight, cell_volume=cell_volume,
                     ln_lambda=ln_lambda, cell_volume_arr=cell_volume_arr, ln_lambda_arr=ln_lambda_arr,
-                    flags=flags)
+                    flags=flags, step_dev=step_dev)
     rc = _lib.load().coulomb_collide(
         _ptr(v), max(ldv, n), _ptr(cell), _ptr(out.v_out), _ptr(out.cell_out), _ptr(out.perm_out),
         n, cells, cell_base, dt, C.byref(p), seed, step,
@@ -290,3 +294,66 @@ def cc_diag_sum_ranks(gathered: torch.Tensor) -> torch.Tensor:
                                        C.c_void_p(_stream(dev)))
     check(rc, "cc_diag_sum_ranks")
     return out
+
+
+# ---------------------------------------------------------------- NEXT f2: push
+
+
+@dataclass
+class Grid:
+    """Regular grid of the push (cc_grid): ``dims`` axes, ``n`` cells and cell size
+    ``d`` per axis, ``periodic`` bit a = axis a periodic (else absorbing)."""
+    dims: int
+    n: tuple
+    d: tuple
+    periodic: int = 0
+
+    def c(self) -> "_lib.CCGrid":
+        g = _lib.CCGrid()
+        g.dims = self.dims
+        for a in range(3):
+            g.n[a] = int(self.n[a]) if a < len(self.n) else 1
+            g.d[a] = float(self.d[a]) if a < len(self.d) else 1.0
+        g.periodic = self.periodic
+        return g
+
+    @property
+    def cells(self) -> int:
+        c = 1
+        for a in range(self.dims):
+            c *= int(self.n[a])
+        return c
+
+
+def cc_push(x_in: torch.Tensor, v: torch.Tensor, cell: torch.Tensor, grid: Grid, *, dt: float,
+            q_over_m: float = -Q_E / M_E, E: Optional[torch.Tensor] = None, perm: Optional[torch.Tensor] = None,
+            x_out: Optional[torch.Tensor] = None, cells: Optional[int] = None, cell_base: int = 0) -> torch.Tensor:
+    """Steps S2b + S2c (Table 2): v += dt (q/m) E[cell] and x' = x + dt v' (v, cell in place;
+    cell: local in, GLOBAL out).  x_in rows are read through ``perm`` (coulomb_collide's
+    perm_out) if given.  Returns x_out [3][n]."""
+    dev = cell.device
+    _need(cell, "cell", torch.int32, dev)
+    n = cell.numel()
+    ldx = _soa(x_in, "x_in", dev)
+    ldv = _soa(v, "v", dev)
+    if x_out is None:
+        x_out = torch.empty((3, n), dtype=torch.float64, device=dev)
+    ldo = _soa(x_out, "x_out", dev)
+    if perm is not None:
+        _need(perm, "perm", torch.int32, dev)
+    cells = grid.cells if cells is None else cells
+    ldE = 0
+    if E is not None:
+        ldE = _soa(E, "E", dev)
+    g = grid.c()
+    rc = _lib.load().cc_push(_ptr(x_in), max(ldx, n), _ptr(perm), _ptr(x_out), max(ldo, n), _ptr(v), max(ldv, n),
+                             _ptr(cell), n, cells, cell_base, C.byref(g), _ptr(E), max(ldE, cells) if E is not None
+                             else 0, q_over_m, dt, C.c_void_p(_stream(dev)))
+    check(rc, "cc_push")
+    return x_out
+
+
+def cc_step_advance(step_dev: torch.Tensor, inc: int) -> None:
+    _need(step_dev, "step_dev", torch.int32, step_dev.device)
+    check(_lib.load().cc_step_advance(_ptr(step_dev), inc, C.c_void_p(_stream(step_dev.device))),
+          "cc_step_advance")

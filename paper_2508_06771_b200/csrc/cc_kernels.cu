@@ -282,7 +282,8 @@ k_scan_cells(const int32_t* __restrict__ cnt, int M, int32_t* __restrict__ off, 
 // Feistel keys (R1, R3), and the chunk -> cell table of k_collide_large.
 __global__ void k_cell_setup(const int32_t* __restrict__ cnt, const int32_t* __restrict__ chunk_off, int M,
                              int32_t* __restrict__ chunk_cell, double* __restrict__ Cj, cc::U4* __restrict__ keys,
-                             CellConst cc_, uint32_t cell_base, uint32_t step, uint32_t s0, uint32_t s1)
+                             CellConst cc_, uint32_t cell_base, uint32_t step, uint32_t s0, uint32_t s1,
+                             const uint32_t* __restrict__ step_dev)
 {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= M) return;
@@ -291,6 +292,7 @@ __global__ void k_cell_setup(const int32_t* __restrict__ cnt, const int32_t* __r
     const double lnL = cc_.ln_lambda_arr ? cc_.ln_lambda_arr[j] : cc_.ln_lambda;
     const double nj = static_cast<double>(N) * cc_.weight / V;
     Cj[j] = fmax(cc_.K * nj * lnL, 0.0);
+    if (step_dev) step += *step_dev;          // graph replay: effective step read on the device
     keys[j] = cc::philox4x32_10(cc::U4{0u, cell_base + static_cast<uint32_t>(j), step, 1u}, s0, s1);
     for (int32_t c = chunk_off[j]; c < chunk_off[j + 1]; ++c) chunk_cell[c] = j;
 }
@@ -498,7 +500,13 @@ struct CollideArgs {
     double* trec;               // [M][kRec] triplet moment records of large odd cells (triplet mode)
     int pair_vec;               // outputs aligned for 16-byte (v) / 8-byte (cell, perm) pair stores
     uint32_t cell_base, step, s0, s1;
+    const uint32_t* step_dev;   // NULL, or DEVICE offset added to `step` (cc_params.step_dev)
 };
+
+__device__ __forceinline__ uint32_t eff_step(const CollideArgs& A)
+{
+    return A.step + (A.step_dev ? __ldg(A.step_dev) : 0u);
+}
 
 // Post-collision moment accumulator about a per-cell shift r:
 // [0..2] sum (v - r), [3..5] sum (v - r)^2.  (Pre-collision sums come from
@@ -557,9 +565,10 @@ __device__ __forceinline__ void write_pair_out(const CollideArgs& A, int32_t pa,
 }
 
 // CCS4: one Philox call per pair, ctr = (k, G, step, 0) -> (u1, u2) (R3).
-__device__ __forceinline__ void pair_uniforms(const CollideArgs& A, int32_t j, uint32_t k, double& u1, double& u2)
+__device__ __forceinline__ void pair_uniforms(const CollideArgs& A, int32_t j, uint32_t k, uint32_t step, double& u1,
+                                              double& u2)
 {
-    const cc::U4 r = cc::philox4x32_10(cc::U4{k, A.cell_base + static_cast<uint32_t>(j), A.step, 0u}, A.s0, A.s1);
+    const cc::U4 r = cc::philox4x32_10(cc::U4{k, A.cell_base + static_cast<uint32_t>(j), step, 0u}, A.s0, A.s1);
     u1 = cc::u01(r.x, r.y);
     u2 = cc::u01(r.z, r.w);
 }
@@ -575,11 +584,11 @@ __device__ __forceinline__ void warp_reduce(double (&a)[NV])
 
 // R19: TA77 odd-count triplet — (1,2), (2,3), (3,1) in order, each with C/2,
 // randoms Philox(ctr = (q, G, step, 3)) for sub-collision q; r[] in place.
-__device__ __forceinline__ void triplet_update(const CollideArgs& A, uint32_t G, double C, Rec (&r)[3])
+__device__ __forceinline__ void triplet_update(const CollideArgs& A, uint32_t G, double C, uint32_t step, Rec (&r)[3])
 {
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-        const cc::U4 x = cc::philox4x32_10(cc::U4{static_cast<uint32_t>(q), G, A.step, 3u}, A.s0, A.s1);
+        const cc::U4 x = cc::philox4x32_10(cc::U4{static_cast<uint32_t>(q), G, step, 3u}, A.s0, A.s1);
         Rec& a = r[q];
         Rec& b = r[(q + 1) % 3];
         cc::collide_model(a.x, a.y, a.z, b.x, b.y, b.z, 0.5 * C, cc::u01(x.x, x.y), cc::u01(x.z, x.w), A.model);
@@ -599,7 +608,8 @@ k_collide_small(CollideArgs A)
     if (N == 0 || N > cc::kSmallCell) return;
     const int32_t o = A.off[j];
     const uint32_t G = A.cell_base + static_cast<uint32_t>(j);
-    cc::small_cell_perm(static_cast<uint32_t>(N), G, A.step, A.s0, A.s1, lane, pi_sm[w]);
+    const uint32_t step = eff_step(A);
+    cc::small_cell_perm(static_cast<uint32_t>(N), G, step, A.s0, A.s1, lane, pi_sm[w]);
     const double C = A.Cj[j];
     Acc acc;
     acc.zero();
@@ -611,7 +621,7 @@ k_collide_small(CollideArgs A)
         Rec r[3];
 #pragma unroll
         for (int q = 0; q < 3; ++q) r[q] = load_slot(A, o + pi_sm[w][N - 3 + q]);
-        triplet_update(A, G, C, r);
+        triplet_update(A, G, C, step, r);
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
             write_out(A, o + N - 3 + q, j, r[q]);
@@ -623,7 +633,7 @@ k_collide_small(CollideArgs A)
         if (2 * k + 1 < static_cast<uint32_t>(N)) {
             Rec b = load_slot(A, o + pi_sm[w][2 * k + 1]);
             double u1, u2;
-            pair_uniforms(A, j, k, u1, u2);
+            pair_uniforms(A, j, k, step, u1, u2);
             cc::collide_model(a.x, a.y, a.z, b.x, b.y, b.z, C, u1, u2, A.model);
             write_out(A, pa + 1, j, b);
             acc.post(b.x, b.y, b.z, 0.0, 0.0, 0.0);
@@ -714,6 +724,7 @@ k_collide_large(CollideArgs A)
         }
     }
     const int32_t N = A.cnt[j], o = A.off[j];
+    const uint32_t step = eff_step(A);
     const uint32_t items = static_cast<uint32_t>(N + 1) / 2;
     const uint32_t i0 = static_cast<uint32_t>(c - A.chunk_off[j]) * kChunk;
     const uint32_t i1 = min(i0 + static_cast<uint32_t>(kChunk), items);
@@ -748,7 +759,7 @@ k_collide_large(CollideArgs A)
 #pragma unroll
         for (int t = 0; t < kItemsPerThread; ++t) {    // independent Philox calls, interleaved
             if (CC_ABLATE & 4) { u1[t] = 0.3; u2[t] = 0.7; continue; }
-            pair_uniforms(A, j, i0 + threadIdx.x + t * kCollideThreads, u1[t], u2[t]);
+            pair_uniforms(A, j, i0 + threadIdx.x + t * kCollideThreads, step, u1[t], u2[t]);
         }
 #pragma unroll
         for (int t = 0; t < kItemsPerThread; ++t) {
@@ -840,7 +851,7 @@ __global__ void k_triplets(CollideArgs A)
         Rec r[3];
 #pragma unroll
         for (int q = 0; q < 3; ++q) r[q] = load_slot(A, o + static_cast<int64_t>(cc::feistel_pi(f, N - 3 + q)));
-        triplet_update(A, A.cell_base + static_cast<uint32_t>(j), A.Cj[j], r);
+        triplet_update(A, A.cell_base + static_cast<uint32_t>(j), A.Cj[j], eff_step(A), r);
         const double* cr = A.cellref + 4 * static_cast<int64_t>(j);
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
@@ -1113,6 +1124,71 @@ __global__ void k_gather(const double* __restrict__ v, int64_t ldv, const int32_
     }
 }
 
+// ------------------------------------------------------------------ NEXT f2: push (S2b + S2c)
+struct PushGrid {
+    int dims;
+    int n[3];
+    double d[3], L[3];
+    uint32_t periodic;
+};
+
+// Thread per particle (grid-stride).  Every product and sum is an explicitly
+// rounded IEEE operation (__dmul_rn / __dadd_rn / __ddiv_rn), as in the
+// oracle (compiled without FMA contraction), so the result is bit-exact.
+__global__ void __launch_bounds__(256)
+k_push(const double* __restrict__ xin, int64_t ldxi, const int32_t* __restrict__ perm, double* __restrict__ xo,
+       int64_t ldxo, double* __restrict__ v, int64_t ldv, int32_t* __restrict__ cell, int64_t n, PushGrid g,
+       const double* __restrict__ E, int64_t ldE, double qm, double dt)
+{
+    const double kick = __dmul_rn(dt, qm);
+    for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < n;
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t src = perm ? static_cast<int64_t>(perm[p]) : p;
+        double x[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) x[a] = xin[a * ldxi + src];
+        const int32_t j = cell[p];
+        if (j < 0) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) xo[a * ldxo + p] = x[a];
+            continue;
+        }
+        double vn[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const double e = E ? E[c * ldE + j] : 0.0;
+            vn[c] = __dadd_rn(v[c * ldv + p], __dmul_rn(kick, e));
+            v[c * ldv + p] = vn[c];
+        }
+        bool alive = true;
+        int64_t G = 0, stride = 1;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            if (a < g.dims) {
+                double xa = __dadd_rn(x[a], __dmul_rn(dt, vn[a]));
+                const double L = g.L[a];
+                if (g.periodic & (1u << a)) {
+                    while (xa < 0.0) xa = __dadd_rn(xa, L);
+                    while (xa >= L) xa = __dsub_rn(xa, L);
+                } else if (xa < 0.0 || xa >= L) {
+                    alive = false;
+                }
+                x[a] = xa;
+                if (alive) {
+                    int64_t i = static_cast<int64_t>(floor(__ddiv_rn(xa, g.d[a])));
+                    if (i > g.n[a] - 1) i = g.n[a] - 1;
+                    G += i * stride;
+                }
+            }
+            stride *= g.n[a];
+            xo[a * ldxo + p] = x[a];
+        }
+        cell[p] = alive ? static_cast<int32_t>(G) : -1;
+    }
+}
+
+__global__ void k_step_advance(uint32_t* step, uint32_t inc) { *step += inc; }
+
 __global__ void k_owner(const int32_t* __restrict__ cell, int64_t n, const int32_t* __restrict__ bounds, int P,
                         int32_t* __restrict__ owner)
 {
@@ -1193,7 +1269,7 @@ void mark(void* const* ev, int i, cudaStream_t st)
 
 int run_binning(const double* v_in, int64_t ldv, const int32_t* cell_in, int n, int M, const Layout& L,
                 void* ws, const CellConst& k, uint32_t cell_base, uint32_t step, uint64_t seed,
-                cudaStream_t st, void* const* ev, bool allow_sorted_skip)
+                cudaStream_t st, void* const* ev, bool allow_sorted_skip, const uint32_t* step_dev = nullptr)
 {
     int32_t* err = at<int32_t>(ws, L.o_err);
     if (cudaMemsetAsync(err + 1, 0, sizeof(int32_t), st) != cudaSuccess) return CC_ECUDA;   // "unsorted" flag
@@ -1218,7 +1294,7 @@ int run_binning(const double* v_in, int64_t ldv, const int32_t* cell_in, int n, 
     k_scan_cells<<<1, 1024, 0, st>>>(cnt, M, off, chunk_off);
     k_cell_setup<<<(M + 255) / 256, 256, 0, st>>>(cnt, chunk_off, M, at<int32_t>(ws, L.o_chunkcell), Cj, keys, k,
                                                    cell_base, step, static_cast<uint32_t>(seed),
-                                                   static_cast<uint32_t>(seed >> 32));
+                                                   static_cast<uint32_t>(seed >> 32), step_dev);
     mark(ev, 2, st);
     if (v_in)
         k_scatter<true><<<L.T, 32 * L.W, smem, st>>>(v_in, ldv, cell_in, n, M, L.W, tcount, off, wsv, skip,
@@ -1332,7 +1408,7 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     const int nn = static_cast<int>(n);
     void* const* ev = p.stage_events;
     int rc = run_binning(v_in, ldv, cell_in, nn, M, L, workspace, k, cell_base, static_cast<uint32_t>(step), seed,
-                         st, ev, true);
+                         st, ev, true, p.step_dev);
     if (rc) return rc;
 
     CollideArgs A;
@@ -1353,6 +1429,7 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     A.M = M;
     A.cell_base = cell_base;
     A.step = static_cast<uint32_t>(step);
+    A.step_dev = p.step_dev;
     A.s0 = static_cast<uint32_t>(seed);
     A.s1 = static_cast<uint32_t>(seed >> 32);
     A.pf_dist = prefetch_distance();
@@ -1509,6 +1586,51 @@ int cc_coulomb_log(const double* moments, int32_t cells, double* out, void* stre
     cudaGetLastError();   // launch errors below are ours, not a stale earlier one
     if (!moments || !out || cells < 1) return CC_EINVAL;
     k_coulomb_log<<<(cells + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(moments, cells, out);
+    return launch_ok();
+}
+
+int cc_push(const double* x_in, int64_t ldx_in, const int32_t* perm, double* x_out, int64_t ldx_out, double* v,
+            int64_t ldv, int32_t* cell, int64_t n, int32_t cells, uint32_t cell_base, const cc_grid* grid,
+            const double* E, int64_t ldE, double q_over_m, double dt, void* stream)
+{
+    cudaGetLastError();   // launch errors below are ours, not a stale earlier one
+    (void)cell_base;      // E is indexed by the local cell; the output ids are global by construction
+    if (!grid || n < 0 || cells < 1 || !std::isfinite(q_over_m) || !std::isfinite(dt)) return CC_EINVAL;
+    if (grid->dims < 1 || grid->dims > 3) return CC_EINVAL;
+    PushGrid g;
+    g.dims = grid->dims;
+    g.periodic = grid->periodic;
+    int64_t total = 1;
+    for (int a = 0; a < 3; ++a) {
+        if (a < grid->dims) {
+            if (grid->n[a] < 1 || !finite_pos(grid->d[a])) return CC_EINVAL;
+            g.n[a] = grid->n[a];
+            g.d[a] = grid->d[a];
+        } else {
+            g.n[a] = 1;
+            g.d[a] = 1.0;
+        }
+        g.L[a] = static_cast<double>(g.n[a]) * g.d[a];
+        total *= g.n[a];
+    }
+    if (total >= (1ll << 31)) return CC_EINVAL;
+    if (n == 0) return CC_OK;
+    if (!x_in || !x_out || !v || !cell || ldx_in < n || ldx_out < n || ldv < n || (E && ldE < cells))
+        return CC_EINVAL;
+    if (perm && overlaps(x_in, sizeof(double) * static_cast<size_t>(2 * ldx_in + n), x_out,
+                         sizeof(double) * static_cast<size_t>(2 * ldx_out + n)))
+        return CC_EINVAL;
+    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 16));
+    k_push<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(x_in, ldx_in, perm, x_out, ldx_out, v, ldv, cell,
+                                                                  n, g, E, ldE, q_over_m, dt);
+    return launch_ok();
+}
+
+int cc_step_advance(uint32_t* step_dev, uint32_t inc, void* stream)
+{
+    cudaGetLastError();
+    if (!step_dev) return CC_EINVAL;
+    k_step_advance<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(step_dev, inc);
     return launch_ok();
 }
 

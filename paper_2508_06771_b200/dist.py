@@ -84,10 +84,11 @@ class Migrated:
     cell: torch.Tensor     # [n_new] int32, LOCAL cell ids of the receiving rank (-1 dead)
     sent: list             # particles sent to each rank (incl. self)
     received: list         # particles received from each rank (incl. self)
+    payload: Optional[torch.Tensor] = None   # [3][n_new] fp64 rows carried along (e.g. positions)
 
 
 def migrate(v: torch.Tensor, cell_global: torch.Tensor, global_cells: int, ops: DistOps,
-            group=None, keep_dead: bool = False) -> Migrated:
+            group=None, keep_dead: bool = False, payload: Optional[torch.Tensor] = None) -> Migrated:
     """Move every particle to the rank owning its (global) cell.
 
     1. owner rank of every particle (dead particles: dropped unless keep_dead,
@@ -96,6 +97,8 @@ def migrate(v: torch.Tensor, cell_global: torch.Tensor, global_cells: int, ops: 
     3. all_to_all of the per-destination counts;
     4. pack (gather in partition order) and all_to_all of velocities and cells;
     5. arrivals concatenated in source-rank order; global -> local cell ids.
+    ``payload`` ([3][n] fp64, e.g. the positions of the NEXT f2 push) travels
+    with the particles (same pack order, same exchange).
     """
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
@@ -123,7 +126,15 @@ def migrate(v: torch.Tensor, cell_global: torch.Tensor, global_cells: int, ops: 
     base = bounds[rank]
     ident = torch.arange(n_recv, dtype=torch.int32, device=dev)
     lv, lc = ops.gather(rv, rc, ident, base)
-    return Migrated(lv, lc, send, recv)
+    lp = None
+    if payload is not None:
+        px, _ = ops.gather(payload, cell_global, perm[:n_send], 0)
+        rx = torch.empty((3, n_recv), dtype=payload.dtype, device=dev)
+        for c in range(3):
+            dist.all_to_all_single(rx[c], px[c].contiguous(), output_split_sizes=recv, input_split_sizes=send,
+                                   group=group)
+        lp = rx
+    return Migrated(lv, lc, send, recv, lp)
 
 
 def init_from_env(backend: Optional[str] = None):

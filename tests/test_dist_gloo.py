@@ -68,8 +68,11 @@ def _worker(rank, world, port, q):
         cell = rng.integers(-1, G, n).astype(np.int32)
         v = rng.standard_normal((3, n))
         v[0] = np.arange(n) + 1000 * rank             # tag: source rank and index
-        m = migrate(torch.from_numpy(v), torch.from_numpy(cell), G, ops)
+        x = rng.standard_normal((3, n))
+        x[1] = v[0] + 0.5                             # positions (NEXT f2 payload) carry the same tag
+        m = migrate(torch.from_numpy(v), torch.from_numpy(cell), G, ops, payload=torch.from_numpy(x))
         res["mig"] = (m.v.numpy(), m.cell.numpy(), m.sent, m.received)
+        res["payload"] = m.payload.numpy()
         res["src"] = (v, cell)
         q.put((rank, res))
     finally:
@@ -115,6 +118,7 @@ def test_world2_diag_and_migration():
             expect_tags.append(sv[0][sel])
             expect_cells.append(sc[sel] - bounds[r])
         assert np.array_equal(v[0], np.concatenate(expect_tags))
+        assert np.array_equal(out[r]["payload"][1], v[0] + 0.5)      # payload travels with its particle
         assert np.array_equal(c, np.concatenate(expect_cells))
         assert sum(recv) == v.shape[1]
     total_live = sum(int(np.sum(out[s]["src"][1] >= 0)) for s in range(world))
