@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--dist-backend", default="nccl", help="torch.distributed backend for N > 1 (nccl; gloo "
                     "only to smoke-test the multi-rank path when fewer GPUs than ranks are available)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-pic", action="store_true", help="skip the NEXT f2 PIC-loop section")
     ap.add_argument("--cpu-cells", type=int, default=96,
                     help="cells of the C4 workload the CPU baseline processes per step")
     return ap.parse_args()
@@ -259,6 +260,85 @@ def drift_cells(cell, nx, ny, frac, gen):
     cy = torch.where(mv & (d == 2), torch.remainder(cy + 1, ny), cy)
     cy = torch.where(mv & (d == 3), torch.remainder(cy - 1, ny), cy)
     cell.copy_(torch.where(live, cy * nx + cx, cell))
+
+
+def hbm_peak_gbs() -> float:
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 6650.0
+
+
+def pic_section(args, dev, w, K):
+    """NEXT f2: the subcycled PIC loop (PicLoop: per substep coulomb_collide + cc_push,
+    every 10 substeps the Coulomb-log feedback), one GPU.  C4 grid (64 x 64 cells of
+    5 mm, periodic, field-free, dt = 1e-10 s: ~1.9% of the electrons change cell per
+    step) timed over whole field steps replayed from a CUDA graph; C1 / C2 (launch-
+    bound, one cell) with the graph and eagerly."""
+    import torch
+    import workloads as W
+    import paper_2508_06771_b200 as cc
+    from paper_2508_06771_b200.pic import PicLoop
+
+    def timed(loop, F):
+        loop.field_step()                      # capture (graph) / warm-up; re-sorts cold input
+        loop.field_step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(F):
+            loop.field_step()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / (F * loop.k)
+
+    out = {}
+    nx, ny = args.nx, args.ny
+    x = torch.from_numpy(W.positions_in_cells(w.cell, nx, ny, seed=77)).to(dev)
+    grid = cc.Grid(2, (nx, ny), (W.PIC_DX, W.PIC_DX), 3)
+    prm = dict(dt=w.dt, weight=w.weight, cell_volume=w.cell_volume)
+    loop = PicLoop(x, torch.from_numpy(w.v).to(dev), torch.from_numpy(w.cell).to(dev), grid, subcycles=10,
+                   graph=True, **prm)
+    F = max(1, K // 10)
+    ms = timed(loop, F)
+    pairs = float(loop.diag[2].item())
+    # the push alone, on the loop's current state (eager, events on the stream)
+    xs, vs, cs = loop.state
+    perm = torch.arange(w.n, dtype=torch.int32, device=dev)
+    v2, c2 = vs.clone(), cs.clone()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    xo = torch.empty_like(xs)
+    cc.cc_push(xs, v2, c2, grid, dt=w.dt, perm=perm, x_out=xo)
+    e0.record()
+    for _ in range(3):                         # single GPU: output ids are valid input ids again
+        cc.cc_push(xs, v2, c2, grid, dt=w.dt, perm=perm, x_out=xo)
+    e1.record()
+    torch.cuda.synchronize()
+    push_ms = e0.elapsed_time(e1) / 3
+    # cc_push algorithmic bytes, 2D field-free: read perm 4 + cell 4 + v 24 + x 16, write x 16 + cell 4
+    push_bytes = 68 * w.n
+    peak = hbm_peak_gbs()
+    out["c4"] = {"ms_per_substep": ms, "pair_collisions_per_s": pairs / (ms * 1e-3),
+                 "push_ms": push_ms,
+                 "push_roofline": {"kernel": "k_push", "bound": "hbm", "achieved": push_bytes / (push_ms * 1e-3) / 1e9,
+                                   "peak": peak, "unit": "GB/s",
+                                   "frac": push_bytes / (push_ms * 1e-3) / 1e9 / peak,
+                                   "algorithmic_bytes_per_particle": 68},
+                 "field_steps_timed": F, "subcycles": 10,
+                 "cells_changed_per_step": "~1.9% (5 mm cells, 2 eV, dt 1e-10 s)",
+                 "what": "PicLoop field steps replayed from one CUDA graph (collide + push per substep)"}
+    del loop, x, xs, vs, cs, v2, c2, xo, perm
+    for name, wl in (("c1", W.c1()), ("c2", W.c2())):
+        g1 = cc.Grid(1, (1,), (W.PIC_DX,), 1)
+        xx = torch.from_numpy(W.positions_in_cells(wl.cell, 1, 1, seed=78)).to(dev)
+        r = {}
+        for mode in ("graph", "eager"):
+            lp = PicLoop(xx, torch.from_numpy(wl.v).to(dev), torch.from_numpy(wl.cell).to(dev), g1, subcycles=10,
+                         graph=(mode == "graph"), dt=wl.dt, weight=wl.weight, cell_volume=wl.cell_volume)
+            r[mode + "_ms_per_substep"] = timed(lp, 5)
+        r["n"] = wl.n
+        out[name] = r
+    return out
 
 
 def run_ours(args):
@@ -482,6 +562,11 @@ def run_ours(args):
         "gpu_launches": 10 * K + (K if world > 1 else 0),
         "clocks": clk.summary(),
     }
+    if world == 1 and not args.no_pic:
+        try:
+            line["pic"] = pic_section(args, dev, w, K)
+        except Exception as e:  # the NEXT-row measurement must never kill the headline
+            line["pic"] = {"error": repr(e)}
     if world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = time_oracle_on(w, args)

@@ -212,9 +212,11 @@ typedef struct cc_grid {
  *   cell' = global cell of x', or -1 if absorbed.
  *  x_in   [3][ldx_in] fp64 positions; row a of particle p is read at index
  *         perm[p] (perm = coulomb_collide's perm_out, or NULL = p).
- *  x_out  [3][ldx_out] fp64, written for all n (rows >= dims copied).
+ *  x_out  [3][ldx_out] fp64, rows a < dims written for all n (rows >= dims
+ *         are neither read nor written).
  *         Must not alias x_in unless perm == NULL and the rows coincide.
- *  v      [3][ldv] fp64, updated in place (live particles).
+ *  v      [3][ldv] fp64, updated in place (live particles; not rewritten when
+ *         E is NULL, v + 0 being v).
  *  cell   [n] int32, in place: in = LOCAL cell of the collision call (-1 dead,
  *         E row), out = GLOBAL cell after the push (-1 dead).
  *  cells, cell_base  the local cell range (rows of E; global id of local 0).

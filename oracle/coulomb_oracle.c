@@ -711,8 +711,9 @@ int or_num_threads(void)
  * L = n_a d_a), i_a = floor(x_a / d_a) clamped to n_a - 1 (x just below L
  * can divide to n_a), global cell = i_0 + n_0 (i_1 + n_1 i_2).
  *
- * Particle p (output order of the collision call): x_in row a at index
- * perm[p] (perm NULL = p) -> x_out[a][p]; v[c][p] updated in place;
+ * Particle p (output order of the collision call): x_in row a < dims at
+ * index perm[p] (perm NULL = p) -> x_out[a][p] (rows >= dims untouched);
+ * v[c][p] updated in place;
  * cell[p]: in = LOCAL cell of the collision call (-1 dead), out = GLOBAL
  * cell after the push (-1 dead).  Dead particles keep x and v.
  * E: [3][ldE] rows x, y, z per LOCAL cell, or NULL (no field).             */
@@ -723,11 +724,11 @@ void or_push(const double *x_in, int64_t ldx_in, const int64_t *perm, double *x_
     const double kick = dt * q_over_m;
     for (int64_t p = 0; p < n; ++p) {
         const int64_t src = perm ? perm[p] : p;
-        double x[3];
-        for (int a = 0; a < 3; ++a) x[a] = x_in[a * ldx_in + src];
+        double x[3] = {0.0, 0.0, 0.0};
+        for (int a = 0; a < dims; ++a) x[a] = x_in[a * ldx_in + src];
         const int32_t j = cell[p];
         if (j < 0) {                                      /* dead: unchanged */
-            for (int a = 0; a < 3; ++a) x_out[a * ldx_out + p] = x[a];
+            for (int a = 0; a < dims; ++a) x_out[a * ldx_out + p] = x[a];
             continue;
         }
         /* S2b + S2c kick: v' = v + dt (q/m) E_j */
@@ -758,7 +759,7 @@ void or_push(const double *x_in, int64_t ldx_in, const int64_t *perm, double *x_
                 }
             }
             stride *= nc[a];
-            x_out[a * ldx_out + p] = x[a];
+            if (a < dims) x_out[a * ldx_out + p] = x[a];
         }
         cell[p] = alive ? (int32_t)G : -1;
     }

@@ -1135,6 +1135,9 @@ struct PushGrid {
 // Thread per particle (grid-stride).  Every product and sum is an explicitly
 // rounded IEEE operation (__dmul_rn / __dadd_rn / __ddiv_rn), as in the
 // oracle (compiled without FMA contraction), so the result is bit-exact.
+// HAS_E = false (field-free): v is read but not rewritten (v + 0 == v).
+// Only the position rows a < DIMS are read and written.
+template <bool HAS_E, int DIMS>
 __global__ void __launch_bounds__(256)
 k_push(const double* __restrict__ xin, int64_t ldxi, const int32_t* __restrict__ perm, double* __restrict__ xo,
        int64_t ldxo, double* __restrict__ v, int64_t ldv, int32_t* __restrict__ cell, int64_t n, PushGrid g,
@@ -1143,48 +1146,61 @@ k_push(const double* __restrict__ xin, int64_t ldxi, const int32_t* __restrict__
     const double kick = __dmul_rn(dt, qm);
     for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < n;
          p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t src = perm ? static_cast<int64_t>(perm[p]) : p;
-        double x[3];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) x[a] = xin[a * ldxi + src];
+        const int64_t src = perm ? static_cast<int64_t>(__ldg(perm + p)) : p;
         const int32_t j = cell[p];
+        double x[DIMS];
+#pragma unroll
+        for (int a = 0; a < DIMS; ++a) x[a] = __ldg(xin + a * ldxi + src);
         if (j < 0) {
 #pragma unroll
-            for (int a = 0; a < 3; ++a) xo[a * ldxo + p] = x[a];
+            for (int a = 0; a < DIMS; ++a) xo[a * ldxo + p] = x[a];
             continue;
         }
-        double vn[3];
+        double vn[DIMS];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const double e = E ? E[c * ldE + j] : 0.0;
-            vn[c] = __dadd_rn(v[c * ldv + p], __dmul_rn(kick, e));
-            v[c * ldv + p] = vn[c];
+        for (int c = 0; c < (HAS_E ? 3 : DIMS); ++c) {
+            double vc = v[c * ldv + p];
+            if (HAS_E) {
+                vc = __dadd_rn(vc, __dmul_rn(kick, __ldg(E + c * ldE + j)));
+                v[c * ldv + p] = vc;
+            }
+            if (c < DIMS) vn[c] = vc;
         }
         bool alive = true;
         int64_t G = 0, stride = 1;
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            if (a < g.dims) {
-                double xa = __dadd_rn(x[a], __dmul_rn(dt, vn[a]));
-                const double L = g.L[a];
-                if (g.periodic & (1u << a)) {
-                    while (xa < 0.0) xa = __dadd_rn(xa, L);
-                    while (xa >= L) xa = __dsub_rn(xa, L);
-                } else if (xa < 0.0 || xa >= L) {
-                    alive = false;
-                }
-                x[a] = xa;
-                if (alive) {
-                    int64_t i = static_cast<int64_t>(floor(__ddiv_rn(xa, g.d[a])));
-                    if (i > g.n[a] - 1) i = g.n[a] - 1;
-                    G += i * stride;
-                }
+        for (int a = 0; a < DIMS; ++a) {
+            double xa = __dadd_rn(x[a], __dmul_rn(dt, vn[a]));
+            const double L = g.L[a];
+            if (g.periodic & (1u << a)) {
+                while (xa < 0.0) xa = __dadd_rn(xa, L);
+                while (xa >= L) xa = __dsub_rn(xa, L);
+            } else if (xa < 0.0 || xa >= L) {
+                alive = false;
+            }
+            if (alive) {
+                int64_t i = static_cast<int64_t>(floor(__ddiv_rn(xa, g.d[a])));
+                if (i > g.n[a] - 1) i = g.n[a] - 1;
+                G += i * stride;
             }
             stride *= g.n[a];
-            xo[a * ldxo + p] = x[a];
+            xo[a * ldxo + p] = xa;
         }
         cell[p] = alive ? static_cast<int32_t>(G) : -1;
     }
+}
+
+template <bool HAS_E>
+void launch_push(unsigned blocks, cudaStream_t st, const double* x_in, int64_t ldx_in, const int32_t* perm,
+                 double* x_out, int64_t ldx_out, double* v, int64_t ldv, int32_t* cell, int64_t n, const PushGrid& g,
+                 const double* E, int64_t ldE, double qm, double dt)
+{
+    if (g.dims == 1)
+        k_push<HAS_E, 1><<<blocks, 256, 0, st>>>(x_in, ldx_in, perm, x_out, ldx_out, v, ldv, cell, n, g, E, ldE, qm, dt);
+    else if (g.dims == 2)
+        k_push<HAS_E, 2><<<blocks, 256, 0, st>>>(x_in, ldx_in, perm, x_out, ldx_out, v, ldv, cell, n, g, E, ldE, qm, dt);
+    else
+        k_push<HAS_E, 3><<<blocks, 256, 0, st>>>(x_in, ldx_in, perm, x_out, ldx_out, v, ldv, cell, n, g, E, ldE, qm, dt);
 }
 
 __global__ void k_step_advance(uint32_t* step, uint32_t inc) { *step += inc; }
@@ -1621,8 +1637,9 @@ int cc_push(const double* x_in, int64_t ldx_in, const int32_t* perm, double* x_o
                          sizeof(double) * static_cast<size_t>(2 * ldx_out + n)))
         return CC_EINVAL;
     const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 16));
-    k_push<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(x_in, ldx_in, perm, x_out, ldx_out, v, ldv, cell,
-                                                                  n, g, E, ldE, q_over_m, dt);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (E) launch_push<true>(blocks, st, x_in, ldx_in, perm, x_out, ldx_out, v, ldv, cell, n, g, E, ldE, q_over_m, dt);
+    else launch_push<false>(blocks, st, x_in, ldx_in, perm, x_out, ldx_out, v, ldv, cell, n, g, E, ldE, q_over_m, dt);
     return launch_ok();
 }
 

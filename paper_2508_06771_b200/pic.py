@@ -69,7 +69,7 @@ class PicLoop:
         n = cell.numel()
         self.n = n
         f64 = dict(dtype=torch.float64, device=self.dev)
-        self.x = [x.clone(), torch.empty((3, n), **f64)]
+        self.x = [x.clone(), torch.zeros((3, n), **f64)]     # rows >= dims are never written by cc_push
         self.v = [v.clone(), torch.empty((3, n), **f64)]
         self.cell = [cell.clone(), torch.empty(n, dtype=torch.int32, device=self.dev)]
         self.perm = torch.empty(n, dtype=torch.int32, device=self.dev)

@@ -191,3 +191,25 @@ def random_cells(n, M, *, seed, dead_frac=0.0, T_eV=2.0, skew=False) -> Workload
     v = rng.standard_normal((3, n)) * s
     return Workload(f"random n={n} M={M}", np.ascontiguousarray(v), np.ascontiguousarray(cell),
                     max(M, 1), weight=weight_for(max(n / max(M, 1), 1.0)))
+
+
+# NEXT f2 (PIC loop): grid geometry and positions consistent with the cell ids.
+PIC_DX = 5e-3            # m; 2D cell 5 mm x 5 mm x 4 cm deep = CELL_VOLUME.  At 2 eV and dt = 1e-10 s
+PIC_DEPTH = CELL_VOLUME / (PIC_DX * PIC_DX)   # ~0.95% of the electrons cross each cell face pair per step
+
+
+def positions_in_cells(cell, nx, ny, dx=PIC_DX, dy=PIC_DX, *, seed) -> np.ndarray:
+    """[3][n] positions uniform inside each particle's cell of an nx x ny grid
+    (cell = ix + nx iy); dead particles (-1) get x = y = 0.  Row z = 0."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    cell = np.asarray(cell)
+    n = cell.size
+    c = np.where(cell >= 0, cell, 0)
+    ix, iy = c % nx, c // nx
+    x = np.zeros((3, n), np.float64)
+    x[0] = (ix + rng.random(n)) * dx
+    x[1] = (iy + rng.random(n)) * dy
+    x[0] = np.minimum(x[0], np.nextafter((ix + 1) * dx, 0))
+    x[1] = np.minimum(x[1], np.nextafter((iy + 1) * dy, 0))
+    x[:, cell < 0] = 0.0
+    return x
