@@ -228,6 +228,28 @@ int cc_push(const double *x_in, int64_t ldx_in, const int32_t *perm, double *x_o
             double *v, int64_t ldv, int32_t *cell, int64_t n, int32_t cells, uint32_t cell_base,
             const cc_grid *grid, const double *E, int64_t ldE, double q_over_m, double dt, void *stream);
 
+/* ---- NEXT f4: the paper's own P2C and replicated-grid scheme ---- */
+
+/* Step S3a/S3b P2C the paper's way: a block reduction over UNSORTED
+ * particles by fp64 atomics, each cell split into `sub` auxiliary sub-bins
+ * omega_jm ("to [reduce] atomic updates congestion"; the sub-bin of
+ * particle p is p mod sub), then V^j = sum_m V^jm in fixed order.
+ *  v [3][ldv], cell [n] (LOCAL ids; -1 / out-of-range ignored).
+ *  raw_out DEVICE [cells][7] = {N_j, sum v_x, v_y, v_z, sum v_x^2, v_y^2, v_z^2}.
+ *  scratch DEVICE, >= cc_p2c_scratch_bytes(cells, sub) bytes, 8-byte aligned.
+ * In the paper's multi-GPU scheme (replicated grid) every rank
+ * deposits its own particles and raw_out is summed over ranks (one O(M)
+ * all-reduce) before cc_p2c_moments.  Agrees with a sequential sum to
+ * rounding (atomic order), not bitwise.                                      */
+size_t cc_p2c_scratch_bytes(int32_t cells, int32_t sub);                  /* HOST */
+int cc_p2c(const double *v, int64_t ldv, const int32_t *cell, int64_t n, int32_t cells, int32_t sub,
+           double *raw_out, void *scratch, size_t scratch_bytes, void *stream);
+
+/* Raw sums [cells][7] (cc_p2c, possibly all-reduced) -> moments [cells][7] in
+ * coulomb_collide's layout {n_j, <v> (3), T_x, T_y, T_z} (reading R13; n_j =
+ * N_j weight / V_j with params->weight, cell_volume(_arr); empty cells 0).  */
+int cc_p2c_moments(const double *raw, int32_t cells, const cc_params *params, double *moments_out, void *stream);
+
 /* Graph-friendly step counter (CUDA-graph replay of a subcycled loop):
  * *step_dev += inc on the device (cc_params.step_dev; see coulomb_collide). */
 int cc_step_advance(uint32_t *step_dev, uint32_t inc, void *stream);

@@ -31,7 +31,7 @@ STAGE_NAMES = ("count", "scan", "scatter", "collide", "finalize")
 EXPORTS = ("cc_default_params", "cc_workspace_bytes", "coulomb_collide", "cc_device_status",
            "cc_strerror", "cc_bin", "cc_pairs", "cc_philox", "cc_ppnd16", "cc_ta_pairs",
            "cc_moments", "cc_coulomb_log", "cc_gather", "cc_owner", "cc_diag_sum_ranks", "cc_push",
-           "cc_step_advance")
+           "cc_step_advance", "cc_p2c_scratch_bytes", "cc_p2c", "cc_p2c_moments")
 
 
 class CCParams(C.Structure):
@@ -100,6 +100,12 @@ def load():
     L.cc_diag_sum_ranks.restype = C.c_int
     L.cc_push.argtypes = [vp, i64, vp, vp, i64, vp, i64, vp, i64, i32, u32, C.POINTER(CCGrid), vp, i64, dbl, dbl, vp]
     L.cc_push.restype = C.c_int
+    L.cc_p2c_scratch_bytes.argtypes = [i32, i32]
+    L.cc_p2c_scratch_bytes.restype = sz
+    L.cc_p2c.argtypes = [vp, i64, vp, i64, i32, i32, vp, vp, sz, vp]
+    L.cc_p2c.restype = C.c_int
+    L.cc_p2c_moments.argtypes = [vp, i32, C.POINTER(CCParams), vp, vp]
+    L.cc_p2c_moments.restype = C.c_int
     L.cc_step_advance.argtypes = [vp, u32, vp]
     L.cc_step_advance.restype = C.c_int
     _lib = L

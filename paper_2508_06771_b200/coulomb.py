@@ -357,3 +357,38 @@ def cc_step_advance(step_dev: torch.Tensor, inc: int) -> None:
     _need(step_dev, "step_dev", torch.int32, step_dev.device)
     check(_lib.load().cc_step_advance(_ptr(step_dev), inc, C.c_void_p(_stream(step_dev.device))),
           "cc_step_advance")
+
+
+# ---------------------------------------------------------------- NEXT f4: atomic P2C
+
+
+def cc_p2c(v: torch.Tensor, cell: torch.Tensor, cells: int, *, sub: int = 1,
+           scratch: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """The paper's atomic particle-to-cell block reduction over unsorted
+    particles with `sub` sub-bins per cell -> raw sums [cells][7]
+    {N, sum v (3), sum v^2 (3)}."""
+    dev = cell.device
+    _need(cell, "cell", torch.int32, dev)
+    n = cell.numel()
+    ldv = _soa(v, "v", dev)
+    L = _lib.load()
+    nb = int(L.cc_p2c_scratch_bytes(cells, sub))
+    if scratch is None or scratch.numel() * scratch.element_size() < nb:
+        scratch = torch.empty(max(nb // 8, 1), dtype=torch.float64, device=dev)
+    raw = torch.empty((cells, 7), dtype=torch.float64, device=dev)
+    check(L.cc_p2c(_ptr(v), max(ldv, n), _ptr(cell), n, cells, sub, _ptr(raw), _ptr(scratch),
+                   scratch.numel() * scratch.element_size(), C.c_void_p(_stream(dev))), "cc_p2c")
+    return raw
+
+
+def cc_p2c_moments(raw: torch.Tensor, *, weight: float = 1.0, cell_volume: float = 1.0,
+                   cell_volume_arr: Optional[torch.Tensor] = None, mass: float = M_E, charge: float = Q_E):
+    """Raw P2C sums [cells][7] -> moments [cells][7] (coulomb_collide's layout)."""
+    dev = raw.device
+    _need(raw, "raw", torch.float64, dev)
+    cells = raw.shape[0]
+    p = make_params(mass=mass, charge=charge, weight=weight, cell_volume=cell_volume, cell_volume_arr=cell_volume_arr)
+    out = torch.empty((cells, CC_MOMENTS_LEN), dtype=torch.float64, device=dev)
+    check(_lib.load().cc_p2c_moments(_ptr(raw.contiguous()), cells, C.byref(p), _ptr(out), C.c_void_p(_stream(dev))),
+          "cc_p2c_moments")
+    return out

@@ -1124,6 +1124,64 @@ __global__ void k_gather(const double* __restrict__ v, int64_t ldv, const int32_
     }
 }
 
+// ------------------------------------------------------------------ NEXT f4: atomic P2C (S3a)
+// The paper's particle-to-cell kernel: a block reduction over
+// UNSORTED particles by atomics, with each cell split into `sub` auxiliary
+// sub-bins omega_jm to spread atomic congestion, then V^j = sum_m V^jm.
+// Raw sums per (cell, sub-bin): {N, sum v_x, v_y, v_z, sum v_x^2, v_y^2, v_z^2};
+// the sub-bin of particle p is p mod sub.  fp64 global atomics (red.add.f64):
+// results agree with a sequential sum to rounding, not bitwise (order).
+constexpr int kRaw = 7;
+
+__global__ void __launch_bounds__(256)
+k_p2c_atomic(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__ cell, int64_t n, int M, int sub,
+             double* __restrict__ acc)
+{
+    for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < n;
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int32_t j = __ldg(cell + p);
+        if (j < 0 || j >= M) continue;
+        const double x = __ldg(v + p), y = __ldg(v + ldv + p), z = __ldg(v + 2 * ldv + p);
+        double* a = acc + (static_cast<int64_t>(j) * sub + p % sub) * kRaw;
+        atomicAdd(a + 0, 1.0);
+        atomicAdd(a + 1, x);
+        atomicAdd(a + 2, y);
+        atomicAdd(a + 3, z);
+        atomicAdd(a + 4, x * x);
+        atomicAdd(a + 5, y * y);
+        atomicAdd(a + 6, z * z);
+    }
+}
+
+// thread per cell: raw[j] = sum over its sub-bins in fixed order
+__global__ void k_p2c_reduce(const double* __restrict__ acc, int M, int sub, double* __restrict__ raw)
+{
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= M) return;
+    double s[kRaw] = {0, 0, 0, 0, 0, 0, 0};
+    for (int m = 0; m < sub; ++m)
+#pragma unroll
+        for (int q = 0; q < kRaw; ++q) s[q] += acc[(static_cast<int64_t>(j) * sub + m) * kRaw + q];
+#pragma unroll
+    for (int q = 0; q < kRaw; ++q) raw[static_cast<int64_t>(j) * kRaw + q] = s[q];
+}
+
+// thread per cell: raw sums (possibly all-reduced over replicated ranks) -> moments [M][7]
+__global__ void k_p2c_moments(const double* __restrict__ raw, int M, MomConst mc, double* __restrict__ out)
+{
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= M) return;
+    const double* r = raw + static_cast<int64_t>(j) * kRaw;
+    double* o = out + static_cast<int64_t>(j) * CC_MOMENTS_LEN;
+    if (!(r[0] > 0.0)) {
+#pragma unroll
+        for (int q = 0; q < CC_MOMENTS_LEN; ++q) o[q] = 0.0;
+        return;
+    }
+    const double V = mc.volume_arr ? mc.volume_arr[j] : mc.volume;
+    moments_from_sums(r + 1, r[0], 0.0, 0.0, 0.0, V, mc, o);
+}
+
 // ------------------------------------------------------------------ NEXT f2: push (S2b + S2c)
 struct PushGrid {
     int dims;
@@ -1640,6 +1698,41 @@ int cc_push(const double* x_in, int64_t ldx_in, const int32_t* perm, double* x_o
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (E) launch_push<true>(blocks, st, x_in, ldx_in, perm, x_out, ldx_out, v, ldv, cell, n, g, E, ldE, q_over_m, dt);
     else launch_push<false>(blocks, st, x_in, ldx_in, perm, x_out, ldx_out, v, ldv, cell, n, g, E, ldE, q_over_m, dt);
+    return launch_ok();
+}
+
+size_t cc_p2c_scratch_bytes(int32_t cells, int32_t sub)
+{
+    if (cells < 1 || sub < 1) return 0;
+    return sizeof(double) * kRaw * static_cast<size_t>(cells) * static_cast<size_t>(sub);
+}
+
+int cc_p2c(const double* v, int64_t ldv, const int32_t* cell, int64_t n, int32_t cells, int32_t sub, double* raw_out,
+           void* scratch, size_t scratch_bytes, void* stream)
+{
+    cudaGetLastError();   // launch errors below are ours, not a stale earlier one
+    if (n < 0 || cells < 1 || sub < 1 || sub > 1024 || !raw_out || ldv < n) return CC_EINVAL;
+    if (n > 0 && (!v || !cell)) return CC_EINVAL;
+    if (!scratch || scratch_bytes < cc_p2c_scratch_bytes(cells, sub)) return CC_EWORKSPACE;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    double* acc = static_cast<double*>(scratch);
+    if (cudaMemsetAsync(acc, 0, cc_p2c_scratch_bytes(cells, sub), st) != cudaSuccess) return CC_ECUDA;
+    if (n > 0) {
+        const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 16));
+        k_p2c_atomic<<<blocks, 256, 0, st>>>(v, ldv, cell, n, cells, sub, acc);
+    }
+    k_p2c_reduce<<<(cells + 255) / 256, 256, 0, st>>>(acc, cells, sub, raw_out);
+    return launch_ok();
+}
+
+int cc_p2c_moments(const double* raw, int32_t cells, const cc_params* params, double* moments_out, void* stream)
+{
+    cudaGetLastError();   // launch errors below are ours, not a stale earlier one
+    if (!raw || !moments_out || cells < 1) return CC_EINVAL;
+    cc_params p;
+    if (params) p = *params; else cc_default_params(&p);
+    MomConst mc{p.weight, p.cell_volume, p.cell_volume_arr, p.mass / p.charge};
+    k_p2c_moments<<<(cells + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(raw, cells, mc, moments_out);
     return launch_ok();
 }
 

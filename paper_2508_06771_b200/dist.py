@@ -53,6 +53,8 @@ class DistOps:
     gather: Callable      # (v [3][n], cell [n], perm [n], cell_shift) -> (v [3][n], cell [n]) permuted
     sum_ranks: Callable   # (gathered [P][16]) -> [16] rank-ascending sum
     owner: Callable       # (cell_global int32 [n], bounds list) -> owner rank int32 [n]; dead (-1) -> -1
+    p2c: Optional[Callable] = None          # (v, cell, cells, sub) -> raw sums [cells][7] (NEXT f4)
+    p2c_moments: Optional[Callable] = None  # (raw [cells][7], weight, cell_volume) -> moments [cells][7]
 
 
 def cuda_ops() -> DistOps:
@@ -67,7 +69,14 @@ def cuda_ops() -> DistOps:
     def owner(cell_global, bounds):
         return cc.cc_owner(cell_global, bounds)
 
-    return DistOps(partition=partition, gather=gather, sum_ranks=cc.cc_diag_sum_ranks, owner=owner)
+    def p2c(v, cell, cells, sub):
+        return cc.cc_p2c(v, cell, cells, sub=sub)
+
+    def p2c_moments(raw, weight, cell_volume):
+        return cc.cc_p2c_moments(raw, weight=weight, cell_volume=cell_volume)
+
+    return DistOps(partition=partition, gather=gather, sum_ranks=cc.cc_diag_sum_ranks, owner=owner, p2c=p2c,
+                   p2c_moments=p2c_moments)
 
 
 def reduce_diag(diag: torch.Tensor, ops: DistOps, group=None) -> torch.Tensor:
@@ -135,6 +144,32 @@ def migrate(v: torch.Tensor, cell_global: torch.Tensor, global_cells: int, ops: 
                                    group=group)
         lp = rx
     return Migrated(lv, lc, send, recv, lp)
+
+
+# ---------------------------------------------------------------- NEXT f4: the paper's replicated grid
+# "each task owns N/P electrons and replicates all M cells.  Steps S1-S2 ... are done in an
+# embarrassingly parallel manner at each task.  Steps S3a and S3b are where the communication takes
+# place: a local P2C operation, ... followed by an all-reduce with message size O(M)".
+# The comparison point for the cell-range shards above: each rank runs coulomb_collide on ALL cells
+# (cell_base 0) with its own particles, a rank-distinct random stream (replica_seed) and weight
+# P x w (its N/P particles sample the whole plasma: "P simulations of N/P particles");
+# pairs never cross ranks (the paper's within-rank pairing).
+
+
+def replica_seed(seed: int, rank: int) -> int:
+    """Rank-distinct Philox key of replica `rank` (independent streams; rank 0 keeps `seed`)."""
+    return (seed + rank * 0x9E3779B97F4A7C15) % (1 << 64)
+
+
+def replicated_moments(v: torch.Tensor, cell: torch.Tensor, cells: int, ops: DistOps, *, weight: float,
+                       cell_volume: float, sub: int = 16, group=None) -> torch.Tensor:
+    """S3a/S3b of the replicated-grid scheme: local atomic P2C (sub-binned) of this rank's
+    particles, one all-reduce (sum) of the [cells][7] raw sums, moments of the union of all ranks'
+    particles with the physical weight w."""
+    raw = ops.p2c(v, cell, cells, sub)
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(raw, op=dist.ReduceOp.SUM, group=group)
+    return ops.p2c_moments(raw, weight, cell_volume)
 
 
 def init_from_env(backend: Optional[str] = None):

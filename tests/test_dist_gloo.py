@@ -12,7 +12,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2508_06771_b200.dist import DistOps, migrate, owner_bounds, reduce_diag, shard_cells
+from paper_2508_06771_b200.dist import (DistOps, migrate, owner_bounds, reduce_diag, replica_seed,
+                                        replicated_moments, shard_cells)
 
 
 def cpu_ops() -> DistOps:
@@ -41,7 +42,22 @@ def cpu_ops() -> DistOps:
         r[(c < b[0]) | (c >= b[-1])] = -1
         return torch.from_numpy(r.astype(np.int32))
 
-    return DistOps(partition, gather, sum_ranks, owner)
+    def p2c(v, cell, cells, sub):
+        # plain per-cell sums (the CUDA version is the atomic, sub-binned kernel)
+        c = cell.numpy()
+        vv = v.numpy()
+        raw = np.zeros((cells, 7))
+        ok = (c >= 0) & (c < cells)
+        raw[:, 0] = np.bincount(c[ok], minlength=cells)
+        for q in range(3):
+            raw[:, 1 + q] = np.bincount(c[ok], weights=vv[q][ok], minlength=cells)
+            raw[:, 4 + q] = np.bincount(c[ok], weights=vv[q][ok] ** 2, minlength=cells)
+        return torch.from_numpy(raw)
+
+    def p2c_moments(raw, weight, volume):
+        return raw.clone()           # the test compares the all-reduced raw sums directly
+
+    return DistOps(partition, gather, sum_ranks, owner, p2c, p2c_moments)
 
 
 def free_port():
@@ -73,6 +89,9 @@ def _worker(rank, world, port, q):
         m = migrate(torch.from_numpy(v), torch.from_numpy(cell), G, ops, payload=torch.from_numpy(x))
         res["mig"] = (m.v.numpy(), m.cell.numpy(), m.sent, m.received)
         res["payload"] = m.payload.numpy()
+        # NEXT f4: replicated grid — every rank deposits its own particles; one all-reduce
+        res["repl"] = replicated_moments(torch.from_numpy(v), torch.from_numpy(cell), G, ops, weight=1.0,
+                                         cell_volume=1.0).numpy()
         res["src"] = (v, cell)
         q.put((rank, res))
     finally:
@@ -122,4 +141,14 @@ def test_world2_diag_and_migration():
         assert np.array_equal(c, np.concatenate(expect_cells))
         assert sum(recv) == v.shape[1]
     total_live = sum(int(np.sum(out[s]["src"][1] >= 0)) for s in range(world))
+    # replicated-grid P2C: every rank holds the sums over the union of all ranks' particles
+    allv = np.concatenate([out[s]["src"][0] for s in range(world)], axis=1)
+    allc = np.concatenate([out[s]["src"][1] for s in range(world)])
+    ok = allc >= 0
+    for r in range(world):
+        raw = out[r]["repl"]
+        assert np.array_equal(raw[:, 0], np.bincount(allc[ok], minlength=10))
+        assert np.allclose(raw[:, 1], np.bincount(allc[ok], weights=allv[0][ok], minlength=10), rtol=1e-12)
+        assert np.array_equal(raw, out[0]["repl"])
+    assert replica_seed(42, 0) == 42 and len({replica_seed(42, r) for r in range(8)}) == 8
     assert sum(out[r]["mig"][0].shape[1] for r in range(world)) == total_live
