@@ -233,7 +233,9 @@ int cc_push(const double *x_in, int64_t ldx_in, const int32_t *perm, double *x_o
 /* Step S3a/S3b P2C the paper's way: a block reduction over UNSORTED
  * particles by fp64 atomics, each cell split into `sub` auxiliary sub-bins
  * omega_jm ("to [reduce] atomic updates congestion"; the sub-bin of
- * particle p is p mod sub), then V^j = sum_m V^jm in fixed order.
+ * particle p is (p / 32) mod sub), then V^j = sum_m V^jm in fixed order.  A
+ * warp of 32 particles of one cell (sorted input) is reduced with shuffles
+ * before its atomics.
  *  v [3][ldv], cell [n] (LOCAL ids; -1 / out-of-range ignored).
  *  raw_out DEVICE [cells][7] = {N_j, sum v_x, v_y, v_z, sum v_x^2, v_y^2, v_z^2}.
  *  scratch DEVICE, >= cc_p2c_scratch_bytes(cells, sub) bytes, 8-byte aligned.

@@ -1129,27 +1129,50 @@ __global__ void k_gather(const double* __restrict__ v, int64_t ldv, const int32_
 // UNSORTED particles by atomics, with each cell split into `sub` auxiliary
 // sub-bins omega_jm to spread atomic congestion, then V^j = sum_m V^jm.
 // Raw sums per (cell, sub-bin): {N, sum v_x, v_y, v_z, sum v_x^2, v_y^2, v_z^2};
-// the sub-bin of particle p is p mod sub.  fp64 global atomics (red.add.f64):
-// results agree with a sequential sum to rounding, not bitwise (order).
+// the sub-bin of particle p is (p / 32) mod sub (one per warp-aligned group of
+// 32 particles).  fp64 global atomics (red.add.f64): results agree with a
+// sequential sum to rounding, not bitwise (order).  A warp whose 32 particles
+// all sit in one cell (cell-sorted input) first reduces them with shuffles and
+// issues one set of 7 atomics instead of 32 — the congestion the paper's
+// sub-bins address, removed at the source.
 constexpr int kRaw = 7;
 
 __global__ void __launch_bounds__(256)
 k_p2c_atomic(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__ cell, int64_t n, int M, int sub,
              double* __restrict__ acc)
 {
-    for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < n;
-         p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int32_t j = __ldg(cell + p);
-        if (j < 0 || j >= M) continue;
-        const double x = __ldg(v + p), y = __ldg(v + ldv + p), z = __ldg(v + 2 * ldv + p);
-        double* a = acc + (static_cast<int64_t>(j) * sub + p % sub) * kRaw;
-        atomicAdd(a + 0, 1.0);
-        atomicAdd(a + 1, x);
-        atomicAdd(a + 2, y);
-        atomicAdd(a + 3, z);
-        atomicAdd(a + 4, x * x);
-        atomicAdd(a + 5, y * y);
-        atomicAdd(a + 6, z * z);
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t g = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; g * 32 < n; g += nwarps) {
+        const int64_t p = g * 32 + lane;
+        const int32_t j = p < n ? __ldg(cell + p) : -1;
+        const bool ok = j >= 0 && j < M;
+        double x = 0.0, y = 0.0, z = 0.0;
+        if (ok) { x = __ldg(v + p); y = __ldg(v + ldv + p); z = __ldg(v + 2 * ldv + p); }
+        const int32_t j0 = __shfl_sync(0xFFFFFFFFu, j, 0);
+        const int64_t bin = g % sub;
+        if (__all_sync(0xFFFFFFFFu, ok && j == j0)) {
+            double r[kRaw] = {1.0, x, y, z, x * x, y * y, z * z};
+#pragma unroll
+            for (int q = 0; q < kRaw; ++q)
+#pragma unroll
+                for (int d = 16; d > 0; d >>= 1) r[q] += __shfl_xor_sync(0xFFFFFFFFu, r[q], d);
+            if (lane < kRaw) {
+                double val = r[0];
+#pragma unroll
+                for (int q = 1; q < kRaw; ++q) val = (lane == q) ? r[q] : val;
+                atomicAdd(acc + (static_cast<int64_t>(j0) * sub + bin) * kRaw + lane, val);
+            }
+        } else if (ok) {
+            double* a = acc + (static_cast<int64_t>(j) * sub + bin) * kRaw;
+            atomicAdd(a + 0, 1.0);
+            atomicAdd(a + 1, x);
+            atomicAdd(a + 2, y);
+            atomicAdd(a + 3, z);
+            atomicAdd(a + 4, x * x);
+            atomicAdd(a + 5, y * y);
+            atomicAdd(a + 6, z * z);
+        }
     }
 }
 
