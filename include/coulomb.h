@@ -127,6 +127,28 @@ int coulomb_collide(const double *v_in, int64_t ldv, const int32_t *cell_in,
                     double *moments_out, double *diag_out,
                     void *workspace, size_t workspace_bytes, void *stream);
 
+/* End-to-end entry with HOST buffers: the same operator as coulomb_collide, with
+ * the host->device copies of the inputs and the device->host copies of the
+ * results enqueued on `stream` around it (asynchronous: results are valid after
+ * the stream is synchronised; pinned host memory gives full PCIe rate and lets
+ * the copies overlap other streams).
+ *  h_v_in [3][ldv], h_cell_in [n]       HOST inputs (read).
+ *  h_v_out [3][ldv], h_cell_out [n]     HOST outputs; h_perm_out [n], h_moments_out
+ *                                       [cells][7], h_diag_out [16] HOST or NULL.
+ *  dev_buffer  DEVICE scratch of >= cc_host_buffer_bytes(n, cells) bytes, 256-byte
+ *              aligned, holding device copies of the inputs/outputs and the
+ *              workspace; one per call in flight.
+ * Consecutive calls on two streams with two dev_buffers overlap one call's
+ * device->host copies with the next call's host->device copies (PCIe is full
+ * duplex); bench.py's e2e does exactly that.  Errors as coulomb_collide.    */
+size_t cc_host_buffer_bytes(int64_t n, int32_t cells);                    /* HOST */
+int coulomb_collide_host(const double *h_v_in, int64_t ldv, const int32_t *h_cell_in,
+                         double *h_v_out, int32_t *h_cell_out, int32_t *h_perm_out,
+                         int64_t n, int32_t cells, uint32_t cell_base, double dt,
+                         const cc_params *params, uint64_t seed, uint64_t step,
+                         double *h_moments_out, double *h_diag_out,
+                         void *dev_buffer, size_t dev_bytes, void *stream);
+
 /* Synchronises `stream` and returns CC_ECELL if a previous call on this
  * workspace saw an invalid cell id (the flag is then cleared), CC_ECUDA on a
  * CUDA error, else CC_OK.                                                     */

@@ -31,7 +31,8 @@ STAGE_NAMES = ("count", "scan", "scatter", "collide", "finalize")
 EXPORTS = ("cc_default_params", "cc_workspace_bytes", "coulomb_collide", "cc_device_status",
            "cc_strerror", "cc_bin", "cc_pairs", "cc_philox", "cc_ppnd16", "cc_ta_pairs",
            "cc_moments", "cc_coulomb_log", "cc_gather", "cc_owner", "cc_diag_sum_ranks", "cc_push",
-           "cc_step_advance", "cc_p2c_scratch_bytes", "cc_p2c", "cc_p2c_moments")
+           "cc_step_advance", "cc_p2c_scratch_bytes", "cc_p2c", "cc_p2c_moments",
+           "cc_host_buffer_bytes", "coulomb_collide_host")
 
 
 class CCParams(C.Structure):
@@ -106,6 +107,11 @@ def load():
     L.cc_p2c.restype = C.c_int
     L.cc_p2c_moments.argtypes = [vp, i32, C.POINTER(CCParams), vp, vp]
     L.cc_p2c_moments.restype = C.c_int
+    L.cc_host_buffer_bytes.argtypes = [i64, i32]
+    L.cc_host_buffer_bytes.restype = sz
+    L.coulomb_collide_host.argtypes = [vp, i64, vp, vp, vp, vp, i64, i32, u32, dbl, C.POINTER(CCParams),
+                                       u64, u64, vp, vp, vp, sz, vp]
+    L.coulomb_collide_host.restype = C.c_int
     L.cc_step_advance.argtypes = [vp, u32, vp]
     L.cc_step_advance.restype = C.c_int
     _lib = L

@@ -392,3 +392,44 @@ def cc_p2c_moments(raw: torch.Tensor, *, weight: float = 1.0, cell_volume: float
     check(_lib.load().cc_p2c_moments(_ptr(raw.contiguous()), cells, C.byref(p), _ptr(out), C.c_void_p(_stream(dev))),
           "cc_p2c_moments")
     return out
+
+
+# ---------------------------------------------------------------- end-to-end entry with host buffers
+
+
+def alloc_host_buffer(n: int, cells: int, device) -> torch.Tensor:
+    nbytes = int(_lib.load().cc_host_buffer_bytes(n, cells))
+    buf = torch.empty(nbytes + 256, dtype=torch.uint8, device=device)
+    pad = (-buf.data_ptr()) % 256
+    buf = buf[pad:pad + nbytes]
+    return buf
+
+
+def coulomb_collide_host(v: torch.Tensor, cell: torch.Tensor, cells: int, *, dt: float, out_v: torch.Tensor,
+                         out_cell: torch.Tensor, out_perm: Optional[torch.Tensor] = None,
+                         out_moments: Optional[torch.Tensor] = None, out_diag: Optional[torch.Tensor] = None,
+                         dev_buffer: torch.Tensor, stream: Optional[torch.cuda.Stream] = None, weight: float = 1.0,
+                         cell_volume: float = 1.0, ln_lambda: float = 10.0, cell_base: int = 0, seed: int = 42,
+                         step: int = 0, mass: float = M_E, charge: float = Q_E, eps0: float = EPS0,
+                         flags: int = 0) -> None:
+    """coulomb_collide on HOST (CPU, ideally pinned) tensors: copies in, the operator, copies out,
+    all enqueued on `stream` (asynchronous; synchronise before reading the outputs)."""
+    cpu = torch.device("cpu")
+    _need(cell, "cell", torch.int32, cpu)
+    n = cell.numel()
+    ldv = _soa(v, "v", cpu)
+    if _soa(out_v, "out_v", cpu) != ldv and n > 0:
+        raise ValueError("v and out_v must have the same row stride")
+    for t, nm, dt_ in ((out_cell, "out_cell", torch.int32), (out_perm, "out_perm", torch.int32),
+                       (out_moments, "out_moments", torch.float64), (out_diag, "out_diag", torch.float64)):
+        if t is not None:
+            _need(t, nm, dt_, cpu)
+    dev = dev_buffer.device
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    p = make_params(mass=mass, charge=charge, eps0=eps0, weight=weight, cell_volume=cell_volume,
+                    ln_lambda=ln_lambda, flags=flags)
+    rc = _lib.load().coulomb_collide_host(
+        _ptr(v), max(ldv, n), _ptr(cell), _ptr(out_v), _ptr(out_cell), _ptr(out_perm), n, cells, cell_base, dt,
+        C.byref(p), seed, step, _ptr(out_moments), _ptr(out_diag), _ptr(dev_buffer), dev_buffer.numel(),
+        C.c_void_p(st.cuda_stream))
+    check(rc, "coulomb_collide_host")

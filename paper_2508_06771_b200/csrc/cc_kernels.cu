@@ -1558,6 +1558,92 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     return launch_ok();
 }
 
+// ---------------------------------------------------------------- host-buffer entry (end-to-end path)
+namespace {
+struct HostLayout {
+    int64_t ldd = 0;   // device row stride (even, so the pair-vectorised stores apply)
+    size_t o_vin = 0, o_cin = 0, o_vout = 0, o_cout = 0, o_perm = 0, o_mom = 0, o_diag = 0, o_ws = 0, total = 0;
+};
+
+HostLayout host_layout(int64_t n, int32_t cells)
+{
+    HostLayout H;
+    H.ldd = std::max<int64_t>(2, n + (n & 1));
+    size_t o = 0;
+    H.o_vin = o;  o = align256(o + sizeof(double) * 3 * static_cast<size_t>(H.ldd));
+    H.o_vout = o; o = align256(o + sizeof(double) * 3 * static_cast<size_t>(H.ldd));
+    H.o_cin = o;  o = align256(o + sizeof(int32_t) * static_cast<size_t>(std::max<int64_t>(n, 1)));
+    H.o_cout = o; o = align256(o + sizeof(int32_t) * static_cast<size_t>(std::max<int64_t>(n, 1)));
+    H.o_perm = o; o = align256(o + sizeof(int32_t) * static_cast<size_t>(std::max<int64_t>(n, 1)));
+    H.o_mom = o;  o = align256(o + sizeof(double) * CC_MOMENTS_LEN * static_cast<size_t>(cells));
+    H.o_diag = o; o = align256(o + sizeof(double) * CC_DIAG_LEN);
+    H.o_ws = o;   o = align256(o + cc_workspace_bytes(n, cells));
+    H.total = o;
+    return H;
+}
+}  // namespace
+
+size_t cc_host_buffer_bytes(int64_t n, int32_t cells)
+{
+    if (n < 0 || cells < 1) return 0;
+    return host_layout(n, cells).total;
+}
+
+int coulomb_collide_host(const double* h_v_in, int64_t ldv, const int32_t* h_cell_in, double* h_v_out,
+                         int32_t* h_cell_out, int32_t* h_perm_out, int64_t n, int32_t cells, uint32_t cell_base,
+                         double dt, const cc_params* params, uint64_t seed, uint64_t step, double* h_moments_out,
+                         double* h_diag_out, void* dev_buffer, size_t dev_bytes, void* stream)
+{
+    cudaGetLastError();   // launch errors below are ours, not a stale earlier one
+    if (n < 0 || cells < 1 || ldv < n) return CC_EINVAL;
+    if (n >= (1ll << 31) || cells > CC_MAX_CELLS) return CC_ECOUNT;
+    if (n > 0 && (!h_v_in || !h_cell_in || !h_v_out || !h_cell_out)) return CC_EINVAL;
+    const HostLayout H = host_layout(n, cells);
+    if (!dev_buffer || !aligned(dev_buffer, 256) || dev_bytes < H.total) return CC_EWORKSPACE;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    char* b = static_cast<char*>(dev_buffer);
+    double* d_vin = reinterpret_cast<double*>(b + H.o_vin);
+    double* d_vout = reinterpret_cast<double*>(b + H.o_vout);
+    int32_t* d_cin = reinterpret_cast<int32_t*>(b + H.o_cin);
+    int32_t* d_cout = reinterpret_cast<int32_t*>(b + H.o_cout);
+    int32_t* d_perm = reinterpret_cast<int32_t*>(b + H.o_perm);
+    double* d_mom = reinterpret_cast<double*>(b + H.o_mom);
+    double* d_diag = reinterpret_cast<double*>(b + H.o_diag);
+    const size_t row = sizeof(double) * static_cast<size_t>(n);
+    if (n > 0) {
+        // H2D: cell ids first (the count pass needs only them), then the three velocity rows
+        if (cudaMemcpyAsync(d_cin, h_cell_in, sizeof(int32_t) * n, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+            cudaMemcpy2DAsync(d_vin, sizeof(double) * H.ldd, h_v_in, sizeof(double) * ldv, row, 3,
+                              cudaMemcpyHostToDevice, st) != cudaSuccess) {
+            cudaGetLastError();
+            return CC_ECUDA;
+        }
+    }
+    int rc = coulomb_collide(d_vin, H.ldd, d_cin, d_vout, d_cout, h_perm_out ? d_perm : nullptr, n, cells, cell_base,
+                             dt, params, seed, step, h_moments_out ? d_mom : nullptr, h_diag_out ? d_diag : nullptr,
+                             b + H.o_ws, H.total - H.o_ws, stream);
+    if (rc) return rc;
+    bool ok = true;
+    if (n > 0) {
+        ok = ok && cudaMemcpy2DAsync(h_v_out, sizeof(double) * ldv, d_vout, sizeof(double) * H.ldd, row, 3,
+                                     cudaMemcpyDeviceToHost, st) == cudaSuccess;
+        ok = ok && cudaMemcpyAsync(h_cell_out, d_cout, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st) == cudaSuccess;
+        if (h_perm_out)
+            ok = ok && cudaMemcpyAsync(h_perm_out, d_perm, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st) == cudaSuccess;
+    }
+    if (h_moments_out)
+        ok = ok && cudaMemcpyAsync(h_moments_out, d_mom, sizeof(double) * CC_MOMENTS_LEN * cells,
+                                   cudaMemcpyDeviceToHost, st) == cudaSuccess;
+    if (h_diag_out)
+        ok = ok && cudaMemcpyAsync(h_diag_out, d_diag, sizeof(double) * CC_DIAG_LEN, cudaMemcpyDeviceToHost, st) ==
+                       cudaSuccess;
+    if (!ok) {
+        cudaGetLastError();
+        return CC_ECUDA;
+    }
+    return CC_OK;
+}
+
 int cc_device_status(void* workspace, void* stream)
 {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
