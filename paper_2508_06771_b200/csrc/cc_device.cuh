@@ -342,7 +342,7 @@ __device__ __forceinline__ void ta_update(double& ax, double& ay, double& az,
 
 // ---------------------------------------------------------------- Nanbu (R20)
 // s = 2 <delta^2>; A solves coth A - 1/A = exp(-s) (inverse Langevin: Newton
-// from Cohen's Pade start; Taylor series of L and L' below A = 1/4; A = 1/(1 -
+// from Jedynak's start; Taylor series of L and L' below A = 1/4; A = 1/(1 -
 // exp(-s)) when that exceeds 40); 1 - cos(chi) = -log1p((1-u1) expm1(-2A)) / A.
 __constant__ double kLangC[8] = {1.0 / 3.0, -1.0 / 45.0, 2.0 / 945.0, -1.0 / 4725.0, 2.0 / 93555.0,
                                  -1382.0 / 638512875.0, 4.0 / 18243225.0, -3617.0 / 162820783125.0};
@@ -359,9 +359,12 @@ __device__ __forceinline__ double langevin(double A, double* dL)
         *dL = d;
         return A * s;
     }
-    const double sh = sinh(A);
-    *dL = 1.0 / (A * A) - 1.0 / (sh * sh);
-    return 1.0 / tanh(A) - 1.0 / A;
+    // coth A = -(2 + em) / em and 1 / sinh^2 A = 4 (1 + em) / em^2 with em = expm1(-2A):
+    // one transcendental instead of tanh + sinh (same values to rounding as the oracle's forms)
+    const double em = expm1(-2.0 * A);
+    const double ie = 1.0 / em, ia = 1.0 / A;
+    *dL = ia * ia - 4.0 * (1.0 + em) * ie * ie;
+    return -(2.0 + em) * ie - ia;
 }
 
 // returns A; +inf means "no scattering" (s = 0), 0 means isotropic
@@ -372,12 +375,15 @@ __device__ __forceinline__ double nanbu_A(double s)
     if (x <= 0.0) return 0.0;
     const double omx = -expm1(-s);
     if (omx < 1.0 / 40.0) return 1.0 / omx;
-    double A = x * (3.0 - x * x) / (1.0 - x * x);
+    // Jedynak's (2015) inverse-Langevin approximation (<= 1.4% off) as the start; Newton is
+    // quadratic, so once a step is below 1e-9 A the remaining error is ~1e-18 A: stop there
+    // (the oracle iterates to a 1e-15 step from Cohen's start: the same root to ~1e-15).
+    double A = x * (3.0 - x * (2.6 - 0.7 * x)) / ((1.0 - x) * (1.0 + 0.1 * x));
     for (int it = 0; it < 60; ++it) {
         double dL;
         const double dA = (langevin(A, &dL) - x) / dL;
         A -= dA;
-        if (fabs(dA) <= 1e-15 * A) break;
+        if (fabs(dA) <= 1e-9 * A) break;
     }
     return A;
 }
