@@ -250,6 +250,27 @@ int cc_push(const double *x_in, int64_t ldx_in, const int32_t *perm, double *x_o
             double *v, int64_t ldv, int32_t *cell, int64_t n, int32_t cells, uint32_t cell_base,
             const cc_grid *grid, const double *E, int64_t ldE, double q_over_m, double dt, void *stream);
 
+/* ---- NEXT f3: three-body recombination C5 ---------------------- */
+
+/* Table 4 RS0-RS5 (SPEC recomb S:271-330) on the OUTPUT of a
+ * coulomb_collide call (v_out / cell_out: cell-sorted, random pair order inside
+ * a cell, dead last), in place, one pass, no atomics on the particle data:
+ *  RS0 (R25) position q of cell j is a primary iff U(Philox(ctr = (q, cell_base+j,
+ *      step, 4), key = seed)) < prob[j]  (prob DEVICE [cells]: the caller's
+ *      1 - exp(-dt k_r n_i n_e));
+ *  RS1-RS3 (R26) the i-th primary of the cell (position order) is matched to the
+ *      i-th non-primary ("catalyte") for i < min(P_j, N_j - P_j) — unique and
+ *      cell-local by construction; the other primaries are "starved" (unchanged);
+ *  RS4 (R27) catalyte keeps its direction, |v_c'|^2 = |v_c|^2 + |v_p|^2 + 2 eps_bind/mass
+ *      (a catalyte at rest takes the primary's direction, +x if both rest);
+ *  RS5 (R28) the primary dies: cell -1 (velocity kept).
+ * stats_out DEVICE uint64 [3] = {recombined, starved, primaries} (overwritten).
+ * Must be called on an unmodified coulomb_collide output (it locates cells by
+ * binary search in cell_out).  Bit-exact with the oracle.                  */
+int cc_recombine(double *v, int64_t ldv, int32_t *cell, int64_t n, int32_t cells, uint32_t cell_base,
+                 const double *prob, double eps_bind, double mass, uint64_t seed, uint64_t step,
+                 unsigned long long *stats_out, void *stream);
+
 /* ---- NEXT f4: the paper's own P2C and replicated-grid scheme ---- */
 
 /* Step S3a/S3b P2C the paper's way: a block reduction over UNSORTED

@@ -105,6 +105,9 @@ def lib():
                               C.c_void_p, C.c_void_p, C.c_uint32,                        # nc[3], d[3], periodic
                               C.c_void_p, C.c_int64, C.c_double, C.c_double]             # E, ldE, q/m, dt
         L.or_push.restype = None
+        L.or_recombine.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32, C.c_uint32,
+                                   C.c_void_p, C.c_double, C.c_double, C.c_uint64, C.c_uint64, C.c_void_p]
+        L.or_recombine.restype = None
         L.or_num_threads.argtypes = []
         L.or_num_threads.restype = C.c_int
         _lib = L
@@ -301,6 +304,19 @@ def push(x, v, cell, *, dims, nc, d, periodic, dt, q_over_m=-Q_E / M_E, E=None, 
     lib().or_push(_ptr(x), x.shape[1], _ptr(pm), _ptr(x_out), n, _ptr(v_out), n, _ptr(cell_out), n, dims,
                   _ptr(nc3), _ptr(d3), periodic, _ptr(Ea), 0 if Ea is None else Ea.shape[1], q_over_m, dt)
     return x_out, v_out, cell_out
+
+
+def recombine(v, cell, cells, prob, *, eps_bind, cell_base=0, seed=42, step=0, mass=M_E):
+    """NEXT f3: recombination C5 (Table 4 RS0-RS5, readings R25-R28) on a collision call's
+    cell-sorted output.  Returns (v_out, cell_out, stats {recombined, starved, primaries})."""
+    v_out = np.array(v, dtype=np.float64, order="C", copy=True)
+    cell_out = np.array(cell, dtype=np.int32, copy=True)
+    pr = np.ascontiguousarray(prob, dtype=np.float64)
+    st = np.zeros(3, np.int64)
+    n = cell_out.size
+    lib().or_recombine(_ptr(v_out), n, _ptr(cell_out), n, cells, cell_base, _ptr(pr), eps_bind, mass, seed, step,
+                       _ptr(st))
+    return v_out, cell_out, st
 
 
 def num_threads() -> int:

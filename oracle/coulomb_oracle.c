@@ -764,3 +764,68 @@ void or_push(const double *x_in, int64_t ldx_in, const int64_t *perm, double *x_
         cell[p] = alive ? (int32_t)G : -1;
     }
 }
+
+/* ------------------------------------------------------------------------ */
+/* NEXT f3: three-body recombination C5, Table 4 RS0-RS5
+ * (P:262-290), on the OUTPUT of a collision call (cell-sorted; inside a cell
+ * the slots are in the step's random pair order, R14).  Readings R25-R28:
+ *  RS0 (R25) the particle at position q of cell j (global id G) is a primary
+ *      iff U(Philox(ctr = (q, G, step, 4), key = seed)) < prob[j] (SPEC S:289's
+ *      per-particle probability, supplied per cell by the caller);
+ *  RS1-RS3 (R26) the i-th primary of the cell (position order) is matched to
+ *      the i-th non-primary ("catalyte", position order) for i < min(P_j,
+ *      N_j - P_j): unique and cell-local by construction, and uniform because
+ *      the position order is a fresh random permutation every step; primaries
+ *      beyond the catalyte count are starved and left unchanged;
+ *  RS4 (R27) the catalyte keeps its direction and takes the primary's kinetic
+ *      energy plus the binding energy e_b: |v_c'|^2 = |v_c|^2 + |v_p|^2 + 2 e_b/m
+ *      (SPEC S:321); a catalyte at rest takes the primary's direction (+x if
+ *      that is zero too);
+ *  RS5 (R28) the primary dies (cell -1, velocity kept).
+ * cell: [n] in place; v [3][ldv] in place; stats {recombined, starved, primaries}. */
+static double or_rc_norm2(double x, double y, double z) { return x * x + y * y + z * z; }
+
+void or_recombine(double *v, int64_t ldv, int32_t *cell, int64_t n, int32_t M, uint32_t cell_base,
+                  const double *prob, double eps_bind, double mass, uint64_t seed, uint64_t step, int64_t stats[3])
+{
+    stats[0] = stats[1] = stats[2] = 0;
+    const double vb2 = 2.0 * eps_bind / mass;
+    int64_t *prim = malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+    int64_t *cat = malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+    int64_t lo = 0;
+    for (int32_t j = 0; j < M; ++j) {
+        int64_t hi = lo;
+        while (hi < n && cell[hi] == j) ++hi;         /* cell-sorted input */
+        const int64_t N = hi - lo;
+        const uint32_t G = cell_base + (uint32_t)j;
+        int64_t np = 0, nc = 0;
+        for (int64_t q = 0; q < N; ++q) {             /* RS0 */
+            uint32_t ctr[4] = {(uint32_t)q, G, (uint32_t)step, 4u};
+            uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+            uint32_t x[4];
+            or_philox4x32_10(ctr, key, x);
+            if (or_u01(x[0], x[1]) < prob[j]) prim[np++] = lo + q;
+            else cat[nc++] = lo + q;
+        }
+        const int64_t m = np < nc ? np : nc;
+        for (int64_t i = 0; i < m; ++i) {             /* RS3-RS5 */
+            const int64_t a = prim[i], c = cat[i];
+            const double px = v[a], py = v[ldv + a], pz = v[2 * ldv + a];
+            const double cx = v[c], cy = v[ldv + c], cz = v[2 * ldv + c];
+            const double c2 = or_rc_norm2(cx, cy, cz), p2 = or_rc_norm2(px, py, pz);
+            const double t2 = c2 + p2 + vb2;          /* |v_c'|^2 */
+            double ux = cx, uy = cy, uz = cz, s2 = c2;  /* direction source */
+            if (c2 == 0.0) { ux = px; uy = py; uz = pz; s2 = p2; }
+            if (s2 == 0.0) { ux = 1.0; uy = 0.0; uz = 0.0; s2 = 1.0; }
+            const double f = sqrt(t2 / s2);
+            v[c] = ux * f; v[ldv + c] = uy * f; v[2 * ldv + c] = uz * f;
+            cell[a] = -1;
+        }
+        stats[0] += m;
+        stats[1] += np - m;
+        stats[2] += np;
+        lo = hi;
+    }
+    free(prim);
+    free(cat);
+}

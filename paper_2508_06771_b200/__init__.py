@@ -8,4 +8,4 @@ from .coulomb import (Collider, CollideOut, alloc_workspace, cc_bin, cc_device_s
                       cc_diag_sum_ranks, cc_moments, cc_pairs, cc_philox, cc_ppnd16, cc_strerror,
                       cc_ta_pairs, cc_workspace_bytes, coulomb_collide, make_params, cc_gather, cc_owner, cc_coulomb_log,
                       Grid, cc_push, cc_step_advance, cc_p2c, cc_p2c_moments, alloc_host_buffer,
-                      coulomb_collide_host)
+                      coulomb_collide_host, cc_recombine)

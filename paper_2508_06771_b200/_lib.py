@@ -32,7 +32,7 @@ EXPORTS = ("cc_default_params", "cc_workspace_bytes", "coulomb_collide", "cc_dev
            "cc_strerror", "cc_bin", "cc_pairs", "cc_philox", "cc_ppnd16", "cc_ta_pairs",
            "cc_moments", "cc_coulomb_log", "cc_gather", "cc_owner", "cc_diag_sum_ranks", "cc_push",
            "cc_step_advance", "cc_p2c_scratch_bytes", "cc_p2c", "cc_p2c_moments",
-           "cc_host_buffer_bytes", "coulomb_collide_host")
+           "cc_host_buffer_bytes", "coulomb_collide_host", "cc_recombine")
 
 
 class CCParams(C.Structure):
@@ -112,6 +112,8 @@ def load():
     L.coulomb_collide_host.argtypes = [vp, i64, vp, vp, vp, vp, i64, i32, u32, dbl, C.POINTER(CCParams),
                                        u64, u64, vp, vp, vp, sz, vp]
     L.coulomb_collide_host.restype = C.c_int
+    L.cc_recombine.argtypes = [vp, i64, vp, i64, i32, u32, vp, dbl, dbl, u64, u64, vp, vp]
+    L.cc_recombine.restype = C.c_int
     L.cc_step_advance.argtypes = [vp, u32, vp]
     L.cc_step_advance.restype = C.c_int
     _lib = L

@@ -433,3 +433,23 @@ def coulomb_collide_host(v: torch.Tensor, cell: torch.Tensor, cells: int, *, dt:
         C.byref(p), seed, step, _ptr(out_moments), _ptr(out_diag), _ptr(dev_buffer), dev_buffer.numel(),
         C.c_void_p(st.cuda_stream))
     check(rc, "coulomb_collide_host")
+
+
+# ---------------------------------------------------------------- NEXT f3: recombination C5
+
+
+def cc_recombine(v: torch.Tensor, cell: torch.Tensor, prob: torch.Tensor, *, eps_bind: float, cell_base: int = 0,
+                 seed: int = 42, step: int = 0, mass: float = M_E) -> torch.Tensor:
+    """Recombination C5 (Table 4) in place on a coulomb_collide output (v_out, cell_out);
+    prob [cells] per-cell primary probability.  Returns stats {recombined, starved, primaries}
+    (int64 [3], on the device)."""
+    dev = cell.device
+    _need(cell, "cell", torch.int32, dev)
+    _need(prob, "prob", torch.float64, dev)
+    n = cell.numel()
+    ldv = _soa(v, "v", dev)
+    stats = torch.empty(3, dtype=torch.int64, device=dev)
+    check(_lib.load().cc_recombine(_ptr(v), max(ldv, n), _ptr(cell), n, prob.numel(), cell_base, _ptr(prob),
+                                   eps_bind, mass, seed, step, _ptr(stats), C.c_void_p(_stream(dev))),
+          "cc_recombine")
+    return stats

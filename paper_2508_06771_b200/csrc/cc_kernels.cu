@@ -1205,6 +1205,100 @@ __global__ void k_p2c_moments(const double* __restrict__ raw, int M, MomConst mc
     moments_from_sums(r + 1, r[0], 0.0, 0.0, 0.0, V, mc, o);
 }
 
+// ------------------------------------------------------------------ NEXT f3: recombination C5
+// Table 4 RS0-RS5 on a collision call's cell-sorted output, one CTA
+// per cell.  The paper builds per-cell catalyte lists with atomics over
+// unsorted particles (RS1, "the majority of time") and pops them atomically
+// (RS3); here the particles already sit cell-major in a fresh random order
+// (the pair order, R14), so RS1 is a block scan and the matching is the
+// deterministic rank match of R26: i-th primary <-> i-th non-primary.
+constexpr int kRecWin = 2048;   // primaries matched per pass over the cell
+
+__device__ __forceinline__ bool rc_primary(int32_t q, uint32_t G, uint32_t step, uint32_t s0, uint32_t s1, double prob)
+{
+    const cc::U4 x = cc::philox4x32_10(cc::U4{static_cast<uint32_t>(q), G, step, 4u}, s0, s1);
+    return cc::u01(x.x, x.y) < prob;
+}
+
+__device__ __forceinline__ int32_t rc_key(int32_t c, int M) { return (c < 0 || c >= M) ? M : c; }
+
+__global__ void __launch_bounds__(256)
+k_recombine(double* __restrict__ v, int64_t ldv, int32_t* __restrict__ cell, int64_t n, int M, uint32_t cell_base,
+            const double* __restrict__ prob, double vb2, uint32_t step, uint32_t s0, uint32_t s1,
+            unsigned long long* __restrict__ stats)
+{
+    __shared__ int64_t s_lo, s_hi;
+    __shared__ int32_t s_wsum[8];
+    __shared__ int32_t ppos[kRecWin], cpos[kRecWin];
+    const int j = blockIdx.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {             // the cell's slot range: binary search in the cell-sorted ids
+        int64_t a = 0, b = n;
+        while (a < b) { const int64_t m = (a + b) >> 1; if (rc_key(cell[m], M) < j) a = m + 1; else b = m; }
+        s_lo = a;
+        b = n;
+        while (a < b) { const int64_t m = (a + b) >> 1; if (rc_key(cell[m], M) <= j) a = m + 1; else b = m; }
+        s_hi = a;
+    }
+    __syncthreads();
+    const int64_t lo = s_lo;
+    const int32_t N = static_cast<int32_t>(s_hi - lo);
+    const double pr = prob[j];
+    if (N == 0 || !(pr > 0.0)) return;
+    const uint32_t G = cell_base + static_cast<uint32_t>(j);
+    // RS0: count the primaries
+    int32_t np = 0;
+    for (int32_t q = threadIdx.x; q < N; q += blockDim.x) np += rc_primary(q, G, step, s0, s1, pr);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) np += __shfl_xor_sync(0xFFFFFFFFu, np, d);
+    if (lane == 0) s_wsum[w] = np;
+    __syncthreads();
+    int32_t P = 0;
+    for (int i = 0; i < 8; ++i) P += s_wsum[i];
+    const int32_t m = min(P, N - P);
+    // RS1-RS5 in windows of kRecWin ranks: positions of primaries / catalytes of rank in the window
+    for (int32_t w0 = 0; w0 < m; w0 += kRecWin) {
+        __syncthreads();
+        int32_t base = 0;               // primaries before the current 256-position chunk
+        for (int32_t q0 = 0; q0 < N; q0 += blockDim.x) {
+            const int32_t q = q0 + threadIdx.x;
+            const bool isp = q < N && rc_primary(q, G, step, s0, s1, pr);
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, isp);
+            __syncthreads();
+            if (lane == 0) s_wsum[w] = __popc(bal);
+            __syncthreads();
+            int32_t before = base;
+            for (int i = 0; i < w; ++i) before += s_wsum[i];
+            const int32_t rp = before + __popc(bal & ((1u << lane) - 1u));   // primary rank of q
+            if (q < N) {
+                const int32_t r = isp ? rp : q - rp;                           // catalyte rank = q - rp
+                if (r >= w0 && r < w0 + kRecWin && r < m) (isp ? ppos : cpos)[r - w0] = q;
+            }
+            for (int i = 0; i < 8; ++i) base += s_wsum[i];
+        }
+        __syncthreads();
+        for (int32_t i = threadIdx.x; i < min(kRecWin, m - w0); i += blockDim.x) {
+            const int64_t a = lo + ppos[i], c = lo + cpos[i];
+            const double px = v[a], py = v[ldv + a], pz = v[2 * ldv + a];
+            const double cx = v[c], cy = v[ldv + c], cz = v[2 * ldv + c];
+            const double c2 = __dadd_rn(__dadd_rn(__dmul_rn(cx, cx), __dmul_rn(cy, cy)), __dmul_rn(cz, cz));
+            const double p2 = __dadd_rn(__dadd_rn(__dmul_rn(px, px), __dmul_rn(py, py)), __dmul_rn(pz, pz));
+            const double t2 = __dadd_rn(__dadd_rn(c2, p2), vb2);
+            double ux = cx, uy = cy, uz = cz, s2 = c2;
+            if (c2 == 0.0) { ux = px; uy = py; uz = pz; s2 = p2; }
+            if (s2 == 0.0) { ux = 1.0; uy = 0.0; uz = 0.0; s2 = 1.0; }
+            const double f = __dsqrt_rn(__ddiv_rn(t2, s2));
+            v[c] = __dmul_rn(ux, f); v[ldv + c] = __dmul_rn(uy, f); v[2 * ldv + c] = __dmul_rn(uz, f);
+            cell[a] = -1;
+        }
+    }
+    if (threadIdx.x == 0) {
+        atomicAdd(stats + 0, static_cast<unsigned long long>(m));
+        atomicAdd(stats + 1, static_cast<unsigned long long>(P - m));
+        atomicAdd(stats + 2, static_cast<unsigned long long>(P));
+    }
+}
+
 // ------------------------------------------------------------------ NEXT f2: push (S2b + S2c)
 struct PushGrid {
     int dims;
@@ -1842,6 +1936,25 @@ int cc_p2c_moments(const double* raw, int32_t cells, const cc_params* params, do
     if (params) p = *params; else cc_default_params(&p);
     MomConst mc{p.weight, p.cell_volume, p.cell_volume_arr, p.mass / p.charge};
     k_p2c_moments<<<(cells + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(raw, cells, mc, moments_out);
+    return launch_ok();
+}
+
+int cc_recombine(double* v, int64_t ldv, int32_t* cell, int64_t n, int32_t cells, uint32_t cell_base,
+                 const double* prob, double eps_bind, double mass, uint64_t seed, uint64_t step,
+                 unsigned long long* stats_out, void* stream)
+{
+    cudaGetLastError();   // launch errors below are ours, not a stale earlier one
+    if (n < 0 || cells < 1 || ldv < n || !prob || !stats_out || !finite_pos(mass) || !std::isfinite(eps_bind) ||
+        eps_bind < 0.0 || step >= (1ull << 32))
+        return CC_EINVAL;
+    if (n >= (1ll << 31) || cells > CC_MAX_CELLS) return CC_ECOUNT;
+    if (n > 0 && (!v || !cell)) return CC_EINVAL;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (cudaMemsetAsync(stats_out, 0, 3 * sizeof(unsigned long long), st) != cudaSuccess) return CC_ECUDA;
+    if (n == 0) return CC_OK;
+    k_recombine<<<cells, 256, 0, st>>>(v, ldv, cell, n, cells, cell_base, prob, 2.0 * eps_bind / mass,
+                                       static_cast<uint32_t>(step), static_cast<uint32_t>(seed),
+                                       static_cast<uint32_t>(seed >> 32), stats_out);
     return launch_ok();
 }
 
