@@ -370,7 +370,27 @@ def p2c_section(dev, w):
             out[f"{name}_sub{sub}_hbm_frac"] = 28 * w.n / (ms * 1e-3) / 1e9 / peak
     out["what"] = ("atomic P2C (7 fp64 red.add per particle into [cells][sub] bins) + fixed-order sub-bin "
                    "reduction + moments; algorithmic 28 B/particle")
-    return out
+    # NEXT f3: recombination C5 on a collision output (cell-sorted, pair order), per-cell primary probability
+    res = cc.coulomb_collide(v, cell, w.cells, step=1, dt=w.dt, weight=w.weight, cell_volume=w.cell_volume)
+    rec = {}
+    for pr in (1e-3, 0.1):
+        prob = torch.full((w.cells,), pr, dtype=torch.float64, device=dev)
+        times = []
+        for rep in range(3):               # each call on a fresh copy of the collision output (precondition)
+            vv, ccell = res.v_out.clone(), res.cell_out.clone()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            st = cc.cc_recombine(vv, ccell, prob, eps_bind=15.76 * 1.602176634e-19, step=1 + rep)
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+        ms = min(times[1:])
+        rec[f"prob_{pr:g}"] = {"ms": ms, "particles_per_s": w.n / (ms * 1e-3), "stats": st.tolist()}
+    rec["what"] = ("cc_recombine on the C4 collision output (fresh copy per call; min of 2 after a warm-up); "
+                   "two Philox draws per particle (count + match pass), no per-particle memory traffic except the "
+                   "matched pairs: bound by integer ALU, not HBM")
+    return {"p2c": out, "recombination": rec}
 
 
 def run_ours(args):
@@ -612,7 +632,7 @@ def run_ours(args):
             line["pic"] = {"error": repr(e)}
     if world == 1 and not args.no_pic:
         try:
-            line["p2c"] = p2c_section(dev, w)
+            line.update(p2c_section(dev, w))
         except Exception as e:
             line["p2c"] = {"error": repr(e)}
     if world == 1 and not args.no_cpu_baseline:
