@@ -10,6 +10,9 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_c
    python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > /dev/null 2>&1; echo collide rc=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_scatter" -s 4 -c 1 -o gpurun_out/${TAG}_scatter \
    python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > /dev/null 2>&1; echo scatter rc=$?
+# NEXT-row kernels: one launch each of k_push, k_p2c_atomic, k_recombine from the bench's pic/p2c sections
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_push|k_p2c_atomic|k_recombine" -c 3 \
+   -o gpurun_out/${TAG}_next python bench.py --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 1 > /dev/null 2>&1; echo next rc=$?
 python tools/traffic_from_ncu.py gpurun_out/${TAG}_collide.ncu-rep gpurun_out/${TAG}_scatter.ncu-rep > /dev/null
 timeout 900 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; cat gpurun_out/${TAG}_bench.json | cut -c1-400
 cp profiles/traffic.json gpurun_out/${TAG}_traffic.json
