@@ -41,8 +41,18 @@ constexpr int kCountThreads = 256;
 constexpr int kSub = 4096;               // elements per warp sub-range in k_scatter
 constexpr int kScatterUnrollA = 16;      // cell loads in flight per lane, counting pass
 constexpr int kScatterUnrollB = 6;       // (cell, v) loads in flight per lane, scatter pass
-constexpr int kCollideThreads = 256;
-constexpr int kChunk = 768;              // items (pairs or sitter) per k_collide_large CTA
+// k_collide_large shape (tools/collide_shape.sh overrides them for design studies)
+#ifndef CC_COLLIDE_THREADS
+#define CC_COLLIDE_THREADS 192
+#endif
+#ifndef CC_CHUNK
+#define CC_CHUNK 576
+#endif
+#ifndef CC_COLLIDE_CTAS
+#define CC_COLLIDE_CTAS 4
+#endif
+constexpr int kCollideThreads = CC_COLLIDE_THREADS;
+constexpr int kChunk = CC_CHUNK;         // items (pairs or sitter) per k_collide_large CTA
 constexpr int kRec = 8;                  // chunk moment record: S1' (3), S2' (3), pad
 constexpr int kSmallRec = 12;            // small-cell record: S1', S2' about the exact mean, the mean (3), pad
 constexpr int kCellSum = 4;              // per-cell raw post-collision sums: v (3), |v|^2
@@ -695,7 +705,7 @@ constexpr size_t kCollideSmem = 2ull * kChunk * 4 * sizeof(double);
 static_assert(kChunk % kCollideThreads == 0, "chunk must be a whole number of thread items");
 
 template <bool NANBU>
-__global__ void __launch_bounds__(kCollideThreads, 3)
+__global__ void __launch_bounds__(kCollideThreads, CC_COLLIDE_CTAS)
 k_collide_large(CollideArgs A)
 {
     extern __shared__ __align__(16) double stage[];       // [2][kChunk][4]

@@ -1,0 +1,14 @@
+# k_collide_large shape study: threads per CTA x chunk items x CTAs per SM (launch bounds).
+# Rebuilds the library per variant into the in-tree .so (restored at the end) and times the
+# steady-state bench.  usage (GPU box): bash tools/collide_shape.sh 256,768,3 192,576,4 ...
+python -c "import __graft_entry__ as g; g.build()"
+cp paper_2508_06771_b200/lib/libcoulomb.so /tmp/libcoulomb_orig.so
+for v in "$@"; do
+  set -- ${v//,/ }
+  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared \
+    -DCC_COLLIDE_THREADS=$1 -DCC_CHUNK=$2 -DCC_COLLIDE_CTAS=$3 \
+    -o paper_2508_06771_b200/lib/libcoulomb.so paper_2508_06771_b200/csrc/cc_kernels.cu 2>/dev/null || { echo "$v build failed"; continue; }
+  timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-pic --e2e-steps 1 > gpurun_out/shape.json 2>/dev/null
+  python -c "import json; d=json.load(open('gpurun_out/shape.json')); print('threads chunk ctas $v: collide', round(d['stages_ms']['collide'],3), 'cold', round(d['cold']['stages_ms']['collide'],3), 'warm', round(d['warm']['stages_ms']['collide'],3))"
+done
+cp /tmp/libcoulomb_orig.so paper_2508_06771_b200/lib/libcoulomb.so
