@@ -70,3 +70,33 @@ def test_reduce_diag_and_migrate_one_rank(nccl1):
     assert np.array_equal(m.v.cpu().numpy(), v[:, live])
     assert np.array_equal(m.cell.cpu().numpy(), cell[live])
     assert m.sent == [int(live.sum())] and m.received == [int(live.sum())]
+
+
+def test_pic_loop_dist_path_one_rank(nccl1):
+    """PicLoop's multi-GPU path (migrate with the positions as payload after every push)
+    through a real 1-rank NCCL group equals the single-GPU loop on the live particles
+    (absorbed electrons are dropped by the migration instead of kept as dead slots)."""
+    import workloads as W
+    from paper_2508_06771_b200.pic import PicLoop
+    rng = np.random.default_rng(4)
+    nx, ny, per = 8, 8, 400
+    n = nx * ny * per
+    d = 2e-4
+    x = np.zeros((3, n))
+    x[0], x[1] = rng.uniform(0, nx * d, n), rng.uniform(0, ny * d, n)
+    cell = (np.minimum((x[0] / d).astype(int), nx - 1) + nx * np.minimum((x[1] / d).astype(int), ny - 1))
+    v = rng.normal(0, W.sigma_v(2.0), (3, n))
+    v[0] += 2e5
+    g = cc.Grid(2, (nx, ny), (d, d), 2)                 # x absorbing: some electrons leave
+    prm = dict(dt=1e-11, weight=W.weight_for(per), cell_volume=W.CELL_VOLUME, subcycles=4)
+    args = (torch.from_numpy(x).to(DEV), torch.from_numpy(v).to(DEV), torch.from_numpy(cell.astype(np.int32)).to(DEV), g)
+    a = PicLoop(*args, graph=False, **prm)
+    b = PicLoop(*args, dist_ops=ccd.cuda_ops(), **prm)
+    for _ in range(2):
+        a.field_step()
+        b.field_step()
+    xa, va, ca = a.state
+    xb, vb, cb = b.state
+    live = ca >= 0
+    assert int((~live).sum()) > 0 and cb.numel() == int(live.sum())
+    assert torch.equal(ca[live], cb) and torch.equal(va[:, live], vb) and torch.equal(xa[:2, live], xb[:2])
