@@ -38,7 +38,10 @@
 namespace {
 
 constexpr int kCountThreads = 256;
-constexpr int kSub = 4096;               // elements per warp sub-range in k_scatter
+#ifndef CC_SUB
+#define CC_SUB 4096
+#endif
+constexpr int kSub = CC_SUB;             // elements per warp sub-range in k_scatter
 constexpr int kScatterUnrollA = 16;      // cell loads in flight per lane, counting pass
 constexpr int kScatterUnrollB = 6;       // (cell, v) loads in flight per lane, scatter pass
 // k_collide_large shape (tools/collide_shape.sh overrides them for design studies)

@@ -5,10 +5,11 @@ python -c "import __graft_entry__ as g; g.build()"
 cp paper_2508_06771_b200/lib/libcoulomb.so /tmp/libcoulomb_orig.so
 for v in "$@"; do
   set -- ${v//,/ }
+  SUB=${4:-4096}
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared \
-    -DCC_COLLIDE_THREADS=$1 -DCC_CHUNK=$2 -DCC_COLLIDE_CTAS=$3 \
+    -DCC_COLLIDE_THREADS=$1 -DCC_CHUNK=$2 -DCC_COLLIDE_CTAS=$3 -DCC_SUB=$SUB \
     -o paper_2508_06771_b200/lib/libcoulomb.so paper_2508_06771_b200/csrc/cc_kernels.cu 2>/dev/null || { echo "$v build failed"; continue; }
   timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-pic --e2e-steps 1 > gpurun_out/shape.json 2>/dev/null
-  python -c "import json; d=json.load(open('gpurun_out/shape.json')); print('threads chunk ctas $v: collide', round(d['stages_ms']['collide'],3), 'cold', round(d['cold']['stages_ms']['collide'],3), 'warm', round(d['warm']['stages_ms']['collide'],3))"
+  python -c "import json; d=json.load(open('gpurun_out/shape.json')); print('threads chunk ctas [sub] $v: step', round(d['ms_per_step'],3), {k: round(x,3) for k,x in d['stages_ms'].items()}, 'cold', round(d['cold']['ms_per_step'],3), 'warm', round(d['warm']['ms_per_step'],3))"
 done
 cp /tmp/libcoulomb_orig.so paper_2508_06771_b200/lib/libcoulomb.so
