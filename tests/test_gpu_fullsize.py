@@ -22,7 +22,7 @@ import paper_2508_06771_b200 as cc  # noqa: E402
 DEV = torch.device("cuda:0")
 
 
-def sampled_cell_parity(O, w, out, cells_to_check, step):
+def sampled_cell_parity(O, w, out, cells_to_check, step, flags=0):
     off = np.concatenate([[0], np.cumsum(np.bincount(w.cell[w.cell >= 0], minlength=w.cells))])
     v_out = out.v_out
     perm = out.perm_out
@@ -31,7 +31,8 @@ def sampled_cell_parity(O, w, out, cells_to_check, step):
         idx = np.nonzero(w.cell == j)[0]
         ref = O.coulomb_collide(w.v[:, idx], np.zeros(idx.size, np.int32), 1, dt=w.dt, weight=w.weight,
                                 cell_volume=w.cell_volume, ln_lambda=w.ln_lambda,
-                                cell_base=w.cell_base + j, seed=w.seed, step=step, want_pairs=False)
+                                cell_base=w.cell_base + j, seed=w.seed, step=step, want_pairs=False,
+                                flags=flags)
         a, b = off[j], off[j + 1]
         g = v_out[:, a:b].cpu().numpy()
         assert np.array_equal(perm[a:b].cpu().numpy(), idx[ref.perm_out])
@@ -88,3 +89,16 @@ def test_c5_shard_equals_global_cells(O):
     assert np.array_equal(out.perm_out.cpu().numpy(), ref.perm_out)
     scale = np.maximum(np.linalg.norm(ref.v_out, axis=0), 1.0)
     assert np.max(np.abs(out.v_out.cpu().numpy() - ref.v_out) / scale) <= 1e-12
+
+
+@pytest.mark.parametrize("flags", [cc._lib.CC_ODD_TRIPLET, cc._lib.CC_NANBU])
+def test_full_size_variants_sampled(O, flags):
+    """NEXT f1 variants at full C4 size (odd-count triplet on the C4b profile, whose cells have
+    odd and even counts; Nanbu on C4), sampled cells vs the oracle."""
+    w = W.c4b() if flags == cc._lib.CC_ODD_TRIPLET else W.c4()
+    out = cc.coulomb_collide(torch.from_numpy(w.v).to(DEV), torch.from_numpy(w.cell).to(DEV), w.cells,
+                             step=4, flags=flags, **w.params())
+    torch.cuda.synchronize()
+    counts = np.bincount(w.cell[w.cell >= 0], minlength=w.cells)
+    odd = [int(j) for j in np.nonzero(counts % 2 == 1)[0][:3]]
+    sampled_cell_parity(O, w, out, sorted(set([0, w.cells // 3, w.cells - 1] + odd)), 4, flags=flags)
