@@ -393,6 +393,40 @@ def p2c_section(dev, w):
     return {"p2c": out, "recombination": rec}
 
 
+def configs_section(dev):
+    """BASELINE configs C1-C3 (parity-test sizes) timed through the operator: cold (the
+    workload's random order every step) and warm (each step consumes the previous output),
+    mean of 20 calls after 3 warm-up calls, CUDA events; C1/C2 are launch/latency-bound."""
+    import torch
+    import workloads as W
+    import paper_2508_06771_b200 as cc
+    out = {}
+    for name, w in (("C1", W.c1()), ("C2", W.c2()), ("C3", W.c3())):
+        v0, c0 = torch.from_numpy(w.v).to(dev), torch.from_numpy(w.cell).to(dev)
+        col = cc.Collider(w.n, w.cells, dev, **w.params())
+        r = {"n": w.n, "cells": w.cells}
+        for mode in ("cold", "warm"):
+            v, c = v0, c0
+            for s in range(3):
+                o = col.step(v, c, step=s)
+                if mode == "warm":
+                    v, c = o.v_out, o.cell_out
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for s in range(20):
+                o = col.step(v, c, step=10 + s)
+                if mode == "warm":
+                    v, c = o.v_out, o.cell_out
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / 20
+            r[f"{mode}_ms_per_step"] = ms
+            r[f"{mode}_pair_collisions_per_s"] = float(o.diag[2].item()) / (ms * 1e-3)
+        out[name] = r
+    return out
+
+
 def run_ours(args):
     import ctypes as C
 
@@ -631,6 +665,10 @@ def run_ours(args):
         except Exception as e:  # the NEXT-row measurement must never kill the headline
             line["pic"] = {"error": repr(e)}
     if world == 1 and not args.no_pic:
+        try:
+            line["configs"] = configs_section(dev)
+        except Exception as e:
+            line["configs"] = {"error": repr(e)}
         try:
             line.update(p2c_section(dev, w))
         except Exception as e:

@@ -66,7 +66,8 @@ static_assert(kMaxScatterWarps * kSub <= 65536, "per-warp 16-bit cell counters m
 
 // ------------------------------------------------------------------ layout
 struct Layout {
-    int W = 1, tile = kSub, T = 0;
+    int W = 1, sub = kSub, tile = kSub, T = 0;
+    int chunk = kChunk;                  // pairs per k_collide_large CTA (multiple of kCollideThreads)
     int64_t max_chunks = 0;
     size_t o_err = 0, o_tcount = 0, o_cnt = 0, o_off = 0, o_chunk = 0, o_C = 0, o_keys = 0;
     size_t o_small = 0, o_recs = 0, o_cellsum = 0, o_ref = 0, o_tilesum = 0, o_chunkcell = 0, o_trec = 0, o_wsv = 0, total = 0;
@@ -86,9 +87,15 @@ Layout make_layout(int64_t n, int32_t M)
 {
     Layout L;
     L.W = scatter_warps(M);
-    L.tile = L.W * kSub;
+    // small inputs: shorter warp sub-ranges and collide chunks so that the binning tiles and the
+    // collide CTAs still fill the GPU (C2/C3-sized calls); C4-sized calls keep kSub / kChunk
+    constexpr int64_t kTargetTiles = 2 * 148 * 2, kTargetChunks = 4 * 148;
+    while (L.sub > 256 && (n + static_cast<int64_t>(L.W) * L.sub - 1) / (static_cast<int64_t>(L.W) * L.sub) < kTargetTiles)
+        L.sub /= 2;
+    while (L.chunk > kCollideThreads && (n / 2) / L.chunk < kTargetChunks) L.chunk -= kCollideThreads;
+    L.tile = L.W * L.sub;
     L.T = static_cast<int>((n + L.tile - 1) / L.tile);
-    L.max_chunks = (n + M) / 2 / kChunk + M + 1;
+    L.max_chunks = (n + M) / 2 / L.chunk + M + 1;
     size_t o = 0;
     L.o_err = o;      o = align256(o + 64 * sizeof(int32_t));
     L.o_tcount = o;   o = align256(o + static_cast<size_t>(L.T > 0 ? L.T : 1) * (M + 1) * sizeof(int32_t));
@@ -238,23 +245,24 @@ struct CellConst {
     const double* ln_lambda_arr;
 };
 
-__device__ __forceinline__ int32_t n_chunks(int32_t N)
+__device__ __forceinline__ int32_t n_chunks(int32_t N, int32_t chunk)
 {
     if (N <= cc::kSmallCell) return 0;
     const int32_t items = (N + 1) / 2;
-    return (items + kChunk - 1) / kChunk;
+    return (items + chunk - 1) / chunk;
 }
 
 // single CTA of 1024 threads
 __global__ void __launch_bounds__(1024)
-k_scan_cells(const int32_t* __restrict__ cnt, int M, int32_t* __restrict__ off, int32_t* __restrict__ chunk_off)
+k_scan_cells(const int32_t* __restrict__ cnt, int M, int32_t* __restrict__ off, int32_t* __restrict__ chunk_off,
+             int chunk)
 {
     __shared__ int32_t wsum_a[32], wsum_b[32];
     const int tid = threadIdx.x, nt = blockDim.x;
     const int per = (M + nt - 1) / nt;
     const int j0 = min(tid * per, M), j1 = min(j0 + per, M);
     int32_t a = 0, b = 0;
-    for (int j = j0; j < j1; ++j) { a += cnt[j]; b += n_chunks(cnt[j]); }
+    for (int j = j0; j < j1; ++j) { a += cnt[j]; b += n_chunks(cnt[j], chunk); }
     // block exclusive scan of (a, b)
     const int lane = tid & 31, wid = tid >> 5;
     int32_t ia = a, ib = b;
@@ -286,7 +294,7 @@ k_scan_cells(const int32_t* __restrict__ cnt, int M, int32_t* __restrict__ off, 
         off[j] = ra;
         chunk_off[j] = rb;
         ra += N;
-        rb += n_chunks(N);
+        rb += n_chunks(N, chunk);
     }
     if (tid == nt - 1) { off[M] = ra; chunk_off[M] = rb; }
 }
@@ -374,7 +382,7 @@ __device__ __forceinline__ void load_batch(const double* __restrict__ v, int64_t
 template <bool HAS_V>
 __global__ void __launch_bounds__(32 * kMaxScatterWarps, 2)
 k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__ cell, int n, int M,
-          int W, const int32_t* __restrict__ tbase, const int32_t* __restrict__ off,
+          int W, int sub, const int32_t* __restrict__ tbase, const int32_t* __restrict__ off,
           double* __restrict__ wsv, const int32_t* __restrict__ flags, double* __restrict__ tilesum)
 {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -383,8 +391,8 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
     if (flags && flags[1] == 0) {
         // input already cell-sorted: the stable order is the identity, so the
         // records are written in place (a streaming SoA -> 32-byte-record pack)
-        const int64_t t0 = static_cast<int64_t>(blockIdx.x) * W * kSub;
-        const int64_t t1 = min(t0 + static_cast<int64_t>(W) * kSub, static_cast<int64_t>(n));
+        const int64_t t0 = static_cast<int64_t>(blockIdx.x) * W * sub;
+        const int64_t t1 = min(t0 + static_cast<int64_t>(W) * sub, static_cast<int64_t>(n));
         for (int64_t i0 = t0 + static_cast<int64_t>(w) * 32 * kScatterUnrollB; i0 < t1;
              i0 += static_cast<int64_t>(W) * 32 * kScatterUnrollB) {
             double x[kScatterUnrollB], y[kScatterUnrollB], z[kScatterUnrollB];
@@ -412,8 +420,8 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
     for (int i = threadIdx.x; i < W * MW; i += blockDim.x) wcnt[i] = 0u;
     __syncthreads();
 
-    const int64_t s0 = static_cast<int64_t>(blockIdx.x) * W * kSub + static_cast<int64_t>(w) * kSub;
-    const int64_t s1 = min(s0 + kSub, static_cast<int64_t>(n));
+    const int64_t s0 = static_cast<int64_t>(blockIdx.x) * W * sub + static_cast<int64_t>(w) * sub;
+    const int64_t s1 = min(s0 + sub, static_cast<int64_t>(n));
     uint32_t* my = wcnt + w * MW;
     const uint32_t lt = (1u << lane) - 1u;
 
@@ -514,6 +522,7 @@ struct CollideArgs {
     int pair_vec;               // outputs aligned for 16-byte (v) / 8-byte (cell, perm) pair stores
     uint32_t cell_base, step, s0, s1;
     const uint32_t* step_dev;   // NULL, or DEVICE offset added to `step` (cc_params.step_dev)
+    int chunk;                  // pairs per k_collide_large CTA (<= kChunk, multiple of kCollideThreads)
 };
 
 __device__ __forceinline__ uint32_t eff_step(const CollideArgs& A)
@@ -739,8 +748,8 @@ k_collide_large(CollideArgs A)
     const int32_t N = A.cnt[j], o = A.off[j];
     const uint32_t step = eff_step(A);
     const uint32_t items = static_cast<uint32_t>(N + 1) / 2;
-    const uint32_t i0 = static_cast<uint32_t>(c - A.chunk_off[j]) * kChunk;
-    const uint32_t i1 = min(i0 + static_cast<uint32_t>(kChunk), items);
+    const uint32_t i0 = static_cast<uint32_t>(c - A.chunk_off[j]) * static_cast<uint32_t>(A.chunk);
+    const uint32_t i1 = min(i0 + static_cast<uint32_t>(A.chunk), items);
     const bool triplet = (A.model & cc::kOddTriplet) && (N & 1);   // N > 64 here
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     // phase 1: pi_j (keyed Feistel, R1) of each item's two slots in lock step
@@ -1495,16 +1504,16 @@ int run_binning(const double* v_in, int64_t ldv, const int32_t* cell_in, int n, 
     k_count<<<L.T, kCountThreads, sizeof(int32_t) * M1, st>>>(cell_in, n, M, L.tile, tcount, err);
     mark(ev, 1, st);
     k_scan_tiles<<<(M1 + 31) / 32, dim3(32, kScanRows), 0, st>>>(tcount, L.T, M1, cnt);
-    k_scan_cells<<<1, 1024, 0, st>>>(cnt, M, off, chunk_off);
+    k_scan_cells<<<1, 1024, 0, st>>>(cnt, M, off, chunk_off, L.chunk);
     k_cell_setup<<<(M + 255) / 256, 256, 0, st>>>(cnt, chunk_off, M, at<int32_t>(ws, L.o_chunkcell), Cj, keys, k,
                                                    cell_base, step, static_cast<uint32_t>(seed),
                                                    static_cast<uint32_t>(seed >> 32), step_dev);
     mark(ev, 2, st);
     if (v_in)
-        k_scatter<true><<<L.T, 32 * L.W, smem, st>>>(v_in, ldv, cell_in, n, M, L.W, tcount, off, wsv, skip,
+        k_scatter<true><<<L.T, 32 * L.W, smem, st>>>(v_in, ldv, cell_in, n, M, L.W, L.sub, tcount, off, wsv, skip,
                                                      at<double>(ws, L.o_tilesum));
     else
-        k_scatter<false><<<L.T, 32 * L.W, smem, st>>>(nullptr, 0, cell_in, n, M, L.W, tcount, off, wsv, skip,
+        k_scatter<false><<<L.T, 32 * L.W, smem, st>>>(nullptr, 0, cell_in, n, M, L.W, L.sub, tcount, off, wsv, skip,
                                                       nullptr);
     return launch_ok();
 }
@@ -1634,6 +1643,7 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     A.cell_base = cell_base;
     A.step = static_cast<uint32_t>(step);
     A.step_dev = p.step_dev;
+    A.chunk = L.chunk;
     A.s0 = static_cast<uint32_t>(seed);
     A.s1 = static_cast<uint32_t>(seed >> 32);
     A.pf_dist = prefetch_distance();
