@@ -42,6 +42,35 @@ __global__ void __launch_bounds__(kThreads) k_ldgsts(const double* __restrict__ 
     if (acc == 1.2345) out[0] = acc;
 }
 
+// (c) 256-bit register loads (one LDG.E.256 request per record), then 2 x st.shared.v2
+__global__ void __launch_bounds__(kThreads) k_ld256(const double* __restrict__ rec, const int32_t* __restrict__ idx,
+                                                    int64_t n, double* __restrict__ out)
+{
+    extern __shared__ __align__(16) double st[];
+    double acc = 0.0;
+    const int64_t nch = n / kChunk;
+    constexpr int R = kChunk / kThreads;      // 6 records per thread
+    for (int64_t c = blockIdx.x; c < nch; c += gridDim.x) {
+        double a[R], b[R], cc[R], d[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int e = threadIdx.x + r * kThreads;
+            const double* g = rec + 4 * static_cast<int64_t>(idx[c * kChunk + e]);
+            asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a[r]), "=d"(b[r]), "=d"(cc[r]), "=d"(d[r]) : "l"(g));
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int e = threadIdx.x + r * kThreads;
+            reinterpret_cast<double2*>(st + 4 * e)[0] = make_double2(a[r], b[r]);
+            reinterpret_cast<double2*>(st + 4 * e)[1] = make_double2(cc[r], d[r]);
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < kChunk; e += kThreads) acc += st[4 * e] + st[4 * e + 3];
+        __syncthreads();
+    }
+    if (acc == 1.2345) out[0] = acc;
+}
+
 __global__ void __launch_bounds__(kThreads) k_gather4(const __grid_constant__ CUtensorMap tmap,
                                                       const int32_t* __restrict__ idx, int64_t n,
                                                       double* __restrict__ out)
@@ -182,10 +211,64 @@ int main()
                 cudaEventSynchronize(b);
                 cudaEventElapsedTime(&ms[k], a, b);
             }
+            {
+                float m3 = 0;
+                cudaFuncSetAttribute(k_ld256, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                for (int rep = 0; rep < 2; ++rep) {
+                    if (rep == 1) cudaEventRecord(a);
+                    k_ld256<<<148 * ctas, kThreads, smem>>>(rec, idx, n, out);
+                    if (rep == 1) cudaEventRecord(b);
+                }
+                cudaEventSynchronize(b);
+                cudaEventElapsedTime(&m3, a, b);
+                printf("span %10lld, %d CTAs/SM: LDG.256 %.3f ms\n", (long long)S, ctas, m3);
+            }
             printf("span %10lld, %d CTAs/SM: LDGSTS %.3f ms (%.0f GB/s)  TMA gather4 %.3f ms (%.0f GB/s)  err=%s\n",
                    (long long)S, ctas, ms[0], n * 32.0 / ms[0] / 1e6, ms[1], n * 32.0 / ms[1] / 1e6,
                    cudaGetErrorString(cudaGetLastError()));
         }
+    }
+    {   // L2-resident gathers: 1e8 random gathers out of a 48 MB (1.5M-record) array
+        const int64_t small = 1536000;
+        for (int64_t i = 0; i < n; ++i) h[i] = static_cast<int32_t>(rng() % small);
+        cudaMemcpy(idx, h.data(), n * 4, cudaMemcpyHostToDevice);
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        for (int ctas : {4, 6}) {
+            float ms = 0;
+            for (int rep = 0; rep < 2; ++rep) {
+                if (rep == 1) cudaEventRecord(a);
+                k_ldgsts<<<148 * ctas, kThreads, smem>>>(rec, idx, n, out);
+                if (rep == 1) cudaEventRecord(b);
+            }
+            cudaEventSynchronize(b);
+            cudaEventElapsedTime(&ms, a, b);
+            float ms2 = 0;
+            cudaFuncSetAttribute(k_ld256, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            for (int rep = 0; rep < 2; ++rep) {
+                if (rep == 1) cudaEventRecord(a);
+                k_ld256<<<148 * ctas, kThreads, smem>>>(rec, idx, n, out);
+                if (rep == 1) cudaEventRecord(b);
+            }
+            cudaEventSynchronize(b);
+            cudaEventElapsedTime(&ms2, a, b);
+            printf("L2-resident (48 MB) random gathers, %d CTAs/SM: LDGSTS %.3f ms (%.2f G records/s)  LDG.256 %.3f ms "
+                   "(%.2f G records/s) err=%s\n", ctas, ms, n / ms / 1e6, ms2, n / ms2 / 1e6,
+                   cudaGetErrorString(cudaGetLastError()));
+        }
+        // sequential gathers (idx = i): the DRAM streaming reference
+        for (int64_t i = 0; i < n; ++i) h[i] = static_cast<int32_t>(i);
+        cudaMemcpy(idx, h.data(), n * 4, cudaMemcpyHostToDevice);
+        float ms = 0;
+        for (int rep = 0; rep < 2; ++rep) {
+            if (rep == 1) cudaEventRecord(a);
+            k_ldgsts<<<148 * 4, kThreads, smem>>>(rec, idx, n, out);
+            if (rep == 1) cudaEventRecord(b);
+        }
+        cudaEventSynchronize(b);
+        cudaEventElapsedTime(&ms, a, b);
+        printf("sequential records (3.2 GB from DRAM): LDGSTS %.3f ms (%.0f GB/s)\n", ms, n * 32.0 / ms / 1e6);
     }
     cudaFuncSetAttribute(k_scatter4, cudaFuncAttributeMaxDynamicSharedMemorySize, kThreads / 32 * 32 * 32 * 2 + 128);
     for (int64_t S : {int64_t(25000), int64_t(1) << 20, n}) {
