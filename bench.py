@@ -542,29 +542,34 @@ def run_ours(args):
     clk.stop()
     # NEXT f1 collision-model variants, steady state (shorter runs)
     variants = {}
-    for name, fl in (("odd_triplet", _lib.CC_ODD_TRIPLET), ("nanbu", _lib.CC_NANBU)):
+    for name, fl in (("odd_triplet", _lib.CC_ODD_TRIPLET), ("nanbu", _lib.CC_NANBU),
+                     ("preserve_order", _lib.CC_PRESERVE_ORDER)):
         model["flags"] = fl
         r = run_mode("steady", max(3, K // 4), W, 400_000 + 1000 * fl)
         variants[name] = {"flags": fl, "ms_per_step": r["ms"], "stages_ms": r["stages"],
                           "value": r["pairs"] / (r["ms"] * 1e-3)}
+        if fl == _lib.CC_PRESERVE_ORDER:
+            variants[name]["what"] = ("outputs in input order: the chain keeps the C4 input's random order "
+                                      "(a cold-order step plus the scattered output stores)")
     model["flags"] = 0
 
     # ---- end to end through the host-buffer entry coulomb_collide_host (cold input): every step
-    # copies its inputs host->device and its results (v, cell, perm) device->host inside the
-    # library call.  Two streams and two device buffers: step s+1's host->device copies overlap
-    # step s's device->host copies (PCIe is full duplex); each step still moves all its bytes.
+    # copies its inputs (v, cell ids) host->device and its result — the post-collision
+    # velocities in the caller's own particle order (CC_PRESERVE_ORDER, so no cell ids or perm
+    # need to come back) — device->host inside the library call.  Two streams and two device
+    # buffers: step s+1's host->device copies overlap step s's device->host copies (PCIe is
+    # full duplex); each step still moves all its bytes.
     v_pin = v_host.pin_memory()
     c_pin = c_host.pin_memory()
-    houts = [(torch.empty((3, n), dtype=torch.float64).pin_memory(), torch.empty(n, dtype=torch.int32).pin_memory(),
-              torch.empty(n, dtype=torch.int32).pin_memory()) for _ in range(2)]
+    houts = [torch.empty((3, n), dtype=torch.float64).pin_memory() for _ in range(2)]
     devbufs = [cc.alloc_host_buffer(n, M, dev) for _ in range(2)]
     streams = [torch.cuda.Stream(dev) for _ in range(2)]
     E = max(args.e2e_steps, 1)
 
     def e2e_call(s):
         k = s % 2
-        cc.coulomb_collide_host(v_pin, c_pin, M, out_v=houts[k][0], out_cell=houts[k][1], out_perm=houts[k][2],
-                                dev_buffer=devbufs[k], stream=streams[k], step=300_000 + s, **p)
+        cc.coulomb_collide_host(v_pin, c_pin, M, out_v=houts[k], dev_buffer=devbufs[k], stream=streams[k],
+                                step=300_000 + s, flags=_lib.CC_PRESERVE_ORDER, **p)
 
     e2e_call(0)                                 # warm-up (not timed)
     torch.cuda.synchronize()
@@ -652,9 +657,10 @@ def run_ours(args):
         "warm": dict(summary(res["warm"]), what="chained steps, no drift (input already cell-sorted)"),
         "e2e": {"value": res["cold"]["pairs"] / (e2e_ms * 1e-3), "unit": UNIT,
                 "h2d_bytes_per_step": int(v_host.numel() * 8 + c_host.numel() * 4),
-                "d2h_bytes_per_step": int(n * 24 + n * 8), "ms_per_step": e2e_ms,
-                "what": "coulomb_collide_host (C-ABI host-buffer entry) on pinned host memory: per step H2D of v "
-                        "and cell ids, D2H of v, cell, perm; two streams, consecutive steps' copies overlap"},
+                "d2h_bytes_per_step": int(n * 24), "ms_per_step": e2e_ms,
+                "what": "coulomb_collide_host (C-ABI host-buffer entry, CC_PRESERVE_ORDER) on pinned host memory: "
+                        "per step H2D of v and cell ids, D2H of the post-collision v in the caller's order; two "
+                        "streams, consecutive steps' copies overlap"},
         "variants": variants,
         "gpu_launches": 10 * K + (K if world > 1 else 0),
         "clocks": clk.summary(),

@@ -56,6 +56,15 @@ extern "C" {
  *                  coth A - 1/A = exp(-s), cos chi = 1 + ln(u1 + (1-u1) e^{-2A})/A.      */
 #define CC_ODD_TRIPLET 1u
 #define CC_NANBU 2u
+/* Output order:
+ *  CC_PRESERVE_ORDER  outputs in INPUT order instead of the default cell-sorted pair
+ *                     order: v_out[:, i], cell_out[i] are input particle i's post-collision
+ *                     velocity and (validated) cell, -1 if dead or invalid; perm_out, if
+ *                     given, is the identity.  Same per-particle values, moments and
+ *                     diagnostics; the stores scatter to the input positions (no paired
+ *                     16-byte stores).  Lets a caller keep its own particle order (and
+ *                     skip copying cell_out / perm_out back, see coulomb_collide_host).  */
+#define CC_PRESERVE_ORDER 4u
 
 #define CC_MAX_CELLS 32768  /* binning keeps per-warp cell counters in shared memory */
 #define CC_DIAG_LEN 16
@@ -73,7 +82,8 @@ typedef struct cc_params {
     const double *cell_volume_arr;/* DEVICE [cells] or NULL                                */
     double ln_lambda;             /* Coulomb logarithm, used when ln_lambda_arr == NULL    */
     const double *ln_lambda_arr;  /* DEVICE [cells] or NULL                                */
-    uint32_t flags;               /* 0 (TA77, odd sitter) or CC_ODD_TRIPLET | CC_NANBU      */
+    uint32_t flags;               /* 0 (TA77, odd sitter) or CC_ODD_TRIPLET | CC_NANBU,
+                                     optionally | CC_PRESERVE_ORDER                          */
     const uint32_t *step_dev;     /* DEVICE uint32 or NULL: when set, the effective step is
                                      (step + *step_dev) mod 2^32, read on the device, so a
                                      captured CUDA graph replays with advancing randoms
@@ -133,8 +143,11 @@ int coulomb_collide(const double *v_in, int64_t ldv, const int32_t *cell_in,
  * the stream is synchronised; pinned host memory gives full PCIe rate and lets
  * the copies overlap other streams).
  *  h_v_in [3][ldv], h_cell_in [n]       HOST inputs (read).
- *  h_v_out [3][ldv], h_cell_out [n]     HOST outputs; h_perm_out [n], h_moments_out
- *                                       [cells][7], h_diag_out [16] HOST or NULL.
+ *  h_v_out [3][ldv]                     HOST output; h_cell_out [n], h_perm_out [n],
+ *                                       h_moments_out [cells][7], h_diag_out [16] HOST or
+ *                                       NULL (not copied back).  With CC_PRESERVE_ORDER the
+ *                                       velocities come back in the caller's own order, so
+ *                                       cell ids and perm need not be copied at all.
  *  dev_buffer  DEVICE scratch of >= cc_host_buffer_bytes(n, cells) bytes, 256-byte
  *              aligned, holding device copies of the inputs/outputs and the
  *              workspace; one per call in flight.

@@ -225,6 +225,7 @@ class OracleResult:
 
 ODD_TRIPLET = 1
 NANBU = 2
+PRESERVE_ORDER = 4
 
 
 def nanbu_A(s: float) -> float:

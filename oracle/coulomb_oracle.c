@@ -473,6 +473,7 @@ void or_nanbu_pair(double va[3], double vb[3], double C, double u1, double u2)
 
 #define OR_ODD_TRIPLET 1u
 #define OR_NANBU 2u
+#define OR_PRESERVE_ORDER 4u
 
 /* one binary collision of the selected model */
 void or_collide_pair(double va[3], double vb[3], double C, double u1, double u2, uint32_t flags)
@@ -683,6 +684,26 @@ int or_coulomb_collide(const double *v_in, int64_t ldv, const int32_t *cell_in,
         diag_out[2] = (double)pair_off[M];
         diag_out[3] = (double)odd;
         for (int q = 0; q < 4; ++q) { diag_out[4 + q] = (double)sb[q]; diag_out[8 + q] = (double)sa[q]; }
+    }
+
+    if (flags & OR_PRESERVE_ORDER) {
+        /* O8 / SURVEY §8(b) CC_PRESERVE_ORDER: the same per-particle results, returned in
+         * input order — the un-permute v_final[perm[p]] = v_out[p], cell likewise;
+         * perm becomes the identity.  Moments and diagnostics above are unchanged. */
+        double *tv = malloc(sizeof(double) * 3 * (size_t)(n > 0 ? n : 1));
+        int32_t *tc = malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+        for (int64_t p = 0; p < n; ++p) {
+            for (int c = 0; c < 3; ++c) tv[c * n + p] = v_out[c * ldv + p];
+            tc[p] = cell_out[p];
+        }
+        for (int64_t p = 0; p < n; ++p) {
+            const int64_t l = perm_out[p];
+            for (int c = 0; c < 3; ++c) v_out[c * ldv + l] = tv[c * n + p];
+            cell_out[l] = tc[p];
+        }
+        for (int64_t l = 0; l < n; ++l) perm_out[l] = l;
+        free(tv);
+        free(tc);
     }
 
     free(counts); free(off); free(P); free(pair_off);

@@ -25,6 +25,7 @@ CC_MOMENTS_LEN = 7
 CC_NUM_STAGES = 5
 CC_ODD_TRIPLET = 1
 CC_NANBU = 2
+CC_PRESERVE_ORDER = 4
 STAGE_NAMES = ("count", "scan", "scatter", "collide", "finalize")
 
 # every symbol include/coulomb.h declares

@@ -406,7 +406,7 @@ def alloc_host_buffer(n: int, cells: int, device) -> torch.Tensor:
 
 
 def coulomb_collide_host(v: torch.Tensor, cell: torch.Tensor, cells: int, *, dt: float, out_v: torch.Tensor,
-                         out_cell: torch.Tensor, out_perm: Optional[torch.Tensor] = None,
+                         out_cell: Optional[torch.Tensor] = None, out_perm: Optional[torch.Tensor] = None,
                          out_moments: Optional[torch.Tensor] = None, out_diag: Optional[torch.Tensor] = None,
                          dev_buffer: torch.Tensor, stream: Optional[torch.cuda.Stream] = None, weight: float = 1.0,
                          cell_volume: float = 1.0, ln_lambda: float = 10.0, cell_base: int = 0, seed: int = 42,

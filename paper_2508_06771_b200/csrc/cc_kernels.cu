@@ -70,7 +70,7 @@ struct Layout {
     int chunk = kChunk;                  // pairs per k_collide_large CTA (multiple of kCollideThreads)
     int64_t max_chunks = 0;
     size_t o_err = 0, o_tcount = 0, o_cnt = 0, o_off = 0, o_chunk = 0, o_C = 0, o_keys = 0;
-    size_t o_small = 0, o_recs = 0, o_cellsum = 0, o_ref = 0, o_tilesum = 0, o_chunkcell = 0, o_trec = 0, o_wsv = 0, total = 0;
+    size_t o_perm = 0, o_small = 0, o_recs = 0, o_cellsum = 0, o_ref = 0, o_tilesum = 0, o_chunkcell = 0, o_trec = 0, o_wsv = 0, total = 0;
 };
 
 size_t align256(size_t x) { return (x + 255u) & ~static_cast<size_t>(255u); }
@@ -111,6 +111,7 @@ Layout make_layout(int64_t n, int32_t M)
     L.o_trec = o;     o = align256(o + static_cast<size_t>(M) * kRec * sizeof(double));
     L.o_tilesum = o;  o = align256(o + static_cast<size_t>(L.T > 0 ? L.T : 1) * kTileSum * sizeof(double));
     L.o_chunkcell = o; o = align256(o + static_cast<size_t>(L.max_chunks) * sizeof(int32_t));
+    L.o_perm = o;     o = align256(o + static_cast<size_t>(n > 0 ? n : 1) * sizeof(int32_t));   // CC_PRESERVE_ORDER
     L.o_wsv = o;      o = align256(o + static_cast<size_t>(n > 0 ? n : 1) * 4 * sizeof(double));
     L.total = o;
     return L;
@@ -638,42 +639,45 @@ k_collide_small(CollideArgs A)
     const uint32_t items = static_cast<uint32_t>(N + 1) / 2;
     const uint32_t k = static_cast<uint32_t>(lane);
     const bool triplet = (A.model & cc::kOddTriplet) && N >= 3 && (N & 1);
+    Rec mine[3];                  // this lane's post-collision particles (pair, sitter or triplet)
+    int nmine = 0;
     if (triplet && k == items - 2) {
         // R19: the last three of the pair order collide as a TA77 triplet
-        Rec r[3];
 #pragma unroll
-        for (int q = 0; q < 3; ++q) r[q] = load_slot(A, o + pi_sm[w][N - 3 + q]);
-        triplet_update(A, G, C, step, r);
+        for (int q = 0; q < 3; ++q) mine[q] = load_slot(A, o + pi_sm[w][N - 3 + q]);
+        triplet_update(A, G, C, step, mine);
 #pragma unroll
-        for (int q = 0; q < 3; ++q) {
-            write_out(A, o + N - 3 + q, j, r[q]);
-            acc.post(r[q].x, r[q].y, r[q].z, 0.0, 0.0, 0.0);
-        }
+        for (int q = 0; q < 3; ++q) write_out(A, o + N - 3 + q, j, mine[q]);
+        nmine = 3;
     } else if (k < items && !(triplet && k == items - 1)) {
         const int32_t pa = o + 2 * static_cast<int32_t>(k);
-        Rec a = load_slot(A, o + pi_sm[w][2 * k]);
+        mine[0] = load_slot(A, o + pi_sm[w][2 * k]);
+        nmine = 1;
         if (2 * k + 1 < static_cast<uint32_t>(N)) {
-            Rec b = load_slot(A, o + pi_sm[w][2 * k + 1]);
+            mine[1] = load_slot(A, o + pi_sm[w][2 * k + 1]);
             double u1, u2;
             pair_uniforms(A, j, k, step, u1, u2);
-            cc::collide_model(a.x, a.y, a.z, b.x, b.y, b.z, C, u1, u2, A.model);
-            write_out(A, pa + 1, j, b);
-            acc.post(b.x, b.y, b.z, 0.0, 0.0, 0.0);
+            cc::collide_model(mine[0].x, mine[0].y, mine[0].z, mine[1].x, mine[1].y, mine[1].z, C, u1, u2, A.model);
+            write_out(A, pa + 1, j, mine[1]);
+            nmine = 2;
         }
-        write_out(A, pa, j, a);
-        acc.post(a.x, a.y, a.z, 0.0, 0.0, 0.0);
+        write_out(A, pa, j, mine[0]);
     }
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+        if (q < nmine) acc.post(mine[q].x, mine[q].y, mine[q].z, 0.0, 0.0, 0.0);
     warp_reduce(acc.a);
-    // pass 2: sums about the exact mean (values re-read from v_out, L1/L2 hot)
+    // pass 2: sums about the exact mean, from the lane's own particles (registers; the
+    // output may be in input order, CC_PRESERVE_ORDER)
     const double inv = 1.0 / static_cast<double>(N);
     const double mx = __shfl_sync(0xFFFFFFFFu, acc.a[0], 0) * inv;
     const double my = __shfl_sync(0xFFFFFFFFu, acc.a[1], 0) * inv;
     const double mz = __shfl_sync(0xFFFFFFFFu, acc.a[2], 0) * inv;
-    __syncwarp();
     Acc q;
     q.zero();
-    for (int32_t t = lane; t < N; t += 32)
-        q.post(A.v_out[o + t], A.v_out[A.ldv + o + t], A.v_out[2 * A.ldv + o + t], mx, my, mz);
+#pragma unroll
+    for (int t = 0; t < 3; ++t)
+        if (t < nmine) q.post(mine[t].x, mine[t].y, mine[t].z, mx, my, mz);
     warp_reduce(q.a);
     if (lane == 0) {
         double* r = A.small_recs + static_cast<int64_t>(j) * kSmallRec;
@@ -884,6 +888,34 @@ __global__ void k_triplets(CollideArgs A)
 #pragma unroll
     for (int q = 0; q < 6; ++q) tr[q] = acc.a[q];
     tr[6] = tr[7] = 0.0;
+}
+
+// CC_PRESERVE_ORDER, pass 1: output position p -> a 32-byte record {v, cell} at the
+// particle's input position perm[p] in the (now free) record array.
+__global__ void k_unpermute(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__ cell,
+                            const int32_t* __restrict__ perm, int64_t n, double* __restrict__ wsv)
+{
+    for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < n;
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = perm[p];
+        st256(wsv + 4 * i, v[p], v[ldv + p], v[2 * ldv + p], __longlong_as_double(static_cast<long long>(cell[p])));
+    }
+}
+
+// pass 2: the records, now in input order, back to the SoA outputs (streaming); perm = identity
+__global__ void k_unpack(const double* __restrict__ wsv, int64_t n, double* __restrict__ v, int64_t ldv,
+                         int32_t* __restrict__ cell, int32_t* __restrict__ perm)
+{
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double x, y, z, w;
+        ld256(wsv + 4 * i, x, y, z, w);
+        v[i] = x;
+        v[ldv + i] = y;
+        v[2 * ldv + i] = z;
+        cell[i] = static_cast<int32_t>(__double_as_longlong(w));
+        if (perm) perm[i] = static_cast<int32_t>(i);
+    }
 }
 
 // Dead (and invalid) particles: slots [L, n), copied unchanged.
@@ -1594,7 +1626,7 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     if (n >= (1ll << 31) || cells > CC_MAX_CELLS) return CC_ECOUNT;
     if (!finite_pos(p.mass) || !finite_pos(p.charge) || !finite_pos(p.eps0) || !std::isfinite(p.weight) ||
         p.weight < 0.0 || (!p.cell_volume_arr && !finite_pos(p.cell_volume)) ||
-        (!p.ln_lambda_arr && !std::isfinite(p.ln_lambda)) || (p.flags & ~(CC_ODD_TRIPLET | CC_NANBU)) != 0)
+        (!p.ln_lambda_arr && !std::isfinite(p.ln_lambda)) || (p.flags & ~(CC_ODD_TRIPLET | CC_NANBU | CC_PRESERVE_ORDER)) != 0)
         return CC_EINVAL;
     if (!workspace || !aligned(workspace, 256)) return CC_EWORKSPACE;
     const Layout L = make_layout(n, cells);
@@ -1636,7 +1668,12 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     A.v_out = v_out;
     A.ldv = ldv;
     A.cell_out = cell_out;
-    A.perm_out = perm_out;
+    const bool preserve = (p.flags & CC_PRESERVE_ORDER) != 0;
+    // CC_PRESERVE_ORDER: the kernels below produce the default (pair-ordered) output, which
+    // k_unpermute / k_unpack then put back in input order; perm is needed for that even
+    // when the caller does not ask for it
+    int32_t* perm_pair = perm_out ? perm_out : (preserve ? at<int32_t>(workspace, L.o_perm) : nullptr);
+    A.perm_out = perm_pair;
     A.recs = at<double>(workspace, L.o_recs);
     A.small_recs = at<double>(workspace, L.o_small);
     A.M = M;
@@ -1647,7 +1684,7 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     A.s0 = static_cast<uint32_t>(seed);
     A.s1 = static_cast<uint32_t>(seed >> 32);
     A.pf_dist = prefetch_distance();
-    A.model = p.flags;
+    A.model = p.flags & (CC_ODD_TRIPLET | CC_NANBU);
     A.trec = at<double>(workspace, L.o_trec);
     A.pair_vec = aligned(v_out, 16) && (ldv % 2 == 0) && aligned(cell_out, 8) && (!perm_out || aligned(perm_out, 8));
 
@@ -1662,6 +1699,11 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
         k_collide_large<false><<<static_cast<unsigned>(L.max_chunks), kCollideThreads, kCollideSmem, st>>>(A);
     if (A.model & CC_ODD_TRIPLET) k_triplets<<<(M + 255) / 256, 256, 0, st>>>(A);
     k_copy_dead<<<148 * 4, 256, 0, st>>>(A, nn);
+    if (preserve) {
+        const unsigned g = static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 16));
+        k_unpermute<<<g, 256, 0, st>>>(v_out, ldv, cell_out, perm_pair, n, at<double>(workspace, L.o_wsv));
+        k_unpack<<<g, 256, 0, st>>>(A.wsv, n, v_out, ldv, cell_out, perm_out);
+    }
 
     MomConst mc{p.weight, p.cell_volume, p.cell_volume_arr, p.mass / p.charge};
     double* cellsum = at<double>(workspace, L.o_cellsum);
@@ -1714,7 +1756,7 @@ int coulomb_collide_host(const double* h_v_in, int64_t ldv, const int32_t* h_cel
     cudaGetLastError();   // launch errors below are ours, not a stale earlier one
     if (n < 0 || cells < 1 || ldv < n) return CC_EINVAL;
     if (n >= (1ll << 31) || cells > CC_MAX_CELLS) return CC_ECOUNT;
-    if (n > 0 && (!h_v_in || !h_cell_in || !h_v_out || !h_cell_out)) return CC_EINVAL;
+    if (n > 0 && (!h_v_in || !h_cell_in || !h_v_out)) return CC_EINVAL;
     const HostLayout H = host_layout(n, cells);
     if (!dev_buffer || !aligned(dev_buffer, 256) || dev_bytes < H.total) return CC_EWORKSPACE;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1744,7 +1786,8 @@ int coulomb_collide_host(const double* h_v_in, int64_t ldv, const int32_t* h_cel
     if (n > 0) {
         ok = ok && cudaMemcpy2DAsync(h_v_out, sizeof(double) * ldv, d_vout, sizeof(double) * H.ldd, row, 3,
                                      cudaMemcpyDeviceToHost, st) == cudaSuccess;
-        ok = ok && cudaMemcpyAsync(h_cell_out, d_cout, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st) == cudaSuccess;
+        if (h_cell_out)
+            ok = ok && cudaMemcpyAsync(h_cell_out, d_cout, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st) == cudaSuccess;
         if (h_perm_out)
             ok = ok && cudaMemcpyAsync(h_perm_out, d_perm, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st) == cudaSuccess;
     }

@@ -62,3 +62,17 @@ def test_host_entry_strided_rows_and_two_streams():
         assert torch.equal(outs[s][0][:, :n], ref.v_out.cpu())
         assert torch.all(outs[s][0][:, n:] == 7.0)
         assert torch.equal(outs[s][1], ref.cell_out.cpu())
+
+
+def test_host_entry_preserve_order_velocities_only():
+    """The e2e pattern of bench.py: CC_PRESERVE_ORDER, only the velocities copied back."""
+    n, M = 80_000, 50
+    w = W.random_cells(n, M, seed=8, skew=True)
+    p = w.params()
+    f = cc._lib.CC_PRESERVE_ORDER
+    ref = cc.coulomb_collide(torch.from_numpy(w.v).to(DEV), torch.from_numpy(w.cell).to(DEV), M, step=3, flags=f, **p)
+    ov = torch.zeros((3, n), dtype=torch.float64).pin_memory()
+    cc.coulomb_collide_host(torch.from_numpy(w.v).pin_memory(), torch.from_numpy(w.cell).pin_memory(), M, out_v=ov,
+                            dev_buffer=cc.alloc_host_buffer(n, M, DEV), step=3, flags=f, **p)
+    torch.cuda.synchronize()
+    assert torch.equal(ov, ref.v_out.cpu())

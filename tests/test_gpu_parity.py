@@ -346,3 +346,20 @@ def test_coulomb_log_matches_oracle(O):
     r2 = O.coulomb_collide(out.v_out.cpu().numpy(), out.cell_out.cpu().numpy(), w.cells, step=1,
                            ln_lambda_arr=ref, want_pairs=False, **w.params())
     assert vel_err(out2.v_out.cpu().numpy(), r2.v_out, 1.0) <= TOL
+
+
+@pytest.mark.parametrize("flags", [0, 1, 2])
+@pytest.mark.parametrize("n,M,dead,skew", [(120_007, 4096, 0.02, True), (50_000, 40, 0.0, False), (999, 1, 0.1, False)])
+def test_preserve_order_parity(O, flags, n, M, dead, skew):
+    """CC_PRESERVE_ORDER: outputs in input order vs the oracle's un-permute,
+    small (N <= 64, warp path) and large cells, dead particles, f1 variants."""
+    w = W.random_cells(n, M, seed=n + M + flags, dead_frac=dead, skew=skew)
+    p = w.params()
+    f = flags | cc._lib.CC_PRESERVE_ORDER
+    out = cc.coulomb_collide(to_dev(w.v), to_dev(w.cell), M, step=6, flags=f, **p)
+    ref = O.coulomb_collide(w.v, w.cell, M, step=6, flags=f, want_pairs=False, **p)
+    assert np.array_equal(out.perm_out.cpu().numpy(), np.arange(n))
+    assert np.array_equal(out.cell_out.cpu().numpy(), ref.cell_out)
+    assert vel_err(out.v_out.cpu().numpy(), ref.v_out, 1e-3 * W.sigma_v(2.0)) <= TOL
+    check_moments(out.moments.cpu().numpy(), ref.moments, w)
+    check_diag(out.diag.cpu().numpy(), ref.diag, ref.v_out)

@@ -159,3 +159,23 @@ def test_thread_count_invariance(oracle_mod, tmp_path):
         subprocess.check_call([sys.executable, "-c", code, f], env=env)
         outs.append(np.load(f))
     assert np.array_equal(outs[0], outs[1])
+
+
+def test_preserve_order_is_the_unpermuted_default(oracle_mod):
+    """SURVEY §8(b) CC_PRESERVE_ORDER: the same per-particle results in input order —
+    v_pres[:, perm_default[p]] == v_default[:, p] exactly, cell_out == the validated input
+    ids (invalid -> -1), perm the identity; moments and diagnostics unchanged."""
+    O = oracle_mod
+    w = W.random_cells(20_000, 37, seed=31, dead_frac=0.05, skew=True)
+    cell = w.cell.copy()
+    cell[[3, 999]] = [37, -9]                       # invalid ids are treated as dead (R11)
+    p = w.params()
+    with pytest.raises(ValueError):
+        O.coulomb_collide(w.v, cell, 37, step=2, want_pairs=False, **p)   # the oracle rejects invalid ids
+    for flags in (0, O.ODD_TRIPLET, O.NANBU):
+        d = O.coulomb_collide(w.v, w.cell, 37, step=2, want_pairs=False, flags=flags, **p)
+        r = O.coulomb_collide(w.v, w.cell, 37, step=2, want_pairs=False, flags=flags | O.PRESERVE_ORDER, **p)
+        assert np.array_equal(r.v_out[:, d.perm_out], d.v_out)
+        assert np.array_equal(r.cell_out, np.where(w.cell >= 0, w.cell, -1))
+        assert np.array_equal(r.perm_out, np.arange(w.n))
+        assert np.array_equal(r.moments, d.moments) and np.array_equal(r.diag, d.diag)
