@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--nx", type=int, default=64)
     ap.add_argument("--ny", type=int, default=64)
     ap.add_argument("--e2e-steps", type=int, default=4)
+    ap.add_argument("--e2e-buffers", type=int, default=2, help="streams / device buffers of the e2e pipeline")
     ap.add_argument("--drift", type=float, default=0.02, help="fraction of electrons changing cell per step")
     ap.add_argument("--dist-backend", default="nccl", help="torch.distributed backend for N > 1 (nccl; gloo "
                     "only to smoke-test the multi-rank path when fewer GPUs than ranks are available)")
@@ -561,13 +562,14 @@ def run_ours(args):
     # full duplex); each step still moves all its bytes.
     v_pin = v_host.pin_memory()
     c_pin = c_host.pin_memory()
-    houts = [torch.empty((3, n), dtype=torch.float64).pin_memory() for _ in range(2)]
-    devbufs = [cc.alloc_host_buffer(n, M, dev) for _ in range(2)]
-    streams = [torch.cuda.Stream(dev) for _ in range(2)]
+    NB = max(1, args.e2e_buffers)
+    houts = [torch.empty((3, n), dtype=torch.float64).pin_memory() for _ in range(NB)]
+    devbufs = [cc.alloc_host_buffer(n, M, dev) for _ in range(NB)]
+    streams = [torch.cuda.Stream(dev) for _ in range(NB)]
     E = max(args.e2e_steps, 1)
 
     def e2e_call(s):
-        k = s % 2
+        k = s % NB
         cc.coulomb_collide_host(v_pin, c_pin, M, out_v=houts[k], dev_buffer=devbufs[k], stream=streams[k],
                                 step=300_000 + s, flags=_lib.CC_PRESERVE_ORDER, **p)
 
@@ -659,8 +661,8 @@ def run_ours(args):
                 "h2d_bytes_per_step": int(v_host.numel() * 8 + c_host.numel() * 4),
                 "d2h_bytes_per_step": int(n * 24), "ms_per_step": e2e_ms,
                 "what": "coulomb_collide_host (C-ABI host-buffer entry, CC_PRESERVE_ORDER) on pinned host memory: "
-                        "per step H2D of v and cell ids, D2H of the post-collision v in the caller's order; two "
-                        "streams, consecutive steps' copies overlap"},
+                        "per step H2D of v and cell ids, D2H of the post-collision v in the caller's order; "
+                        f"{NB} streams / device buffers, consecutive steps' copies overlap"},
         "variants": variants,
         "gpu_launches": 10 * K + (K if world > 1 else 0),
         "clocks": clk.summary(),
