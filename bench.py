@@ -437,7 +437,8 @@ def run_ours(args):
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist_ops = ccd.cuda_ops()
+        # NCCL: the library's own communicator (C ABI cc_dist_*); gloo smoke runs: torch collectives
+        dist_ops = ccd.cuda_ops(ccd.NcclComm() if args.dist_backend == "nccl" else None)
     local = local % torch.cuda.device_count()
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)

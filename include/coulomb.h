@@ -222,6 +222,33 @@ int cc_gather(const double *v, int64_t ldv, const int32_t *cell, const int32_t *
 int cc_owner(const int32_t *cell, int64_t n, const int32_t *bounds, int32_t nranks,
              int32_t *owner_out, void *stream);
 
+/* ---- Multi-GPU over NCCL (csrc/cc_dist.cu) ----------------------
+ * One process per GPU.  Bootstrap: rank 0 calls cc_nccl_get_unique_id, the caller
+ * broadcasts the CC_NCCL_ID_BYTES bytes (e.g. torch.distributed), every rank calls
+ * cc_nccl_comm_init (collective).  `comm` is an ncclComm_t passed as void*. */
+#define CC_NCCL_ID_BYTES 128
+int cc_nccl_get_unique_id(void *id_out);                                  /* HOST */
+int cc_nccl_comm_init(void **comm_out, int32_t nranks, int32_t rank, const void *id);   /* HOST */
+int cc_nccl_comm_destroy(void *comm);                                    /* HOST */
+
+/* a8 across ranks: diag DEVICE [16] in place <- rank-ascending sum of every rank's
+ * vector (ncclAllGather into scratch DEVICE [nranks][16], then cc_diag_sum_ranks):
+ * the same bits on every rank for a given world size.         */
+int cc_dist_diag_reduce(double *diag, double *scratch, void *comm, void *stream);
+
+/* Particle migration, step 1: send_counts DEVICE int64 [nranks] (particles this rank
+ * sends to each rank) -> recv_counts DEVICE int64 [nranks] (grouped ncclSend/Recv). */
+int cc_dist_alltoall_counts(const int64_t *send_counts, int64_t *recv_counts, void *comm, void *stream);
+
+/* Particle migration, step 2: exchange `nrows` rows of elem_bytes-sized (4 or 8)
+ * elements.  Row r of the send buffer starts at send + r*lds elements and holds
+ * the particles for rank p at [send_off[p], send_off[p+1]) (HOST int64 [nranks+1],
+ * send_off[0] = 0); received particles from rank p land at [recv_off[p],
+ * recv_off[p+1]) of each receive row (HOST offsets).  Grouped ncclSend/ncclRecv,
+ * arrivals in source-rank order (deterministic).                               */
+int cc_dist_exchange(const void *send, int64_t lds, void *recv, int64_t ldr, int32_t nrows, int32_t elem_bytes,
+                     const int64_t *send_off, const int64_t *recv_off, void *comm, void *stream);
+
 /* Multi-GPU: rank-ascending sum of P gathered diagnostics vectors
  * gathered [P][16] -> out [16] (deterministic for a given P).   */
 int cc_diag_sum_ranks(const double *gathered, int32_t nranks, double *out, void *stream);

@@ -25,6 +25,7 @@ CC_MOMENTS_LEN = 7
 CC_NUM_STAGES = 5
 CC_ODD_TRIPLET = 1
 CC_NANBU = 2
+CC_NCCL_ID_BYTES = 128
 CC_PRESERVE_ORDER = 4
 STAGE_NAMES = ("count", "scan", "scatter", "collide", "finalize")
 
@@ -33,7 +34,9 @@ EXPORTS = ("cc_default_params", "cc_workspace_bytes", "coulomb_collide", "cc_dev
            "cc_strerror", "cc_bin", "cc_pairs", "cc_philox", "cc_ppnd16", "cc_ta_pairs",
            "cc_moments", "cc_coulomb_log", "cc_gather", "cc_owner", "cc_diag_sum_ranks", "cc_push",
            "cc_step_advance", "cc_p2c_scratch_bytes", "cc_p2c", "cc_p2c_moments",
-           "cc_host_buffer_bytes", "coulomb_collide_host", "cc_recombine")
+           "cc_host_buffer_bytes", "coulomb_collide_host", "cc_recombine",
+           "cc_nccl_get_unique_id", "cc_nccl_comm_init", "cc_nccl_comm_destroy", "cc_dist_diag_reduce",
+           "cc_dist_alltoall_counts", "cc_dist_exchange")
 
 
 class CCParams(C.Structure):
@@ -115,6 +118,18 @@ def load():
     L.coulomb_collide_host.restype = C.c_int
     L.cc_recombine.argtypes = [vp, i64, vp, i64, i32, u32, vp, dbl, dbl, u64, u64, vp, vp]
     L.cc_recombine.restype = C.c_int
+    L.cc_nccl_get_unique_id.argtypes = [vp]
+    L.cc_nccl_get_unique_id.restype = C.c_int
+    L.cc_nccl_comm_init.argtypes = [C.POINTER(C.c_void_p), i32, i32, vp]
+    L.cc_nccl_comm_init.restype = C.c_int
+    L.cc_nccl_comm_destroy.argtypes = [vp]
+    L.cc_nccl_comm_destroy.restype = C.c_int
+    L.cc_dist_diag_reduce.argtypes = [vp, vp, vp, vp]
+    L.cc_dist_diag_reduce.restype = C.c_int
+    L.cc_dist_alltoall_counts.argtypes = [vp, vp, vp, vp]
+    L.cc_dist_alltoall_counts.restype = C.c_int
+    L.cc_dist_exchange.argtypes = [vp, i64, vp, i64, i32, i32, vp, vp, vp, vp]
+    L.cc_dist_exchange.restype = C.c_int
     L.cc_step_advance.argtypes = [vp, u32, vp]
     L.cc_step_advance.restype = C.c_int
     _lib = L

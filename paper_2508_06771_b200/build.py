@@ -6,7 +6,7 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SOURCES = [os.path.join(HERE, "csrc", "cc_kernels.cu")]
+SOURCES = [os.path.join(HERE, "csrc", "cc_kernels.cu"), os.path.join(HERE, "csrc", "cc_dist.cu")]
 HEADERS = [os.path.join(HERE, "csrc", "cc_device.cuh"), os.path.join(ROOT, "include", "coulomb.h")]
 OUT = os.path.join(HERE, "lib", "libcoulomb.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -24,7 +24,7 @@ def stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or stale():
         os.makedirs(os.path.dirname(OUT), exist_ok=True)
-        cmd = [NVCC, *FLAGS, "-o", OUT, *SOURCES]
+        cmd = [NVCC, *FLAGS, "-o", OUT, *SOURCES, "-lnccl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)

@@ -55,9 +55,75 @@ class DistOps:
     owner: Callable       # (cell_global int32 [n], bounds list) -> owner rank int32 [n]; dead (-1) -> -1
     p2c: Optional[Callable] = None          # (v, cell, cells, sub) -> raw sums [cells][7] (NEXT f4)
     p2c_moments: Optional[Callable] = None  # (raw [cells][7], weight, cell_volume) -> moments [cells][7]
+    nccl: Optional["NcclComm"] = None       # the library's own NCCL communicator (C ABI cc_dist_*), or
+                                            # None: torch.distributed collectives (gloo tests)
 
 
-def cuda_ops() -> DistOps:
+class NcclComm:
+    """An NCCL communicator owned by the C library (cc_nccl_comm_init): rank 0 draws the
+    unique id, torch.distributed broadcasts it, every rank joins.  Used by reduce_diag /
+    migrate through the C ABI entries cc_dist_diag_reduce / cc_dist_alltoall_counts /
+    cc_dist_exchange (grouped ncclSend / ncclRecv)."""
+
+    def __init__(self, group=None):
+        import ctypes as C
+        from . import _lib
+        L = _lib.load()
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        uid = (C.c_char * _lib.CC_NCCL_ID_BYTES)()
+        if self.rank == 0:
+            _lib.check(L.cc_nccl_get_unique_id(uid), "cc_nccl_get_unique_id")
+        obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        uid = (C.c_char * _lib.CC_NCCL_ID_BYTES).from_buffer_copy(obj[0])
+        self.comm = C.c_void_p()
+        _lib.check(L.cc_nccl_comm_init(C.byref(self.comm), self.world, self.rank, uid), "cc_nccl_comm_init")
+
+    def close(self):
+        from . import _lib
+        if self.comm:
+            _lib.check(_lib.load().cc_nccl_comm_destroy(self.comm), "cc_nccl_comm_destroy")
+            self.comm = None
+
+    @staticmethod
+    def _stream(t):
+        import ctypes as C
+        return C.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+
+    def diag_reduce(self, diag: torch.Tensor) -> torch.Tensor:
+        import ctypes as C
+        from . import _lib
+        out = diag.contiguous().clone()
+        scratch = torch.empty((self.world, out.numel()), dtype=out.dtype, device=out.device)
+        _lib.check(_lib.load().cc_dist_diag_reduce(C.c_void_p(out.data_ptr()), C.c_void_p(scratch.data_ptr()),
+                                                   self.comm, self._stream(out)), "cc_dist_diag_reduce")
+        return out
+
+    def alltoall_counts(self, send: torch.Tensor) -> torch.Tensor:
+        import ctypes as C
+        from . import _lib
+        recv = torch.empty_like(send)
+        _lib.check(_lib.load().cc_dist_alltoall_counts(C.c_void_p(send.data_ptr()), C.c_void_p(recv.data_ptr()),
+                                                       self.comm, self._stream(send)), "cc_dist_alltoall_counts")
+        return recv
+
+    def exchange(self, send: torch.Tensor, recv: torch.Tensor, send_off: list, recv_off: list) -> None:
+        """rows of send [r][lds] -> recv [r][ldr] by the per-rank offsets (host lists)."""
+        import ctypes as C
+        import numpy as np
+        from . import _lib
+        so = np.asarray(send_off, dtype=np.int64)
+        ro = np.asarray(recv_off, dtype=np.int64)
+        s2 = send.reshape(-1, send.shape[-1]) if send.dim() > 1 else send.reshape(1, -1)
+        r2 = recv.reshape(-1, recv.shape[-1]) if recv.dim() > 1 else recv.reshape(1, -1)
+        _lib.check(_lib.load().cc_dist_exchange(
+            C.c_void_p(s2.data_ptr()), s2.stride(0) if s2.shape[1] > 0 else 0, C.c_void_p(r2.data_ptr()),
+            r2.stride(0) if r2.shape[1] > 0 else 0, s2.shape[0], s2.element_size(), so.ctypes.data_as(C.c_void_p),
+            ro.ctypes.data_as(C.c_void_p), self.comm, self._stream(send)), "cc_dist_exchange")
+
+
+def cuda_ops(nccl: Optional[NcclComm] = None) -> DistOps:
     from . import coulomb as cc
 
     def partition(key, nkeys):
@@ -76,11 +142,13 @@ def cuda_ops() -> DistOps:
         return cc.cc_p2c_moments(raw, weight=weight, cell_volume=cell_volume)
 
     return DistOps(partition=partition, gather=gather, sum_ranks=cc.cc_diag_sum_ranks, owner=owner, p2c=p2c,
-                   p2c_moments=p2c_moments)
+                   p2c_moments=p2c_moments, nccl=nccl)
 
 
 def reduce_diag(diag: torch.Tensor, ops: DistOps, group=None) -> torch.Tensor:
     """All-gather every rank's 16-double diagnostics and sum them in rank order."""
+    if ops.nccl is not None:
+        return ops.nccl.diag_reduce(diag)
     world = dist.get_world_size(group)
     flat = torch.empty(world * diag.numel(), dtype=diag.dtype, device=diag.device)
     dist.all_gather_into_tensor(flat, diag.contiguous().view(-1), group=group)
@@ -121,17 +189,36 @@ def migrate(v: torch.Tensor, cell_global: torch.Tensor, global_cells: int, ops: 
     send = [off_l[r + 1] - off_l[r] for r in range(world)]
     n_send = off_l[world]
     send_t = torch.tensor(send, dtype=torch.int64, device=dev)
-    recv_t = torch.empty(world, dtype=torch.int64, device=dev)
-    dist.all_to_all_single(recv_t, send_t, group=group)
+    if ops.nccl is not None:
+        recv_t = ops.nccl.alltoall_counts(send_t)
+    else:
+        recv_t = torch.empty(world, dtype=torch.int64, device=dev)
+        dist.all_to_all_single(recv_t, send_t, group=group)
     recv = [int(x) for x in recv_t.cpu().tolist()]
     pv, pc = ops.gather(v, cell_global, perm[:n_send], 0)
     n_recv = sum(recv)
     rv = torch.empty((3, n_recv), dtype=v.dtype, device=dev)
-    for c in range(3):
-        dist.all_to_all_single(rv[c], pv[c].contiguous(), output_split_sizes=recv, input_split_sizes=send,
-                               group=group)
     rc = torch.empty(n_recv, dtype=torch.int32, device=dev)
-    dist.all_to_all_single(rc, pc.contiguous(), output_split_sizes=recv, input_split_sizes=send, group=group)
+
+    def exchange_rows(src, dst):
+        if ops.nccl is not None:
+            so = [0]
+            for x in send:
+                so.append(so[-1] + x)
+            ro = [0]
+            for x in recv:
+                ro.append(ro[-1] + x)
+            ops.nccl.exchange(src.contiguous(), dst, so, ro)
+        elif src.dim() == 1:
+            dist.all_to_all_single(dst, src.contiguous(), output_split_sizes=recv, input_split_sizes=send,
+                                   group=group)
+        else:
+            for c in range(src.shape[0]):
+                dist.all_to_all_single(dst[c], src[c].contiguous(), output_split_sizes=recv,
+                                       input_split_sizes=send, group=group)
+
+    exchange_rows(pv, rv)
+    exchange_rows(pc, rc)
     base = bounds[rank]
     ident = torch.arange(n_recv, dtype=torch.int32, device=dev)
     lv, lc = ops.gather(rv, rc, ident, base)
@@ -139,9 +226,7 @@ def migrate(v: torch.Tensor, cell_global: torch.Tensor, global_cells: int, ops: 
     if payload is not None:
         px, _ = ops.gather(payload, cell_global, perm[:n_send], 0)
         rx = torch.empty((3, n_recv), dtype=payload.dtype, device=dev)
-        for c in range(3):
-            dist.all_to_all_single(rx[c], px[c].contiguous(), output_split_sizes=recv, input_split_sizes=send,
-                                   group=group)
+        exchange_rows(px, rx)
         lp = rx
     return Migrated(lv, lc, send, recv, lp)
 

@@ -100,3 +100,25 @@ def test_pic_loop_dist_path_one_rank(nccl1):
     live = ca >= 0
     assert int((~live).sum()) > 0 and cb.numel() == int(live.sum())
     assert torch.equal(ca[live], cb) and torch.equal(va[:, live], vb) and torch.equal(xa[:2, live], xb[:2])
+
+
+def test_library_nccl_comm_one_rank(nccl1):
+    """The C ABI's own NCCL path (cc_nccl_comm_init, cc_dist_diag_reduce,
+    cc_dist_alltoall_counts, cc_dist_exchange) through a real 1-rank communicator:
+    same results as the torch.distributed path."""
+    comm = ccd.NcclComm()
+    try:
+        ops_c, ops_t = ccd.cuda_ops(comm), ccd.cuda_ops()
+        d = torch.arange(16, dtype=torch.float64, device=DEV) * 1.5
+        assert torch.equal(ccd.reduce_diag(d, ops_c), ccd.reduce_diag(d, ops_t))
+        rng = np.random.default_rng(5)
+        n = 30_000
+        v = torch.from_numpy(rng.standard_normal((3, n))).to(DEV)
+        cell = torch.from_numpy(rng.integers(-1, 64, n).astype(np.int32)).to(DEV)
+        x = torch.from_numpy(rng.standard_normal((3, n))).to(DEV)
+        a = ccd.migrate(v, cell, 64, ops_c, payload=x)
+        b = ccd.migrate(v, cell, 64, ops_t, payload=x)
+        assert torch.equal(a.v, b.v) and torch.equal(a.cell, b.cell) and torch.equal(a.payload, b.payload)
+        assert a.sent == b.sent and a.received == b.received
+    finally:
+        comm.close()
