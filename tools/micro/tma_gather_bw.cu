@@ -160,6 +160,42 @@ __global__ void __launch_bounds__(kThreads) k_scatter4(const __grid_constant__ C
     if ((lane & 3) == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// gather (LDGSTS) + contiguous output of the same bytes, per chunk: (A) st.global.v2 by every
+// thread from shared memory, (B) one TMA bulk store (cp.async.bulk.global.shared::cta) of the chunk
+template <bool TMA_STORE>
+__global__ void __launch_bounds__(kThreads) k_gather_store(const double* __restrict__ rec,
+                                                           const int32_t* __restrict__ idx, int64_t n,
+                                                           double* __restrict__ outp)
+{
+    extern __shared__ __align__(16) double sraw2[];
+    double* st = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(sraw2) + 127) & ~uintptr_t(127));
+    const int64_t nch = n / kChunk;
+    for (int64_t c = blockIdx.x; c < nch; c += gridDim.x) {
+        if (TMA_STORE && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncthreads();
+        for (int e = threadIdx.x; e < kChunk; e += kThreads) {
+            const double* g = rec + 4 * static_cast<int64_t>(idx[c * kChunk + e]);
+            cp16(st + 4 * e, g);
+            cp16(st + 4 * e + 2, g + 2);
+        }
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+        __syncthreads();
+        double* o = outp + 4 * c * kChunk;
+        if (TMA_STORE) {
+            if (threadIdx.x == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(o),
+                             "r"((unsigned)__cvta_generic_to_shared(st)), "r"(kChunk * 32) : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+        } else {
+            for (int e = threadIdx.x; e < 2 * kChunk; e += kThreads)
+                reinterpret_cast<double2*>(o)[e] = reinterpret_cast<const double2*>(st)[e];
+        }
+    }
+    if (TMA_STORE && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 int main()
 {
     const int64_t n = 100000000 / kChunk * kChunk;
@@ -227,6 +263,32 @@ int main()
                    (long long)S, ctas, ms[0], n * 32.0 / ms[0] / 1e6, ms[1], n * 32.0 / ms[1] / 1e6,
                    cudaGetErrorString(cudaGetLastError()));
         }
+    }
+    {   // gathers (cell-sized spans) + output stores of the same bytes to a second 3.2 GB array
+        double* outp;
+        cudaMalloc(&outp, n * 32);
+        for (int64_t i = 0; i < n; ++i) h[i] = static_cast<int32_t>(i);
+        for (int64_t b = 0; b < n; b += 25000) std::shuffle(h.begin() + b, h.begin() + std::min(n, b + 25000), rng);
+        cudaMemcpy(idx, h.data(), n * 4, cudaMemcpyHostToDevice);
+        cudaFuncSetAttribute(k_gather_store<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_gather_store<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        float ms[2];
+        for (int k = 0; k < 2; ++k) {
+            for (int rep = 0; rep < 2; ++rep) {
+                if (rep == 1) cudaEventRecord(a);
+                if (k == 0) k_gather_store<false><<<148 * 4, kThreads, smem>>>(rec, idx, n, outp);
+                else k_gather_store<true><<<148 * 4, kThreads, smem>>>(rec, idx, n, outp);
+                if (rep == 1) cudaEventRecord(b);
+            }
+            cudaEventSynchronize(b);
+            cudaEventElapsedTime(&ms[k], a, b);
+        }
+        printf("gather (25000 spans) + contiguous store of the chunk: st.global %.3f ms, TMA bulk store %.3f ms  err=%s\n",
+               ms[0], ms[1], cudaGetErrorString(cudaGetLastError()));
+        cudaFree(outp);
     }
     {   // L2-resident gathers: 1e8 random gathers out of a 48 MB (1.5M-record) array
         const int64_t small = 1536000;
