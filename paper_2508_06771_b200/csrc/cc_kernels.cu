@@ -517,7 +517,6 @@ struct CollideArgs {
     double* small_recs;
     double* cellref;            // [M][4] shift of large cells (pre-collision v of the first slot)
     int M;
-    int pf_dist;                // k_collide_large: L2-prefetch the slice share of chunk c + pf_dist
     uint32_t model;             // CC_ODD_TRIPLET | CC_NANBU (NEXT f1 collision-model variants)
     double* trec;               // [M][kRec] triplet moment records of large odd cells (triplet mode)
     int pair_vec;               // outputs aligned for 16-byte (v) / 8-byte (cell, perm) pair stores
@@ -732,23 +731,6 @@ k_collide_large(CollideArgs A)
     const int c = blockIdx.x;
     if (c >= A.chunk_off[A.M]) return;      // grid is an upper bound on the chunk count
     const int j = A.chunk_cell[c];
-    if (A.pf_dist > 0 && threadIdx.x < 4) {
-        // Every chunk gathers from its whole cell slice at random; prefetch a later
-        // chunk's share of its cell slice into L2 with sequential bulk requests.
-        const int c2 = c + A.pf_dist;
-        if (c2 < A.chunk_off[A.M]) {
-            const int j2 = A.chunk_cell[c2];
-            const int64_t N2 = A.cnt[j2], nch = A.chunk_off[j2 + 1] - A.chunk_off[j2], q = c2 - A.chunk_off[j2];
-            const int64_t r0 = A.off[j2] + q * N2 / nch, r1 = A.off[j2] + (q + 1) * N2 / nch;
-            const int64_t per = (r1 - r0 + 3) / 4;
-            const int64_t a = r0 + threadIdx.x * per, b = min(r1, a + per);
-            if (b > a) {
-                const double* g = A.wsv + 4 * a;
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g),
-                             "r"(static_cast<unsigned>((b - a) * 32)) : "memory");
-            }
-        }
-    }
     const int32_t N = A.cnt[j], o = A.off[j];
     const uint32_t step = eff_step(A);
     const uint32_t items = static_cast<uint32_t>(N + 1) / 2;
@@ -1566,16 +1548,6 @@ CellConst cell_const(const cc_params& p, double dt)
 
 bool finite_pos(double x) { return std::isfinite(x) && x > 0.0; }
 
-// L2 prefetch distance of k_collide_large in chunks (tuning knob; env CC_PREFETCH_DIST).
-int prefetch_distance()
-{
-    static const int d = [] {
-        const char* e = std::getenv("CC_PREFETCH_DIST");
-        return e ? std::atoi(e) : 0;
-    }();
-    return d;
-}
-
 }  // namespace
 
 // ====================================================================== C ABI
@@ -1683,7 +1655,6 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     A.chunk = L.chunk;
     A.s0 = static_cast<uint32_t>(seed);
     A.s1 = static_cast<uint32_t>(seed >> 32);
-    A.pf_dist = prefetch_distance();
     A.model = p.flags & (CC_ODD_TRIPLET | CC_NANBU);
     A.trec = at<double>(workspace, L.o_trec);
     A.pair_vec = aligned(v_out, 16) && (ldv % 2 == 0) && aligned(cell_out, 8) && (!perm_out || aligned(perm_out, 8));
