@@ -63,6 +63,30 @@ def test_argument_errors_are_reported_before_any_launch():
     assert rc == _lib.CC_ECOUNT          # cells > CC_MAX_CELLS
 
 
+def test_next_row_entry_points_validate_arguments():
+    """NEXT-row and multi-GPU entries reject bad arguments host-side (no device needed)."""
+    from paper_2508_06771_b200 import _lib
+    import ctypes as C
+    L = _lib.load()
+    null = None
+    g = _lib.CCGrid()
+    g.dims = 4                                             # invalid dims
+    assert L.cc_push(null, 0, null, null, 0, null, 0, null, 10, 1, 0, C.byref(g), null, 0, -1.0, 1e-10,
+                     null) == _lib.CC_EINVAL
+    g.dims, g.n[0], g.d[0] = 1, 0, 1.0                     # zero cells on an axis
+    assert L.cc_push(null, 0, null, null, 0, null, 0, null, 10, 1, 0, C.byref(g), null, 0, -1.0, 1e-10,
+                     null) == _lib.CC_EINVAL
+    assert L.cc_recombine(null, 0, null, -1, 1, 0, null, 0.0, 1.0, 0, 0, null, null) == _lib.CC_EINVAL
+    assert L.cc_p2c(null, 0, null, 10, 4, 0, null, null, 0, null) == _lib.CC_EINVAL          # sub < 1
+    assert L.cc_p2c_scratch_bytes(4096, 16) == 4096 * 16 * 7 * 8
+    assert L.cc_host_buffer_bytes(1000, 4) > L.cc_workspace_bytes(1000, 4)
+    assert L.coulomb_collide_host(null, 10, null, null, null, null, 10, 0, 0, 1e-10, null, 0, 0, null, null,
+                                  null, 0, null) == _lib.CC_EINVAL                      # cells < 1
+    assert L.cc_nccl_comm_init(null, 2, 0, null) == _lib.CC_EINVAL
+    assert L.cc_dist_exchange(null, 0, null, 0, 1, 3, null, null, null, null) == _lib.CC_EINVAL   # elem 3
+    assert L.cc_step_advance(null, 1, null) == _lib.CC_EINVAL
+
+
 def test_product_package_never_imports_oracle():
     """The product path must not route through the oracle (or any CPU fallback)."""
     pkg = os.path.join(ROOT, "paper_2508_06771_b200")
