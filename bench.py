@@ -635,6 +635,22 @@ def run_ours(args):
                 "algorithmic_bytes_per_launch": STAGE_BYTES[dom] * n,
                 "algorithmic_bytes_per_particle": STAGE_BYTES[dom], "peak_source": peak_src}
 
+    STEP_KERNELS = ("k_count", "k_scan_tiles", "k_scan_cells", "k_cell_setup", "k_scatter", "k_collide_small",
+                    "k_collide_large", "k_copy_dead", "k_finalize_cells", "k_finalize_diag")
+
+    def step_achieved(ms):
+        """SURVEY §8(d) reading (1) of the NS target: ncu DRAM bytes of every kernel of one call
+        (profiles/traffic.json, captured on this config) over the call's time, against the peak;
+        guard: those bytes <= 1.15 x the design traffic (128 B/particle)."""
+        if world != 1 or not all(k in traffic for k in STEP_KERNELS):
+            return {"achieved_dram_frac": None}
+        b = sum(traffic[k]["dram_bytes_per_launch"] for k in STEP_KERNELS)
+        return {"achieved_dram_bytes_per_step": b, "achieved_dram_bytes_per_particle": b / n,
+                "achieved_dram_gbs": b / (ms * 1e-3) / 1e9,
+                "achieved_dram_frac": b / (ms * 1e-3) / 1e9 / hbm_peak,
+                "design_bytes_per_particle": 128, "guard_ok": b / n <= 1.15 * 128,
+                "source": "profiles/traffic.json (ncu dram__bytes_read/write.sum per kernel, one steady call)"}
+
     def summary(r):
         return {"value": r["pairs"] / (r["ms"] * 1e-3), "ms_per_step": r["ms"], "wall_ms_per_step": r["wall_ms"],
                 "stages_ms": r["stages"], "roofline": roofline(r),
@@ -655,7 +671,8 @@ def run_ours(args):
         "roofline": roofline(head, with_traffic=True),
         "stages_ms": head["stages"],
         "step_hbm": {"algorithmic_bytes_per_particle": STEP_BYTES_PER_PARTICLE,
-                     "frac": STEP_BYTES_PER_PARTICLE * n / (head["ms"] * 1e-3) / 1e9 / hbm_peak},
+                     "frac": STEP_BYTES_PER_PARTICLE * n / (head["ms"] * 1e-3) / 1e9 / hbm_peak,
+                     **step_achieved(head["ms"])},
         "cold": dict(summary(res["cold"]), what="every step bins the same randomly ordered input"),
         "warm": dict(summary(res["warm"]), what="chained steps, no drift (input already cell-sorted)"),
         "e2e": {"value": res["cold"]["pairs"] / (e2e_ms * 1e-3), "unit": UNIT,

@@ -13,6 +13,12 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_s
 # NEXT-row kernels: one launch each of k_push, k_p2c_atomic, k_recombine from the bench's pic/p2c sections
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_push|k_p2c_atomic|k_recombine" -c 3 \
    -o gpurun_out/${TAG}_next python bench.py --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 1 > /dev/null 2>&1; echo next rc=$?
-python tools/traffic_from_ncu.py gpurun_out/${TAG}_collide.ncu-rep gpurun_out/${TAG}_scatter.ncu-rep > /dev/null
+# DRAM bytes of every kernel of one steady-state call (the bench's step_hbm achieved fraction):
+# skip the 3 warm-up calls (10 kernels each), capture the next call's 10 kernels
+timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+   -k regex:"^k_" -s 30 -c 10 -o gpurun_out/${TAG}_step python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
+   --no-pic --e2e-steps 1 > /dev/null 2>&1; echo step rc=$?
+python tools/traffic_from_ncu.py gpurun_out/${TAG}_step.ncu-rep gpurun_out/${TAG}_collide.ncu-rep \
+   gpurun_out/${TAG}_scatter.ncu-rep > /dev/null
 timeout 900 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; cat gpurun_out/${TAG}_bench.json | cut -c1-400
 cp profiles/traffic.json gpurun_out/${TAG}_traffic.json
