@@ -204,9 +204,21 @@ def time_oracle_on(w, args):
     t0 = time.perf_counter()
     r = oracle.coulomb_collide(w.v, w.cell, w.cells, step=0, want_pairs=False, **p)
     dt = time.perf_counter() - t0
-    return {"value": float(r.diag[2]) / dt, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+    cores = oracle.num_threads()
+    # the oracle also single-threaded on C1-C3 and on all cores on C3 (one step each)
+    import workloads as W
+    per_config = {}
+    for name, wl, threads in (("C1_1_thread", W.c1(), 1), ("C2_1_thread", W.c2(), 1), ("C3_1_thread", W.c3(), 1),
+                              (f"C3_{cores}_threads", W.c3(), cores)):
+        oracle.set_num_threads(threads)
+        t1 = time.perf_counter()
+        rr = oracle.coulomb_collide(wl.v, wl.cell, wl.cells, step=0, want_pairs=False, **wl.params())
+        s1 = time.perf_counter() - t1
+        per_config[name] = {"seconds": s1, "pair_collisions_per_s": float(rr.diag[2]) / s1}
+    oracle.set_num_threads(cores)
+    return {"value": float(r.diag[2]) / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"the full C4 input ({w.n:.4g} e-, {int(r.diag[2])} pairs), 1 step, {dt:.1f} s wall",
-            "seconds": dt}
+            "seconds": dt, "configs": per_config}
 
 
 def run_reference(args):

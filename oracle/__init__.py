@@ -108,6 +108,8 @@ def lib():
         L.or_recombine.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32, C.c_uint32,
                                    C.c_void_p, C.c_double, C.c_double, C.c_uint64, C.c_uint64, C.c_void_p]
         L.or_recombine.restype = None
+        L.or_set_num_threads.argtypes = [C.c_int]
+        L.or_set_num_threads.restype = None
         L.or_num_threads.argtypes = []
         L.or_num_threads.restype = C.c_int
         _lib = L
@@ -318,6 +320,10 @@ def recombine(v, cell, cells, prob, *, eps_bind, cell_base=0, seed=42, step=0, m
     lib().or_recombine(_ptr(v_out), n, _ptr(cell_out), n, cells, cell_base, _ptr(pr), eps_bind, mass, seed, step,
                        _ptr(st))
     return v_out, cell_out, st
+
+
+def set_num_threads(n: int) -> None:
+    lib().or_set_num_threads(n)
 
 
 def num_threads() -> int:

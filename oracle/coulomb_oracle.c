@@ -850,3 +850,13 @@ void or_recombine(double *v, int64_t ldv, int32_t *cell, int64_t n, int32_t M, u
     free(prim);
     free(cat);
 }
+
+/* Thread count of the OpenMP cell loop (bench.py's single-thread oracle timings). */
+void or_set_num_threads(int n)
+{
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
