@@ -407,14 +407,15 @@ def p2c_section(dev, w):
 
 
 def configs_section(dev):
-    """BASELINE configs C1-C3 (parity-test sizes) timed through the operator: cold (the
+    """BASELINE configs C1-C3 (parity-test sizes) and C4b (C4 with a 2D sine density profile, cells
+    up to ~62,000 e-) timed through the operator: cold (the
     workload's random order every step) and warm (each step consumes the previous output),
     mean of 20 calls after 3 warm-up calls, CUDA events; C1/C2 are launch/latency-bound."""
     import torch
     import workloads as W
     import paper_2508_06771_b200 as cc
     out = {}
-    for name, w in (("C1", W.c1()), ("C2", W.c2()), ("C3", W.c3())):
+    for name, w in (("C1", W.c1()), ("C2", W.c2()), ("C3", W.c3()), ("C4b", W.c4b())):
         v0, c0 = torch.from_numpy(w.v).to(dev), torch.from_numpy(w.cell).to(dev)
         col = cc.Collider(w.n, w.cells, dev, **w.params())
         r = {"n": w.n, "cells": w.cells}
