@@ -363,3 +363,26 @@ def test_preserve_order_parity(O, flags, n, M, dead, skew):
     assert vel_err(out.v_out.cpu().numpy(), ref.v_out, 1e-3 * W.sigma_v(2.0)) <= TOL
     check_moments(out.moments.cpu().numpy(), ref.moments, w)
     check_diag(out.diag.cpu().numpy(), ref.diag, ref.v_out)
+
+
+def test_preserve_order_edge_cases(O):
+    """CC_PRESERVE_ORDER with no particles, all dead, strided rows (ldv > n) and no perm output."""
+    f = cc._lib.CC_PRESERVE_ORDER
+    out = cc.coulomb_collide(torch.zeros((3, 0), dtype=torch.float64, device=DEV),
+                             torch.zeros(0, dtype=torch.int32, device=DEV), 3, step=0, flags=f, dt=1e-10)
+    assert out.v_out.numel() == 0
+    w = W.random_cells(5000, 7, seed=3, dead_frac=1.0)
+    out = cc.coulomb_collide(to_dev(w.v), to_dev(w.cell), 7, step=0, flags=f, **w.params())
+    assert torch.equal(out.v_out.cpu(), torch.from_numpy(w.v)) and bool((out.cell_out == -1).all())
+    w = W.random_cells(10_001, 13, seed=4, skew=True, dead_frac=0.1)
+    big = torch.zeros((3, w.n + 7), dtype=torch.float64, device=DEV)
+    big[:, : w.n] = to_dev(w.v)
+    vout = torch.full((3, w.n + 7), 5.0, dtype=torch.float64, device=DEV)
+    res = cc.CollideOut(vout[:, : w.n], torch.empty(w.n, dtype=torch.int32, device=DEV), None,
+                        torch.empty((13, 7), dtype=torch.float64, device=DEV),
+                        torch.empty(16, dtype=torch.float64, device=DEV))
+    cc.coulomb_collide(big[:, : w.n], to_dev(w.cell), 13, step=1, out=res, flags=f, **w.params())
+    ref = O.coulomb_collide(w.v, w.cell, 13, step=1, flags=f, want_pairs=False, **w.params())
+    assert vel_err(vout[:, : w.n].cpu().numpy(), ref.v_out, 1.0) <= TOL
+    assert torch.all(vout[:, w.n:] == 5.0)
+    assert np.array_equal(res.cell_out.cpu().numpy(), ref.cell_out)
