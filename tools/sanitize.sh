@@ -10,7 +10,7 @@ for (n, M, dead, skew) in [(5003, 37, 0.05, True), (40_000, 3, 0.0, False), (300
     out2 = cc.coulomb_collide(out.v_out, out.cell_out, M, step=2, **w.params())
     perm, off = cc.cc_bin(torch.from_numpy(w.cell).cuda(), M)
     cc.cc_pairs(off, M)
-    for fl in (1, 2):                                  # f1 variants
+    for fl in (1, 2, 4):                               # f1 variants, CC_PRESERVE_ORDER
         cc.coulomb_collide(torch.from_numpy(w.v).cuda(), torch.from_numpy(w.cell).cuda(), M, step=3, flags=fl,
                            **w.params())
     # f2 push, f3 recombination, f4 P2C, host-buffer entry
