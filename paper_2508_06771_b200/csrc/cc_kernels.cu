@@ -1742,9 +1742,12 @@ int coulomb_collide_host(const double* h_v_in, int64_t ldv, const int32_t* h_cel
     const size_t row = sizeof(double) * static_cast<size_t>(n);
     if (n > 0) {
         // H2D: cell ids first (the count pass needs only them), then the three velocity rows
+        // (contiguous rows on both sides: one linear copy of 3n doubles)
+        const bool lin = (ldv == n && H.ldd == n);
         if (cudaMemcpyAsync(d_cin, h_cell_in, sizeof(int32_t) * n, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-            cudaMemcpy2DAsync(d_vin, sizeof(double) * H.ldd, h_v_in, sizeof(double) * ldv, row, 3,
-                              cudaMemcpyHostToDevice, st) != cudaSuccess) {
+            (lin ? cudaMemcpyAsync(d_vin, h_v_in, 3 * row, cudaMemcpyHostToDevice, st)
+                 : cudaMemcpy2DAsync(d_vin, sizeof(double) * H.ldd, h_v_in, sizeof(double) * ldv, row, 3,
+                                     cudaMemcpyHostToDevice, st)) != cudaSuccess) {
             cudaGetLastError();
             return CC_ECUDA;
         }
@@ -1755,8 +1758,10 @@ int coulomb_collide_host(const double* h_v_in, int64_t ldv, const int32_t* h_cel
     if (rc) return rc;
     bool ok = true;
     if (n > 0) {
-        ok = ok && cudaMemcpy2DAsync(h_v_out, sizeof(double) * ldv, d_vout, sizeof(double) * H.ldd, row, 3,
-                                     cudaMemcpyDeviceToHost, st) == cudaSuccess;
+        ok = ok && ((ldv == n && H.ldd == n)
+                        ? cudaMemcpyAsync(h_v_out, d_vout, 3 * row, cudaMemcpyDeviceToHost, st)
+                        : cudaMemcpy2DAsync(h_v_out, sizeof(double) * ldv, d_vout, sizeof(double) * H.ldd, row, 3,
+                                            cudaMemcpyDeviceToHost, st)) == cudaSuccess;
         if (h_cell_out)
             ok = ok && cudaMemcpyAsync(h_cell_out, d_cout, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st) == cudaSuccess;
         if (h_perm_out)
