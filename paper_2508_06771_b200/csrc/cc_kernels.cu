@@ -419,6 +419,9 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
     int32_t* base = reinterpret_cast<int32_t*>(smem);                       // [M1]
     uint32_t* wcnt = reinterpret_cast<uint32_t*>(smem + sizeof(int32_t) * M1);  // [W][MW] packed u16 pairs
     for (int i = threadIdx.x; i < W * MW; i += blockDim.x) wcnt[i] = 0u;
+    // CTA base = cell offset + tile offset (independent of pass A: its loads overlap pass A's)
+    const int32_t* trow = tbase + static_cast<int64_t>(blockIdx.x) * M1;
+    for (int c = threadIdx.x; c < M1; c += blockDim.x) base[c] = off[c] + trow[c];   // off[M] = L: dead last
     __syncthreads();
 
     const int64_t s0 = static_cast<int64_t>(blockIdx.x) * W * sub + static_cast<int64_t>(w) * sub;
@@ -446,8 +449,7 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
         }
     }
     __syncthreads();
-    // exclusive scan over warps per cell; CTA base = cell offset + tile offset
-    const int32_t* trow = tbase + static_cast<int64_t>(blockIdx.x) * M1;
+    // exclusive scan over warps per cell
     for (int c = threadIdx.x; c < M1; c += blockDim.x) {
         const uint32_t sh = (static_cast<uint32_t>(c) & 1u) << 4;
         uint32_t run = 0;
@@ -459,7 +461,6 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
             atomicAdd(wd, (run - x) << sh);    // half := run (mod 2^16, no carry: run, x < 2^16)
             run += x;
         }
-        base[c] = off[c] + trow[c];           // off[M] = L: dead slots follow the live ones
     }
     __syncthreads();
 
