@@ -70,6 +70,33 @@ extern "C" {
 #define CC_DIAG_LEN 16
 #define CC_MOMENTS_LEN 7
 
+/* Regular grid of the push (HOST struct).  Global cell id of a position:
+ * i_a = floor(x_a / d[a]) clamped to n[a]-1, G = i_0 + n[0] (i_1 + n[1] i_2)
+ * (SPEC S:449 "j = floor(x/dx)"; readings R22-R24).                         */
+typedef struct cc_grid {
+    int32_t dims;            /* 1, 2 or 3 position components in use (x, y, z) */
+    int32_t n[3];            /* global cells per axis; n[a] = 1 for a >= dims   */
+    double d[3];             /* cell size per axis [m]                          */
+    uint32_t periodic;       /* bit a set: axis a periodic (wraps by L_a = n[a] d[a]);
+                                clear: absorbing, a particle leaving [0, L_a) dies
+                                (Table 3 CS7, SPEC S:212-214)                    */
+} cc_grid;
+
+/* NEXT f2: the push fused into coulomb_collide's output stage (HOST struct; see
+ * cc_params.push).  x_in [3][ldx_in] DEVICE positions in INPUT order (row a of input
+ * particle l at x_in[a*ldx_in + l]); x_out [3][ldx_out] DEVICE, rows a < dims written in
+ * OUTPUT order; E DEVICE [3][ldE] per local cell or NULL.  Must not alias.           */
+typedef struct cc_push_params {
+    const cc_grid *grid;          /* HOST                                                    */
+    const double *E;
+    int64_t ldE;
+    double q_over_m;
+    const double *x_in;
+    int64_t ldx_in;
+    double *x_out;
+    int64_t ldx_out;
+} cc_push_params;
+
 /* Physical parameters (HOST struct).  Defaults from cc_default_params():
  * CODATA 2018 electron mass/charge and eps0, weight 1, cell_volume 1,
  * ln_lambda 10 (reading R7), no per-cell arrays, flags 0.                     */
@@ -84,6 +111,13 @@ typedef struct cc_params {
     const double *ln_lambda_arr;  /* DEVICE [cells] or NULL                                */
     uint32_t flags;               /* 0 (TA77, odd sitter) or CC_ODD_TRIPLET | CC_NANBU,
                                      optionally | CC_PRESERVE_ORDER                          */
+    const cc_push_params *push;   /* HOST or NULL: when set, every output particle is also pushed
+                                     (S2b + S2c with this call's dt, exactly cc_push's arithmetic):
+                                     v_out = kicked velocity, x_out = drifted position, cell_out =
+                                     post-push GLOBAL cell (-1 if absorbed); moments and diagnostics
+                                     stay those of the post-collision, pre-kick particles.  Equal,
+                                     bit for bit, to coulomb_collide then cc_push(x_in, perm_out, ...),
+                                     without re-reading v, cell and perm.  Not with CC_PRESERVE_ORDER. */
     const uint32_t *step_dev;     /* DEVICE uint32 or NULL: when set, the effective step is
                                      (step + *step_dev) mod 2^32, read on the device, so a
                                      captured CUDA graph replays with advancing randoms
@@ -255,17 +289,7 @@ int cc_diag_sum_ranks(const double *gathered, int32_t nranks, double *out, void 
 
 /* ---- NEXT f2: the kinetic push of a subcycled PIC loop ---------- */
 
-/* Regular grid of the push (HOST struct).  Global cell id of a position:
- * i_a = floor(x_a / d[a]) clamped to n[a]-1, G = i_0 + n[0] (i_1 + n[1] i_2)
- * (SPEC S:449 "j = floor(x/dx)"; readings R22-R24).                         */
-typedef struct cc_grid {
-    int32_t dims;            /* 1, 2 or 3 position components in use (x, y, z) */
-    int32_t n[3];            /* global cells per axis; n[a] = 1 for a >= dims   */
-    double d[3];             /* cell size per axis [m]                          */
-    uint32_t periodic;       /* bit a set: axis a periodic (wraps by L_a = n[a] d[a]);
-                                clear: absorbing, a particle leaving [0, L_a) dies
-                                (Table 3 CS7, SPEC S:212-214)                    */
-} cc_grid;
+
 
 /* Steps S2b + S2c of Table 2 (SPEC push S:204-210) for n particles
  * in the OUTPUT order of a coulomb_collide call:

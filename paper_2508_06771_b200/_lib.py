@@ -39,17 +39,23 @@ EXPORTS = ("cc_default_params", "cc_workspace_bytes", "coulomb_collide", "cc_dev
            "cc_dist_alltoall_counts", "cc_dist_exchange")
 
 
+class CCGrid(C.Structure):
+    _fields_ = [("dims", C.c_int32), ("n", C.c_int32 * 3), ("d", C.c_double * 3), ("periodic", C.c_uint32)]
+
+
+class CCPushParams(C.Structure):
+    _fields_ = [("grid", C.POINTER(CCGrid)), ("E", C.c_void_p), ("ldE", C.c_int64), ("q_over_m", C.c_double),
+                ("x_in", C.c_void_p), ("ldx_in", C.c_int64), ("x_out", C.c_void_p), ("ldx_out", C.c_int64)]
+
+
 class CCParams(C.Structure):
     _fields_ = [("mass", C.c_double), ("charge", C.c_double), ("eps0", C.c_double),
                 ("weight", C.c_double), ("cell_volume", C.c_double),
                 ("cell_volume_arr", C.c_void_p), ("ln_lambda", C.c_double),
                 ("ln_lambda_arr", C.c_void_p), ("flags", C.c_uint32),
+                ("push", C.POINTER(CCPushParams)),
                 ("step_dev", C.c_void_p),
                 ("stage_events", C.POINTER(C.c_void_p))]
-
-
-class CCGrid(C.Structure):
-    _fields_ = [("dims", C.c_int32), ("n", C.c_int32 * 3), ("d", C.c_double * 3), ("periodic", C.c_uint32)]
 
 
 class CCError(RuntimeError):

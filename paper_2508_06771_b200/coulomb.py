@@ -98,7 +98,8 @@ def coulomb_collide(v: torch.Tensor, cell: torch.Tensor, cells: int, *, dt: floa
                     seed: int = 42, step: int = 0, mass: float = M_E, charge: float = Q_E,
                     eps0: float = EPS0, out: Optional[CollideOut] = None,
                     workspace: Optional[torch.Tensor] = None, moments: bool = True,
-                    diag: bool = True, flags: int = 0, step_dev: Optional[torch.Tensor] = None) -> CollideOut:
+                    diag: bool = True, flags: int = 0, step_dev: Optional[torch.Tensor] = None,
+                    push: Optional[dict] = None) -> CollideOut:
     """One step of the Coulomb collision operator on CUDA tensors (see coulomb.h)."""
     dev = cell.device
     if dev.type != "cuda":
@@ -131,6 +132,23 @@ def coulomb_collide(v: torch.Tensor, cell: torch.Tensor, cells: int, *, dt: floa
     p = make_params(mass=mass, charge=charge, eps0=eps0, weight=weight, cell_volume=cell_volume,
                     ln_lambda=ln_lambda, cell_volume_arr=cell_volume_arr, ln_lambda_arr=ln_lambda_arr,
                     flags=flags, step_dev=step_dev)
+    keep = []
+    if push is not None:
+        # NEXT f2 fused push: dict(grid=Grid, x_in=[3][n] (input order), x_out=[3][n], E=None|[3][cells],
+        # q_over_m=-e/m_e); cell_out becomes the post-push GLOBAL cell
+        g = push["grid"].c()
+        xi, xo, E = push["x_in"], push["x_out"], push.get("E")
+        for t, nm in ((xi, "x_in"), (xo, "x_out")):
+            _soa(t, nm, dev)
+        q = _lib.CCPushParams()
+        q.grid = C.pointer(g)
+        q.E = None if E is None else E.data_ptr()
+        q.ldE = 0 if E is None else _soa(E, "E", dev)
+        q.q_over_m = push.get("q_over_m", -Q_E / M_E)
+        q.x_in, q.ldx_in = xi.data_ptr(), max(int(xi.stride(0)), n)
+        q.x_out, q.ldx_out = xo.data_ptr(), max(int(xo.stride(0)), n)
+        p.push = C.pointer(q)
+        keep += [g, q]
     rc = _lib.load().coulomb_collide(
         _ptr(v), max(ldv, n), _ptr(cell), _ptr(out.v_out), _ptr(out.cell_out), _ptr(out.perm_out),
         n, cells, cell_base, dt, C.byref(p), seed, step,

@@ -502,6 +502,36 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
 }
 
 // ------------------------------------------------------------------ CCS4 + CCS5 items
+// NEXT f2 push geometry (cc_grid with L_a = n_a d_a precomputed)
+struct PushGrid {
+    int dims;
+    int n[3];
+    double d[3], L[3];
+    uint32_t periodic;
+};
+
+// S2c drift of one position row a (R22-R24), explicitly rounded as in the oracle:
+// x' = x + dt v', periodic wrap or absorption, cell index along a.  Returns x'.
+__device__ __forceinline__ double drift_axis(const PushGrid& g, int a, double x, double v, double dt, bool& alive,
+                                             int64_t& G, int64_t& stride)
+{
+    double xa = __dadd_rn(x, __dmul_rn(dt, v));
+    const double L = g.L[a];
+    if (g.periodic & (1u << a)) {
+        while (xa < 0.0) xa = __dadd_rn(xa, L);
+        while (xa >= L) xa = __dsub_rn(xa, L);
+    } else if (xa < 0.0 || xa >= L) {
+        alive = false;
+    }
+    if (alive) {
+        int64_t i = static_cast<int64_t>(floor(__ddiv_rn(xa, g.d[a])));
+        if (i > g.n[a] - 1) i = g.n[a] - 1;
+        G += i * stride;
+    }
+    stride *= g.n[a];
+    return xa;
+}
+
 struct CollideArgs {
     const double* wsv;          // cell-sorted 32-byte records (cold input)
     int64_t ldv;                // row stride of v_out
@@ -524,6 +554,17 @@ struct CollideArgs {
     uint32_t cell_base, step, s0, s1;
     const uint32_t* step_dev;   // NULL, or DEVICE offset added to `step` (cc_params.step_dev)
     int chunk;                  // pairs per k_collide_large CTA (<= kChunk, multiple of kCollideThreads)
+    // fused S2b + S2c push of the outputs (cc_params.push; NEXT f2): x_in is read at the
+    // particle's input index, x_out / v_out / cell_out written at the output slot
+    int push;
+    PushGrid pg;
+    const double* E;
+    int64_t ldE;
+    double kick, dt;
+    const double* x_in;
+    int64_t ldxi;
+    double* x_out;
+    int64_t ldxo;
 };
 
 __device__ __forceinline__ uint32_t eff_step(const CollideArgs& A)
@@ -561,29 +602,88 @@ __device__ __forceinline__ Rec load_slot(const CollideArgs& A, int64_t s)
     return r;
 }
 
+// Fused push of one particle (cell j = its LOCAL collision cell, -1 dead): kick v (if E),
+// drift its position read at input index l, write x_out[.][p]; returns the post-push
+// GLOBAL cell (or -1).  The arithmetic is k_push's (drift_axis), so the result is
+// bit-identical to coulomb_collide followed by cc_push.
+__device__ __forceinline__ int32_t push_one(const CollideArgs& A, int32_t p, int32_t j, int32_t l, double& vx,
+                                            double& vy, double& vz)
+{
+    const PushGrid& g = A.pg;
+    double v3[3] = {vx, vy, vz};
+    if (j < 0) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+            if (a < g.dims) A.x_out[a * A.ldxo + p] = __ldg(A.x_in + a * A.ldxi + l);
+        return -1;
+    }
+    if (A.E) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) v3[c] = __dadd_rn(v3[c], __dmul_rn(A.kick, __ldg(A.E + c * A.ldE + j)));
+        vx = v3[0]; vy = v3[1]; vz = v3[2];
+    }
+    bool alive = true;
+    int64_t G = 0, stride = 1;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+        if (a < g.dims)
+            A.x_out[a * A.ldxo + p] = drift_axis(g, a, __ldg(A.x_in + a * A.ldxi + l), v3[a], A.dt, alive, G, stride);
+    return alive ? static_cast<int32_t>(G) : -1;
+}
+
+template <bool PUSH = false>
 __device__ __forceinline__ void write_out(const CollideArgs& A, int32_t p, int32_t j, const Rec& r)
 {
-    A.v_out[p] = r.x;
-    A.v_out[A.ldv + p] = r.y;
-    A.v_out[2 * A.ldv + p] = r.z;
-    A.cell_out[p] = j;
+    double x = r.x, y = r.y, z = r.z;
+    int32_t cj = j;
+    if (PUSH) cj = push_one(A, p, j, unpack_perm(r.w), x, y, z);
+    A.v_out[p] = x;
+    A.v_out[A.ldv + p] = y;
+    A.v_out[2 * A.ldv + p] = z;
+    A.cell_out[p] = cj;
     if (A.perm_out) A.perm_out[p] = unpack_perm(r.w);
 }
 
 // Both members of pair k: slots pa, pa+1 of every output row.  With an even
 // pa and aligned outputs this is one 16-byte store per velocity row and one
 // 8-byte store for the cell ids and for perm.
-__device__ __forceinline__ void write_pair_out(const CollideArgs& A, int32_t pa, int32_t j, const Rec& a, const Rec& b)
+// fused push: start the position loads of input particle l early (L1 prefetch, no registers)
+__device__ __forceinline__ void prefetch_x(const CollideArgs& A, int32_t l)
 {
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+        if (a < A.pg.dims) asm volatile("prefetch.global.L1 [%0];" ::"l"(A.x_in + a * A.ldxi + l));
+}
+
+// small kernels (k_collide_small, k_triplets, k_copy_dead): runtime choice
+__device__ __forceinline__ void write_out_any(const CollideArgs& A, int32_t p, int32_t j, const Rec& r)
+{
+    if (A.push) write_out<true>(A, p, j, r);
+    else write_out<false>(A, p, j, r);
+}
+
+// PUSH (k_collide_large<.., true>): both members are pushed first (push_one writes x_out),
+// then the same paired stores carry the kicked velocities and post-push cells.
+template <bool PUSH = false>
+__device__ __forceinline__ void write_pair_out(const CollideArgs& A, int32_t pa, int32_t j, Rec a, Rec b)
+{
+    int32_t ca = j, cb = j;
+    if (PUSH) {
+        ca = push_one(A, pa, j, unpack_perm(a.w), a.x, a.y, a.z);
+        cb = push_one(A, pa + 1, j, unpack_perm(b.w), b.x, b.y, b.z);
+    }
     if (A.pair_vec && (pa & 1) == 0) {
         *reinterpret_cast<double2*>(A.v_out + pa) = make_double2(a.x, b.x);
         *reinterpret_cast<double2*>(A.v_out + A.ldv + pa) = make_double2(a.y, b.y);
         *reinterpret_cast<double2*>(A.v_out + 2 * A.ldv + pa) = make_double2(a.z, b.z);
-        *reinterpret_cast<int2*>(A.cell_out + pa) = make_int2(j, j);
+        *reinterpret_cast<int2*>(A.cell_out + pa) = make_int2(ca, cb);
         if (A.perm_out) *reinterpret_cast<int2*>(A.perm_out + pa) = make_int2(unpack_perm(a.w), unpack_perm(b.w));
     } else {
-        write_out(A, pa, j, a);
-        write_out(A, pa + 1, j, b);
+        A.v_out[pa] = a.x; A.v_out[A.ldv + pa] = a.y; A.v_out[2 * A.ldv + pa] = a.z;
+        A.v_out[pa + 1] = b.x; A.v_out[A.ldv + pa + 1] = b.y; A.v_out[2 * A.ldv + pa + 1] = b.z;
+        A.cell_out[pa] = ca;
+        A.cell_out[pa + 1] = cb;
+        if (A.perm_out) { A.perm_out[pa] = unpack_perm(a.w); A.perm_out[pa + 1] = unpack_perm(b.w); }
     }
 }
 
@@ -647,7 +747,7 @@ k_collide_small(CollideArgs A)
         for (int q = 0; q < 3; ++q) mine[q] = load_slot(A, o + pi_sm[w][N - 3 + q]);
         triplet_update(A, G, C, step, mine);
 #pragma unroll
-        for (int q = 0; q < 3; ++q) write_out(A, o + N - 3 + q, j, mine[q]);
+        for (int q = 0; q < 3; ++q) write_out_any(A, o + N - 3 + q, j, mine[q]);
         nmine = 3;
     } else if (k < items && !(triplet && k == items - 1)) {
         const int32_t pa = o + 2 * static_cast<int32_t>(k);
@@ -658,10 +758,10 @@ k_collide_small(CollideArgs A)
             double u1, u2;
             pair_uniforms(A, j, k, step, u1, u2);
             cc::collide_model(mine[0].x, mine[0].y, mine[0].z, mine[1].x, mine[1].y, mine[1].z, C, u1, u2, A.model);
-            write_out(A, pa + 1, j, mine[1]);
+            write_out_any(A, pa + 1, j, mine[1]);
             nmine = 2;
         }
-        write_out(A, pa, j, mine[0]);
+        write_out_any(A, pa, j, mine[0]);
     }
 #pragma unroll
     for (int q = 0; q < 3; ++q)
@@ -720,7 +820,7 @@ constexpr int kWarpItems = 32 * kItemsPerThread;            // items of one warp
 constexpr size_t kCollideSmem = 2ull * kChunk * 4 * sizeof(double);
 static_assert(kChunk % kCollideThreads == 0, "chunk must be a whole number of thread items");
 
-template <bool NANBU>
+template <bool NANBU, bool PUSH>
 __global__ void __launch_bounds__(kCollideThreads, CC_COLLIDE_CTAS)
 k_collide_large(CollideArgs A)
 {
@@ -815,15 +915,19 @@ k_collide_large(CollideArgs A)
                 const double2 b01 = *reinterpret_cast<const double2*>(stage + 4 * (kChunk + e));
                 const double2 b23 = *reinterpret_cast<const double2*>(stage + 4 * (kChunk + e) + 2);
                 Rec b{b01.x, b01.y, b23.x, b23.y};
+                if (PUSH) {                                // the push's position gathers, in flight
+                    prefetch_x(A, unpack_perm(a.w));       // during the collision arithmetic
+                    prefetch_x(A, unpack_perm(b.w));
+                }
                 const int slot = t * 32 + lane;
                 if (NANBU)
                     cc::nanbu_update(a.x, a.y, a.z, b.x, b.y, b.z, C, zq[w][slot], u2q[w][slot]);
                 else if (!(CC_ABLATE & 1))
                     cc::ta_update_z(a.x, a.y, a.z, b.x, b.y, b.z, C, zq[w][slot], u2q[w][slot]);
-                write_pair_out(A, pa, j, a, b);
+                write_pair_out<PUSH>(A, pa, j, a, b);
                 acc.post(b.x, b.y, b.z, ref.x, ref.y, ref.z);
             } else {
-                write_out(A, pa, j, a);
+                write_out<PUSH>(A, pa, j, a);
             }
             acc.post(a.x, a.y, a.z, ref.x, ref.y, ref.z);
         }
@@ -864,7 +968,7 @@ __global__ void k_triplets(CollideArgs A)
         const double* cr = A.cellref + 4 * static_cast<int64_t>(j);
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
-            write_out(A, o + N - 3 + q, j, r[q]);
+            write_out_any(A, o + N - 3 + q, j, r[q]);
             acc.post(r[q].x, r[q].y, r[q].z, cr[0], cr[1], cr[2]);
         }
     }
@@ -908,7 +1012,7 @@ __global__ void k_copy_dead(CollideArgs A, int n)
     for (int64_t p = L + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < n;
          p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const Rec r = load_slot(A, p);
-        write_out(A, static_cast<int32_t>(p), -1, r);
+        write_out_any(A, static_cast<int32_t>(p), -1, r);
     }
 }
 
@@ -1337,13 +1441,6 @@ k_recombine(double* __restrict__ v, int64_t ldv, int32_t* __restrict__ cell, int
 }
 
 // ------------------------------------------------------------------ NEXT f2: push (S2b + S2c)
-struct PushGrid {
-    int dims;
-    int n[3];
-    double d[3], L[3];
-    uint32_t periodic;
-};
-
 // Thread per particle (grid-stride).  Every product and sum is an explicitly
 // rounded IEEE operation (__dmul_rn / __dadd_rn / __ddiv_rn), as in the
 // oracle (compiled without FMA contraction), so the result is bit-exact.
@@ -1381,23 +1478,7 @@ k_push(const double* __restrict__ xin, int64_t ldxi, const int32_t* __restrict__
         bool alive = true;
         int64_t G = 0, stride = 1;
 #pragma unroll
-        for (int a = 0; a < DIMS; ++a) {
-            double xa = __dadd_rn(x[a], __dmul_rn(dt, vn[a]));
-            const double L = g.L[a];
-            if (g.periodic & (1u << a)) {
-                while (xa < 0.0) xa = __dadd_rn(xa, L);
-                while (xa >= L) xa = __dsub_rn(xa, L);
-            } else if (xa < 0.0 || xa >= L) {
-                alive = false;
-            }
-            if (alive) {
-                int64_t i = static_cast<int64_t>(floor(__ddiv_rn(xa, g.d[a])));
-                if (i > g.n[a] - 1) i = g.n[a] - 1;
-                G += i * stride;
-            }
-            stride *= g.n[a];
-            xo[a * ldxo + p] = xa;
-        }
+        for (int a = 0; a < DIMS; ++a) xo[a * ldxo + p] = drift_axis(g, a, x[a], vn[a], dt, alive, G, stride);
         cell[p] = alive ? static_cast<int32_t>(G) : -1;
     }
 }
@@ -1601,6 +1682,19 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
         p.weight < 0.0 || (!p.cell_volume_arr && !finite_pos(p.cell_volume)) ||
         (!p.ln_lambda_arr && !std::isfinite(p.ln_lambda)) || (p.flags & ~(CC_ODD_TRIPLET | CC_NANBU | CC_PRESERVE_ORDER)) != 0)
         return CC_EINVAL;
+    if (p.push) {                            // fused push (NEXT f2): same checks as cc_push
+        const cc_push_params& q = *p.push;
+        if (!q.grid || q.grid->dims < 1 || q.grid->dims > 3 || !std::isfinite(q.q_over_m) ||
+            (p.flags & CC_PRESERVE_ORDER) || (n > 0 && (!q.x_in || !q.x_out)) || q.ldx_in < n || q.ldx_out < n ||
+            (q.E && q.ldE < cells))
+            return CC_EINVAL;
+        int64_t total = 1;
+        for (int a = 0; a < q.grid->dims; ++a) {
+            if (q.grid->n[a] < 1 || !finite_pos(q.grid->d[a])) return CC_EINVAL;
+            total *= q.grid->n[a];
+        }
+        if (total >= (1ll << 31)) return CC_EINVAL;
+    }
     if (!workspace || !aligned(workspace, 256)) return CC_EWORKSPACE;
     const Layout L = make_layout(n, cells);
     if (workspace_bytes < L.total) return CC_EWORKSPACE;
@@ -1654,6 +1748,26 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     A.step = static_cast<uint32_t>(step);
     A.step_dev = p.step_dev;
     A.chunk = L.chunk;
+    A.push = 0;
+    A.E = nullptr; A.x_in = nullptr; A.x_out = nullptr;
+    A.ldE = A.ldxi = A.ldxo = 0;
+    A.kick = A.dt = 0.0;
+    if (p.push) {
+        const cc_push_params& q = *p.push;
+        A.push = 1;
+        A.pg.dims = q.grid->dims;
+        A.pg.periodic = q.grid->periodic;
+        for (int a = 0; a < 3; ++a) {
+            A.pg.n[a] = a < q.grid->dims ? q.grid->n[a] : 1;
+            A.pg.d[a] = a < q.grid->dims ? q.grid->d[a] : 1.0;
+            A.pg.L[a] = static_cast<double>(A.pg.n[a]) * A.pg.d[a];
+        }
+        A.E = q.E; A.ldE = q.ldE;
+        A.kick = dt * q.q_over_m;            // = __dmul_rn(dt, qm) of k_push (host IEEE double product)
+        A.dt = dt;
+        A.x_in = q.x_in; A.ldxi = q.ldx_in;
+        A.x_out = q.x_out; A.ldxo = q.ldx_out;
+    }
     A.s0 = static_cast<uint32_t>(seed);
     A.s1 = static_cast<uint32_t>(seed >> 32);
     A.model = p.flags & (CC_ODD_TRIPLET | CC_NANBU);
@@ -1661,14 +1775,23 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     A.pair_vec = aligned(v_out, 16) && (ldv % 2 == 0) && aligned(cell_out, 8) && (!perm_out || aligned(perm_out, 8));
 
     mark(ev, 3, st);
-    rc = want_smem(k_collide_large<false>, kCollideSmem);
-    if (!rc) rc = want_smem(k_collide_large<true>, kCollideSmem);
+    rc = want_smem(k_collide_large<false, false>, kCollideSmem);
+    if (!rc) rc = want_smem(k_collide_large<true, false>, kCollideSmem);
+    if (!rc) rc = want_smem(k_collide_large<false, true>, kCollideSmem);
+    if (!rc) rc = want_smem(k_collide_large<true, true>, kCollideSmem);
     if (rc) return rc;
     k_collide_small<<<(M + 7) / 8, 256, 0, st>>>(A);
-    if (A.model & CC_NANBU)
-        k_collide_large<true><<<static_cast<unsigned>(L.max_chunks), kCollideThreads, kCollideSmem, st>>>(A);
-    else
-        k_collide_large<false><<<static_cast<unsigned>(L.max_chunks), kCollideThreads, kCollideSmem, st>>>(A);
+    {
+        const unsigned grid = static_cast<unsigned>(L.max_chunks);
+        const bool nb = (A.model & CC_NANBU) != 0;
+        if (A.push) {
+            if (nb) k_collide_large<true, true><<<grid, kCollideThreads, kCollideSmem, st>>>(A);
+            else k_collide_large<false, true><<<grid, kCollideThreads, kCollideSmem, st>>>(A);
+        } else {
+            if (nb) k_collide_large<true, false><<<grid, kCollideThreads, kCollideSmem, st>>>(A);
+            else k_collide_large<false, false><<<grid, kCollideThreads, kCollideSmem, st>>>(A);
+        }
+    }
     if (A.model & CC_ODD_TRIPLET) k_triplets<<<(M + 255) / 256, 256, 0, st>>>(A);
     k_copy_dead<<<148 * 4, 256, 0, st>>>(A, nn);
     if (preserve) {

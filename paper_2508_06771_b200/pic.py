@@ -11,8 +11,10 @@ that loop restricted to the path:
   per substep   S1   coulomb_collide: bins the pushed particles (nearly sorted:
                      the previous output order), pairs, collides; its
                      per-cell moments are the P2C of the post-collision state
-                S2b+S2c cc_push: v += dt (q/m) E[cell], x += dt v, boundary, new
-                     cell id; positions follow the particles through perm_out
+                S2b+S2c the push: v += dt (q/m) E[cell], x += dt v, boundary, new
+                     cell id — fused into the collision call's output stage
+                     (cc_params.push, default) or as a separate cc_push reading
+                     the positions through perm_out (fused=False); same bits
   per field step     (every ``subcycles`` substeps) the lagged per-cell Coulomb
                      logarithm from the last moments (R21, cc_coulomb_log), fed to
                      the next substeps as ln_lambda_arr; E is held fixed (the PDE
@@ -44,7 +46,7 @@ class PicLoop:
                  weight: float, cell_volume: float, E: Optional[torch.Tensor] = None,
                  q_over_m: float = -Q_E / M_E, seed: int = 42, subcycles: int = 10, ln_lambda: float = 10.0,
                  coulomb_log_feedback: bool = True, graph: bool = True, flags: int = 0,
-                 dist_ops=None, group=None, cell_base: int = 0, cells: Optional[int] = None):
+                 dist_ops=None, group=None, cell_base: int = 0, cells: Optional[int] = None, fused: bool = False):
         if subcycles < 1 or subcycles % 2:
             raise ValueError("subcycles must be a positive even number (ping-pong buffers)")
         self.dev = cell.device
@@ -56,6 +58,7 @@ class PicLoop:
         self.cell_base = cell_base
         self.cells = grid.cells if cells is None else cells
         self.use_graph = graph and dist_ops is None
+        self.fused = fused            # push inside the collision call's output stage (cc_params.push)
         self.field_steps = 0
         self.step_dev = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.lnl = torch.full((self.cells,), float(ln_lambda), dtype=torch.float64, device=self.dev)
@@ -85,12 +88,16 @@ class PicLoop:
     def _substep(self, s: int):
         a, b = self.a, self.a ^ 1
         out = cc.CollideOut(self.v[b], self.cell[b], self.perm, self.moments, self.diag)
+        push = None
+        if self.fused:
+            push = dict(grid=self.grid, x_in=self.x[a], x_out=self.x[b], E=self.E, q_over_m=self.qm)
         cc.coulomb_collide(self.v[a], self.cell[a], self.cells, dt=self.dt, weight=self.weight,
                            cell_volume=self.volume, ln_lambda_arr=self.lnl, cell_base=self.cell_base,
                            seed=self.seed, step=s, out=out, workspace=self.ws, flags=self.flags,
-                           step_dev=self.step_dev)
-        cc.cc_push(self.x[a], self.v[b], self.cell[b], self.grid, dt=self.dt, q_over_m=self.qm, E=self.E,
-                   perm=self.perm, x_out=self.x[b], cells=self.cells, cell_base=self.cell_base)
+                           step_dev=self.step_dev, push=push)
+        if not self.fused:
+            cc.cc_push(self.x[a], self.v[b], self.cell[b], self.grid, dt=self.dt, q_over_m=self.qm, E=self.E,
+                       perm=self.perm, x_out=self.x[b], cells=self.cells, cell_base=self.cell_base)
         self.a = b
 
     def _field_step_body(self):

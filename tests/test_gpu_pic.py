@@ -162,3 +162,42 @@ def test_pic_loop_vs_oracle(O):
     assert np.max(np.abs(gv - rv) / scale) <= 1e-12
     assert np.max(np.abs(gx - rx)) <= 1e-12 * 16 * 2e-4
     assert (rc < 0).sum() > 0                       # the absorbing walls took some electrons
+
+
+@pytest.mark.parametrize("flags", [0, 1, 2])
+@pytest.mark.parametrize("dims,periodic,field", [(2, 2, True), (1, 0, False), (3, 7, True)])
+def test_fused_push_equals_collide_then_push(dims, periodic, field, flags):
+    """cc_params.push (the push inside the collision call's output stage) is bit for bit
+    coulomb_collide followed by cc_push through perm_out."""
+    rng = np.random.default_rng(dims * 7 + periodic + flags)
+    nc = [12, 9, 5][:dims]
+    d = [2e-4, 3e-4, 5e-4][:dims]
+    M = int(np.prod(nc))
+    w = W.random_cells(150_001, M, seed=3 + dims, dead_frac=0.02, skew=True)
+    x = np.zeros((3, w.n))
+    for a in range(dims):
+        x[a] = rng.uniform(0, nc[a] * d[a], w.n)
+    E = to_dev(rng.normal(0, 3e3, (3, M))) if field else None
+    g = cc.Grid(dims, tuple(nc), tuple(d), periodic)
+    p = w.params()
+    v, c, xin = to_dev(w.v), to_dev(w.cell), to_dev(x)
+    ref = cc.coulomb_collide(v, c, M, step=4, flags=flags, **p)
+    xr = cc.cc_push(xin, ref.v_out, ref.cell_out, g, dt=w.dt, E=E, perm=ref.perm_out, cells=M)
+    xo = torch.zeros((3, w.n), dtype=torch.float64, device=DEV)
+    out = cc.coulomb_collide(v, c, M, step=4, flags=flags, push=dict(grid=g, x_in=xin, x_out=xo, E=E), **p)
+    assert torch.equal(out.cell_out, ref.cell_out) and torch.equal(out.v_out, ref.v_out)
+    assert torch.equal(xo[:dims], xr[:dims]) and torch.equal(out.perm_out, ref.perm_out)
+    assert torch.equal(out.moments, ref.moments) and torch.equal(out.diag, ref.diag)
+
+
+def test_pic_loop_fused_equals_unfused():
+    x, v, cell, E, grid, prm, M = pic_setup()
+    g = cc.Grid(grid["dims"], tuple(grid["nc"]), tuple(grid["d"]), grid["periodic"])
+    a = PicLoop(to_dev(x), to_dev(v), to_dev(cell), g, E=to_dev(E), subcycles=4, graph=True, fused=True, **prm)
+    b = PicLoop(to_dev(x), to_dev(v), to_dev(cell), g, E=to_dev(E), subcycles=4, graph=True, fused=False, **prm)
+    for _ in range(2):
+        a.field_step()
+        b.field_step()
+    torch.cuda.synchronize()
+    for p_, q_ in zip(a.state, b.state):
+        assert torch.equal(p_, q_)
