@@ -24,7 +24,8 @@ def stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or stale():
         os.makedirs(os.path.dirname(OUT), exist_ok=True)
-        cmd = [NVCC, *FLAGS, "-o", OUT, *SOURCES, "-lnccl"]
+        # CC_NVCC_EXTRA: extra -D switches for design studies (tools/collide_shape.sh); unset in product builds
+        cmd = [NVCC, *FLAGS, *os.environ.get("CC_NVCC_EXTRA", "").split(), "-o", OUT, *SOURCES, "-lnccl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)

@@ -46,14 +46,22 @@ constexpr int kScatterUnrollA = 16;      // cell loads in flight per lane, count
 constexpr int kScatterUnrollB = 6;       // (cell, v) loads in flight per lane, scatter pass
 // k_collide_large shape (tools/collide_shape.sh overrides them for design studies)
 #ifndef CC_COLLIDE_THREADS
-#define CC_COLLIDE_THREADS 192
+#define CC_COLLIDE_THREADS 128
 #endif
 #ifndef CC_CHUNK
-#define CC_CHUNK 576
+#define CC_CHUNK 384
 #endif
 #ifndef CC_COLLIDE_CTAS
-#define CC_COLLIDE_CTAS 4
+#define CC_COLLIDE_CTAS 6
 #endif
+// unroll factors of k_collide_large's phase-1 (Feistel + gathers) and phase-2b (TA + stores) item loops
+#ifndef CC_P1_UNROLL
+#define CC_P1_UNROLL 1
+#endif
+#ifndef CC_P2B_UNROLL
+#define CC_P2B_UNROLL 3
+#endif
+constexpr int kP1Unroll = CC_P1_UNROLL, kP2BUnroll = CC_P2B_UNROLL;
 constexpr int kCollideThreads = CC_COLLIDE_THREADS;
 constexpr int kChunk = CC_CHUNK;         // items (pairs or sitter) per k_collide_large CTA
 constexpr int kRec = 8;                  // chunk moment record: S1' (3), S2' (3), pad
@@ -843,7 +851,7 @@ k_collide_large(CollideArgs A)
     // (rare cycle walks afterwards), gathers issued item by item
     {
         const cc::Feistel f = cc::make_feistel(static_cast<uint32_t>(N), A.keys[j]);
-#pragma unroll
+#pragma unroll kP1Unroll
         for (int q = 0; q < kItemsPerThread; ++q) {
             const uint32_t k = i0 + threadIdx.x + q * kCollideThreads;
             if (k < i1) {
@@ -902,7 +910,7 @@ k_collide_large(CollideArgs A)
     // phase 2b: CCS5 TA update out of shared memory, pair-ordered coalesced output
     Acc acc;
     acc.zero();
-#pragma unroll
+#pragma unroll kP2BUnroll
     for (int t = 0; t < kItemsPerThread; ++t) {
         const uint32_t k = i0 + threadIdx.x + t * kCollideThreads;
         if (k < i1 && !(triplet && k + 2 >= items)) {     // the triplet's two items: k_triplets
