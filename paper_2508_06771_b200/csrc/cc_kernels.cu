@@ -42,8 +42,21 @@ constexpr int kCountThreads = 256;
 #define CC_SUB 4096
 #endif
 constexpr int kSub = CC_SUB;             // elements per warp sub-range in k_scatter
-constexpr int kScatterUnrollA = 16;      // cell loads in flight per lane, counting pass
-constexpr int kScatterUnrollB = 6;       // (cell, v) loads in flight per lane, scatter pass
+// k_scatter shape (design-study knobs, tools/scatter_shape.sh)
+#ifndef CC_SCATTER_UA
+#define CC_SCATTER_UA 16
+#endif
+#ifndef CC_SCATTER_UB
+#define CC_SCATTER_UB 4
+#endif
+#ifndef CC_SCATTER_BUDGET_KB
+#define CC_SCATTER_BUDGET_KB 96
+#endif
+#ifndef CC_SCATTER_CTAS
+#define CC_SCATTER_CTAS 2
+#endif
+constexpr int kScatterUnrollA = CC_SCATTER_UA;   // cell loads in flight per lane, counting pass
+constexpr int kScatterUnrollB = CC_SCATTER_UB;   // (cell, v) loads in flight per lane, scatter pass
 // k_collide_large shape (tools/collide_shape.sh overrides them for design studies)
 #ifndef CC_COLLIDE_THREADS
 #define CC_COLLIDE_THREADS 128
@@ -68,8 +81,11 @@ constexpr int kRec = 8;                  // chunk moment record: S1' (3), S2' (3
 constexpr int kSmallRec = 12;            // small-cell record: S1', S2' about the exact mean, the mean (3), pad
 constexpr int kCellSum = 4;              // per-cell raw post-collision sums: v (3), |v|^2
 constexpr int kTileSum = 4;              // per-tile raw pre-collision sums of live particles: v (3), |v|^2
-constexpr int kScatterSmemBudget = 96 * 1024;   // per-warp counters of one CTA
-constexpr int kMaxScatterWarps = 12;
+constexpr int kScatterSmemBudget = CC_SCATTER_BUDGET_KB * 1024;   // per-warp counters of one CTA
+#ifndef CC_SCATTER_MAXW
+#define CC_SCATTER_MAXW 12
+#endif
+constexpr int kMaxScatterWarps = CC_SCATTER_MAXW;
 static_assert(kMaxScatterWarps * kSub <= 65536, "per-warp 16-bit cell counters must hold a whole tile");
 
 // ------------------------------------------------------------------ layout
@@ -389,7 +405,7 @@ __device__ __forceinline__ void load_batch(const double* __restrict__ v, int64_t
 }
 
 template <bool HAS_V>
-__global__ void __launch_bounds__(32 * kMaxScatterWarps, 2)
+__global__ void __launch_bounds__(32 * kMaxScatterWarps, CC_SCATTER_CTAS)
 k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__ cell, int n, int M,
           int W, int sub, const int32_t* __restrict__ tbase, const int32_t* __restrict__ off,
           double* __restrict__ wsv, const int32_t* __restrict__ flags, double* __restrict__ tilesum)
