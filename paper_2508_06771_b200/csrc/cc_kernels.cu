@@ -59,13 +59,13 @@ constexpr int kScatterUnrollA = CC_SCATTER_UA;   // cell loads in flight per lan
 constexpr int kScatterUnrollB = CC_SCATTER_UB;   // (cell, v) loads in flight per lane, scatter pass
 // k_collide_large shape (tools/collide_shape.sh overrides them for design studies)
 #ifndef CC_COLLIDE_THREADS
-#define CC_COLLIDE_THREADS 128
+#define CC_COLLIDE_THREADS 64
 #endif
 #ifndef CC_CHUNK
-#define CC_CHUNK 384
+#define CC_CHUNK 192
 #endif
 #ifndef CC_COLLIDE_CTAS
-#define CC_COLLIDE_CTAS 6
+#define CC_COLLIDE_CTAS 12
 #endif
 // unroll factors of k_collide_large's phase-1 (Feistel + gathers) and phase-2b (TA + stores) item loops
 #ifndef CC_P1_UNROLL
@@ -1067,11 +1067,24 @@ __global__ void k_finalize_cells(const int32_t* __restrict__ cnt, const int32_t*
                                  const double* __restrict__ cellref, const double* __restrict__ trec, int M,
                                  MomConst mc, double* __restrict__ moments_out, double* __restrict__ cellsum)
 {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    // warp per cell: the lanes add the cell's chunk records in a fixed strided order, then a
+    // fixed shuffle tree (deterministic); lane 0 finishes the cell
+    const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (j >= M) return;
     const int32_t N = cnt[j];
     double s[6] = {0, 0, 0, 0, 0, 0};
     double rx = 0, ry = 0, rz = 0;
+    if (N > cc::kSmallCell) {
+        for (int32_t c = chunk_off[j] + lane; c < chunk_off[j + 1]; c += 32)
+#pragma unroll
+            for (int q = 0; q < 6; ++q) s[q] += recs[static_cast<int64_t>(c) * kRec + q];
+#pragma unroll
+        for (int q = 0; q < 6; ++q)
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) s[q] += __shfl_down_sync(0xFFFFFFFFu, s[q], d);
+    }
+    if (lane != 0) return;
     if (N > 0) {
         if (N <= cc::kSmallCell) {
             const double* r = small_recs + static_cast<int64_t>(j) * kSmallRec;
@@ -1081,9 +1094,6 @@ __global__ void k_finalize_cells(const int32_t* __restrict__ cnt, const int32_t*
         } else {
             const double* cr = cellref + 4 * static_cast<int64_t>(j);
             rx = cr[0]; ry = cr[1]; rz = cr[2];
-            for (int32_t c = chunk_off[j]; c < chunk_off[j + 1]; ++c)
-#pragma unroll
-                for (int q = 0; q < 6; ++q) s[q] += recs[static_cast<int64_t>(c) * kRec + q];
             if (trec)
 #pragma unroll
                 for (int q = 0; q < 6; ++q) s[q] += trec[static_cast<int64_t>(j) * kRec + q];
@@ -1827,7 +1837,7 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     MomConst mc{p.weight, p.cell_volume, p.cell_volume_arr, p.mass / p.charge};
     double* cellsum = at<double>(workspace, L.o_cellsum);
     mark(ev, 4, st);
-    k_finalize_cells<<<(M + 255) / 256, 256, 0, st>>>(A.cnt, A.chunk_off, A.recs, A.small_recs, A.cellref,
+    k_finalize_cells<<<(M + 7) / 8, 256, 0, st>>>(A.cnt, A.chunk_off, A.recs, A.small_recs, A.cellref,
                                                       (A.model & CC_ODD_TRIPLET) ? A.trec : nullptr, M, mc,
                                                       moments_out, cellsum);
     if (diag_out)
