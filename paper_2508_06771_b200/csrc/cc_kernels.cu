@@ -113,7 +113,7 @@ Layout make_layout(int64_t n, int32_t M)
     L.W = scatter_warps(M);
     // small inputs: shorter warp sub-ranges and collide chunks so that the binning tiles and the
     // collide CTAs still fill the GPU (C2/C3-sized calls); C4-sized calls keep kSub / kChunk
-    constexpr int64_t kTargetTiles = 2 * 148 * 2, kTargetChunks = 4 * 148;
+    constexpr int64_t kTargetTiles = 2 * 148 * 2, kTargetChunks = CC_COLLIDE_CTAS * 148;
     while (L.sub > 256 && (n + static_cast<int64_t>(L.W) * L.sub - 1) / (static_cast<int64_t>(L.W) * L.sub) < kTargetTiles)
         L.sub /= 2;
     while (L.chunk > kCollideThreads && (n / 2) / L.chunk < kTargetChunks) L.chunk -= kCollideThreads;
