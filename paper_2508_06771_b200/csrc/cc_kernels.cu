@@ -37,7 +37,10 @@
 
 namespace {
 
-constexpr int kCountThreads = 256;
+#ifndef CC_COUNT_THREADS
+#define CC_COUNT_THREADS 256
+#endif
+constexpr int kCountThreads = CC_COUNT_THREADS;
 #ifndef CC_SUB
 #define CC_SUB 4096
 #endif
