@@ -367,17 +367,24 @@ __device__ __forceinline__ double langevin(double A, double* dL)
     return -(2.0 + em) * ie - ia;
 }
 
-// returns A; +inf means "no scattering" (s = 0), 0 means isotropic
-__device__ __forceinline__ double nanbu_A(double s)
+// Cheap cases of A(s): returns true and sets A (+inf: no scattering, s = 0; 0: isotropic;
+// 1/(1 - e^-s) when that exceeds 40); false when the Newton solve is needed, x = e^-s set.
+__device__ __forceinline__ bool nanbu_A_direct(double s, double& A, double& x)
 {
-    if (!(s > 0.0)) return __longlong_as_double(0x7FF0000000000000ll);
-    const double x = exp(-s);
-    if (x <= 0.0) return 0.0;
+    if (!(s > 0.0)) { A = __longlong_as_double(0x7FF0000000000000ll); return true; }
+    x = exp(-s);
+    if (x <= 0.0) { A = 0.0; return true; }
     const double omx = -expm1(-s);
-    if (omx < 1.0 / 40.0) return 1.0 / omx;
-    // Jedynak's (2015) inverse-Langevin approximation (<= 1.4% off) as the start; Newton is
-    // quadratic, so once a step is below 1e-9 A the remaining error is ~1e-18 A: stop there
-    // (the oracle iterates to a 1e-15 step from Cohen's start: the same root to ~1e-15).
+    if (omx < 1.0 / 40.0) { A = 1.0 / omx; return true; }
+    return false;
+}
+
+// Newton solve of coth A - 1/A = x.  Jedynak's (2015) inverse-Langevin approximation (<= 1.4%
+// off) as the start; Newton is quadratic, so once a step is below 1e-9 A the remaining error
+// is ~1e-18 A: stop there (the oracle iterates to a 1e-15 step from Cohen's start: the same
+// root to ~1e-15).
+__device__ __forceinline__ double nanbu_newton(double x)
+{
     double A = x * (3.0 - x * (2.6 - 0.7 * x)) / ((1.0 - x) * (1.0 + 0.1 * x));
     for (int it = 0; it < 60; ++it) {
         double dL;
@@ -388,21 +395,43 @@ __device__ __forceinline__ double nanbu_A(double s)
     return A;
 }
 
-__device__ __forceinline__ void nanbu_update(double& ax, double& ay, double& az, double& bx, double& by, double& bz,
-                                             double C, double u1, double u2)
+// returns A; +inf means "no scattering" (s = 0), 0 means isotropic
+__device__ __forceinline__ double nanbu_A(double s)
+{
+    double A, x;
+    return nanbu_A_direct(s, A, x) ? A : nanbu_newton(x);
+}
+
+// s = 2 <delta^2> = 2 C / |u|^3 of a pair (u = v_a - v_b); 0 for u = 0 (no scattering)
+__device__ __forceinline__ double nanbu_s(double ax, double ay, double az, double bx, double by, double bz, double C)
+{
+    const double ux = ax - bx, uy = ay - by, uz = az - bz;
+    if (ux == 0.0 && uy == 0.0 && uz == 0.0) return 0.0;
+    const double usq = fma(ux, ux, fma(uy, uy, uz * uz));
+    const double u = sqrt(usq);
+    return 2.0 * C / (usq * u);
+}
+
+// the Nanbu rotation for a given A (R20)
+__device__ __forceinline__ void nanbu_apply(double& ax, double& ay, double& az, double& bx, double& by, double& bz,
+                                            double A, double u1, double u2)
 {
     const double ux = ax - bx, uy = ay - by, uz = az - bz;
     if (ux == 0.0 && uy == 0.0 && uz == 0.0) return;
+    if (isinf(A)) return;
     const double usq = fma(ux, ux, fma(uy, uy, uz * uz));
     const double u = sqrt(usq);
-    const double s = 2.0 * C / (usq * u);
-    const double A = nanbu_A(s);
-    if (isinf(A)) return;
     // 1 - cos chi = -ln(u1 + (1-u1) e^{-2A}) / A = -log1p((1-u1) expm1(-2A)) / A (no cancellation)
     double omc = (A == 0.0) ? 2.0 - 2.0 * u1 : -log1p((1.0 - u1) * expm1(-2.0 * A)) / A;
     omc = fmin(fmax(omc, 0.0), 2.0);
     const double sinT = sqrt(omc * (2.0 - omc));
     rotate_pair(ax, ay, az, bx, by, bz, ux, uy, uz, u, sinT, omc, u2);
+}
+
+__device__ __forceinline__ void nanbu_update(double& ax, double& ay, double& az, double& bx, double& by, double& bz,
+                                             double C, double u1, double u2)
+{
+    nanbu_apply(ax, ay, az, bx, by, bz, nanbu_A(nanbu_s(ax, ay, az, bx, by, bz, C)), u1, u2);
 }
 
 constexpr uint32_t kOddTriplet = 1u;   // CC_ODD_TRIPLET

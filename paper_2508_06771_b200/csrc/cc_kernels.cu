@@ -854,7 +854,8 @@ k_collide_large(CollideArgs A)
     extern __shared__ __align__(16) double stage[];       // [2][kChunk][4]
     __shared__ double zq[kCollideThreads / 32][kWarpItems];  // normal variate z = Phi^-1(u1) per item
     __shared__ double u2q[kCollideThreads / 32][kWarpItems]; // u2 per item
-    __shared__ int16_t tq[kCollideThreads / 32][kWarpItems]; // compacted AS241-tail items
+    __shared__ int16_t tq[kCollideThreads / 32][kWarpItems]; // compacted AS241-tail (Nanbu: Newton) items
+    __shared__ double aq[NANBU ? kCollideThreads / 32 : 1][NANBU ? kWarpItems : 1];  // Nanbu A per item
     __shared__ double red[kCollideThreads / 32][6];
     const int c = blockIdx.x;
     if (c >= A.chunk_off[A.M]) return;      // grid is an upper bound on the chunk count
@@ -927,6 +928,39 @@ k_collide_large(CollideArgs A)
     __syncthreads();
 
     // phase 2b: CCS5 TA update out of shared memory, pair-ordered coalesced output
+    if (NANBU) {
+        // Nanbu: A(s) of every pair first.  The cheap cases are set in place; pairs that need the
+        // inverse-Langevin Newton solve are compacted across the warp (tq, unused by Nanbu in
+        // phase 2a) and solved with all lanes busy, instead of each warp iterating for its
+        // slowest lane.  aq[slot] holds A (or x = e^-s until solved).
+        const uint32_t lt = (1u << lane) - 1u;
+        int qn = 0;
+#pragma unroll
+        for (int t = 0; t < kItemsPerThread; ++t) {
+            const uint32_t k = i0 + threadIdx.x + t * kCollideThreads;
+            const uint32_t e = k - i0;
+            const int slot = t * 32 + lane;
+            bool newton = false;
+            if (k < i1 && !(triplet && k + 2 >= items) && 2 * k + 1 < static_cast<uint32_t>(N)) {
+                const double2 a01 = *reinterpret_cast<const double2*>(stage + 4 * e);
+                const double az = stage[4 * e + 2];
+                const double2 b01 = *reinterpret_cast<const double2*>(stage + 4 * (kChunk + e));
+                const double bz = stage[4 * (kChunk + e) + 2];
+                double Av, x;
+                newton = !cc::nanbu_A_direct(cc::nanbu_s(a01.x, a01.y, az, b01.x, b01.y, bz, C), Av, x);
+                aq[w][slot] = newton ? x : Av;
+            }
+            const uint32_t nm = __ballot_sync(0xFFFFFFFFu, newton);
+            if (newton) tq[w][qn + __popc(nm & lt)] = static_cast<int16_t>(slot);
+            qn += __popc(nm);
+        }
+        __syncwarp();
+        for (int q = lane; q < qn; q += 32) {
+            const int slot = tq[w][q];
+            aq[w][slot] = cc::nanbu_newton(aq[w][slot]);
+        }
+        __syncwarp();
+    }
     Acc acc;
     acc.zero();
 #pragma unroll kP2BUnroll
@@ -948,7 +982,7 @@ k_collide_large(CollideArgs A)
                 }
                 const int slot = t * 32 + lane;
                 if (NANBU)
-                    cc::nanbu_update(a.x, a.y, a.z, b.x, b.y, b.z, C, zq[w][slot], u2q[w][slot]);
+                    cc::nanbu_apply(a.x, a.y, a.z, b.x, b.y, b.z, aq[w][slot], zq[w][slot], u2q[w][slot]);
                 else if (!(CC_ABLATE & 1))
                     cc::ta_update_z(a.x, a.y, a.z, b.x, b.y, b.z, C, zq[w][slot], u2q[w][slot]);
                 write_pair_out<PUSH>(A, pa, j, a, b);
