@@ -459,6 +459,9 @@ def run_ours(args):
         import torch.distributed as dist
         # NCCL: the library's own communicator (C ABI cc_dist_*); gloo smoke runs: torch collectives
         dist_ops = ccd.cuda_ops(ccd.NcclComm() if args.dist_backend == "nccl" else None)
+    if not torch.cuda.is_available():
+        sys.exit("bench.py: no CUDA device — the product path runs only on the GPU (no CPU fallback); "
+                 "`--impl reference` times the CPU oracle")
     local = local % torch.cuda.device_count()
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
