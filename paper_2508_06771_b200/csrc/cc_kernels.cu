@@ -327,23 +327,29 @@ k_scan_cells(const int32_t* __restrict__ cnt, int M, int32_t* __restrict__ off, 
     if (tid == nt - 1) { off[M] = ra; chunk_off[M] = rb; }
 }
 
-// Per-cell constants (thread per cell, many CTAs): TA constant C_j (R5-R7),
-// Feistel keys (R1, R3), and the chunk -> cell table of k_collide_large.
-__global__ void k_cell_setup(const int32_t* __restrict__ cnt, const int32_t* __restrict__ chunk_off, int M,
-                             int32_t* __restrict__ chunk_cell, double* __restrict__ Cj, cc::U4* __restrict__ keys,
-                             CellConst cc_, uint32_t cell_base, uint32_t step, uint32_t s0, uint32_t s1,
-                             const uint32_t* __restrict__ step_dev)
+// Per-cell constants (warp per cell, 8 cells per CTA): TA constant C_j (R5-R7),
+// Feistel keys (R1, R3) from lane 0, and the chunk -> cell table of
+// k_collide_large written by the whole warp (coalesced).
+__global__ void __launch_bounds__(256)
+k_cell_setup(const int32_t* __restrict__ cnt, const int32_t* __restrict__ chunk_off, int M,
+             int32_t* __restrict__ chunk_cell, double* __restrict__ Cj, cc::U4* __restrict__ keys,
+             CellConst cc_, uint32_t cell_base, uint32_t step, uint32_t s0, uint32_t s1,
+             const uint32_t* __restrict__ step_dev)
 {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
     if (j >= M) return;
-    const int32_t N = cnt[j];
-    const double V = cc_.volume_arr ? cc_.volume_arr[j] : cc_.volume;
-    const double lnL = cc_.ln_lambda_arr ? cc_.ln_lambda_arr[j] : cc_.ln_lambda;
-    const double nj = static_cast<double>(N) * cc_.weight / V;
-    Cj[j] = fmax(cc_.K * nj * lnL, 0.0);
-    if (step_dev) step += *step_dev;          // graph replay: effective step read on the device
-    keys[j] = cc::philox4x32_10(cc::U4{0u, cell_base + static_cast<uint32_t>(j), step, 1u}, s0, s1);
-    for (int32_t c = chunk_off[j]; c < chunk_off[j + 1]; ++c) chunk_cell[c] = j;
+    if (lane == 0) {
+        const int32_t N = cnt[j];
+        const double V = cc_.volume_arr ? cc_.volume_arr[j] : cc_.volume;
+        const double lnL = cc_.ln_lambda_arr ? cc_.ln_lambda_arr[j] : cc_.ln_lambda;
+        const double nj = static_cast<double>(N) * cc_.weight / V;
+        Cj[j] = fmax(cc_.K * nj * lnL, 0.0);
+        if (step_dev) step += *step_dev;          // graph replay: effective step read on the device
+        keys[j] = cc::philox4x32_10(cc::U4{0u, cell_base + static_cast<uint32_t>(j), step, 1u}, s0, s1);
+    }
+    const int32_t c1 = chunk_off[j + 1];
+    for (int32_t c = chunk_off[j] + lane; c < c1; c += 32) chunk_cell[c] = j;
 }
 
 // ------------------------------------------------------------------ CCS3: stable scatter
@@ -1168,6 +1174,8 @@ k_finalize_diag(const int32_t* __restrict__ cnt, const double* __restrict__ cell
     double s[12];
 #pragma unroll
     for (int q = 0; q < 12; ++q) s[q] = 0.0;
+    // unrolled so each thread's loads are in flight together (same per-thread summation order)
+#pragma unroll 4
     for (int j = threadIdx.x; j < M; j += blockDim.x) {
         const int32_t N = cnt[j];
         s[0] += N;
@@ -1176,6 +1184,7 @@ k_finalize_diag(const int32_t* __restrict__ cnt, const double* __restrict__ cell
 #pragma unroll
         for (int q = 0; q < 4; ++q) s[7 + q] += cellsum[static_cast<int64_t>(j) * kCellSum + q];
     }
+#pragma unroll 4
     for (int t = threadIdx.x; t < T; t += blockDim.x)
 #pragma unroll
         for (int q = 0; q < 4; ++q) s[3 + q] += tilesum[static_cast<int64_t>(t) * kTileSum + q];
@@ -1672,7 +1681,7 @@ int run_binning(const double* v_in, int64_t ldv, const int32_t* cell_in, int n, 
     mark(ev, 1, st);
     k_scan_tiles<<<(M1 + 31) / 32, dim3(32, kScanRows), 0, st>>>(tcount, L.T, M1, cnt);
     k_scan_cells<<<1, 1024, 0, st>>>(cnt, M, off, chunk_off, L.chunk);
-    k_cell_setup<<<(M + 255) / 256, 256, 0, st>>>(cnt, chunk_off, M, at<int32_t>(ws, L.o_chunkcell), Cj, keys, k,
+    k_cell_setup<<<(M + 7) / 8, 256, 0, st>>>(cnt, chunk_off, M, at<int32_t>(ws, L.o_chunkcell), Cj, keys, k,
                                                    cell_base, step, static_cast<uint32_t>(seed),
                                                    static_cast<uint32_t>(seed >> 32), step_dev);
     mark(ev, 2, st);
