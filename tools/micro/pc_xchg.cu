@@ -1,0 +1,380 @@
+// Prototype (round 2), design B: the cell exchange as a persistent producer /
+// consumer kernel through L2.  Work items (claimed in ticket order, P1 items run
+// ahead of P2 items by a window):
+//   P1(j, g): source segment g of cell j — load its slots' velocities (coalesced),
+//             p = pi^-1(s) (keyed Feistel, R1), counting-sort the records by
+//             destination segment d = p / S in shared memory, store them back
+//             contiguously into the scratch (the cell's own slot range) plus a
+//             row of K bucket offsets; then done[j] += 1.
+//   P2(j, d): wait done[j] == K; read sub-run d of every source segment (K short
+//             contiguous runs), place by p into shared memory, collide adjacent
+//             pairs, write the pair-ordered output (coalesced).
+// mode 0: identity (validated on the host); 1: Philox + AS241 + TA77.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o pc_xchg pc_xchg.cu
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "../../paper_2508_06771_b200/csrc/cc_device.cuh"
+
+#ifndef THR
+#define THR 256
+#endif
+#ifndef SMAX
+#define SMAX 2048
+#endif
+#ifndef OCC
+#define OCC 3
+#endif
+constexpr int kThr = THR;
+constexpr int kSmax = SMAX;           // records per segment
+constexpr int kKmax = 32;             // segments per cell -> N <= 65536
+constexpr int kB = 4;                 // records per thread per batch
+
+struct __align__(16) Sm {
+    double buf[4 * kSmax];            // P1: sort buffer; P2: placement stage
+    uint32_t ps[kSmax];               // P1: p of the segment's slots
+    int32_t cnt[kKmax + 1];
+    int32_t pre[kKmax + 1];
+    int32_t lo[kKmax];
+    int32_t prep[2 * kKmax];          // P2: sub-run starts, padded with INT_MAX
+    int32_t item;
+};
+
+__device__ __forceinline__ uint32_t feistel_Einv(const cc::Feistel& f, uint32_t y)
+{
+    const uint32_t amask = (1u << f.bL) - 1u;
+    uint32_t L = y & amask, R = y >> f.bL;
+#pragma unroll
+    for (int r = 7; r >= 0; --r) {
+        if ((r & 1) == 0) {
+            L ^= cc::fmix32_small(R, f.kp[r]) & amask;
+        } else {
+            const uint32_t t = __umulhi(cc::fmix32_small(L, f.kp[r]), f.m);
+            R = (R >= t) ? R - t : R + f.m - t;
+        }
+    }
+    return L + (R << f.bL);
+}
+
+__device__ __forceinline__ uint32_t feistel_pi_inv(const cc::Feistel& f, uint32_t s)
+{
+    uint32_t x = feistel_Einv(f, s);
+    while (x >= f.N) x = feistel_Einv(f, x);
+    return x;
+}
+
+__device__ __forceinline__ void seg_shape(int32_t N, int& K, int32_t& S)
+{
+    K = (N + kSmax - 1) / kSmax;
+    S = (N + K - 1) / K;
+    S = (S + 3) & ~3;
+}
+
+__device__ __forceinline__ void st_v4(double* p, double a, double b, double c, double d)
+{
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
+__device__ __forceinline__ void ld_v4_cg(const double* p, double& a, double& b, double& c, double& d)
+{
+    asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThr, OCC)
+k_pc(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__ off, const int32_t* __restrict__ segoff,
+     const int32_t* __restrict__ segcell, int M, int T, int Lw, double* __restrict__ vout, int32_t* __restrict__ cout, int32_t* __restrict__ pout,
+     double* __restrict__ scr, int32_t* __restrict__ hdr, int* __restrict__ done, int* __restrict__ ticket, double C,
+     double* __restrict__ sink)
+{
+    extern __shared__ __align__(16) unsigned char smraw[];
+    Sm& S_ = *reinterpret_cast<Sm*>(smraw);
+    const int tid = threadIdx.x, lane = tid & 31;
+    double accm = 0.0;
+    if (tid == 0) S_.item = atomicAdd(ticket, 1);
+    __syncthreads();
+    for (;;) {
+        const int t = S_.item;
+        __syncthreads();
+        if (tid == 0) S_.item = atomicAdd(ticket, 1);      // next item's ticket, in flight during this one
+        if (t >= 2 * T) break;
+        bool p1;
+        int idx;
+        if (t < Lw) { p1 = true; idx = t; }
+        else {
+            const int u = t - Lw;
+            if (u < 2 * (T - Lw)) { p1 = (u & 1) == 0; idx = p1 ? Lw + u / 2 : u / 2; }
+            else { p1 = false; idx = u - (T - Lw); }
+        }
+        const int j = __ldg(segcell + idx), g = idx - __ldg(segoff + j);
+        const int32_t o = off[j], N = off[j + 1] - o;
+        int K;
+        int32_t S;
+        seg_shape(N, K, S);
+        const int32_t s0 = g * S, Sg = min(S, N - s0);
+        if (p1) {
+            const cc::U4 keys = cc::philox4x32_10(cc::U4{0u, static_cast<uint32_t>(j), 7u, 1u}, 42u, 0u);
+            const cc::Feistel f = cc::make_feistel(static_cast<uint32_t>(N), keys);
+            if (tid <= kKmax) S_.cnt[tid] = 0;
+            if (tid < 3) {
+                const double* a0 = v + tid * ldv + o + s0;
+                const uintptr_t lo = reinterpret_cast<uintptr_t>(a0) & ~uintptr_t(15);
+                const uintptr_t hi = (reinterpret_cast<uintptr_t>(a0 + Sg) + 15) & ~uintptr_t(15);
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"(static_cast<uint32_t>(hi - lo)) : "memory");
+            }
+            __syncthreads();
+            // pass 1: p of my slots, histogram by destination segment
+            for (int32_t e = tid; e < Sg; e += kThr) {
+                const uint32_t p = feistel_pi_inv(f, static_cast<uint32_t>(s0 + e));
+                S_.ps[e] = p;
+                const uint32_t d = p / static_cast<uint32_t>(S);
+                const uint32_t peers = __match_any_sync(__activemask(), d);
+                if (lane == __ffs(peers) - 1) atomicAdd(&S_.cnt[d], __popc(peers));
+            }
+            __syncthreads();
+            if (tid < 32) {
+                const int32_t x = tid < K ? S_.cnt[tid] : 0;
+                int32_t s = x;
+#pragma unroll
+                for (int dd = 1; dd < 32; dd <<= 1) {
+                    const int32_t y = __shfl_up_sync(0xFFFFFFFFu, s, dd);
+                    if (tid >= dd) s += y;
+                }
+                if (tid < K) {
+                    S_.pre[tid] = s - x;                                  // bucket base (cursor)
+                    hdr[static_cast<int64_t>(idx) * (kKmax + 1) + tid] = s - x;
+                }
+                if (tid == 0) hdr[static_cast<int64_t>(idx) * (kKmax + 1) + K] = Sg;
+            }
+            __syncthreads();
+            // pass 2: records into the sort buffer at their bucket position (v loads batched)
+            for (int32_t e0 = 0; e0 < Sg; e0 += kThr * kB) {
+                double x[kB], y[kB], z[kB];
+                uint32_t pp[kB];
+#pragma unroll
+                for (int u = 0; u < kB; ++u) {
+                    const int32_t e = min(e0 + tid + u * kThr, Sg - 1);
+                    const int64_t i = o + s0 + e;
+                    x[u] = __ldg(v + i); y[u] = __ldg(v + ldv + i); z[u] = __ldg(v + 2 * ldv + i);
+                    pp[u] = S_.ps[e];
+                }
+#pragma unroll
+                for (int u = 0; u < kB; ++u) {
+                    const int32_t e = e0 + tid + u * kThr;
+                    if (e < Sg) {
+                        const uint32_t d = pp[u] / static_cast<uint32_t>(S);
+                        const int32_t r = atomicAdd(&S_.pre[d], 1);
+                        const double w = __longlong_as_double((static_cast<long long>(pp[u] - d * S) << 32) |
+                                                              static_cast<uint32_t>(o + s0 + e));
+                        double2* q = reinterpret_cast<double2*>(S_.buf + 4 * r);
+                        q[0] = make_double2(x[u], y[u]);
+                        q[1] = make_double2(z[u], w);
+                    }
+                }
+            }
+            __syncthreads();
+            for (int32_t e = tid; e < Sg; e += kThr) {
+                const double2 q0 = reinterpret_cast<const double2*>(S_.buf + 4 * e)[0];
+                const double2 q1 = reinterpret_cast<const double2*>(S_.buf + 4 * e)[1];
+                st_v4(scr + 4ll * (o + s0 + e), q0.x, q0.y, q1.x, q1.y);
+            }
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) atomicAdd(done + j, 1);
+        } else {
+            const int d = g;
+            if (tid == 0) {
+                while (true) {
+                    int x;
+                    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(x) : "l"(done + j) : "memory");
+                    if (x >= K) break;
+                    __nanosleep(200);
+                }
+            }
+            __syncthreads();
+            if (tid < 32) {
+                int32_t len = 0, l0 = 0;
+                if (tid < K) {
+                    const int32_t* h = hdr + static_cast<int64_t>(segoff[j] + tid) * (kKmax + 1);
+                    l0 = h[d];
+                    len = h[d + 1 < K ? d + 1 : K] - l0;
+                    if (d + 1 >= K) len = h[K] - l0;
+                }
+                int32_t s = len;
+#pragma unroll
+                for (int dd = 1; dd < 32; dd <<= 1) {
+                    const int32_t y = __shfl_up_sync(0xFFFFFFFFu, s, dd);
+                    if (tid >= dd) s += y;
+                }
+                if (tid < K) { S_.pre[tid] = s - len; S_.lo[tid] = l0; }
+                if (tid == K - 1) S_.pre[K] = s;
+                S_.prep[tid] = tid < K ? s - len : 0x7FFFFFFF;
+                S_.prep[tid + 32] = 0x7FFFFFFF;
+            }
+            __syncthreads();
+            const int32_t Sd = S_.pre[K];
+            for (int32_t e0 = 0; e0 < Sd; e0 += kThr * kB) {
+                double x[kB], y[kB], z[kB], w[kB];
+#pragma unroll
+                for (int u = 0; u < kB; ++u) {
+                    const int32_t e = min(e0 + tid + u * kThr, Sd - 1);
+                    int gg = 0;
+#pragma unroll
+                    for (int st = 16; st > 0; st >>= 1) gg += (S_.prep[gg + st] <= e) ? st : 0;
+                    const int64_t i = o + static_cast<int64_t>(gg) * S + S_.lo[gg] + (e - S_.pre[gg]);
+                    ld_v4_cg(scr + 4 * i, x[u], y[u], z[u], w[u]);
+                }
+#pragma unroll
+                for (int u = 0; u < kB; ++u) {
+                    if (e0 + tid + u * kThr < Sd) {
+                        const uint32_t pos = static_cast<uint32_t>(__double_as_longlong(w[u]) >> 32);
+                        double2* q = reinterpret_cast<double2*>(S_.buf + 4 * pos);
+                        q[0] = make_double2(x[u], y[u]);
+                        q[1] = make_double2(z[u], w[u]);
+                    }
+                }
+            }
+            __syncthreads();
+            const int32_t p0 = d * S;
+            for (int32_t k = tid; 2 * k < Sd; k += kThr) {
+                const int32_t pa = o + p0 + 2 * k;
+                const double2 a01 = *reinterpret_cast<const double2*>(S_.buf + 8 * k);
+                const double2 a23 = *reinterpret_cast<const double2*>(S_.buf + 8 * k + 2);
+                double ax = a01.x, ay = a01.y, az = a23.x;
+                const int32_t ia = static_cast<int32_t>(__double_as_longlong(a23.y));
+                if (2 * k + 1 < Sd) {
+                    const double2 b01 = *reinterpret_cast<const double2*>(S_.buf + 8 * k + 4);
+                    const double2 b23 = *reinterpret_cast<const double2*>(S_.buf + 8 * k + 6);
+                    double bx = b01.x, by = b01.y, bz = b23.x;
+                    const int32_t ib = static_cast<int32_t>(__double_as_longlong(b23.y));
+                    if (MODE == 1) {
+                        const cc::U4 r = cc::philox4x32_10(
+                            cc::U4{static_cast<uint32_t>(p0 / 2 + k), static_cast<uint32_t>(j), 7u, 0u}, 42u, 0u);
+                        cc::ta_update(ax, ay, az, bx, by, bz, C, cc::u01(r.x, r.y), cc::u01(r.z, r.w));
+                        accm += ax + bx + ay * ay + by * by;
+                    }
+                    *reinterpret_cast<double2*>(vout + pa) = make_double2(ax, bx);
+                    *reinterpret_cast<double2*>(vout + ldv + pa) = make_double2(ay, by);
+                    *reinterpret_cast<double2*>(vout + 2 * ldv + pa) = make_double2(az, bz);
+                    *reinterpret_cast<int2*>(cout + pa) = make_int2(j, j);
+                    *reinterpret_cast<int2*>(pout + pa) = make_int2(ia, ib);
+                } else {
+                    vout[pa] = ax; vout[ldv + pa] = ay; vout[2 * ldv + pa] = az;
+                    cout[pa] = j; pout[pa] = ia;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    if (accm == 1.2345) sink[0] = accm;
+}
+
+__global__ void k_stream(const double* __restrict__ v, int64_t ldv, int64_t n, double* __restrict__ vout,
+                         int32_t* __restrict__ cout, int32_t* __restrict__ pout)
+{
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        vout[i] = v[i]; vout[ldv + i] = v[ldv + i]; vout[2 * ldv + i] = v[2 * ldv + i];
+        cout[i] = 1; pout[i] = static_cast<int32_t>(i);
+    }
+}
+
+int main(int argc, char** argv)
+{
+    const int M = 4096, Nc = argc > 1 ? atoi(argv[1]) : 25000;
+    const int64_t n = static_cast<int64_t>(M) * Nc;
+    std::vector<double> hv(3 * n);
+    for (int64_t i = 0; i < 3 * n; ++i) hv[i] = static_cast<double>(i % 1000003) * 1.5 + 0.25;
+    std::vector<int32_t> hoff(M + 1), hseg(M + 1);
+    std::vector<int32_t> hsc;
+    int K = (Nc + kSmax - 1) / kSmax;
+    for (int j = 0; j <= M; ++j) { hoff[j] = j * Nc; hseg[j] = j * K; }
+    const int T = M * K;
+    for (int j = 0; j < M; ++j) for (int g = 0; g < K; ++g) hsc.push_back(j);
+    double *v, *vo, *scr, *sink;
+    int32_t *off, *seg, *co, *po, *hdr, *sc;
+    int *done, *ticket;
+    cudaMalloc(&v, 24 * n);
+    cudaMalloc(&vo, 24 * n);
+    cudaMalloc(&scr, 32 * n);
+    cudaMalloc(&co, 4 * n);
+    cudaMalloc(&po, 4 * n);
+    cudaMalloc(&off, 4 * (M + 1));
+    cudaMalloc(&seg, 4 * (M + 1));
+    cudaMalloc(&sc, 4 * T);
+    cudaMemcpy(sc, hsc.data(), 4 * T, cudaMemcpyHostToDevice);
+    cudaMalloc(&hdr, 4ll * T * (kKmax + 1));
+    cudaMalloc(&done, 4 * M);
+    cudaMalloc(&ticket, 4);
+    cudaMalloc(&sink, 8);
+    cudaMemcpy(v, hv.data(), 24 * n, cudaMemcpyHostToDevice);
+    cudaMemcpy(off, hoff.data(), 4 * (M + 1), cudaMemcpyHostToDevice);
+    cudaMemcpy(seg, hseg.data(), 4 * (M + 1), cudaMemcpyHostToDevice);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    const size_t smem = sizeof(Sm);
+    auto run = [&](auto kern, const char* name, bool check, int Lw) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThr, smem);
+        const int grid = occ * 148;
+        float best = 1e9;
+        for (int rep = 0; rep < 6; ++rep) {
+            cudaMemsetAsync(done, 0, 4 * M);
+            cudaMemsetAsync(ticket, 0, 4);
+            cudaEventRecord(a);
+            kern<<<grid, kThr, smem>>>(v, n, off, seg, sc, M, T, Lw, vo, co, po, scr, hdr, done, ticket, 1e-3, sink);
+            cudaEventRecord(b);
+            cudaEventSynchronize(b);
+            float ms;
+            cudaEventElapsedTime(&ms, a, b);
+            if (rep > 0) best = std::min(best, ms);
+        }
+        printf("%-34s occ %d Lw %5d  %.3f ms  %.1f GB/s (56 B/particle)  err=%s\n", name, occ, Lw, best,
+               56.0 * n / best / 1e6, cudaGetErrorString(cudaGetLastError()));
+        if (check) {
+            std::vector<double> ho(3 * n);
+            std::vector<int32_t> hp(n);
+            cudaMemcpy(ho.data(), vo, 24 * n, cudaMemcpyDeviceToHost);
+            cudaMemcpy(hp.data(), po, 4 * n, cudaMemcpyDeviceToHost);
+            long bad = 0;
+            for (int j = 0; j < M; j += 97) {
+                std::vector<char> seen(Nc, 0);
+                for (int p = 0; p < Nc; ++p) {
+                    const int64_t q = static_cast<int64_t>(j) * Nc + p;
+                    const int32_t i = hp[q];
+                    if (i < j * Nc || i >= (j + 1) * Nc || seen[i - j * Nc]) { ++bad; continue; }
+                    seen[i - j * Nc] = 1;
+                    for (int c = 0; c < 3; ++c) bad += ho[c * n + q] != hv[c * n + i];
+                }
+            }
+            printf("  check: %ld mismatches\n", bad);
+        }
+    };
+    if (argc > 2) {       // profiling: one config
+        if (atoi(argv[2]) == 0) run(k_pc<0>, "producer/consumer, identity", false, 256);
+        else run(k_pc<1>, "producer/consumer + TA", false, 256);
+        return 0;
+    }
+    run(k_pc<0>, "producer/consumer, identity", true, 64);
+    for (int Lw : {64, 256, 1024}) run(k_pc<0>, "producer/consumer, identity", false, Lw);
+    for (int Lw : {64, 256, 1024}) run(k_pc<1>, "producer/consumer + TA", false, Lw);
+    float best = 1e9;
+    for (int rep = 0; rep < 6; ++rep) {
+        cudaEventRecord(a);
+        k_stream<<<148 * 8, 256>>>(v, n, n, vo, co, po);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        if (rep > 0) best = std::min(best, ms);
+    }
+    printf("%-34s %.3f ms  %.1f GB/s\n", "streaming floor (24 B in, 32 B out)", best, 56.0 * n / best / 1e6);
+    return 0;
+}
