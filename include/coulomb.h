@@ -330,7 +330,9 @@ int cc_push(const double *x_in, int64_t ldx_in, const int32_t *perm, double *x_o
  *  RS5 (R28) the primary dies: cell -1 (velocity kept).
  * stats_out DEVICE uint64 [3] = {recombined, starved, primaries} (overwritten).
  * Must be called on an unmodified coulomb_collide output (it locates cells by
- * binary search in cell_out).  Bit-exact with the oracle.                  */
+ * binary search in cell_out; ids must lie in [-1, cells)).  Kills are written
+ * as order-preserving markers and turned into -1 by a second kernel, so no
+ * search ever sees a half-updated array.  Bit-exact with the oracle.        */
 int cc_recombine(double *v, int64_t ldv, int32_t *cell, int64_t n, int32_t cells, uint32_t cell_base,
                  const double *prob, double eps_bind, double mass, uint64_t seed, uint64_t step,
                  unsigned long long *stats_out, void *stream);

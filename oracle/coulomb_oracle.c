@@ -728,8 +728,9 @@ int or_num_threads(void)
  * x' = x + dt v'" with E the per-cell constant field retrieved by cell id
  * (S:207); boundary (Table 3 CS7): a particle leaving an
  * absorbing axis dies; cell assignment j = floor(x/dx).  Readings
- * R22-R24 of DESIGN.md §3: periodic axes wrap (repeated add/subtract of
- * L = n_a d_a), i_a = floor(x_a / d_a) clamped to n_a - 1 (x just below L
+ * R22-R24 of DESIGN.md §3: periodic axes wrap (add/subtract of L = n_a d_a;
+ * beyond one period first the exact remainder fmod(x, L); a non-finite
+ * position is absorbed), i_a = floor(x_a / d_a) clamped to n_a - 1 (x just below L
  * can divide to n_a), global cell = i_0 + n_0 (i_1 + n_1 i_2).
  *
  * Particle p (output order of the collision call): x_in row a < dims at
@@ -766,7 +767,12 @@ void or_push(const double *x_in, int64_t ldx_in, const int64_t *perm, double *x_
             if (a < dims) {
                 double xa = x[a] + dt * vn[a];
                 const double L = (double)nc[a] * d[a];
-                if (periodic & (1u << a)) {
+                if (!isfinite(xa)) {
+                    alive = 0;                  /* R23: a non-finite position is absorbed */
+                } else if (periodic & (1u << a)) {
+                    /* R23: more than one period away -> the exact remainder first, so the
+                       wrap below is at most one add or subtract */
+                    if (xa < -L || xa >= 2.0 * L) xa = fmod(xa, L);
                     while (xa < 0.0) xa = xa + L;
                     while (xa >= L) xa = xa - L;
                 } else if (xa < 0.0 || xa >= L) {

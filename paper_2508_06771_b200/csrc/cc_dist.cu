@@ -69,11 +69,14 @@ int cc_dist_alltoall_counts(const int64_t* send_counts, int64_t* recv_counts, vo
     if (ncclCommCount(c, &nranks) != ncclSuccess) return CC_ENCCL;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (ncclGroupStart() != ncclSuccess) return CC_ENCCL;
-    for (int p = 0; p < nranks; ++p) {
-        ncclSend(send_counts + p, 1, ncclInt64, p, c, st);
-        ncclRecv(recv_counts + p, 1, ncclInt64, p, c, st);
+    ncclResult_t r = ncclSuccess;
+    for (int p = 0; p < nranks && r == ncclSuccess; ++p) {
+        r = ncclSend(send_counts + p, 1, ncclInt64, p, c, st);
+        if (r == ncclSuccess) r = ncclRecv(recv_counts + p, 1, ncclInt64, p, c, st);
     }
-    return nccl_ok(ncclGroupEnd());
+    // the group is always closed; a failed post aborts it (no half-posted peer set)
+    const ncclResult_t e = ncclGroupEnd();
+    return (r == ncclSuccess && e == ncclSuccess) ? CC_OK : CC_ENCCL;
 }
 
 int cc_dist_exchange(const void* send, int64_t lds, void* recv, int64_t ldr, int32_t nrows, int32_t elem_bytes,
@@ -90,14 +93,16 @@ int cc_dist_exchange(const void* send, int64_t lds, void* recv, int64_t ldr, int
     char* r = static_cast<char*>(recv);
     const size_t eb = static_cast<size_t>(elem_bytes);
     if (ncclGroupStart() != ncclSuccess) return CC_ENCCL;
-    for (int32_t row = 0; row < nrows; ++row)
-        for (int p = 0; p < nranks; ++p) {
+    ncclResult_t res = ncclSuccess;
+    for (int32_t row = 0; row < nrows && res == ncclSuccess; ++row)
+        for (int p = 0; p < nranks && res == ncclSuccess; ++p) {
             const size_t ns = static_cast<size_t>(send_off[p + 1] - send_off[p]);
             const size_t nr = static_cast<size_t>(recv_off[p + 1] - recv_off[p]);
-            if (ns) ncclSend(s + (row * lds + send_off[p]) * eb, ns * eb, ncclUint8, p, c, st);
-            if (nr) ncclRecv(r + (row * ldr + recv_off[p]) * eb, nr * eb, ncclUint8, p, c, st);
+            if (ns) res = ncclSend(s + (row * lds + send_off[p]) * eb, ns * eb, ncclUint8, p, c, st);
+            if (nr && res == ncclSuccess) res = ncclRecv(r + (row * ldr + recv_off[p]) * eb, nr * eb, ncclUint8, p, c, st);
         }
-    return nccl_ok(ncclGroupEnd());
+    const ncclResult_t e = ncclGroupEnd();
+    return (res == ncclSuccess && e == ncclSuccess) ? CC_OK : CC_ENCCL;
 }
 
 }  // extern "C"

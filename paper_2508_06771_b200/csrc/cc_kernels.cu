@@ -550,7 +550,12 @@ __device__ __forceinline__ double drift_axis(const PushGrid& g, int a, double x,
 {
     double xa = __dadd_rn(x, __dmul_rn(dt, v));
     const double L = g.L[a];
-    if (g.periodic & (1u << a)) {
+    if (!isfinite(xa)) {
+        alive = false;                          // R23: a non-finite position is absorbed
+    } else if (g.periodic & (1u << a)) {
+        // R23: more than one period away -> the exact remainder (fmod is exact), so each
+        // loop below runs at most once (no unbounded wrap)
+        if (xa < -L || xa >= 2.0 * L) xa = fmod(xa, L);
         while (xa < 0.0) xa = __dadd_rn(xa, L);
         while (xa >= L) xa = __dsub_rn(xa, L);
     } else if (xa < 0.0 || xa >= L) {
@@ -1441,7 +1446,16 @@ __device__ __forceinline__ bool rc_primary(int32_t q, uint32_t G, uint32_t step,
     return cc::u01(x.x, x.y) < prob;
 }
 
-__device__ __forceinline__ int32_t rc_key(int32_t c, int M) { return (c < 0 || c >= M) ? M : c; }
+// Search key of a slot of the cell-sorted collision output.  A primary killed by this
+// call is first marked -2 - j (not -1): the marker keeps the key j, so the binary
+// searches of CTAs that start later still see a sorted array (writing -1
+// directly let a late CTA's search land on a killed slot of a lower cell).
+// k_recombine_finish turns the markers into -1 after every CTA is done.
+__device__ __forceinline__ int32_t rc_key(int32_t c, int M)
+{
+    if (c <= -2) return -2 - c;
+    return (c < 0 || c >= M) ? M : c;
+}
 
 __global__ void __launch_bounds__(256)
 k_recombine(double* __restrict__ v, int64_t ldv, int32_t* __restrict__ cell, int64_t n, int M, uint32_t cell_base,
@@ -1510,7 +1524,7 @@ k_recombine(double* __restrict__ v, int64_t ldv, int32_t* __restrict__ cell, int
             if (s2 == 0.0) { ux = 1.0; uy = 0.0; uz = 0.0; s2 = 1.0; }
             const double f = __dsqrt_rn(__ddiv_rn(t2, s2));
             v[c] = __dmul_rn(ux, f); v[ldv + c] = __dmul_rn(uy, f); v[2 * ldv + c] = __dmul_rn(uz, f);
-            cell[a] = -1;
+            cell[a] = -2 - j;             // dead, marker keeps the sort key (rc_key)
         }
     }
     if (threadIdx.x == 0) {
@@ -1518,6 +1532,14 @@ k_recombine(double* __restrict__ v, int64_t ldv, int32_t* __restrict__ cell, int
         atomicAdd(stats + 1, static_cast<unsigned long long>(P - m));
         atomicAdd(stats + 2, static_cast<unsigned long long>(P));
     }
+}
+
+// second pass: the kill markers of k_recombine -> -1 (R28: dead)
+__global__ void k_recombine_finish(int32_t* __restrict__ cell, int64_t n)
+{
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        if (cell[i] <= -2) cell[i] = -1;
 }
 
 // ------------------------------------------------------------------ NEXT f2: push (S2b + S2c)
@@ -1710,6 +1732,33 @@ CellConst cell_const(const cc_params& p, double dt)
 
 bool finite_pos(double x) { return std::isfinite(x) && x > 0.0; }
 
+// Host-side argument checks of coulomb_collide (scalars and cc_params), shared with the
+// host-buffer entry so that it rejects bad arguments before enqueueing any copy.
+int check_call(const cc_params& p, int64_t n, int32_t cells, int64_t ldv, double dt, uint64_t step)
+{
+    if (n < 0 || cells < 1 || ldv < n || !(dt > 0.0) || step >= (1ull << 32)) return CC_EINVAL;
+    if (n >= (1ll << 31) || cells > CC_MAX_CELLS) return CC_ECOUNT;
+    if (!finite_pos(p.mass) || !finite_pos(p.charge) || !finite_pos(p.eps0) || !std::isfinite(p.weight) ||
+        p.weight < 0.0 || (!p.cell_volume_arr && !finite_pos(p.cell_volume)) ||
+        (!p.ln_lambda_arr && !std::isfinite(p.ln_lambda)) ||
+        (p.flags & ~(CC_ODD_TRIPLET | CC_NANBU | CC_PRESERVE_ORDER)) != 0)
+        return CC_EINVAL;
+    if (p.push) {                            // fused push (NEXT f2): same checks as cc_push
+        const cc_push_params& q = *p.push;
+        if (!q.grid || q.grid->dims < 1 || q.grid->dims > 3 || !std::isfinite(q.q_over_m) ||
+            (p.flags & CC_PRESERVE_ORDER) || (n > 0 && (!q.x_in || !q.x_out)) || q.ldx_in < n || q.ldx_out < n ||
+            (q.E && q.ldE < cells))
+            return CC_EINVAL;
+        int64_t total = 1;
+        for (int a = 0; a < q.grid->dims; ++a) {
+            if (q.grid->n[a] < 1 || !finite_pos(q.grid->d[a])) return CC_EINVAL;
+            total *= q.grid->n[a];
+        }
+        if (total >= (1ll << 31)) return CC_EINVAL;
+    }
+    return CC_OK;
+}
+
 }  // namespace
 
 // ====================================================================== C ABI
@@ -1756,25 +1805,7 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     cudaGetLastError();   // launch errors below are ours, not a stale earlier one
     cc_params p;
     if (params) p = *params; else cc_default_params(&p);
-    if (n < 0 || cells < 1 || ldv < n || !(dt > 0.0) || step >= (1ull << 32)) return CC_EINVAL;
-    if (n >= (1ll << 31) || cells > CC_MAX_CELLS) return CC_ECOUNT;
-    if (!finite_pos(p.mass) || !finite_pos(p.charge) || !finite_pos(p.eps0) || !std::isfinite(p.weight) ||
-        p.weight < 0.0 || (!p.cell_volume_arr && !finite_pos(p.cell_volume)) ||
-        (!p.ln_lambda_arr && !std::isfinite(p.ln_lambda)) || (p.flags & ~(CC_ODD_TRIPLET | CC_NANBU | CC_PRESERVE_ORDER)) != 0)
-        return CC_EINVAL;
-    if (p.push) {                            // fused push (NEXT f2): same checks as cc_push
-        const cc_push_params& q = *p.push;
-        if (!q.grid || q.grid->dims < 1 || q.grid->dims > 3 || !std::isfinite(q.q_over_m) ||
-            (p.flags & CC_PRESERVE_ORDER) || (n > 0 && (!q.x_in || !q.x_out)) || q.ldx_in < n || q.ldx_out < n ||
-            (q.E && q.ldE < cells))
-            return CC_EINVAL;
-        int64_t total = 1;
-        for (int a = 0; a < q.grid->dims; ++a) {
-            if (q.grid->n[a] < 1 || !finite_pos(q.grid->d[a])) return CC_EINVAL;
-            total *= q.grid->n[a];
-        }
-        if (total >= (1ll << 31)) return CC_EINVAL;
-    }
+    if (const int rc = check_call(p, n, cells, ldv, dt, step)) return rc;
     if (!workspace || !aligned(workspace, 256)) return CC_EWORKSPACE;
     const Layout L = make_layout(n, cells);
     if (workspace_bytes < L.total) return CC_EWORKSPACE;
@@ -1793,7 +1824,14 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     const size_t vbytes = sizeof(double) * static_cast<size_t>(2 * ldv + n);
     if (overlaps(v_in, vbytes, v_out, vbytes) || overlaps(cell_in, 4 * n, cell_out, 4 * n) ||
         overlaps(v_out, vbytes, cell_out, 4 * n) || (perm_out && overlaps(perm_out, 4 * n, v_out, vbytes)) ||
-        (perm_out && overlaps(perm_out, 4 * n, cell_out, 4 * n)) || overlaps(workspace, L.total, v_out, vbytes))
+        (perm_out && overlaps(perm_out, 4 * n, cell_out, 4 * n)))
+        return CC_EINVAL;
+    // the workspace is written by every kernel: it may overlap no input or output
+    if (overlaps(workspace, L.total, v_out, vbytes) || overlaps(workspace, L.total, v_in, vbytes) ||
+        overlaps(workspace, L.total, cell_in, 4 * n) || overlaps(workspace, L.total, cell_out, 4 * n) ||
+        (perm_out && overlaps(workspace, L.total, perm_out, 4 * n)) ||
+        (moments_out && overlaps(workspace, L.total, moments_out, sizeof(double) * CC_MOMENTS_LEN * cells)) ||
+        (diag_out && overlaps(workspace, L.total, diag_out, sizeof(double) * CC_DIAG_LEN)))
         return CC_EINVAL;
 
     const CellConst k = cell_const(p, dt);
@@ -1929,8 +1967,13 @@ int coulomb_collide_host(const double* h_v_in, int64_t ldv, const int32_t* h_cel
                          double* h_diag_out, void* dev_buffer, size_t dev_bytes, void* stream)
 {
     cudaGetLastError();   // launch errors below are ours, not a stale earlier one
-    if (n < 0 || cells < 1 || ldv < n) return CC_EINVAL;
-    if (n >= (1ll << 31) || cells > CC_MAX_CELLS) return CC_ECOUNT;
+    {
+        // every host-side argument error is reported before anything is enqueued (header contract)
+        cc_params p;
+        if (params) p = *params; else cc_default_params(&p);
+        if (p.push) return CC_EINVAL;      // the host entry has no device positions to push
+        if (const int rc = check_call(p, n, cells, ldv, dt, step)) return rc;
+    }
     if (n > 0 && (!h_v_in || !h_cell_in || !h_v_out)) return CC_EINVAL;
     const HostLayout H = host_layout(n, cells);
     if (!dev_buffer || !aligned(dev_buffer, 256) || dev_bytes < H.total) return CC_EWORKSPACE;
@@ -2201,6 +2244,7 @@ int cc_recombine(double* v, int64_t ldv, int32_t* cell, int64_t n, int32_t cells
     k_recombine<<<cells, 256, 0, st>>>(v, ldv, cell, n, cells, cell_base, prob, 2.0 * eps_bind / mass,
                                        static_cast<uint32_t>(step), static_cast<uint32_t>(seed),
                                        static_cast<uint32_t>(seed >> 32), stats_out);
+    k_recombine_finish<<<static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 8)), 256, 0, st>>>(cell, n);
     return launch_ok();
 }
 

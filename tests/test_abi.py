@@ -82,6 +82,18 @@ def test_next_row_entry_points_validate_arguments():
     assert L.cc_host_buffer_bytes(1000, 4) > L.cc_workspace_bytes(1000, 4)
     assert L.coulomb_collide_host(null, 10, null, null, null, null, 10, 0, 0, 1e-10, null, 0, 0, null, null,
                                   null, 0, null) == _lib.CC_EINVAL                      # cells < 1
+    # host entry: a bad dt / flag is reported before any copy is enqueued (here the device buffer is
+    # missing too: the argument error must win over CC_EWORKSPACE)
+    import numpy as np
+    hv, hc = np.zeros((3, 10)), np.zeros(10, np.int32)
+    ptr = lambda a: C.c_void_p(a.ctypes.data)  # noqa: E731
+    assert L.coulomb_collide_host(ptr(hv), 10, ptr(hc), ptr(hv), null, null, 10, 1, 0, -1.0, null, 0, 0, null,
+                                  null, null, 0, null) == _lib.CC_EINVAL                # dt <= 0
+    bad = _lib.CCParams()
+    L.cc_default_params(C.byref(bad))
+    bad.flags = 1 << 20
+    assert L.coulomb_collide_host(ptr(hv), 10, ptr(hc), ptr(hv), null, null, 10, 1, 0, 1e-10, C.byref(bad), 0, 0,
+                                  null, null, null, 0, null) == _lib.CC_EINVAL          # unknown flag
     assert L.cc_nccl_comm_init(null, 2, 0, null) == _lib.CC_EINVAL
     assert L.cc_dist_exchange(null, 0, null, 0, 1, 3, null, null, null, null) == _lib.CC_EINVAL   # elem 3
     assert L.cc_step_advance(null, 1, null) == _lib.CC_EINVAL

@@ -76,6 +76,25 @@ def test_push_without_field_and_perm(O):
     assert np.array_equal(gv.cpu().numpy(), v)
 
 
+@pytest.mark.parametrize("periodic", [1, 0])
+def test_push_far_wrap_and_non_finite(O, periodic):
+    """R23 edge cases: positions many periods away (exact remainder, no unbounded
+    wrap loop) and +-inf / NaN positions (absorbed) — bit-exact with the oracle, and the kernel
+    returns (a hang here would be the old unbounded while-loop)."""
+    L = 4.0
+    dx = np.array([0.125 + 3 * L, 0.125 + 2 ** 40 * L, -(3 * L) + 0.125, -(2 ** 40) * L + 0.125,
+                   np.inf, -np.inf, np.nan, 1e308, 0.3, -0.3])
+    n = dx.size
+    x = np.zeros((3, n)); x[0, 6:] = 1.0
+    v = np.zeros((3, n)); v[0] = dx
+    cell = np.zeros(n, np.int32)
+    gv, gc = to_dev(v), to_dev(cell)
+    gx = cc.cc_push(to_dev(x), gv, gc, cc.Grid(1, (4,), (1.0,), periodic), dt=1.0, cells=1)
+    ox, ov, oc = O.push(x, v, cell, dims=1, nc=[4], d=[1.0], periodic=periodic, dt=1.0)
+    assert np.array_equal(gc.cpu().numpy(), oc)
+    assert np.array_equal(gx.cpu().numpy()[0], ox[0], equal_nan=True)
+
+
 def test_push_rejects_bad_grid():
     t = torch.zeros((3, 4), dtype=torch.float64, device=DEV)
     c = torch.zeros(4, dtype=torch.int32, device=DEV)

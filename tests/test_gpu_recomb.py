@@ -31,7 +31,10 @@ def O():
 
 
 @pytest.mark.parametrize("n,M,pmax,dead", [(200_000, 300, 0.05, 0.01), (40_000, 2, 0.5, 0.0),
-                                          (30_000, 5000, 1.0, 0.02), (1, 1, 1.0, 0.0), (0, 3, 0.5, 0.0)])
+                                          (30_000, 5000, 1.0, 0.02), (1, 1, 1.0, 0.0), (0, 3, 0.5, 0.0),
+                                          # many more cells than resident CTAs, half the slots killed: late
+                                          # CTAs binary-search an array earlier CTAs are writing
+                                          (600_000, 40_000, 0.9, 0.0)])
 def test_recombine_bit_exact(O, n, M, pmax, dead):
     w = W.random_cells(n, M, seed=n + M, dead_frac=dead, skew=True)
     p = w.params()

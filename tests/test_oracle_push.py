@@ -84,6 +84,29 @@ def test_periodic_wrap_and_absorbing_exact():
     assert list(xo[0]) == [L + 0.125, -0.125, 2.25]      # absorbed particles keep the drifted x
 
 
+def test_far_wrap_and_non_finite():
+    """R23: positions many periods away wrap by the exact remainder (dyadic: x = 1/8 + k L lands on
+    1/8 for any k, also k ~ 1e12, where repeated subtraction would take 1e12 steps); +-inf and NaN
+    positions are absorbed (cell -1) on periodic and absorbing axes alike."""
+    dt = 1.0
+    L = 4.0
+    x0 = np.array([0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 1.0, 1.0])
+    dx = np.array([0.125 + 3 * L, 0.125 + 2 ** 40 * L, -(3 * L) + 0.125, -(2 ** 40) * L + 0.125,
+                   np.inf, -np.inf, np.nan, 1e308])
+    n = x0.size
+    x = np.zeros((3, n)); x[0] = x0
+    v = np.zeros((3, n)); v[0] = dx / dt
+    for per in (1, 0):
+        xo, _, co = oracle.push(x, v, np.zeros(n, np.int32), dims=1, nc=[4], d=[1.0], periodic=per, dt=dt)
+        if per:
+            assert list(xo[0, :4]) == [0.125] * 4 and list(co[:4]) == [0] * 4
+            # 1 + 1e308: finite, wrapped by the exact remainder into [0, L)
+            assert 0.0 <= xo[0, 7] < L and xo[0, 7] == np.fmod(1.0 + 1e308, L) + (L if np.fmod(1.0 + 1e308, L) < 0 else 0)
+        else:
+            assert list(co[:4]) == [-1] * 4
+        assert list(co[4:7]) == [-1, -1, -1]
+
+
 def test_dead_untouched_and_perm_gather():
     """Dead particles (cell -1) keep x and v and stay dead; x rows are read through perm."""
     rng = np.random.default_rng(3)
