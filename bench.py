@@ -7,14 +7,25 @@ JSON line on rank 0.  A "step" is one call of the whole hot path
 moments/diagnostics) on one batch of synthetic input resident in HBM.
 
 Workload (BASELINE.json configs[3], "C4"): 64 x 64 = 4096 cells x 25,000
-electrons = 1.024e8 e- per GPU, isotropic Maxwellian 2 eV, particle order
-randomly permuted (the paper stores particles unsorted) — every timed
-step bins the unsorted input from scratch ("cold").  Inputs are 2.87 GB, far
-larger than the 126 MB L2, so no flush is needed between steps.  For N > 1
-(torchrun) each rank owns a C5 shard: global cells [4096 r, 4096 (r+1)),
-its own data seed; cells never cross ranks, so the data path has no
-collective; NCCL all_gather carries only the 16-double diagnostics vector
-(summed in rank order on the device).  Weak scaling.
+electrons = 1.024e8 e- per GPU, isotropic Maxwellian 2 eV.  The headline is
+the steady state of a PIC loop: each step consumes the previous step's
+(cell-sorted, pair-ordered) output after a stand-in drift moved 2% of the
+electrons to a neighbour cell; the first step starts from a random particle
+order (the paper stores particles unsorted).  "cold" (the same randomly
+ordered input every step) and "warm" (sorted input, no drift) are reported
+beside it.  Inputs are 2.87 GB, far larger than the 126 MB L2, so no flush is
+needed between steps.  For N > 1 (torchrun) each rank owns a C5 shard: global
+cells [4096 r, 4096 (r+1)) of a 64 x 64N grid, its own data seed; the stand-in
+drift of SURVEY §8(e) moves particles of the shard's first and last cell rows
+across the shard boundary (p = 0.1), and the step includes their migration to
+the owning rank (NCCL) and the diagnostics reduction.  Weak scaling.
+
+Roofline accounting: the method's algorithmic bytes are 52 per
+particle (read v 24 + cell 4, write v 24); ``roofline`` divides them by the
+dominant kernel's event-timed duration, ``step_hbm`` by the whole step's.  The
+DRAM bytes ncu measured for the same kernels (profiles/traffic.json, stamped
+with the hash of the kernel sources; a stale file is refused) are reported
+beside them with their ratio to the algorithmic bytes.
 
 ``--impl reference`` times the CPU oracle (oracle/, as it stands) on the host
 cores instead, on a bounded sample of the same workload.
@@ -37,11 +48,34 @@ import numpy as np  # noqa: E402
 
 METRIC = "electron-electron pair collisions/sec (TA77 Coulomb operator step, fp64)"
 UNIT = "pair-collisions/s"
-# algorithmic bytes per particle (DESIGN.md §6): the method must read v (24 B)
-# and the cell id (4 B) and write v (24 B) once per step
-STEP_BYTES_PER_PARTICLE = 52
-# per-stage algorithmic bytes per particle (what each kernel's contract must move once)
-STAGE_BYTES = {"count": 4, "scatter": 4 + 24 + 32, "collide": 28 + 32}
+# algorithmic bytes per particle (SURVEY §8(d), DESIGN.md §6): the method must read v (24 B)
+# and the cell id (4 B) and write v (24 B) once per step — the per-unit figure of every roofline
+ALGO_BYTES = 52
+# SURVEY §8(d) design traffic per particle: cold (unsorted input) and warm (cell-sorted input)
+DESIGN_BYTES = {"cold": 112, "warm": 56}
+# what each kernel's own contract moves once per particle (informative, not the roofline)
+STAGE_CONTRACT_BYTES = {"count": 4, "scatter": 4 + 24 + 32, "collide": 28 + 32}
+KERNEL_SOURCES = ("paper_2508_06771_b200/csrc/cc_kernels.cu", "paper_2508_06771_b200/csrc/cc_device.cuh",
+                  "include/coulomb.h")
+
+
+def sources_sha() -> str:
+    """Hash of the kernel sources: stamps profiles/traffic.json so a capture of older kernels is refused."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in KERNEL_SOURCES:
+        h.update(open(os.path.join(ROOT, f), "rb").read())
+    return h.hexdigest()[:16]
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def parse():
@@ -216,7 +250,8 @@ def time_oracle_on(w, args):
         s1 = time.perf_counter() - t1
         per_config[name] = {"seconds": s1, "pair_collisions_per_s": float(rr.diag[2]) / s1}
     oracle.set_num_threads(cores)
-    return {"value": float(r.diag[2]) / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+    return {"value": float(r.diag[2]) / dt, "unit": UNIT, "cores": cores, "cpu_model": cpu_model(),
+            "nproc": os.cpu_count(), "kind": "oracle",
             "sample": f"the full C4 input ({w.n:.4g} e-, {int(r.diag[2])} pairs), 1 step, {dt:.1f} s wall",
             "seconds": dt, "configs": per_config}
 
@@ -247,7 +282,8 @@ def run_reference(args):
         "data": "synthetic",
         "config": {"workload": workload_name(args, 1) + f" — CPU oracle on a {cells}-cell sample per step",
                    "cells_per_step": cells, "electrons_per_step": w.n},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(), "cpu_model": cpu_model(),
+                         "nproc": os.cpu_count(), "kind": "oracle",
                          "sample": f"{cells} of {args.nx * args.ny} C4 cells ({w.n:.3g} e-) per step"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -552,11 +588,13 @@ def run_ours(args):
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
-        op_ms = statistics.mean(ev[s][0].elapsed_time(ev[s][nst + 1]) for s in range(K))
+        per = [ev[s][0].elapsed_time(ev[s][nst + 1]) for s in range(K)]
+        op_ms = statistics.mean(per)
         stages = {name: statistics.mean(ev[s][i].elapsed_time(ev[s][i + 1]) for s in range(K))
                   for i, name in enumerate(_lib.STAGE_NAMES)}
         assert cc.cc_device_status(ws) == 0
-        return {"ms": op_ms, "wall_ms": t0.elapsed_time(t1) / K, "stages": stages,
+        return {"ms": op_ms, "ms_median": statistics.median(per), "ms_min": min(per), "ms_max": max(per),
+                "wall_ms": t0.elapsed_time(t1) / K, "stages": stages,
                 "pairs": float(bufs[(W + K - 1) % 2].diag[2].item())}
 
     K, W = args.steps, args.warmup
@@ -640,44 +678,65 @@ def run_ours(args):
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
 
-    traffic = {}
-    try:      # DRAM bytes per launch from the committed ncu capture of this config (tools/traffic_from_ncu.py)
-        traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+    traffic, traffic_note = {}, None
+    try:      # DRAM bytes per launch from an ncu capture of these kernels (tools/traffic_from_ncu.py)
+        t = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        if t.get("sources_sha") == sources_sha():
+            traffic = t.get("kernels", {})
+        else:
+            traffic_note = "profiles/traffic.json was captured on other kernel sources: refused"
     except Exception:
-        pass
+        traffic_note = "no profiles/traffic.json"
     kernel_of = {"count": "k_count", "scatter": "k_scatter", "collide": "k_collide_large"}
 
     def roofline(r, with_traffic=False):
+        """ALGO_BYTES per particle x n over the dominant kernel's event-timed duration."""
         st = r["stages"]
         dom = max(("count", "scatter", "collide"), key=lambda k: st[k])
-        achieved = STAGE_BYTES[dom] * n / (st[dom] * 1e-3) / 1e9
+        achieved = ALGO_BYTES * n / (st[dom] * 1e-3) / 1e9
         tr = traffic.get(kernel_of[dom], {}).get("dram_bytes_per_launch") if (world == 1 and with_traffic) else None
-        return {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+        return {"kernel": kernel_of[dom], "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "traffic": tr,
-                "traffic_source": "profiles/traffic.json (ncu --set full, same config)" if tr else None,
-                "algorithmic_bytes_per_launch": STAGE_BYTES[dom] * n,
-                "algorithmic_bytes_per_particle": STAGE_BYTES[dom], "peak_source": peak_src}
+                "traffic_over_algorithmic": (tr / (ALGO_BYTES * n)) if tr else None,
+                "traffic_source": ("profiles/traffic.json (ncu --set full, same kernel sources, steady call)"
+                                   if tr else traffic_note),
+                "algorithmic_bytes_per_particle": ALGO_BYTES, "algorithmic_bytes_per_launch": ALGO_BYTES * n,
+                "kernel_contract_bytes_per_particle": STAGE_CONTRACT_BYTES[dom],
+                "kernel_contract_frac": STAGE_CONTRACT_BYTES[dom] * n / (st[dom] * 1e-3) / 1e9 / hbm_peak,
+                "kernel_ms": st[dom], "peak_source": peak_src}
 
     STEP_KERNELS = ("k_count", "k_scan_tiles", "k_scan_cells", "k_cell_setup", "k_scatter", "k_collide_small",
                     "k_collide_large", "k_copy_dead", "k_finalize_cells", "k_finalize_diag")
 
-    def step_achieved(ms):
-        """SURVEY §8(d) reading (1) of the NS target: ncu DRAM bytes of every kernel of one call
-        (profiles/traffic.json, captured on this config) over the call's time, against the peak;
-        guard: those bytes <= 1.15 x the design traffic (128 B/particle)."""
+    def step_hbm(ms):
+        """Whole step: algorithmic 52 B/particle over the step time (SURVEY §8(d) reading 2) and the DRAM
+        bytes ncu measured for every kernel of one steady call (reading 1), with SURVEY §8(d)'s
+        1.15 x design-traffic guard against its cold (112 B) and warm (56 B) designs."""
+        out = {"algorithmic_bytes_per_particle": ALGO_BYTES,
+               "frac": ALGO_BYTES * n / (ms * 1e-3) / 1e9 / hbm_peak,
+               "design_bytes_per_particle": DESIGN_BYTES}
         if world != 1 or not all(k in traffic for k in STEP_KERNELS):
-            return {"achieved_dram_frac": None}
+            out["achieved_dram_frac"] = None
+            out["traffic_note"] = traffic_note
+            return out
         b = sum(traffic[k]["dram_bytes_per_launch"] for k in STEP_KERNELS)
-        return {"achieved_dram_bytes_per_step": b, "achieved_dram_bytes_per_particle": b / n,
-                "achieved_dram_gbs": b / (ms * 1e-3) / 1e9,
-                "achieved_dram_frac": b / (ms * 1e-3) / 1e9 / hbm_peak,
-                "design_bytes_per_particle": 128, "guard_ok": b / n <= 1.15 * 128,
-                "source": "profiles/traffic.json (ncu dram__bytes_read/write.sum per kernel, one steady call)"}
+        out.update({"achieved_dram_bytes_per_particle": b / n,
+                    "traffic_over_algorithmic": b / (ALGO_BYTES * n),
+                    "achieved_dram_gbs": b / (ms * 1e-3) / 1e9,
+                    "achieved_dram_frac": b / (ms * 1e-3) / 1e9 / hbm_peak,
+                    "guard_1.15x_cold_design": b / n <= 1.15 * DESIGN_BYTES["cold"],
+                    "guard_1.15x_warm_design": b / n <= 1.15 * DESIGN_BYTES["warm"],
+                    "source": "profiles/traffic.json (ncu dram__bytes_read/write.sum per kernel, one steady call, "
+                              "same kernel sources)"})
+        return out
+
+    def timing(r):
+        return {"ms_mean": r["ms"], "ms_median": r["ms_median"], "ms_min": r["ms_min"], "ms_max": r["ms_max"]}
 
     def summary(r):
         return {"value": r["pairs"] / (r["ms"] * 1e-3), "ms_per_step": r["ms"], "wall_ms_per_step": r["wall_ms"],
-                "stages_ms": r["stages"], "roofline": roofline(r),
-                "step_hbm_frac": STEP_BYTES_PER_PARTICLE * n * world / (r["ms"] * 1e-3) / 1e9 / world / hbm_peak}
+                "timing": timing(r), "stages_ms": r["stages"], "roofline": roofline(r),
+                "step_hbm_frac": ALGO_BYTES * n / (r["ms"] * 1e-3) / 1e9 / hbm_peak}
 
     head = res["steady"]
     line = {
@@ -688,14 +747,14 @@ def run_ours(args):
                    f"step's output after a stand-in drift moves {100 * args.drift:g}% of the electrons to a "
                    f"neighbour cell (first step: randomly ordered input)",
                    "cells_per_gpu": M, "electrons_per_gpu": n, "pairs_per_step": head["pairs"],
-                   "l2": "inputs 2.87 GB/GPU >> 126 MB L2 (no flush needed)",
-                   "timing": "CUDA events around each operator call (drift excluded), mean of K",
+                   "l2": f"inputs {(w.v.nbytes + w.cell.nbytes) / 1e9:.2f} GB/GPU >> 126 MB L2 (no flush needed)",
+                   "timing": "CUDA events around each operator call (drift excluded); value = mean of K, "
+                             "median/min/max in timing",
                    "parallelism": f"cell-range shards x{world}" if world > 1 else "1 GPU"},
         "roofline": roofline(head, with_traffic=True),
+        "timing": timing(head),
         "stages_ms": head["stages"],
-        "step_hbm": {"algorithmic_bytes_per_particle": STEP_BYTES_PER_PARTICLE,
-                     "frac": STEP_BYTES_PER_PARTICLE * n / (head["ms"] * 1e-3) / 1e9 / hbm_peak,
-                     **step_achieved(head["ms"])},
+        "step_hbm": step_hbm(head["ms"]),
         "cold": dict(summary(res["cold"]), what="every step bins the same randomly ordered input"),
         "warm": dict(summary(res["warm"]), what="chained steps, no drift (input already cell-sorted)"),
         "e2e": {"value": res["cold"]["pairs"] / (e2e_ms * 1e-3), "unit": UNIT,

@@ -1683,6 +1683,7 @@ int run_binning(const double* v_in, int64_t ldv, const int32_t* cell_in, int n, 
                 cudaStream_t st, void* const* ev, bool allow_sorted_skip, const uint32_t* step_dev = nullptr)
 {
     int32_t* err = at<int32_t>(ws, L.o_err);
+    mark(ev, 0, st);                     // the timed region starts before the flag reset
     if (cudaMemsetAsync(err + 1, 0, sizeof(int32_t), st) != cudaSuccess) return CC_ECUDA;   // "unsorted" flag
     int32_t* tcount = at<int32_t>(ws, L.o_tcount);
     int32_t* cnt = at<int32_t>(ws, L.o_cnt);
@@ -1698,7 +1699,6 @@ int run_binning(const double* v_in, int64_t ldv, const int32_t* cell_in, int n, 
     if (!rc) rc = want_smem(k_scatter<false>, smem);
     if (rc) return rc;
     const int32_t* skip = allow_sorted_skip ? err : nullptr;
-    mark(ev, 0, st);
     k_count<<<L.T, kCountThreads, sizeof(int32_t) * M1, st>>>(cell_in, n, M, L.tile, tcount, err);
     mark(ev, 1, st);
     k_scan_tiles<<<(M1 + 31) / 32, dim3(32, kScanRows), 0, st>>>(tcount, L.T, M1, cnt);

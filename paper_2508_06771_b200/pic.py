@@ -12,9 +12,10 @@ that loop restricted to the path:
                      the previous output order), pairs, collides; its
                      per-cell moments are the P2C of the post-collision state
                 S2b+S2c the push: v += dt (q/m) E[cell], x += dt v, boundary, new
-                     cell id — fused into the collision call's output stage
-                     (cc_params.push, default) or as a separate cc_push reading
-                     the positions through perm_out (fused=False); same bits
+                     cell id — a separate cc_push reading the positions through
+                     perm_out (the default, fused=False: measured faster at C4,
+                     DESIGN §6) or fused into the collision call's output stage
+                     (cc_params.push, fused=True); same bits
   per field step     (every ``subcycles`` substeps) the lagged per-cell Coulomb
                      logarithm from the last moments (R21, cc_coulomb_log), fed to
                      the next substeps as ln_lambda_arr; E is held fixed (the PDE

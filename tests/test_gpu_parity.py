@@ -174,8 +174,8 @@ def test_collide_parity(O, n, M, dead, skew):
 
 @pytest.mark.parametrize("n,M,dead", [(50_000, 64, 0.0), (80_000, 300, 0.05), (10_000, 5000, 0.1)])
 def test_sorted_input_fast_path(O, n, M, dead):
-    """Cell-sorted input (dead last): k_scatter is skipped and the collide reads
-    the caller's SoA input directly; results must equal the oracle's."""
+    """Cell-sorted input (dead last): k_count flags it sorted, k_scatter packs the records in
+    place (the identity order, no ranking pass); results must equal the oracle's."""
     w = W.random_cells(n, M, seed=n + M + 1, dead_frac=dead, skew=True)
     key = np.where(w.cell < 0, M, w.cell)
     order = np.argsort(key, kind="stable")

@@ -34,7 +34,7 @@ def O():
                                           (30_000, 5000, 1.0, 0.02), (1, 1, 1.0, 0.0), (0, 3, 0.5, 0.0),
                                           # many more cells than resident CTAs, half the slots killed: late
                                           # CTAs binary-search an array earlier CTAs are writing
-                                          (600_000, 40_000, 0.9, 0.0)])
+                                          (600_000, 30_000, 0.9, 0.0)])
 def test_recombine_bit_exact(O, n, M, pmax, dead):
     w = W.random_cells(n, M, seed=n + M, dead_frac=dead, skew=True)
     p = w.params()

@@ -28,3 +28,9 @@ for w in $WHAT; do
     prof_collide_steady) timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_collide_large" -s 4 -c 1 -o gpurun_out/${TAG}_collide_steady python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/${TAG}_collide_steady.log 2>&1; echo prof_collide_steady rc=$? ;;
   esac
 done
+# DRAM bytes of every kernel of one steady call (the 4th call of bench.py's steady mode) -> profiles/traffic.json
+for w in $WHAT; do
+  case $w in
+    traffic) timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:"k_(count|scan|cell|scatter|collide|copy|finalize)" -s 30 -c 10 -o gpurun_out/${TAG}_step python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-pic --e2e-steps 1 > gpurun_out/${TAG}_step.log 2>&1; echo traffic rc=$? ;;
+  esac
+done

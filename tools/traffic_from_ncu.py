@@ -23,8 +23,12 @@ def main():
             name = r[ik].split("(")[0].split("::")[-1].split("<")[0].strip()
             b = float(r[ir]) * UNIT[units[ir]] + float(r[iw]) * UNIT[units[iw]]
             out[name] = {"dram_bytes_per_launch": b, "ncu_ms": float(r[it]), "report": os.path.basename(rep)}
-    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "traffic.json")
-    json.dump(out, open(path, "w"), indent=1)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import bench
+    path = os.path.join(root, "profiles", "traffic.json")
+    # stamped with the kernel sources' hash: bench.py refuses a capture of other kernels
+    json.dump({"sources_sha": bench.sources_sha(), "kernels": out}, open(path, "w"), indent=1)
     print(json.dumps(out, indent=1))
 
 
