@@ -172,10 +172,16 @@ __device__ __forceinline__ int32_t unpack_perm(double w)
 }
 
 // ------------------------------------------------------------------ CCS1: count
-// flags[0]: sticky invalid-id flag; flags[1]: "input not cell-sorted" (cleared
-// by the host before each call).  Sorted means live ids non-decreasing in input
-// order with every dead/invalid particle after the last live one; then the
-// stable order is the identity and k_scatter packs the records in place.
+// flags[0]: sticky invalid-id flag; flags[1]: "input not cell-sorted"; flags[2]:
+// number of adjacent descents (flags 1-2 cleared before each call).  Sorted means live ids non-decreasing in input order with
+// every dead/invalid particle after the last live one; then the stable order is
+// the identity and k_scatter packs the records in place.
+// Each thread takes 4 consecutive ids (one 16-byte load when the array is
+// 16-byte aligned); the order check uses the neighbour lane's last id (only
+// lane 0 reloads one id), and equal neighbours share one shared-memory atomic —
+// a warp whose 128 ids are one cell (sorted input) issues a single atomic.
+__device__ __forceinline__ int32_t count_key(int32_t c, int M) { return (c >= 0 && c < M) ? c : M; }
+
 __global__ void __launch_bounds__(kCountThreads)
 k_count(const int32_t* __restrict__ cell, int n, int M, int tile, int32_t* __restrict__ tcount,
         int32_t* __restrict__ flags)
@@ -185,24 +191,58 @@ k_count(const int32_t* __restrict__ cell, int n, int M, int tile, int32_t* __res
     __syncthreads();
     const int64_t start = static_cast<int64_t>(blockIdx.x) * tile;
     const int64_t end = min(start + tile, static_cast<int64_t>(n));
-    int bad = 0, unsorted = 0;
-    for (int64_t i = start + threadIdx.x; i < end; i += blockDim.x) {
-        const int32_t c = __ldg(cell + i);
-        const bool live = (c >= 0) && (c < M);
-        bad |= (!live && c != -1);
-        const int32_t key = live ? c : M;
-        if (i > 0) {
-            const int32_t cp = __ldg(cell + i - 1);
-            const int32_t kp = (cp >= 0 && cp < M) ? cp : M;
-            unsorted |= (key < kp);
+    const bool vec = (reinterpret_cast<uintptr_t>(cell) & 15u) == 0;     // start is a multiple of 4 (tile is)
+    const int lane = threadIdx.x & 31;
+    int bad = 0, descents = 0;
+    for (int64_t i = start + 4 * static_cast<int64_t>(threadIdx.x); i < end; i += 4 * static_cast<int64_t>(blockDim.x)) {
+        int32_t c[4];
+        if (vec && i + 3 < end) {
+            const int4 q = __ldg(reinterpret_cast<const int4*>(cell + i));
+            c[0] = q.x; c[1] = q.y; c[2] = q.z; c[3] = q.w;
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) c[u] = (i + u < end) ? __ldg(cell + i + u) : -1;
         }
-        atomicAdd(&hist[key], 1);
+        int32_t k[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const bool live = c[u] >= 0 && c[u] < M;
+            bad |= (i + u < end) && !live && c[u] != -1;
+            k[u] = (i + u < end) ? count_key(c[u], M) : M;
+        }
+        // predecessor of k[0]: the previous lane's k[3] (its 4 ids end at i - 1), lane 0 reloads id i - 1
+        const unsigned act = __activemask();
+        int32_t prev = __shfl_up_sync(act, k[3], 1);
+        if (lane == 0 || !((act >> (lane - 1)) & 1u)) prev = (i > 0) ? count_key(__ldg(cell + i - 1), M) : 0;
+        descents += (k[0] < prev) + (k[1] < k[0]) + (k[2] < k[1]) + (k[3] < k[2]);
+        const int nv = static_cast<int>(min(static_cast<int64_t>(4), end - i));
+        // runs of equal keys -> one atomic each; a warp of one key -> one atomic in total
+        const bool uni = (k[0] == k[3]) && (k[1] == k[0]) && (k[2] == k[0]) && nv == 4;
+        int32_t pk;
+        const unsigned same = __match_all_sync(act, uni ? k[0] : -1 - static_cast<int32_t>(lane), &pk);
+        if (same && uni) {
+            if (lane == __ffs(act) - 1) atomicAdd(&hist[k[0]], 4 * __popc(act));
+        } else {
+            int run = 1;
+#pragma unroll
+            for (int u = 1; u < 4; ++u) {
+                if (u < nv && k[u] == k[u - 1]) { ++run; continue; }
+                if (u < nv) { atomicAdd(&hist[k[u - 1]], run); run = 1; }
+            }
+            atomicAdd(&hist[k[nv - 1]], run);
+        }
     }
+    __shared__ int32_t s_desc;
+    if (threadIdx.x == 0) s_desc = 0;
     const int any_bad = __syncthreads_or(bad);
-    const int any_unsorted = __syncthreads_or(unsorted);
+    if (descents) atomicAdd(&s_desc, descents);
+    const int any_unsorted = __syncthreads_or(descents);
     if (threadIdx.x == 0) {
         if (any_bad) atomicOr(flags, 1);
-        if (any_unsorted) atomicOr(flags + 1, 1);
+        if (any_unsorted) {
+            atomicOr(flags + 1, 1);
+            atomicAdd(flags + 2, s_desc);            // disorder measure: adjacent descents
+        }
     }
     int32_t* row = tcount + static_cast<int64_t>(blockIdx.x) * (M + 1);
     for (int i = threadIdx.x; i <= M; i += blockDim.x) row[i] = hist[i];
@@ -352,6 +392,18 @@ k_cell_setup(const int32_t* __restrict__ cnt, const int32_t* __restrict__ chunk_
     for (int32_t c = chunk_off[j] + lane; c < c1; c += 32) chunk_cell[c] = j;
 }
 
+// Pair-order placement (R1 unchanged, layout only): when the input is far from cell-sorted
+// (more than n/8 adjacent descents: a randomly ordered input has ~n/2, the 2%-drift steady state
+// ~n/25), k_scatter's record writes land at random slots anyway, so it writes each particle of a
+// cell with N_j > 64 straight to its pair-order position off_j + pi_j^-1(rank) and the collide
+// reads both members of pair k from the adjacent records 2k, 2k+1 — a streaming read instead of
+// two random gathers.  Nearly sorted input keeps the stable layout (contiguous scatter writes) and
+// the gathers.  Both give the same pairs, randoms and results: only where the records sit differs.
+__device__ __forceinline__ bool pair_order_mode(const int32_t* flags, int n)
+{
+    return flags && flags[1] != 0 && static_cast<int64_t>(flags[2]) * 8 > n;
+}
+
 // ------------------------------------------------------------------ CCS3: stable scatter
 // Tile = W warps x kSub elements; warp w owns the contiguous sub-range w of the
 // tile, so "input order" = (tile, warp, step, lane).  Per-warp 16-bit counters
@@ -417,7 +469,8 @@ template <bool HAS_V>
 __global__ void __launch_bounds__(32 * kMaxScatterWarps, CC_SCATTER_CTAS)
 k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__ cell, int n, int M,
           int W, int sub, const int32_t* __restrict__ tbase, const int32_t* __restrict__ off,
-          double* __restrict__ wsv, const int32_t* __restrict__ flags, double* __restrict__ tilesum)
+          double* __restrict__ wsv, const int32_t* __restrict__ flags, double* __restrict__ tilesum,
+          const int32_t* __restrict__ cnt, const cc::U4* __restrict__ keys)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -498,6 +551,7 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
     __syncthreads();
 
     // pass B: ranks, destinations, 32-byte records (loads batched, branch-free)
+    const bool po = pair_order_mode(flags, n);
     for (int64_t i0 = s0; i0 < s1; i0 += 32 * kScatterUnrollB) {
         int32_t key[kScatterUnrollB];
         double x[kScatterUnrollB], y[kScatterUnrollB], z[kScatterUnrollB];
@@ -523,7 +577,16 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
             const uint32_t o = __shfl_sync(0xFFFFFFFFu, (old[u] >> ((max(b, 0) & 1) << 4)) & 0xFFFFu,
                                            __ffs(peers[u]) - 1);
             if (b >= 0) {
-                const int32_t dest = base[b] + static_cast<int32_t>(o) + __popc(peers[u] & lt);
+                int32_t dest = base[b] + static_cast<int32_t>(o) + __popc(peers[u] & lt);
+                if (po && b < M) {
+                    const int32_t N = __ldg(cnt + b);
+                    if (N > cc::kSmallCell) {
+                        const int32_t oc = __ldg(off + b);
+                        const cc::U4 kk = keys[b];
+                        const cc::Feistel f = cc::make_feistel(static_cast<uint32_t>(N), kk);
+                        dest = oc + static_cast<int32_t>(cc::feistel_pi_inv(f, static_cast<uint32_t>(dest - oc)));
+                    }
+                }
                 const int64_t i = i0 + 32 * u + lane;
                 st256(wsv + 4 * static_cast<int64_t>(dest), x[u], y[u], z[u],
                       pack_pc(static_cast<int32_t>(i), b < M ? b : -1));
@@ -592,6 +655,8 @@ struct CollideArgs {
     uint32_t cell_base, step, s0, s1;
     const uint32_t* step_dev;   // NULL, or DEVICE offset added to `step` (cc_params.step_dev)
     int chunk;                  // pairs per k_collide_large CTA (<= kChunk, multiple of kCollideThreads)
+    const int32_t* flags;       // workspace order flags (pair_order_mode); NULL: stable layout
+    int n;
     // fused S2b + S2c push of the outputs (cc_params.push; NEXT f2): x_in is read at the
     // particle's input index, x_out / v_out / cell_out written at the output slot
     int push;
@@ -880,6 +945,7 @@ k_collide_large(CollideArgs A)
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     // phase 1: pi_j (keyed Feistel, R1) of each item's two slots in lock step
     // (rare cycle walks afterwards), gathers issued item by item
+    const bool po = pair_order_mode(A.flags, A.n);
     {
         const cc::Feistel f = cc::make_feistel(static_cast<uint32_t>(N), A.keys[j]);
 #pragma unroll kP1Unroll
@@ -888,7 +954,7 @@ k_collide_large(CollideArgs A)
             if (k < i1) {
                 const uint32_t e = k - i0;
                 uint32_t x[2] = {2 * k, 2 * k + 1};
-                if (!(CC_ABLATE & 2)) cc::feistel_E_multi(f, x);
+                if (!po && !(CC_ABLATE & 2)) cc::feistel_E_multi(f, x);   // po: records already in pair order
                 while (x[0] >= f.N) x[0] = cc::feistel_E(f, x[0]);       // cycle walking (rare)
                 stage_slot(A, o + static_cast<int64_t>(x[0]), stage + 4 * e);
                 if (2 * k + 1 < static_cast<uint32_t>(N)) {
@@ -1034,8 +1100,10 @@ __global__ void k_triplets(CollideArgs A)
         const int32_t o = A.off[j];
         const cc::Feistel f = cc::make_feistel(static_cast<uint32_t>(N), A.keys[j]);
         Rec r[3];
+        const bool po = pair_order_mode(A.flags, A.n);
 #pragma unroll
-        for (int q = 0; q < 3; ++q) r[q] = load_slot(A, o + static_cast<int64_t>(cc::feistel_pi(f, N - 3 + q)));
+        for (int q = 0; q < 3; ++q)
+            r[q] = load_slot(A, o + static_cast<int64_t>(po ? static_cast<uint32_t>(N - 3 + q) : cc::feistel_pi(f, N - 3 + q)));
         triplet_update(A, A.cell_base + static_cast<uint32_t>(j), A.Cj[j], eff_step(A), r);
         const double* cr = A.cellref + 4 * static_cast<int64_t>(j);
 #pragma unroll
@@ -1684,7 +1752,7 @@ int run_binning(const double* v_in, int64_t ldv, const int32_t* cell_in, int n, 
 {
     int32_t* err = at<int32_t>(ws, L.o_err);
     mark(ev, 0, st);                     // the timed region starts before the flag reset
-    if (cudaMemsetAsync(err + 1, 0, sizeof(int32_t), st) != cudaSuccess) return CC_ECUDA;   // "unsorted" flag
+    if (cudaMemsetAsync(err + 1, 0, 2 * sizeof(int32_t), st) != cudaSuccess) return CC_ECUDA;   // order flags
     int32_t* tcount = at<int32_t>(ws, L.o_tcount);
     int32_t* cnt = at<int32_t>(ws, L.o_cnt);
     int32_t* off = at<int32_t>(ws, L.o_off);
@@ -1709,10 +1777,10 @@ int run_binning(const double* v_in, int64_t ldv, const int32_t* cell_in, int n, 
     mark(ev, 2, st);
     if (v_in)
         k_scatter<true><<<L.T, 32 * L.W, smem, st>>>(v_in, ldv, cell_in, n, M, L.W, L.sub, tcount, off, wsv, skip,
-                                                     at<double>(ws, L.o_tilesum));
+                                                     at<double>(ws, L.o_tilesum), cnt, keys);
     else
         k_scatter<false><<<L.T, 32 * L.W, smem, st>>>(nullptr, 0, cell_in, n, M, L.W, L.sub, tcount, off, wsv, skip,
-                                                      nullptr);
+                                                      nullptr, cnt, keys);
     return launch_ok();
 }
 
@@ -1866,6 +1934,8 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     A.step = static_cast<uint32_t>(step);
     A.step_dev = p.step_dev;
     A.chunk = L.chunk;
+    A.flags = at<int32_t>(workspace, L.o_err);
+    A.n = nn;
     A.push = 0;
     A.E = nullptr; A.x_in = nullptr; A.x_out = nullptr;
     A.ldE = A.ldxi = A.ldxo = 0;

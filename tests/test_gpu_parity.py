@@ -189,6 +189,24 @@ def test_sorted_input_fast_path(O, n, M, dead):
         check_collide(O, w, step=4)
 
 
+@pytest.mark.parametrize("frac", [0.0, 0.02, 0.1, 0.3, 1.0])
+def test_layout_modes_disorder(O, frac):
+    """The two record layouts of k_scatter (stable slots + gathered pairs for nearly sorted input,
+    pair-order placement + streaming pairs when more than n/8 adjacent ids descend) give the
+    oracle's result on either side of the threshold: sorted input with a fraction `frac` of the
+    particles moved to random positions."""
+    n, M = 200_000, 40
+    w = W.random_cells(n, M, seed=77, dead_frac=0.01, skew=True)
+    key = np.where(w.cell < 0, M, w.cell)
+    order = np.argsort(key, kind="stable")
+    rng = np.random.default_rng(5)
+    mv = np.flatnonzero(rng.random(n) < frac)
+    order[mv] = order[rng.permutation(mv)]
+    w.v = np.ascontiguousarray(w.v[:, order])
+    w.cell = np.ascontiguousarray(w.cell[order])
+    check_collide(O, w, step=6)
+
+
 def test_c1_chained_ten_steps(O):
     """Config 1 (1 cell, 1,000 e-, Maxwellian 2 eV, 10 steps): each step's GPU
     output feeds the next GPU step, same for the oracle; parity every step."""
