@@ -209,33 +209,6 @@ __device__ __forceinline__ void feistel_E_multi(const Feistel& f, uint32_t (&x)[
     for (int v = 0; v < NV; ++v) x[v] = L[v] + (R[v] << f.bL);
 }
 
-// E^-1: the rounds of feistel_E undone in reverse order (odd rounds subtract mod m,
-// even rounds xor the same mask) — a bijection of [0, a m) like E.
-__device__ __forceinline__ uint32_t feistel_Einv(const Feistel& f, uint32_t y)
-{
-    const uint32_t amask = (1u << f.bL) - 1u;
-    uint32_t L = y & amask, R = y >> f.bL;
-#pragma unroll
-    for (int r = 7; r >= 0; --r) {
-        if ((r & 1) == 0) {
-            L ^= fmix32_small(R, f.kp[r]) & amask;
-        } else {
-            const uint32_t t = __umulhi(fmix32_small(L, f.kp[r]), f.m);
-            R = (R >= t) ? R - t : R + f.m - t;
-        }
-    }
-    return L + (R << f.bL);
-}
-
-// pi^-1(s): the pair-order position of stable slot s (cycle walking backwards from s;
-// the first E^-k(s) below N is pi^-1(s) because pi(i) is the first E^k(i) below N).
-__device__ __forceinline__ uint32_t feistel_pi_inv(const Feistel& f, uint32_t s)
-{
-    uint32_t x = feistel_Einv(f, s);
-    while (x >= f.N) x = feistel_Einv(f, x);
-    return x;
-}
-
 // pi(i) for the Feistel form: cycle walking from i until the value is < N.
 __device__ __forceinline__ uint32_t feistel_pi(const Feistel& f, uint32_t i)
 {

@@ -172,15 +172,19 @@ __device__ __forceinline__ int32_t unpack_perm(double w)
 }
 
 // ------------------------------------------------------------------ CCS1: count
-// flags[0]: sticky invalid-id flag; flags[1]: "input not cell-sorted"; flags[2]:
-// number of adjacent descents (flags 1-2 cleared before each call).  Sorted means live ids non-decreasing in input order with
-// every dead/invalid particle after the last live one; then the stable order is
-// the identity and k_scatter packs the records in place.
+// flags[0]: sticky invalid-id flag; flags[1]: "input not cell-sorted" (cleared
+// by the host before each call).  Sorted means live ids non-decreasing in input
+// order with every dead/invalid particle after the last live one; then the
+// stable order is the identity and k_scatter packs the records in place.
 // Each thread takes 4 consecutive ids (one 16-byte load when the array is
-// 16-byte aligned); the order check uses the neighbour lane's last id (only
-// lane 0 reloads one id), and equal neighbours share one shared-memory atomic —
-// a warp whose 128 ids are one cell (sorted input) issues a single atomic.
-__device__ __forceinline__ int32_t count_key(int32_t c, int M) { return (c >= 0 && c < M) ? c : M; }
+// 16-byte aligned); the order check takes the previous id from the neighbour
+// lane (only lane 0 reloads one), so every id is read once; a warp whose 128
+// ids are one cell (sorted input) adds them with a single shared atomic instead
+// of 128 same-address ones.
+__device__ __forceinline__ int32_t count_key(int32_t c, int M)
+{
+    return static_cast<uint32_t>(c) < static_cast<uint32_t>(M) ? c : M;
+}
 
 __global__ void __launch_bounds__(kCountThreads)
 k_count(const int32_t* __restrict__ cell, int n, int M, int tile, int32_t* __restrict__ tcount,
@@ -191,58 +195,51 @@ k_count(const int32_t* __restrict__ cell, int n, int M, int tile, int32_t* __res
     __syncthreads();
     const int64_t start = static_cast<int64_t>(blockIdx.x) * tile;
     const int64_t end = min(start + tile, static_cast<int64_t>(n));
-    const bool vec = (reinterpret_cast<uintptr_t>(cell) & 15u) == 0;     // start is a multiple of 4 (tile is)
     const int lane = threadIdx.x & 31;
-    int bad = 0, descents = 0;
-    for (int64_t i = start + 4 * static_cast<int64_t>(threadIdx.x); i < end; i += 4 * static_cast<int64_t>(blockDim.x)) {
-        int32_t c[4];
-        if (vec && i + 3 < end) {
-            const int4 q = __ldg(reinterpret_cast<const int4*>(cell + i));
-            c[0] = q.x; c[1] = q.y; c[2] = q.z; c[3] = q.w;
-        } else {
-#pragma unroll
-            for (int u = 0; u < 4; ++u) c[u] = (i + u < end) ? __ldg(cell + i + u) : -1;
+    int bad = 0, unsorted = 0;
+    // full 4-id groups (a tile starts at a multiple of 4: tile = W x sub, sub >= 256)
+    const int64_t vend = start + ((end - start) & ~static_cast<int64_t>(3));
+    const bool vec = (reinterpret_cast<uintptr_t>(cell) & 15u) == 0;
+    for (int64_t i0 = start; i0 < vend; i0 += 4 * static_cast<int64_t>(blockDim.x)) {
+        const int64_t i = i0 + 4 * static_cast<int64_t>(threadIdx.x);
+        const bool ok = i < vend;
+        const unsigned act = __ballot_sync(0xFFFFFFFFu, ok);
+        if (!ok) break;
+        int4 q;
+        if (vec) q = __ldg(reinterpret_cast<const int4*>(cell + i));
+        else q = make_int4(__ldg(cell + i), __ldg(cell + i + 1), __ldg(cell + i + 2), __ldg(cell + i + 3));
+        // an id is valid iff -1 <= c < M, i.e. (unsigned)(c + 1) <= M
+        bad |= (static_cast<uint32_t>(q.x + 1) > static_cast<uint32_t>(M)) |
+               (static_cast<uint32_t>(q.y + 1) > static_cast<uint32_t>(M)) |
+               (static_cast<uint32_t>(q.z + 1) > static_cast<uint32_t>(M)) |
+               (static_cast<uint32_t>(q.w + 1) > static_cast<uint32_t>(M));
+        const int32_t k0 = count_key(q.x, M), k1 = count_key(q.y, M), k2 = count_key(q.z, M),
+                      k3 = count_key(q.w, M);
+        int32_t prev = __shfl_up_sync(act, k3, 1);
+        if (lane == 0) prev = (i > 0) ? count_key(__ldg(cell + i - 1), M) : 0;
+        unsorted |= (k0 < prev) | (k1 < k0) | (k2 < k1) | (k3 < k2);
+        const int32_t kl = __shfl_sync(act, k0, 0);
+        if (__all_sync(act, (k0 == kl) & (k1 == kl) & (k2 == kl) & (k3 == kl))) {
+            if (lane == 0) atomicAdd(&hist[kl], 4 * __popc(act));
+            continue;
         }
-        int32_t k[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const bool live = c[u] >= 0 && c[u] < M;
-            bad |= (i + u < end) && !live && c[u] != -1;
-            k[u] = (i + u < end) ? count_key(c[u], M) : M;
-        }
-        // predecessor of k[0]: the previous lane's k[3] (its 4 ids end at i - 1), lane 0 reloads id i - 1
-        const unsigned act = __activemask();
-        int32_t prev = __shfl_up_sync(act, k[3], 1);
-        if (lane == 0 || !((act >> (lane - 1)) & 1u)) prev = (i > 0) ? count_key(__ldg(cell + i - 1), M) : 0;
-        descents += (k[0] < prev) + (k[1] < k[0]) + (k[2] < k[1]) + (k[3] < k[2]);
-        const int nv = static_cast<int>(min(static_cast<int64_t>(4), end - i));
-        // runs of equal keys -> one atomic each; a warp of one key -> one atomic in total
-        const bool uni = (k[0] == k[3]) && (k[1] == k[0]) && (k[2] == k[0]) && nv == 4;
-        int32_t pk;
-        const unsigned same = __match_all_sync(act, uni ? k[0] : -1 - static_cast<int32_t>(lane), &pk);
-        if (same && uni) {
-            if (lane == __ffs(act) - 1) atomicAdd(&hist[k[0]], 4 * __popc(act));
-        } else {
-            int run = 1;
-#pragma unroll
-            for (int u = 1; u < 4; ++u) {
-                if (u < nv && k[u] == k[u - 1]) { ++run; continue; }
-                if (u < nv) { atomicAdd(&hist[k[u - 1]], run); run = 1; }
-            }
-            atomicAdd(&hist[k[nv - 1]], run);
-        }
+        atomicAdd(&hist[k0], 1);
+        atomicAdd(&hist[k1], 1);
+        atomicAdd(&hist[k2], 1);
+        atomicAdd(&hist[k3], 1);
     }
-    __shared__ int32_t s_desc;
-    if (threadIdx.x == 0) s_desc = 0;
+    for (int64_t i = vend + threadIdx.x; i < end; i += blockDim.x) {     // tail (< 4 ids)
+        const int32_t c = __ldg(cell + i);
+        bad |= static_cast<uint32_t>(c + 1) > static_cast<uint32_t>(M);
+        const int32_t k = count_key(c, M);
+        if (i > 0) unsorted |= k < count_key(__ldg(cell + i - 1), M);
+        atomicAdd(&hist[k], 1);
+    }
     const int any_bad = __syncthreads_or(bad);
-    if (descents) atomicAdd(&s_desc, descents);
-    const int any_unsorted = __syncthreads_or(descents);
+    const int any_unsorted = __syncthreads_or(unsorted);
     if (threadIdx.x == 0) {
         if (any_bad) atomicOr(flags, 1);
-        if (any_unsorted) {
-            atomicOr(flags + 1, 1);
-            atomicAdd(flags + 2, s_desc);            // disorder measure: adjacent descents
-        }
+        if (any_unsorted) atomicOr(flags + 1, 1);
     }
     int32_t* row = tcount + static_cast<int64_t>(blockIdx.x) * (M + 1);
     for (int i = threadIdx.x; i <= M; i += blockDim.x) row[i] = hist[i];
@@ -392,18 +389,6 @@ k_cell_setup(const int32_t* __restrict__ cnt, const int32_t* __restrict__ chunk_
     for (int32_t c = chunk_off[j] + lane; c < c1; c += 32) chunk_cell[c] = j;
 }
 
-// Pair-order placement (R1 unchanged, layout only): when the input is far from cell-sorted
-// (more than n/8 adjacent descents: a randomly ordered input has ~n/2, the 2%-drift steady state
-// ~n/25), k_scatter's record writes land at random slots anyway, so it writes each particle of a
-// cell with N_j > 64 straight to its pair-order position off_j + pi_j^-1(rank) and the collide
-// reads both members of pair k from the adjacent records 2k, 2k+1 — a streaming read instead of
-// two random gathers.  Nearly sorted input keeps the stable layout (contiguous scatter writes) and
-// the gathers.  Both give the same pairs, randoms and results: only where the records sit differs.
-__device__ __forceinline__ bool pair_order_mode(const int32_t* flags, int n)
-{
-    return flags && flags[1] != 0 && static_cast<int64_t>(flags[2]) * 8 > n;
-}
-
 // ------------------------------------------------------------------ CCS3: stable scatter
 // Tile = W warps x kSub elements; warp w owns the contiguous sub-range w of the
 // tile, so "input order" = (tile, warp, step, lane).  Per-warp 16-bit counters
@@ -469,8 +454,7 @@ template <bool HAS_V>
 __global__ void __launch_bounds__(32 * kMaxScatterWarps, CC_SCATTER_CTAS)
 k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__ cell, int n, int M,
           int W, int sub, const int32_t* __restrict__ tbase, const int32_t* __restrict__ off,
-          double* __restrict__ wsv, const int32_t* __restrict__ flags, double* __restrict__ tilesum,
-          const int32_t* __restrict__ cnt, const cc::U4* __restrict__ keys)
+          double* __restrict__ wsv, const int32_t* __restrict__ flags, double* __restrict__ tilesum)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -551,7 +535,6 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
     __syncthreads();
 
     // pass B: ranks, destinations, 32-byte records (loads batched, branch-free)
-    const bool po = pair_order_mode(flags, n);
     for (int64_t i0 = s0; i0 < s1; i0 += 32 * kScatterUnrollB) {
         int32_t key[kScatterUnrollB];
         double x[kScatterUnrollB], y[kScatterUnrollB], z[kScatterUnrollB];
@@ -577,16 +560,7 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
             const uint32_t o = __shfl_sync(0xFFFFFFFFu, (old[u] >> ((max(b, 0) & 1) << 4)) & 0xFFFFu,
                                            __ffs(peers[u]) - 1);
             if (b >= 0) {
-                int32_t dest = base[b] + static_cast<int32_t>(o) + __popc(peers[u] & lt);
-                if (po && b < M) {
-                    const int32_t N = __ldg(cnt + b);
-                    if (N > cc::kSmallCell) {
-                        const int32_t oc = __ldg(off + b);
-                        const cc::U4 kk = keys[b];
-                        const cc::Feistel f = cc::make_feistel(static_cast<uint32_t>(N), kk);
-                        dest = oc + static_cast<int32_t>(cc::feistel_pi_inv(f, static_cast<uint32_t>(dest - oc)));
-                    }
-                }
+                const int32_t dest = base[b] + static_cast<int32_t>(o) + __popc(peers[u] & lt);
                 const int64_t i = i0 + 32 * u + lane;
                 st256(wsv + 4 * static_cast<int64_t>(dest), x[u], y[u], z[u],
                       pack_pc(static_cast<int32_t>(i), b < M ? b : -1));
@@ -655,8 +629,6 @@ struct CollideArgs {
     uint32_t cell_base, step, s0, s1;
     const uint32_t* step_dev;   // NULL, or DEVICE offset added to `step` (cc_params.step_dev)
     int chunk;                  // pairs per k_collide_large CTA (<= kChunk, multiple of kCollideThreads)
-    const int32_t* flags;       // workspace order flags (pair_order_mode); NULL: stable layout
-    int n;
     // fused S2b + S2c push of the outputs (cc_params.push; NEXT f2): x_in is read at the
     // particle's input index, x_out / v_out / cell_out written at the output slot
     int push;
@@ -945,7 +917,6 @@ k_collide_large(CollideArgs A)
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     // phase 1: pi_j (keyed Feistel, R1) of each item's two slots in lock step
     // (rare cycle walks afterwards), gathers issued item by item
-    const bool po = pair_order_mode(A.flags, A.n);
     {
         const cc::Feistel f = cc::make_feistel(static_cast<uint32_t>(N), A.keys[j]);
 #pragma unroll kP1Unroll
@@ -954,7 +925,7 @@ k_collide_large(CollideArgs A)
             if (k < i1) {
                 const uint32_t e = k - i0;
                 uint32_t x[2] = {2 * k, 2 * k + 1};
-                if (!po && !(CC_ABLATE & 2)) cc::feistel_E_multi(f, x);   // po: records already in pair order
+                if (!(CC_ABLATE & 2)) cc::feistel_E_multi(f, x);
                 while (x[0] >= f.N) x[0] = cc::feistel_E(f, x[0]);       // cycle walking (rare)
                 stage_slot(A, o + static_cast<int64_t>(x[0]), stage + 4 * e);
                 if (2 * k + 1 < static_cast<uint32_t>(N)) {
@@ -1100,10 +1071,8 @@ __global__ void k_triplets(CollideArgs A)
         const int32_t o = A.off[j];
         const cc::Feistel f = cc::make_feistel(static_cast<uint32_t>(N), A.keys[j]);
         Rec r[3];
-        const bool po = pair_order_mode(A.flags, A.n);
 #pragma unroll
-        for (int q = 0; q < 3; ++q)
-            r[q] = load_slot(A, o + static_cast<int64_t>(po ? static_cast<uint32_t>(N - 3 + q) : cc::feistel_pi(f, N - 3 + q)));
+        for (int q = 0; q < 3; ++q) r[q] = load_slot(A, o + static_cast<int64_t>(cc::feistel_pi(f, N - 3 + q)));
         triplet_update(A, A.cell_base + static_cast<uint32_t>(j), A.Cj[j], eff_step(A), r);
         const double* cr = A.cellref + 4 * static_cast<int64_t>(j);
 #pragma unroll
@@ -1752,7 +1721,7 @@ int run_binning(const double* v_in, int64_t ldv, const int32_t* cell_in, int n, 
 {
     int32_t* err = at<int32_t>(ws, L.o_err);
     mark(ev, 0, st);                     // the timed region starts before the flag reset
-    if (cudaMemsetAsync(err + 1, 0, 2 * sizeof(int32_t), st) != cudaSuccess) return CC_ECUDA;   // order flags
+    if (cudaMemsetAsync(err + 1, 0, sizeof(int32_t), st) != cudaSuccess) return CC_ECUDA;   // "unsorted" flag
     int32_t* tcount = at<int32_t>(ws, L.o_tcount);
     int32_t* cnt = at<int32_t>(ws, L.o_cnt);
     int32_t* off = at<int32_t>(ws, L.o_off);
@@ -1777,10 +1746,10 @@ int run_binning(const double* v_in, int64_t ldv, const int32_t* cell_in, int n, 
     mark(ev, 2, st);
     if (v_in)
         k_scatter<true><<<L.T, 32 * L.W, smem, st>>>(v_in, ldv, cell_in, n, M, L.W, L.sub, tcount, off, wsv, skip,
-                                                     at<double>(ws, L.o_tilesum), cnt, keys);
+                                                     at<double>(ws, L.o_tilesum));
     else
         k_scatter<false><<<L.T, 32 * L.W, smem, st>>>(nullptr, 0, cell_in, n, M, L.W, L.sub, tcount, off, wsv, skip,
-                                                      nullptr, cnt, keys);
+                                                      nullptr);
     return launch_ok();
 }
 
@@ -1934,8 +1903,6 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     A.step = static_cast<uint32_t>(step);
     A.step_dev = p.step_dev;
     A.chunk = L.chunk;
-    A.flags = at<int32_t>(workspace, L.o_err);
-    A.n = nn;
     A.push = 0;
     A.E = nullptr; A.x_in = nullptr; A.x_out = nullptr;
     A.ldE = A.ldxi = A.ldxo = 0;
