@@ -311,6 +311,34 @@ def drift_cells(cell, nx, ny, frac, gen):
     cell.copy_(torch.where(live, cy * nx + cx, cell))
 
 
+def drift_cells_global(cell, nx, ny, rank, world, frac, gen, p_boundary=0.1):
+    """The C5 stand-in pusher on several ranks: LOCAL ids in, GLOBAL ids out on the
+    64 x 64P grid whose rows [ny r, ny (r+1)) rank r owns.  Every live particle takes the random
+    neighbour move of drift_cells (periodic over the GLOBAL grid, so the first and last local rows
+    can leave the shard), and a particle in the shard's first or last row additionally moves one
+    row outward, across the shard boundary, with probability p_boundary (a Philox-free torch
+    draw: workload generation, not the operator)."""
+    import torch
+    live = cell >= 0
+    g = torch.where(live, cell + rank * nx * ny, cell)
+    r = torch.rand(cell.numel(), generator=gen, device=cell.device)
+    rb = torch.rand(cell.numel(), generator=gen, device=cell.device)
+    gy_total = ny * world
+    mv = (r < frac) & live
+    d = torch.clamp((r * (4.0 / frac)).to(torch.int32), max=3)
+    cx = torch.remainder(g, nx)
+    cy = torch.div(g, nx, rounding_mode="floor")
+    cx = torch.where(mv & (d == 0), torch.remainder(cx + 1, nx), cx)
+    cx = torch.where(mv & (d == 1), torch.remainder(cx - 1, nx), cx)
+    cy = torch.where(mv & (d == 2), torch.remainder(cy + 1, gy_total), cy)
+    cy = torch.where(mv & (d == 3), torch.remainder(cy - 1, gy_total), cy)
+    ly = cy - rank * ny
+    out = (rb < p_boundary) & live
+    cy = torch.where(out & (ly == 0), torch.remainder(cy - 1, gy_total), cy)
+    cy = torch.where(out & (ly == ny - 1), torch.remainder(cy + 1, gy_total), cy)
+    cell.copy_(torch.where(live, cy * nx + cx, cell))
+
+
 def hbm_peak_gbs() -> float:
     try:
         return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
@@ -507,11 +535,23 @@ def run_ours(args):
     from paper_2508_06771_b200.coulomb import CollideOut
 
     w = workload(args, rank)
-    n, M = w.n, w.cells
+    n_live, M = w.n, w.cells
     v_host = torch.from_numpy(w.v)
     c_host = torch.from_numpy(w.cell)
-    v = v_host.to(dev)
-    cell = c_host.to(dev)
+    n = n_live
+    mig = None
+    if world > 1:
+        # fixed, dead-padded particle slots: the device-side Migrator moves
+        # leavers out and appends arrivals into the dead tail, no count ever reaches the host
+        n = n_live + n_live // 50 + 4096
+        bounds = ccd.owner_bounds(M * world, world)
+        peers = sorted({(rank - 1) % world, (rank + 1) % world} - {rank})
+        mig = ccd.Migrator(n, bounds, rank, max(4096, n_live // 100), dev, comm=dist_ops.nccl, peers=peers,
+                           exchange=None if dist_ops.nccl is not None else ccd.torch_exchange())
+    v = torch.zeros((3, n), dtype=torch.float64, device=dev)
+    v[:, :n_live].copy_(v_host.to(dev))
+    cell = torch.full((n,), -1, dtype=torch.int32, device=dev)
+    cell[:n_live].copy_(c_host.to(dev))
     p = w.params()
     ws = cc.alloc_workspace(n, M, dev)
 
@@ -528,6 +568,7 @@ def run_ours(args):
     lib = _lib.load()
 
     model = {"flags": 0}
+    red_diag = [None]
 
     def call(src_v, src_cell, dst, step, events=None, post=None):
         prm = cc.make_params(weight=p["weight"], cell_volume=p["cell_volume"], ln_lambda=p["ln_lambda"],
@@ -542,27 +583,44 @@ def run_ours(args):
                                  C.c_void_p(ws.data_ptr()), ws.numel(), C.c_void_p(stream.cuda_stream))
         _lib.check(rc, "coulomb_collide")
         if world > 1:
-            ccd.reduce_diag(dst.diag, dist_ops)      # NCCL all_gather + rank-ordered device sum
+            # NCCL all_gather + rank-ordered device sum: the GLOBAL diagnostics (pairs of all ranks)
+            red_diag[0] = ccd.reduce_diag(dst.diag, dist_ops)
         if post is not None:
             post.record(stream)                      # end of the step incl. the diagnostics collective
 
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
 
+    def between(mode, dst, timed_mig=None):
+        """After a call: the stand-in pusher (outside the timed region) and, on several ranks,
+        the device-side migration (timed: events around it)."""
+        if mode == "cold":
+            return
+        if world > 1 and mode == "steady":
+            drift_cells_global(dst.cell_out, args.nx, args.ny, rank, world, args.drift, gen)
+            if timed_mig is not None:
+                timed_mig[0].record(stream)
+            mig(dst.v_out, None, dst.cell_out, dst.diag)
+            if timed_mig is not None:
+                timed_mig[1].record(stream)
+        elif mode in ("steady", "steady_nomig"):
+            drift_cells(dst.cell_out, args.nx, args.ny, args.drift, gen)
+
     def run_mode(mode, K, W, step0, sampler=None):
         """K timed operator calls after W untimed ones.  cold: the same randomly
         ordered input every step; warm: each step consumes the previous step's
-        (cell-sorted) output; steady: warm + the stand-in drift between steps
-        (the drift runs outside the operator's events)."""
+        (cell-sorted) output; steady: warm + the stand-in drift between steps (the
+        drift is not timed); on several ranks the steady step also migrates the
+        particles that crossed a shard boundary (timed) — steady_nomig drifts
+        inside the shard only."""
         cur = (v, cell)
         for s in range(W):
             dst = bufs[s % 2]
             call(*cur, dst, step0 + s)
+            between(mode, dst)
             if mode != "cold":
-                if mode == "steady":
-                    drift_cells(dst.cell_out, args.nx, args.ny, args.drift, gen)
                 cur = (dst.v_out, dst.cell_out)
-        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(nst + 2)] for _ in range(K)]
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(nst + 4)] for _ in range(K)]
         for row in ev:
             for e in row:
                 e.record(stream)          # materialise the cudaEvent_t handles
@@ -577,9 +635,8 @@ def run_ours(args):
         for s in range(K):
             dst = bufs[(W + s) % 2]
             call(*cur, dst, step0 + W + s, ev[s][:nst + 1], ev[s][nst + 1])
+            between(mode, dst, (ev[s][nst + 2], ev[s][nst + 3]))
             if mode != "cold":
-                if mode == "steady":
-                    drift_cells(dst.cell_out, args.nx, args.ny, args.drift, gen)
                 cur = (dst.v_out, dst.cell_out)
         t1.record(stream)
         torch.cuda.synchronize()
@@ -588,14 +645,20 @@ def run_ours(args):
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
-        per = [ev[s][0].elapsed_time(ev[s][nst + 1]) for s in range(K)]
+        migrating = world > 1 and mode == "steady"
+        mig_ms = [ev[s][nst + 2].elapsed_time(ev[s][nst + 3]) if migrating else 0.0 for s in range(K)]
+        per = [ev[s][0].elapsed_time(ev[s][nst + 1]) + mig_ms[s] for s in range(K)]
         op_ms = statistics.mean(per)
         stages = {name: statistics.mean(ev[s][i].elapsed_time(ev[s][i + 1]) for s in range(K))
                   for i, name in enumerate(_lib.STAGE_NAMES)}
+        if migrating:
+            stages["migrate"] = statistics.mean(mig_ms)
         assert cc.cc_device_status(ws) == 0
+        last = bufs[(W + K - 1) % 2]
+        # pairs: the reduced (all-rank) diagnostics on several ranks, the local ones on one
+        pairs = float((red_diag[0] if world > 1 else last.diag)[2].item())
         return {"ms": op_ms, "ms_median": statistics.median(per), "ms_min": min(per), "ms_max": max(per),
-                "wall_ms": t0.elapsed_time(t1) / K, "stages": stages,
-                "pairs": float(bufs[(W + K - 1) % 2].diag[2].item())}
+                "wall_ms": t0.elapsed_time(t1) / K, "stages": stages, "pairs": pairs}
 
     K, W = args.steps, args.warmup
     clk = ClockSampler(local).start()
@@ -603,6 +666,10 @@ def run_ours(args):
            "cold": run_mode("cold", K, W, 100_000),
            "warm": run_mode("warm", K, W, 200_000)}
     clk.stop()
+    if world > 1:
+        res["steady_nomig"] = run_mode("steady_nomig", max(3, K // 2), W, 300_000)
+        mig_status = mig.status.cpu().tolist()
+        assert mig_status[:3] == [0, 0, 0], f"migration overflow {mig_status}"
     # NEXT f1 collision-model variants, steady state (shorter runs)
     variants = {}
     for name, fl in (("odd_triplet", _lib.CC_ODD_TRIPLET), ("nanbu", _lib.CC_NANBU),
@@ -625,8 +692,8 @@ def run_ours(args):
     v_pin = v_host.pin_memory()
     c_pin = c_host.pin_memory()
     NB = max(1, args.e2e_buffers)
-    houts = [torch.empty((3, n), dtype=torch.float64).pin_memory() for _ in range(NB)]
-    devbufs = [cc.alloc_host_buffer(n, M, dev) for _ in range(NB)]
+    houts = [torch.empty((3, n_live), dtype=torch.float64).pin_memory() for _ in range(NB)]
+    devbufs = [cc.alloc_host_buffer(n_live, M, dev) for _ in range(NB)]
     streams = [torch.cuda.Stream(dev) for _ in range(NB)]
     E = max(args.e2e_steps, 1)
 
@@ -653,18 +720,14 @@ def run_ours(args):
     del devbufs
 
     # ---- max over ranks (times), sum over ranks (pairs)
-    names = ["steady", "cold", "warm"]
+    names = [k for k in ("steady", "cold", "warm", "steady_nomig") if k in res]
     if dist is not None:
-        t = torch.tensor([res[k]["ms"] for k in names] + [e2e_ms] + [res[k]["pairs"] for k in names],
-                         dtype=torch.float64, device=dev)
-        mx = t[:4].clone()
+        # time = max over ranks; pairs already come from the reduced (all-rank) diagnostics
+        mx = torch.tensor([res[k]["ms"] for k in names] + [e2e_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        tot = t[4:].clone()
-        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
         for i, k in enumerate(names):
             res[k]["ms"] = float(mx[i])
-            res[k]["pairs"] = float(tot[i])
-        e2e_ms = float(mx[3])
+        e2e_ms = float(mx[len(names)])
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -693,16 +756,16 @@ def run_ours(args):
         """ALGO_BYTES per particle x n over the dominant kernel's event-timed duration."""
         st = r["stages"]
         dom = max(("count", "scatter", "collide"), key=lambda k: st[k])
-        achieved = ALGO_BYTES * n / (st[dom] * 1e-3) / 1e9
+        achieved = ALGO_BYTES * n_live / (st[dom] * 1e-3) / 1e9
         tr = traffic.get(kernel_of[dom], {}).get("dram_bytes_per_launch") if (world == 1 and with_traffic) else None
         return {"kernel": kernel_of[dom], "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "traffic": tr,
-                "traffic_over_algorithmic": (tr / (ALGO_BYTES * n)) if tr else None,
+                "traffic_over_algorithmic": (tr / (ALGO_BYTES * n_live)) if tr else None,
                 "traffic_source": ("profiles/traffic.json (ncu --set full, same kernel sources, steady call)"
                                    if tr else traffic_note),
-                "algorithmic_bytes_per_particle": ALGO_BYTES, "algorithmic_bytes_per_launch": ALGO_BYTES * n,
+                "algorithmic_bytes_per_particle": ALGO_BYTES, "algorithmic_bytes_per_launch": ALGO_BYTES * n_live,
                 "kernel_contract_bytes_per_particle": STAGE_CONTRACT_BYTES[dom],
-                "kernel_contract_frac": STAGE_CONTRACT_BYTES[dom] * n / (st[dom] * 1e-3) / 1e9 / hbm_peak,
+                "kernel_contract_frac": STAGE_CONTRACT_BYTES[dom] * n_live / (st[dom] * 1e-3) / 1e9 / hbm_peak,
                 "kernel_ms": st[dom], "peak_source": peak_src}
 
     STEP_KERNELS = ("k_count", "k_scan_tiles", "k_scan_cells", "k_cell_setup", "k_scatter", "k_collide_small",
@@ -713,19 +776,19 @@ def run_ours(args):
         bytes ncu measured for every kernel of one steady call (reading 1), with SURVEY §8(d)'s
         1.15 x design-traffic guard against its cold (112 B) and warm (56 B) designs."""
         out = {"algorithmic_bytes_per_particle": ALGO_BYTES,
-               "frac": ALGO_BYTES * n / (ms * 1e-3) / 1e9 / hbm_peak,
+               "frac": ALGO_BYTES * n_live / (ms * 1e-3) / 1e9 / hbm_peak,
                "design_bytes_per_particle": DESIGN_BYTES}
         if world != 1 or not all(k in traffic for k in STEP_KERNELS):
             out["achieved_dram_frac"] = None
             out["traffic_note"] = traffic_note
             return out
         b = sum(traffic[k]["dram_bytes_per_launch"] for k in STEP_KERNELS)
-        out.update({"achieved_dram_bytes_per_particle": b / n,
-                    "traffic_over_algorithmic": b / (ALGO_BYTES * n),
+        out.update({"achieved_dram_bytes_per_particle": b / n_live,
+                    "traffic_over_algorithmic": b / (ALGO_BYTES * n_live),
                     "achieved_dram_gbs": b / (ms * 1e-3) / 1e9,
                     "achieved_dram_frac": b / (ms * 1e-3) / 1e9 / hbm_peak,
-                    "guard_1.15x_cold_design": b / n <= 1.15 * DESIGN_BYTES["cold"],
-                    "guard_1.15x_warm_design": b / n <= 1.15 * DESIGN_BYTES["warm"],
+                    "guard_1.15x_cold_design": b / n_live <= 1.15 * DESIGN_BYTES["cold"],
+                    "guard_1.15x_warm_design": b / n_live <= 1.15 * DESIGN_BYTES["warm"],
                     "source": "profiles/traffic.json (ncu dram__bytes_read/write.sum per kernel, one steady call, "
                               "same kernel sources)"})
         return out
@@ -736,7 +799,7 @@ def run_ours(args):
     def summary(r):
         return {"value": r["pairs"] / (r["ms"] * 1e-3), "ms_per_step": r["ms"], "wall_ms_per_step": r["wall_ms"],
                 "timing": timing(r), "stages_ms": r["stages"], "roofline": roofline(r),
-                "step_hbm_frac": ALGO_BYTES * n / (r["ms"] * 1e-3) / 1e9 / hbm_peak}
+                "step_hbm_frac": ALGO_BYTES * n_live / (r["ms"] * 1e-3) / 1e9 / hbm_peak}
 
     head = res["steady"]
     line = {
@@ -745,8 +808,11 @@ def run_ours(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_name(args, world) + f"; steady-state PIC: each step consumes the previous "
                    f"step's output after a stand-in drift moves {100 * args.drift:g}% of the electrons to a "
-                   f"neighbour cell (first step: randomly ordered input)",
-                   "cells_per_gpu": M, "electrons_per_gpu": n, "pairs_per_step": head["pairs"],
+                   f"neighbour cell (first step: randomly ordered input)"
+                   + ("; on several ranks the first/last row of each shard also moves outward with p = 0.1 and the "
+                      "step includes the device-side migration to the owning rank (NCCL, fixed-size slots)"
+                      if world > 1 else ""),
+                   "cells_per_gpu": M, "electrons_per_gpu": n_live, "pairs_per_step": head["pairs"],
                    "l2": f"inputs {(w.v.nbytes + w.cell.nbytes) / 1e9:.2f} GB/GPU >> 126 MB L2 (no flush needed)",
                    "timing": "CUDA events around each operator call (drift excluded); value = mean of K, "
                              "median/min/max in timing",
@@ -759,14 +825,27 @@ def run_ours(args):
         "warm": dict(summary(res["warm"]), what="chained steps, no drift (input already cell-sorted)"),
         "e2e": {"value": res["cold"]["pairs"] / (e2e_ms * 1e-3), "unit": UNIT,
                 "h2d_bytes_per_step": int(v_host.numel() * 8 + c_host.numel() * 4),
-                "d2h_bytes_per_step": int(n * 24), "ms_per_step": e2e_ms,
+                "d2h_bytes_per_step": int(n_live * 24), "ms_per_step": e2e_ms,
                 "what": "coulomb_collide_host (C-ABI host-buffer entry, CC_PRESERVE_ORDER) on pinned host memory: "
                         "per step H2D of v and cell ids, D2H of the post-collision v in the caller's order; "
                         f"{NB} streams / device buffers, consecutive steps' copies overlap"},
         "variants": variants,
-        "gpu_launches": 10 * K + (K if world > 1 else 0),
+        # our kernels per timed step: coulomb_collide 10; on several ranks + cc_diag_sum_ranks 1 and the
+        # migration's k_mig_count / k_mig_scan / k_mig_pack / k_mig_unpack 4 (NCCL's own kernels not counted)
+        "gpu_launches": 10 * K + (5 * K if world > 1 else 0),
         "clocks": clk.summary(),
     }
+    if world > 1:
+        line["multi_gpu"] = {
+            "steady_without_migration": dict(summary(res["steady_nomig"]),
+                                             what="drift inside the shard only, no migration step"),
+            "migration": {"peers": mig.peers, "cap_per_peer": mig.cap, "slot_bytes": mig.slot,
+                          "status": mig_status, "ms_per_step": res["steady"]["stages"].get("migrate"),
+                          "what": "cc_mig_pack + cc_dist_mig_exchange (grouped ncclSend/ncclRecv of whole "
+                                  "fixed-size slots with the two neighbour shards) + cc_mig_unpack, inside the "
+                                  "timed step; status = [dropped: slot full, ids out of range, buffer full, "
+                                  "arrivals] summed over all steps of this rank"},
+            "diagnostics": "value's pair count from the NCCL-reduced diagnostics (cc_dist_diag_reduce)"}
     if world == 1 and not args.no_pic:
         try:
             line["pic"] = pic_section(args, dev, w, K)

@@ -283,6 +283,43 @@ int cc_dist_alltoall_counts(const int64_t *send_counts, int64_t *recv_counts, vo
 int cc_dist_exchange(const void *send, int64_t lds, void *recv, int64_t ldr, int32_t nrows, int32_t elem_bytes,
                      const int64_t *send_off, const int64_t *recv_off, void *comm, void *stream);
 
+/* ---- Device-side particle migration (csrc/cc_migrate.cu) -------
+ * No host synchronisation: every rank keeps its particles in n fixed slots,
+ * dead-padded (cell -1).  coulomb_collide leaves the live particles in [0, L) and
+ * the dead in [L, n), L = diag_out[0]; a push (cc_push) then rewrites the cell ids
+ * as GLOBAL ids in place.  Migration moves every live particle to the rank owning
+ * its cell under the contiguous split bounds (DEVICE int32 [nranks+1]):
+ *  cc_mig_pack   (this rank) particles owned by rank p != rank are copied, in input
+ *                order, into slot p of `send` and marked dead here; the others get
+ *                their LOCAL cell id (cell - bounds[rank]); ids outside every range
+ *                are dropped (status[1]).  Also zeroes the headers of `recv`.
+ *  cc_dist_mig_exchange  grouped ncclSend / ncclRecv of whole slots with the listed
+ *                peer ranks: the message size is the fixed slot size, so no count
+ *                has to reach the host.
+ *  cc_mig_unpack the arrivals, in (source rank, source order), into the free slots
+ *                [L, L + A) with LOCAL cell ids (L from diag, e.g. the last
+ *                coulomb_collide's diag_out; arrivals beyond n: status[2]).
+ * The result is deterministic for a given world size.  send / recv: DEVICE,
+ * nranks * cc_mig_slot_bytes(cap, xrows) bytes, 256-byte aligned; slot p = int64
+ * count, padding to 64 bytes, then SoA rows of `cap` elements: v_x, v_y, v_z, the
+ * xrows (0..3) payload rows of x [xrows][ldx] (fp64, e.g. positions), the cell
+ * (int32, GLOBAL).  status DEVICE int32 [4], accumulated (zero it once): [0]
+ * leavers dropped because their slot was full (cap too small), [1] ids outside
+ * every range, [2] arrivals dropped because [L, n) was full, [3] arrivals
+ * received.  A correct run has status[0..2] == 0.
+ * workspace: DEVICE, cc_mig_workspace_bytes(n, nranks) bytes, 256-byte aligned. */
+#define CC_MIG_MAX_RANKS 64
+size_t cc_mig_slot_bytes(int64_t cap, int32_t xrows);                     /* HOST */
+size_t cc_mig_workspace_bytes(int64_t n, int32_t nranks);                 /* HOST */
+int cc_mig_pack(double *v, int64_t ldv, double *x, int64_t ldx, int32_t xrows, int32_t *cell, int64_t n,
+                const int32_t *bounds, int32_t nranks, int32_t rank, int64_t cap, void *send, void *recv,
+                int32_t *status, void *workspace, size_t workspace_bytes, void *stream);
+int cc_dist_mig_exchange(const void *send, void *recv, size_t slot_bytes, const int32_t *peers, int32_t npeers,
+                         void *comm, void *stream);                       /* peers: HOST int32 [npeers] */
+int cc_mig_unpack(double *v, int64_t ldv, double *x, int64_t ldx, int32_t xrows, int32_t *cell, int64_t n,
+                  const double *diag, const void *recv, const int32_t *bounds, int32_t nranks, int32_t rank,
+                  int64_t cap, int32_t *status, void *stream);
+
 /* Multi-GPU: rank-ascending sum of P gathered diagnostics vectors
  * gathered [P][16] -> out [16] (deterministic for a given P).   */
 int cc_diag_sum_ranks(const double *gathered, int32_t nranks, double *out, void *stream);

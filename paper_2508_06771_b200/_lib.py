@@ -36,7 +36,9 @@ EXPORTS = ("cc_default_params", "cc_workspace_bytes", "coulomb_collide", "cc_dev
            "cc_step_advance", "cc_p2c_scratch_bytes", "cc_p2c", "cc_p2c_moments",
            "cc_host_buffer_bytes", "coulomb_collide_host", "cc_recombine",
            "cc_nccl_get_unique_id", "cc_nccl_comm_init", "cc_nccl_comm_destroy", "cc_dist_diag_reduce",
-           "cc_dist_alltoall_counts", "cc_dist_exchange")
+           "cc_dist_alltoall_counts", "cc_dist_exchange", "cc_mig_slot_bytes", "cc_mig_workspace_bytes",
+           "cc_mig_pack", "cc_dist_mig_exchange", "cc_mig_unpack")
+CC_MIG_MAX_RANKS = 64
 
 
 class CCGrid(C.Structure):
@@ -138,6 +140,16 @@ def load():
     L.cc_dist_exchange.restype = C.c_int
     L.cc_step_advance.argtypes = [vp, u32, vp]
     L.cc_step_advance.restype = C.c_int
+    L.cc_mig_slot_bytes.argtypes = [i64, i32]
+    L.cc_mig_slot_bytes.restype = sz
+    L.cc_mig_workspace_bytes.argtypes = [i64, i32]
+    L.cc_mig_workspace_bytes.restype = sz
+    L.cc_mig_pack.argtypes = [vp, i64, vp, i64, i32, vp, i64, vp, i32, i32, i64, vp, vp, vp, vp, sz, vp]
+    L.cc_mig_pack.restype = C.c_int
+    L.cc_dist_mig_exchange.argtypes = [vp, vp, sz, vp, i32, vp, vp]
+    L.cc_dist_mig_exchange.restype = C.c_int
+    L.cc_mig_unpack.argtypes = [vp, i64, vp, i64, i32, vp, i64, vp, vp, vp, i32, i32, i64, vp, vp]
+    L.cc_mig_unpack.restype = C.c_int
     _lib = L
     return L
 

@@ -6,7 +6,8 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SOURCES = [os.path.join(HERE, "csrc", "cc_kernels.cu"), os.path.join(HERE, "csrc", "cc_dist.cu")]
+SOURCES = [os.path.join(HERE, "csrc", "cc_kernels.cu"), os.path.join(HERE, "csrc", "cc_dist.cu"),
+           os.path.join(HERE, "csrc", "cc_migrate.cu")]
 HEADERS = [os.path.join(HERE, "csrc", "cc_device.cuh"), os.path.join(ROOT, "include", "coulomb.h")]
 OUT = os.path.join(HERE, "lib", "libcoulomb.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -105,4 +105,27 @@ int cc_dist_exchange(const void* send, int64_t lds, void* recv, int64_t ldr, int
     return (res == ncclSuccess && e == ncclSuccess) ? CC_OK : CC_ENCCL;
 }
 
+int cc_dist_mig_exchange(const void* send, void* recv, size_t slot_bytes, const int32_t* peers, int32_t npeers,
+                         void* comm, void* stream)
+{
+    if (!comm || npeers < 0 || (npeers > 0 && (!peers || !send || !recv)) || slot_bytes == 0) return CC_EINVAL;
+    ncclComm_t c = static_cast<ncclComm_t>(comm);
+    int nranks = 0, me = 0;
+    if (ncclCommCount(c, &nranks) != ncclSuccess || ncclCommUserRank(c, &me) != ncclSuccess) return CC_ENCCL;
+    for (int32_t i = 0; i < npeers; ++i)
+        if (peers[i] < 0 || peers[i] >= nranks || peers[i] == me) return CC_EINVAL;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const char* s = static_cast<const char*>(send);
+    char* r = static_cast<char*>(recv);
+    if (ncclGroupStart() != ncclSuccess) return CC_ENCCL;
+    ncclResult_t res = ncclSuccess;
+    for (int32_t i = 0; i < npeers && res == ncclSuccess; ++i) {
+        const size_t p = static_cast<size_t>(peers[i]);
+        res = ncclSend(s + p * slot_bytes, slot_bytes, ncclUint8, peers[i], c, st);   // my slot for p
+        if (res == ncclSuccess) res = ncclRecv(r + p * slot_bytes, slot_bytes, ncclUint8, peers[i], c, st);
+    }
+    const ncclResult_t e = ncclGroupEnd();
+    return (res == ncclSuccess && e == ncclSuccess) ? CC_OK : CC_ENCCL;
+}
+
 }  // extern "C"

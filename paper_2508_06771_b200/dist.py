@@ -123,6 +123,104 @@ class NcclComm:
             ro.ctypes.data_as(C.c_void_p), self.comm, self._stream(send)), "cc_dist_exchange")
 
 
+class Migrator:
+    """Device-side particle migration between cell-range shards, no host synchronisation
+    (C ABI cc_mig_pack -> cc_dist_mig_exchange -> cc_mig_unpack).
+
+    The rank's particles live in ``n`` fixed slots, dead-padded (cell -1): after a
+    ``coulomb_collide`` call the live ones are in [0, L) (L = its diag_out[0]) and the
+    dead in [L, n).  ``__call__(v, x, cell, diag)`` takes the cell ids as GLOBAL ids
+    (a push's output), sends every particle owned by another rank in a fixed-capacity
+    slot (``cap`` particles per peer; the message size never depends on a count, so
+    nothing is read back to the host), marks it dead here, converts the stayers' ids to
+    LOCAL ones and appends the arrivals in (source rank, source order) at [L, L + A).
+    ``status`` (device int32 [4], accumulated): leavers dropped for a full slot, ids
+    outside every range, arrivals dropped for a full buffer, arrivals received.
+
+    ``exchange``: None -> the library's NCCL communicator ``comm`` (grouped
+    ncclSend/ncclRecv of whole slots with ``peers``); a callable(send, recv, slot_bytes)
+    replaces it (the tests run several simulated ranks in one process)."""
+
+    def __init__(self, n: int, bounds: list, rank: int, cap: int, device, *, xrows: int = 0,
+                 comm: Optional[NcclComm] = None, peers: Optional[list] = None, exchange=None):
+        from . import _lib
+        L = _lib.load()
+        self.n, self.rank, self.cap, self.xrows = n, rank, cap, xrows
+        self.P = len(bounds) - 1
+        self.bounds = torch.tensor(bounds, dtype=torch.int32, device=device)
+        self.slot = int(L.cc_mig_slot_bytes(cap, xrows))
+        self.send = torch.empty(self.P * self.slot, dtype=torch.uint8, device=device)
+        self.recv = torch.empty(self.P * self.slot, dtype=torch.uint8, device=device)
+        self.ws = torch.empty(max(int(L.cc_mig_workspace_bytes(n, self.P)), 256), dtype=torch.uint8, device=device)
+        self.status = torch.zeros(4, dtype=torch.int32, device=device)
+        self.comm = comm
+        self.peers = [p for p in range(self.P) if p != rank] if peers is None else list(peers)
+        self.exchange_fn = exchange
+        import numpy as np
+        self._peers = np.asarray(self.peers, dtype=np.int32)
+
+    @staticmethod
+    def _p(t):
+        import ctypes as C
+        return C.c_void_p(t.data_ptr()) if t is not None else None
+
+    def _stream(self):
+        import ctypes as C
+        return C.c_void_p(torch.cuda.current_stream(self.send.device).cuda_stream)
+
+    def pack(self, v, x, cell):
+        from . import _lib
+        ldx = x.stride(0) if (x is not None and self.xrows > 0) else self.n
+        _lib.check(_lib.load().cc_mig_pack(self._p(v), v.stride(0), self._p(x) if self.xrows else None, ldx,
+                                           self.xrows, self._p(cell), self.n, self._p(self.bounds), self.P, self.rank,
+                                           self.cap, self._p(self.send), self._p(self.recv), self._p(self.status),
+                                           self._p(self.ws), self.ws.numel(), self._stream()), "cc_mig_pack")
+
+    def exchange(self):
+        import ctypes as C
+        from . import _lib
+        if self.exchange_fn is not None:
+            self.exchange_fn(self.send, self.recv, self.slot)
+        elif self.peers:
+            _lib.check(_lib.load().cc_dist_mig_exchange(self._p(self.send), self._p(self.recv), self.slot,
+                                                        self._peers.ctypes.data_as(C.c_void_p), len(self.peers),
+                                                        self.comm.comm, self._stream()), "cc_dist_mig_exchange")
+
+    def unpack(self, v, x, cell, diag):
+        from . import _lib
+        ldx = x.stride(0) if (x is not None and self.xrows > 0) else self.n
+        _lib.check(_lib.load().cc_mig_unpack(self._p(v), v.stride(0), self._p(x) if self.xrows else None, ldx,
+                                             self.xrows, self._p(cell), self.n, self._p(diag), self._p(self.recv),
+                                             self._p(self.bounds), self.P, self.rank, self.cap, self._p(self.status),
+                                             self._stream()), "cc_mig_unpack")
+
+    def __call__(self, v, x, cell, diag):
+        self.pack(v, x, cell)
+        self.exchange()
+        self.unpack(v, x, cell, diag)
+
+
+def torch_exchange(group=None):
+    """Migrator exchange through torch.distributed point-to-point ops (batch_isend_irecv of
+    whole slots with every other rank); used when the library's own NCCL communicator is not."""
+    def fn(send, recv, slot):
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        host = dist.get_backend(group) == "gloo"      # gloo point-to-point: host buffers (smoke runs)
+        snd = send.cpu() if host else send
+        rcv = recv.cpu() if host else recv
+        ops = []
+        for p in range(world):
+            if p != rank:
+                ops.append(dist.P2POp(dist.isend, snd[p * slot:(p + 1) * slot], p, group))
+                ops.append(dist.P2POp(dist.irecv, rcv[p * slot:(p + 1) * slot], p, group))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+        if host:
+            recv.copy_(rcv)
+    return fn
+
+
 def cuda_ops(nccl: Optional[NcclComm] = None) -> DistOps:
     from . import coulomb as cc
 

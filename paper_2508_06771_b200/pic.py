@@ -26,8 +26,9 @@ once into a CUDA graph and replayed; the random streams advance through a
 device step counter (cc_params.step_dev: effective step = substep index +
 subcycles x field-step index), so graph replay and eager execution give
 bit-identical results.  Several GPUs (cell-range shards, ``dist``): eager, with
-a migration (``dist.migrate`` carrying the positions as payload) after each
-push — particle counts per rank change, so buffers are re-sized.
+a device-side migration (``dist.Migrator``: fixed-capacity slots, positions as
+payload, no host synchronisation) after each push; the particle buffers have a
+fixed number of dead-padded slots (``capacity``) and are allocated once.
 
 All per-particle arithmetic runs in the library's CUDA kernels; this module
 only sequences calls and owns buffers.
@@ -47,7 +48,8 @@ class PicLoop:
                  weight: float, cell_volume: float, E: Optional[torch.Tensor] = None,
                  q_over_m: float = -Q_E / M_E, seed: int = 42, subcycles: int = 10, ln_lambda: float = 10.0,
                  coulomb_log_feedback: bool = True, graph: bool = True, flags: int = 0,
-                 dist_ops=None, group=None, cell_base: int = 0, cells: Optional[int] = None, fused: bool = False):
+                 dist_ops=None, group=None, cell_base: int = 0, cells: Optional[int] = None, fused: bool = False,
+                 capacity: Optional[int] = None, mig_cap: Optional[int] = None):
         if subcycles < 1 or subcycles % 2:
             raise ValueError("subcycles must be a positive even number (ping-pong buffers)")
         self.dev = cell.device
@@ -65,17 +67,35 @@ class PicLoop:
         self.lnl = torch.full((self.cells,), float(ln_lambda), dtype=torch.float64, device=self.dev)
         self.moments = torch.zeros((self.cells, cc.CC_MOMENTS_LEN), dtype=torch.float64, device=self.dev)
         self.diag = torch.zeros(cc.CC_DIAG_LEN, dtype=torch.float64, device=self.dev)
-        self._alloc(x, v, cell)
+        n0 = cell.numel()
+        if dist_ops is not None and capacity is None:
+            capacity = n0 + n0 // 4 + 1024          # room for arrivals (dead-padded slots)
+        self._alloc(x, v, cell, capacity)
         self._graph = None
+        self.migrator = None
+        if dist_ops is not None:
+            import torch.distributed as tdist
+            from . import dist as ccd
+            world = tdist.get_world_size(group) if tdist.is_initialized() else 1
+            rank = tdist.get_rank(group) if tdist.is_initialized() else 0
+            bounds = ccd.owner_bounds(grid.cells, world)
+            self.migrator = ccd.Migrator(self.n, bounds, rank, mig_cap or max(1024, n0 // 20), self.dev,
+                                         xrows=grid.dims, comm=dist_ops.nccl,
+                                         exchange=None if dist_ops.nccl is not None else ccd.torch_exchange(group))
 
     # ------------------------------------------------------------------ buffers
-    def _alloc(self, x, v, cell):
-        n = cell.numel()
+    def _alloc(self, x, v, cell, capacity=None):
+        n0 = cell.numel()
+        n = max(n0, capacity or n0)
         self.n = n
         f64 = dict(dtype=torch.float64, device=self.dev)
-        self.x = [x.clone(), torch.zeros((3, n), **f64)]     # rows >= dims are never written by cc_push
-        self.v = [v.clone(), torch.empty((3, n), **f64)]
-        self.cell = [cell.clone(), torch.empty(n, dtype=torch.int32, device=self.dev)]
+        self.x = [torch.zeros((3, n), **f64), torch.zeros((3, n), **f64)]   # rows >= dims never written by cc_push
+        self.v = [torch.zeros((3, n), **f64), torch.empty((3, n), **f64)]
+        self.cell = [torch.full((n,), -1, dtype=torch.int32, device=self.dev),
+                     torch.empty(n, dtype=torch.int32, device=self.dev)]
+        self.x[0][:, :n0].copy_(x)
+        self.v[0][:, :n0].copy_(v)
+        self.cell[0][:n0].copy_(cell)                     # slots beyond n0: dead padding
         self.perm = torch.empty(n, dtype=torch.int32, device=self.dev)
         self.ws = cc.alloc_workspace(n, self.cells, self.dev)
         self.a = 0
@@ -137,12 +157,11 @@ class PicLoop:
         self.field_steps += 1
 
     def _field_step_dist(self):
-        from . import dist as ccd
         for s in range(self.k):
             self._substep(s)
-            x, v, cellg = self.x[self.a], self.v[self.a], self.cell[self.a]
-            m = ccd.migrate(v, cellg, self.grid.cells, self.dist_ops, group=self.group, payload=x)
-            self._alloc(m.payload, m.v, m.cell)
+            # device-side migration in the fixed slots (no host sync, no re-allocation):
+            # leavers out, GLOBAL -> LOCAL ids, arrivals into the dead tail [L, n)
+            self.migrator(self.v[self.a], self.x[self.a], self.cell[self.a], self.diag)
         if self.feedback:
             self.lnl.copy_(cc.cc_coulomb_log(self.moments))
         cc.cc_step_advance(self.step_dev, self.k)

@@ -73,9 +73,9 @@ def test_reduce_diag_and_migrate_one_rank(nccl1):
 
 
 def test_pic_loop_dist_path_one_rank(nccl1):
-    """PicLoop's multi-GPU path (migrate with the positions as payload after every push)
-    through a real 1-rank NCCL group equals the single-GPU loop on the live particles
-    (absorbed electrons are dropped by the migration instead of kept as dead slots)."""
+    """PicLoop's multi-GPU path (device-side Migrator with the positions as payload after every
+    push, fixed dead-padded slots) through a real 1-rank NCCL group equals the single-GPU loop
+    bitwise: with one rank nothing leaves, ids are already local, the slots stay where they are."""
     import workloads as W
     from paper_2508_06771_b200.pic import PicLoop
     rng = np.random.default_rng(4)
@@ -90,16 +90,19 @@ def test_pic_loop_dist_path_one_rank(nccl1):
     g = cc.Grid(2, (nx, ny), (d, d), 2)                 # x absorbing: some electrons leave
     prm = dict(dt=1e-11, weight=W.weight_for(per), cell_volume=W.CELL_VOLUME, subcycles=4)
     args = (torch.from_numpy(x).to(DEV), torch.from_numpy(v).to(DEV), torch.from_numpy(cell.astype(np.int32)).to(DEV), g)
-    a = PicLoop(*args, graph=False, **prm)
-    b = PicLoop(*args, dist_ops=ccd.cuda_ops(), **prm)
-    for _ in range(2):
-        a.field_step()
-        b.field_step()
-    xa, va, ca = a.state
-    xb, vb, cb = b.state
-    live = ca >= 0
-    assert int((~live).sum()) > 0 and cb.numel() == int(live.sum())
-    assert torch.equal(ca[live], cb) and torch.equal(va[:, live], vb) and torch.equal(xa[:2, live], xb[:2])
+    for comm in (None, ccd.NcclComm()):                 # torch.distributed P2P and the library's NCCL
+        a = PicLoop(*args, graph=False, capacity=n + 500, **prm)
+        b = PicLoop(*args, dist_ops=ccd.cuda_ops(comm), capacity=n + 500, **prm)
+        for _ in range(2):
+            a.field_step()
+            b.field_step()
+        xa, va, ca = a.state
+        xb, vb, cb = b.state
+        assert int((ca < 0).sum()) > 500                # absorbed electrons (dead slots)
+        assert torch.equal(ca, cb) and torch.equal(va, vb) and torch.equal(xa[:2], xb[:2])
+        assert b.migrator.status.cpu().tolist() == [0, 0, 0, 0]
+        if comm is not None:
+            comm.close()
 
 
 def test_library_nccl_comm_one_rank(nccl1):
