@@ -543,10 +543,13 @@ def run_ours(args):
     if world > 1:
         # fixed, dead-padded particle slots: the device-side Migrator moves
         # leavers out and appends arrivals into the dead tail, no count ever reaches the host
-        n = n_live + n_live // 50 + 4096
+        # slot capacity per peer: twice the expected leavers towards one neighbour (boundary rows
+        # 2/ny x p = 0.1, plus the drift's row moves), the dead padding twice the arrivals
+        cap = int(2 * n_live * (0.1 / args.ny + args.drift / 4 * 2 / args.ny)) * (2 if world == 2 else 1) + 4096
+        n = n_live + 2 * cap + 4096
         bounds = ccd.owner_bounds(M * world, world)
         peers = sorted({(rank - 1) % world, (rank + 1) % world} - {rank})
-        mig = ccd.Migrator(n, bounds, rank, max(4096, n_live // 100), dev, comm=dist_ops.nccl, peers=peers,
+        mig = ccd.Migrator(n, bounds, rank, cap, dev, comm=dist_ops.nccl, peers=peers,
                            exchange=None if dist_ops.nccl is not None else ccd.torch_exchange())
     v = torch.zeros((3, n), dtype=torch.float64, device=dev)
     v[:, :n_live].copy_(v_host.to(dev))
