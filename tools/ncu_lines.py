@@ -1,5 +1,5 @@
 """Per-CUDA-source-line totals of an ncu --set full report (needs -lineinfo):
-python tools/ncu_lines.py rep.ncu-rep [top] -> stall samples and executed warp instructions per line."""
+python tools/ncu_lines.py rep.ncu-rep [top] [kernel-regex] -> stall samples and executed warp instructions per line."""
 import csv
 import io
 import os
@@ -10,7 +10,8 @@ import sys
 def main():
     rep = sys.argv[1]
     top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"],
+    kf = ["--kernel-name", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass", *kf],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     fname, hdr, agg = "?", None, []
