@@ -120,6 +120,18 @@ Layout make_layout(int64_t n, int32_t M)
     while (L.sub > 256 && (n + static_cast<int64_t>(L.W) * L.sub - 1) / (static_cast<int64_t>(L.W) * L.sub) < kTargetTiles)
         L.sub /= 2;
     while (L.chunk > kCollideThreads && (n / 2) / L.chunk < kTargetChunks) L.chunk -= kCollideThreads;
+    {
+        // whole waves of binning tiles (k_scatter: CC_SCATTER_CTAS CTAs on each of the 148 SMs): the
+        // warp sub-range is trimmed, in steps of 128 ids, so that the tiles just fill the last wave
+        const int64_t wave = static_cast<int64_t>(CC_SCATTER_CTAS) * 148;
+        const int64_t t0 = (n + static_cast<int64_t>(L.W) * L.sub - 1) / (static_cast<int64_t>(L.W) * L.sub);
+        if (t0 > wave) {
+            const int64_t waves = (t0 + wave - 1) / wave;
+            const int64_t per = static_cast<int64_t>(L.W) * waves * wave;
+            const int64_t sub = ((n + per - 1) / per + 127) / 128 * 128;
+            if (sub >= 256 && sub <= L.sub) L.sub = static_cast<int>(sub);
+        }
+    }
     L.tile = L.W * L.sub;
     L.T = static_cast<int>((n + L.tile - 1) / L.tile);
     L.max_chunks = (n + M) / 2 / L.chunk + M + 1;
