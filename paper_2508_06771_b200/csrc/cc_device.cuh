@@ -349,22 +349,30 @@ __constant__ double kLangC[8] = {1.0 / 3.0, -1.0 / 45.0, 2.0 / 945.0, -1.0 / 472
 __constant__ double kLangD[8] = {1.0 / 3.0, -1.0 / 15.0, 2.0 / 189.0, -1.0 / 675.0, 2.0 / 10395.0,
                                  -1382.0 / 58046625.0, 4.0 / 1403325.0, -3617.0 / 10854718875.0};
 
-__device__ __forceinline__ double langevin(double A, double* dL)
+// L(A) = coth A - 1/A with L' (dL) and L'' (d2L)
+__device__ __forceinline__ double langevin(double A, double* dL, double* d2L)
 {
     if (A < 0.25) {
         const double z = A * A;
-        double s = kLangC[7], d = kLangD[7];
+        double s = kLangC[7], d = kLangD[7], e = 14.0 * kLangD[7];
 #pragma unroll
-        for (int i = 6; i >= 0; --i) { s = s * z + kLangC[i]; d = d * z + kLangD[i]; }
+        for (int i = 6; i >= 0; --i) {
+            s = s * z + kLangC[i];
+            d = d * z + kLangD[i];
+            if (i > 0) e = e * z + 2.0 * i * kLangD[i];     // L'' = A sum_{i>=1} 2i d_i A^{2(i-1)}
+        }
         *dL = d;
+        *d2L = A * e;
         return A * s;
     }
     // coth A = -(2 + em) / em and 1 / sinh^2 A = 4 (1 + em) / em^2 with em = expm1(-2A):
     // one transcendental instead of tanh + sinh (same values to rounding as the oracle's forms)
     const double em = expm1(-2.0 * A);
-    const double ie = 1.0 / em, ia = 1.0 / A;
-    *dL = ia * ia - 4.0 * (1.0 + em) * ie * ie;
-    return -(2.0 + em) * ie - ia;
+    const double ie = rcp_nr(em), ia = rcp_nr(A);
+    const double cth = -(2.0 + em) * ie, csch2 = 4.0 * (1.0 + em) * ie * ie;
+    *dL = ia * ia - csch2;
+    *d2L = 2.0 * (cth * csch2 - ia * ia * ia);
+    return cth - ia;
 }
 
 // Cheap cases of A(s): returns true and sets A (+inf: no scattering, s = 0; 0: isotropic;
@@ -372,25 +380,27 @@ __device__ __forceinline__ double langevin(double A, double* dL)
 __device__ __forceinline__ bool nanbu_A_direct(double s, double& A, double& x)
 {
     if (!(s > 0.0)) { A = __longlong_as_double(0x7FF0000000000000ll); return true; }
-    x = exp(-s);
-    if (x <= 0.0) { A = 0.0; return true; }
+    // 1 - e^-s first: the direct A = 1/(1 - e^-s) (most pairs at small s) needs no exp
     const double omx = -expm1(-s);
     if (omx < 1.0 / 40.0) { A = 1.0 / omx; return true; }
+    x = exp(-s);
+    if (x <= 0.0) { A = 0.0; return true; }
     return false;
 }
 
-// Newton solve of coth A - 1/A = x.  Jedynak's (2015) inverse-Langevin approximation (<= 1.4%
-// off) as the start; Newton is quadratic, so once a step is below 1e-9 A the remaining error
-// is ~1e-18 A: stop there (the oracle iterates to a 1e-15 step from Cohen's start: the same
-// root to ~1e-15).
+// Root of coth A - 1/A = x by Halley's method (cubic convergence: f = L - x, A -= f / (f' - f f''
+// / (2 f'))) from Jedynak's (2015) inverse-Langevin approximation (<= 1.4% off): the first step
+// leaves ~1e-5 relative, the second ~1e-15, so the loop stops after a step below 1e-5 A (the
+// oracle iterates Newton to a 1e-15 step from Cohen's start: the same root to ~1e-15).
 __device__ __forceinline__ double nanbu_newton(double x)
 {
     double A = x * (3.0 - x * (2.6 - 0.7 * x)) / ((1.0 - x) * (1.0 + 0.1 * x));
-    for (int it = 0; it < 60; ++it) {
-        double dL;
-        const double dA = (langevin(A, &dL) - x) / dL;
+    for (int it = 0; it < 30; ++it) {
+        double dL, d2L;
+        const double f = langevin(A, &dL, &d2L) - x;
+        const double dA = f / (dL - 0.5 * f * d2L / dL);
         A -= dA;
-        if (fabs(dA) <= 1e-9 * A) break;
+        if (fabs(dA) <= 1e-5 * A) break;
     }
     return A;
 }
@@ -408,8 +418,8 @@ __device__ __forceinline__ double nanbu_s(double ax, double ay, double az, doubl
     const double ux = ax - bx, uy = ay - by, uz = az - bz;
     if (ux == 0.0 && uy == 0.0 && uz == 0.0) return 0.0;
     const double usq = fma(ux, ux, fma(uy, uy, uz * uz));
-    const double u = sqrt(usq);
-    return 2.0 * C / (usq * u);
+    const double rs = rsqrt_nr(usq);                 // 1/|u|: 2C/|u|^3 without a sqrt and a divide
+    return 2.0 * C * (rs * rs) * rs;
 }
 
 // the Nanbu rotation for a given A (R20)
@@ -420,9 +430,11 @@ __device__ __forceinline__ void nanbu_apply(double& ax, double& ay, double& az, 
     if (ux == 0.0 && uy == 0.0 && uz == 0.0) return;
     if (isinf(A)) return;
     const double usq = fma(ux, ux, fma(uy, uy, uz * uz));
-    const double u = sqrt(usq);
-    // 1 - cos chi = -ln(u1 + (1-u1) e^{-2A}) / A = -log1p((1-u1) expm1(-2A)) / A (no cancellation)
-    double omc = (A == 0.0) ? 2.0 - 2.0 * u1 : -log1p((1.0 - u1) * expm1(-2.0 * A)) / A;
+    const double u = usq * rsqrt_nr(usq);
+    // 1 - cos chi = -ln(u1 + (1-u1) e^{-2A}) / A = -log1p((1-u1) expm1(-2A)) / A (no cancellation);
+    // expm1(-2A) is -1 to double precision once 2A > 40 (e^-40 < 2^-57), so it is skipped there
+    const double em = (A > 20.0) ? -1.0 : expm1(-2.0 * A);
+    double omc = (A == 0.0) ? 2.0 - 2.0 * u1 : -log1p((1.0 - u1) * em) / A;
     omc = fmin(fmax(omc, 0.0), 2.0);
     const double sinT = sqrt(omc * (2.0 - omc));
     rotate_pair(ax, ay, az, bx, by, bz, ux, uy, uz, u, sinT, omc, u2);

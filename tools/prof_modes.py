@@ -1,5 +1,6 @@
 """Run coulomb_collide on the C4 input in one order mode, for ncu captures of single kernels.
-usage: python tools/prof_modes.py cold|warm|steady [calls]   (the last call is the one to profile)"""
+usage: python tools/prof_modes.py cold|warm|steady [calls] [flags]   (the last call is the one to profile;
+flags: cc_params.flags, e.g. 2 = CC_NANBU)"""
 import os
 import sys
 
@@ -16,6 +17,7 @@ import paper_2508_06771_b200 as cc  # noqa: E402
 def main():
     mode = sys.argv[1]
     calls = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+    flags = int(sys.argv[3]) if len(sys.argv) > 3 else 0
     dev = torch.device("cuda:0")
     w = W.c4()
     v, c = torch.from_numpy(w.v).to(dev), torch.from_numpy(w.cell).to(dev)
@@ -23,7 +25,7 @@ def main():
     gen = torch.Generator(device=dev)
     gen.manual_seed(1)
     for s in range(calls):
-        o = col.step(v, c, step=s)
+        o = col.step(v, c, step=s, flags=flags)
         if mode != "cold":
             v, c = o.v_out.clone(), o.cell_out.clone()
             if mode == "steady":
