@@ -995,7 +995,7 @@ k_collide_large(CollideArgs A)
         // slowest lane.  aq[slot] holds A (or x = e^-s until solved).
         const uint32_t lt = (1u << lane) - 1u;
         int qn = 0;
-#pragma unroll
+#pragma unroll 1
         for (int t = 0; t < kItemsPerThread; ++t) {
             const uint32_t k = i0 + threadIdx.x + t * kCollideThreads;
             const uint32_t e = k - i0;
@@ -1023,7 +1023,10 @@ k_collide_large(CollideArgs A)
     }
     Acc acc;
     acc.zero();
-#pragma unroll kP2BUnroll
+    // (Nanbu's sampler is several transcendentals long: one copy of the loop body keeps the
+    // kernel inside the instruction cache)
+    constexpr int kUnroll2b = NANBU ? 1 : kP2BUnroll;
+#pragma unroll kUnroll2b
     for (int t = 0; t < kItemsPerThread; ++t) {
         const uint32_t k = i0 + threadIdx.x + t * kCollideThreads;
         if (k < i1 && !(triplet && k + 2 >= items)) {     // the triplet's two items: k_triplets
