@@ -213,3 +213,25 @@ def positions_in_cells(cell, nx, ny, dx=PIC_DX, dy=PIC_DX, *, seed) -> np.ndarra
     x[1] = np.minimum(x[1], np.nextafter((iy + 1) * dy, 0))
     x[:, cell < 0] = 0.0
     return x
+
+
+def device_random_cells(n: int, M: int, *, seed: int, device, T_eV: float = 2.0, chunk: int = 1 << 28):
+    """Inputs too large for host memory (the maximum-size parity test): n particles with cell ids
+    uniform over M cells (random order, "cold") and Maxwellian velocities, drawn ON THE DEVICE with
+    a seeded torch generator in chunks (no temporary larger than `chunk` elements).  Returns
+    (v [3][n] float64, cell [n] int32, params dict).  Plain distributions only, like the rest of
+    this module."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    v = torch.empty((3, n), dtype=torch.float64, device=device)
+    cell = torch.empty(n, dtype=torch.int32, device=device)
+    s = sigma_v(T_eV)
+    for a in range(0, n, chunk):
+        b = min(n, a + chunk)
+        cell[a:b] = torch.randint(0, M, (b - a,), generator=g, device=device, dtype=torch.int32)
+        for r in range(3):
+            v[r, a:b].normal_(0.0, s, generator=g)
+    params = dict(dt=DT, weight=weight_for(max(n / M, 1.0)), cell_volume=CELL_VOLUME, ln_lambda=LN_LAMBDA,
+                  cell_base=0, seed=COLLISION_SEED)
+    return v, cell, params
