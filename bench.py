@@ -472,8 +472,9 @@ def p2c_section(dev, w):
         ms = min(times[1:])
         rec[f"prob_{pr:g}"] = {"ms": ms, "particles_per_s": w.n / (ms * 1e-3), "stats": st.tolist()}
     rec["what"] = ("cc_recombine on the C4 collision output (fresh copy per call; min of 2 after a warm-up); "
-                   "two Philox draws per particle (count + match pass), no per-particle memory traffic except the "
-                   "matched pairs: bound by integer ALU, not HBM")
+                   "one Philox draw per particle (per-warp ordered primary lists, catalytes by binary search), "
+                   "no per-particle memory traffic except the matched pairs and the kill-marker pass: bound by "
+                   "integer ALU, not HBM")
     return {"p2c": out, "recombination": rec}
 
 

@@ -1490,7 +1490,27 @@ __global__ void k_p2c_moments(const double* __restrict__ raw, int M, MomConst mc
 // (RS3); here the particles already sit cell-major in a fresh random order
 // (the pair order, R14), so RS1 is a block scan and the matching is the
 // deterministic rank match of R26: i-th primary <-> i-th non-primary.
-constexpr int kRecWin = 2048;   // primaries matched per pass over the cell
+constexpr int kRecWin = 1024;   // primaries matched per pass over the cell (windowed path)
+constexpr int kRecList = 512;   // primaries per warp held by the one-pass list path
+
+// RS4 + RS5 for primary at a and its catalyte at c (R27, R28): the catalyte keeps its direction
+// and takes the primary's kinetic energy plus the binding energy; the primary dies (a marker that
+// keeps the sort key until k_recombine_finish)
+__device__ __forceinline__ void rc_pair(double* __restrict__ v, int64_t ldv, int32_t* __restrict__ cell, int64_t a,
+                                        int64_t c, double vb2, int j)
+{
+    const double px = v[a], py = v[ldv + a], pz = v[2 * ldv + a];
+    const double cx = v[c], cy = v[ldv + c], cz = v[2 * ldv + c];
+    const double c2 = __dadd_rn(__dadd_rn(__dmul_rn(cx, cx), __dmul_rn(cy, cy)), __dmul_rn(cz, cz));
+    const double p2 = __dadd_rn(__dadd_rn(__dmul_rn(px, px), __dmul_rn(py, py)), __dmul_rn(pz, pz));
+    const double t2 = __dadd_rn(__dadd_rn(c2, p2), vb2);
+    double ux = cx, uy = cy, uz = cz, s2 = c2;
+    if (c2 == 0.0) { ux = px; uy = py; uz = pz; s2 = p2; }
+    if (s2 == 0.0) { ux = 1.0; uy = 0.0; uz = 0.0; s2 = 1.0; }
+    const double f = __dsqrt_rn(__ddiv_rn(t2, s2));
+    v[c] = __dmul_rn(ux, f); v[ldv + c] = __dmul_rn(uy, f); v[2 * ldv + c] = __dmul_rn(uz, f);
+    cell[a] = -2 - j;
+}
 
 __device__ __forceinline__ bool rc_primary(int32_t q, uint32_t G, uint32_t step, uint32_t s0, uint32_t s1, double prob)
 {
@@ -1517,6 +1537,8 @@ k_recombine(double* __restrict__ v, int64_t ldv, int32_t* __restrict__ cell, int
     __shared__ int64_t s_lo, s_hi;
     __shared__ int32_t s_wsum[8];
     __shared__ int32_t ppos[kRecWin], cpos[kRecWin];
+    __shared__ int32_t plist[8][kRecList];          // per-warp primaries (list path)
+    __shared__ int32_t prim[8 * kRecList];          // all primaries of the cell, position order
     const int j = blockIdx.x;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if (threadIdx.x == 0) {             // the cell's slot range: binary search in the cell-sorted ids
@@ -1533,16 +1555,40 @@ k_recombine(double* __restrict__ v, int64_t ldv, int32_t* __restrict__ cell, int
     const double pr = prob[j];
     if (N == 0 || !(pr > 0.0)) return;
     const uint32_t G = cell_base + static_cast<uint32_t>(j);
-    // RS0: count the primaries
+    // RS0: the primaries.  Warp w draws the contiguous positions [w C, (w+1) C) and appends its
+    // primaries in position order to its list (so the lists, in warp order, are the cell's
+    // primaries in position order); a list that overflows sends the cell to the windowed path
+    const int32_t C = (N + 7) / 8;
+    const int32_t q0w = min(w * C, N), q1w = min(q0w + C, N);
     int32_t np = 0;
-    for (int32_t q = threadIdx.x; q < N; q += blockDim.x) np += rc_primary(q, G, step, s0, s1, pr);
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) np += __shfl_xor_sync(0xFFFFFFFFu, np, d);
+    for (int32_t q = q0w + lane; q - lane < q1w; q += 32) {
+        const bool isp = q < q1w && rc_primary(q, G, step, s0, s1, pr);
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, isp);
+        const int32_t at = np + __popc(bal & ((1u << lane) - 1u));
+        if (isp && at < kRecList) plist[w][at] = q;
+        np += __popc(bal);
+    }
     if (lane == 0) s_wsum[w] = np;
     __syncthreads();
-    int32_t P = 0;
-    for (int i = 0; i < 8; ++i) P += s_wsum[i];
+    int32_t P = 0, before = 0, longest = 0;
+    for (int i = 0; i < 8; ++i) {
+        before += (i < w) ? s_wsum[i] : 0;
+        P += s_wsum[i];
+        longest = max(longest, s_wsum[i]);
+    }
     const int32_t m = min(P, N - P);
+    if (longest <= kRecList) {
+        // list path: prim[k] = k-th primary position; the i-th catalyte (non-primary in position
+        // order) is c_i = i + #{k : prim[k] - k <= i}, found by binary search on the
+        // non-decreasing prim[k] - k
+        for (int32_t t = lane; t < np; t += 32) prim[before + t] = plist[w][t];
+        __syncthreads();
+        for (int32_t i = threadIdx.x; i < m; i += blockDim.x) {
+            int32_t a = 0, b = P;                 // first k with prim[k] - k > i
+            while (a < b) { const int32_t h = (a + b) >> 1; if (prim[h] - h <= i) a = h + 1; else b = h; }
+            rc_pair(v, ldv, cell, lo + prim[i], lo + i + a, vb2, j);
+        }
+    } else {
     // RS1-RS5 in windows of kRecWin ranks: positions of primaries / catalytes of rank in the window
     for (int32_t w0 = 0; w0 < m; w0 += kRecWin) {
         __syncthreads();
@@ -1564,20 +1610,9 @@ k_recombine(double* __restrict__ v, int64_t ldv, int32_t* __restrict__ cell, int
             for (int i = 0; i < 8; ++i) base += s_wsum[i];
         }
         __syncthreads();
-        for (int32_t i = threadIdx.x; i < min(kRecWin, m - w0); i += blockDim.x) {
-            const int64_t a = lo + ppos[i], c = lo + cpos[i];
-            const double px = v[a], py = v[ldv + a], pz = v[2 * ldv + a];
-            const double cx = v[c], cy = v[ldv + c], cz = v[2 * ldv + c];
-            const double c2 = __dadd_rn(__dadd_rn(__dmul_rn(cx, cx), __dmul_rn(cy, cy)), __dmul_rn(cz, cz));
-            const double p2 = __dadd_rn(__dadd_rn(__dmul_rn(px, px), __dmul_rn(py, py)), __dmul_rn(pz, pz));
-            const double t2 = __dadd_rn(__dadd_rn(c2, p2), vb2);
-            double ux = cx, uy = cy, uz = cz, s2 = c2;
-            if (c2 == 0.0) { ux = px; uy = py; uz = pz; s2 = p2; }
-            if (s2 == 0.0) { ux = 1.0; uy = 0.0; uz = 0.0; s2 = 1.0; }
-            const double f = __dsqrt_rn(__ddiv_rn(t2, s2));
-            v[c] = __dmul_rn(ux, f); v[ldv + c] = __dmul_rn(uy, f); v[2 * ldv + c] = __dmul_rn(uz, f);
-            cell[a] = -2 - j;             // dead, marker keeps the sort key (rc_key)
-        }
+        for (int32_t i = threadIdx.x; i < min(kRecWin, m - w0); i += blockDim.x)
+            rc_pair(v, ldv, cell, lo + ppos[i], lo + cpos[i], vb2, j);
+    }
     }
     if (threadIdx.x == 0) {
         atomicAdd(stats + 0, static_cast<unsigned long long>(m));
