@@ -24,3 +24,4 @@ python tools/traffic_from_ncu.py gpurun_out/${TAG}_step.ncu-rep gpurun_out/${TAG
 cp profiles/traffic.json gpurun_out/${TAG}_traffic.json
 timeout 900 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; cut -c1-400 gpurun_out/${TAG}_bench.json
 bash tools/multirank_smoke.sh > gpurun_out/${TAG}_multirank.log 2>&1; cut -c1-300 gpurun_out/${TAG}_multirank.log
+bash tools/sanitize.sh > gpurun_out/${TAG}_sanitize.txt 2>&1; cat gpurun_out/${TAG}_sanitize.txt | tail -3
