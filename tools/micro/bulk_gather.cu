@@ -23,6 +23,8 @@ __device__ __forceinline__ void cp16(void* s, const void* g)
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa(s)), "l"(g) : "memory");
 }
 
+__device__ int g_pf_waves = 0;    // MODE 4: L2 bulk prefetch this many waves (gridDim chunks) ahead
+
 template <int MODE, bool STORE>
 __global__ void __launch_bounds__(kThreads) k_gather(const double* __restrict__ rec, const int32_t* __restrict__ idx,
                                                      int64_t n, double* __restrict__ outp)
@@ -40,6 +42,14 @@ __global__ void __launch_bounds__(kThreads) k_gather(const double* __restrict__ 
     unsigned phase = 0;
     for (int64_t c = blockIdx.x; c < nch; c += gridDim.x) {
         const int32_t* ix = idx + c * kChunk;
+        if (MODE == 4) {
+            // sequential DRAM reads: prefetch into L2 the chunk-aligned 48 KB of the record array
+            // that chunk c + waves * grid will gather from (its cell span), then gather as MODE 1
+            const int64_t cp = c + static_cast<int64_t>(g_pf_waves) * gridDim.x;
+            if (threadIdx.x == 0 && cp < nch)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rec + 4 * cp * kChunk), "r"(kChunk * 32)
+                             : "memory");
+        }
         if (MODE == 0) {
             for (int e = threadIdx.x; e < kChunk; e += kThreads) {
                 const double* g = rec + 4 * static_cast<int64_t>(ix[e]);
@@ -47,7 +57,7 @@ __global__ void __launch_bounds__(kThreads) k_gather(const double* __restrict__ 
                 cp16(st + 4 * e + 2, g + 2);
             }
             asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
-        } else if (MODE == 1) {
+        } else if (MODE == 1 || MODE == 4) {
             // 2 * kChunk half-records, lane pairs share a record
             for (int h = threadIdx.x; h < 2 * kChunk; h += kThreads) {
                 const int e = h >> 1, half = h & 1;
@@ -131,6 +141,14 @@ int main()
     cudaMemcpy(idx, h.data(), n * 4, cudaMemcpyHostToDevice);
     const int smem = kChunk * 32;
     const char* names[4] = {"ldgsts 2x16B", "lane pairs  ", "bulk1d 32B  ", "ld.v4.f64   "};
+    for (int waves : {0, 1, 2, 4}) {
+        cudaMemcpyToSymbol(g_pf_waves, &waves, sizeof(int));
+        for (int ctas : {4, 6}) {
+            const float g = timeit<4, false>(rec, idx, n, outp, ctas, smem), gs = timeit<4, true>(rec, idx, n, outp, ctas, smem);
+            printf("%d CTAs/SM lane pairs + L2 prefetch %d wave(s) ahead: gathers %.3f ms, gathers + stores %.3f ms  err=%s\n",
+                   ctas, waves, g, gs, cudaGetErrorString(cudaGetLastError()));
+        }
+    }
     for (int ctas : {4, 6}) {
         float g[4], gs[4];
         g[0] = timeit<0, false>(rec, idx, n, outp, ctas, smem); gs[0] = timeit<0, true>(rec, idx, n, outp, ctas, smem);
