@@ -482,7 +482,8 @@ def configs_section(dev):
     """BASELINE configs C1-C3 (parity-test sizes) and C4b (C4 with a 2D sine density profile, cells
     up to ~62,000 e-) timed through the operator: cold (the
     workload's random order every step) and warm (each step consumes the previous output),
-    mean of 20 calls after 3 warm-up calls, CUDA events; C1/C2 are launch/latency-bound."""
+    mean of 20 calls after 3 warm-up calls, CUDA events; C1/C2 are launch/latency-bound, so they are
+    also timed as 20 chained steps replayed from one CUDA graph (graph_ms_per_step)."""
     import torch
     import workloads as W
     import paper_2508_06771_b200 as cc
@@ -509,6 +510,40 @@ def configs_section(dev):
             ms = e0.elapsed_time(e1) / 20
             r[f"{mode}_ms_per_step"] = ms
             r[f"{mode}_pair_collisions_per_s"] = float(o.diag[2].item()) / (ms * 1e-3)
+        if name in ("C1", "C2"):
+            # launch-bound: the operator alone from a CUDA graph of 20 chained steps (the
+            # randoms advance through the device step counter, cc_params.step_dev); no roofline applies
+            sd = torch.zeros(1, dtype=torch.int32, device=dev)
+            ws = cc.alloc_workspace(w.n, w.cells, dev)
+            outs = [cc.coulomb_collide(v0, c0, w.cells, step=0, workspace=ws, step_dev=sd, **w.params())
+                    for _ in range(2)]
+
+            def chain():
+                v, c = v0, c0
+                for s in range(20):
+                    o = cc.coulomb_collide(v, c, w.cells, step=s, workspace=ws, step_dev=sd, out=outs[s % 2],
+                                           **w.params())
+                    v, c = o.v_out, o.cell_out
+                cc.cc_step_advance(sd, 20)
+
+            st = torch.cuda.Stream(dev)
+            st.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(st):
+                chain()                                 # warm-up outside capture
+            torch.cuda.current_stream(dev).wait_stream(st)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                chain()
+            g.replay()
+            torch.cuda.synchronize()
+            e0.record()
+            for _ in range(5):
+                g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            r["graph_ms_per_step"] = e0.elapsed_time(e1) / 100
+            r["graph_pair_collisions_per_s"] = float(outs[1].diag[2].item()) / (r["graph_ms_per_step"] * 1e-3)
         out[name] = r
     return out
 
