@@ -58,6 +58,10 @@ constexpr int kSub = CC_SUB;             // elements per warp sub-range in k_sca
 #ifndef CC_SCATTER_CTAS
 #define CC_SCATTER_CTAS 2
 #endif
+#ifndef CC_SCATTER_PREFETCH
+#define CC_SCATTER_PREFETCH 1
+#endif
+constexpr bool kScatterPrefetch = CC_SCATTER_PREFETCH != 0;   // next batch's cell ids loaded one batch ahead
 constexpr int kScatterUnrollA = CC_SCATTER_UA;   // cell loads in flight per lane, counting pass
 constexpr int kScatterUnrollB = CC_SCATTER_UB;   // (cell, v) loads in flight per lane, scatter pass
 // k_collide_large shape (tools/collide_shape.sh overrides them for design studies)
@@ -511,15 +515,24 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
     uint32_t* my = wcnt + w * MW;
     const uint32_t lt = (1u << lane) - 1u;
 
-    // pass A: per-warp counts of the sub-range (loads batched, branch-free)
+    // pass A: per-warp counts of the sub-range (loads batched, branch-free); the next batch's ids
+    // are loaded before this batch is counted (CC_SCATTER_PREFETCH)
+    int32_t cN[kScatterUnrollA];
+    auto fetchA = [&](int64_t i0) {
+#pragma unroll
+        for (int u = 0; u < kScatterUnrollA; ++u) cN[u] = __ldg(cell + min(i0 + 32 * u + lane, s1 - 1));
+    };
+    if (kScatterPrefetch && s0 < s1) fetchA(s0);
     for (int64_t i0 = s0; i0 < s1; i0 += 32 * kScatterUnrollA) {
         int32_t key[kScatterUnrollA];
+        if (!kScatterPrefetch) fetchA(i0);
 #pragma unroll
         for (int u = 0; u < kScatterUnrollA; ++u) {
             const int64_t i = i0 + 32 * u + lane;
-            const int32_t c = __ldg(cell + min(i, s1 - 1));
+            const int32_t c = cN[u];
             key[u] = (i >= s1) ? -1 - lane : ((c >= 0 && c < M) ? c : M);
         }
+        if (kScatterPrefetch && i0 + 32 * kScatterUnrollA < s1) fetchA(i0 + 32 * kScatterUnrollA);
         uint32_t peers[kScatterUnrollA];
 #pragma unroll
         for (int u = 0; u < kScatterUnrollA; ++u) peers[u] = __match_any_sync(0xFFFFFFFFu, key[u]);
@@ -546,17 +559,28 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
     }
     __syncthreads();
 
-    // pass B: ranks, destinations, 32-byte records (loads batched, branch-free)
+    // pass B: ranks, destinations, 32-byte records (loads batched, branch-free); the next batch's
+    // ids are loaded before this batch is ranked, its velocities at the top of its own iteration
+    int32_t cB[kScatterUnrollB];
+    auto fetchB = [&](int64_t i0) {
+#pragma unroll
+        for (int u = 0; u < kScatterUnrollB; ++u) cB[u] = __ldg(cell + min(i0 + 32 * u + lane, s1 - 1));
+    };
+    if (kScatterPrefetch && s0 < s1) fetchB(s0);
     for (int64_t i0 = s0; i0 < s1; i0 += 32 * kScatterUnrollB) {
         int32_t key[kScatterUnrollB];
         double x[kScatterUnrollB], y[kScatterUnrollB], z[kScatterUnrollB];
+        if (!kScatterPrefetch) fetchB(i0);
 #pragma unroll
         for (int u = 0; u < kScatterUnrollB; ++u) {
             const int64_t i = i0 + 32 * u + lane;
-            int32_t c;
-            load_batch<HAS_V>(v, ldv, cell, min(i, s1 - 1), x[u], y[u], z[u], c);
+            const int64_t ic = min(i, s1 - 1);
+            if (HAS_V) { x[u] = __ldg(v + ic); y[u] = __ldg(v + ldv + ic); z[u] = __ldg(v + 2 * ldv + ic); }
+            else { x[u] = y[u] = z[u] = 0.0; }
+            const int32_t c = cB[u];
             key[u] = (i >= s1) ? -1 - lane : ((c >= 0 && c < M) ? c : M);
         }
+        if (kScatterPrefetch && i0 + 32 * kScatterUnrollB < s1) fetchB(i0 + 32 * kScatterUnrollB);
         uint32_t peers[kScatterUnrollB], old[kScatterUnrollB];
 #pragma unroll
         for (int u = 0; u < kScatterUnrollB; ++u) peers[u] = __match_any_sync(0xFFFFFFFFu, key[u]);
