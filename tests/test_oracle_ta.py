@@ -126,3 +126,25 @@ def test_cell_constant_si_form(oracle_mod):
     urms = np.sqrt(6.0) * W.sigma_v(2.0)
     assert 1e-3 < Cj / urms ** 3 < 2e-2
     assert O.cell_constant(1000, 1e10, 1e-6, -1.0, 1e-10) == 0.0
+
+
+def test_cell_constant_from_rutherford_momentum_transfer(oracle_mod):
+    """C_j pinned by a different route than its own formula: TA's small-angle sampler accumulates
+    <1 - cos Theta> = 2 <delta^2> per step, and for Coulomb scattering that equals the momentum-
+    transfer rate nu_m dt = n sigma_m u dt with the Rutherford cross section integrated over impact
+    parameters, sigma_m = int (1 - cos chi) 2 pi b db = 4 pi b90^2 lnL, b90 = e^2 / (4 pi eps0 m_r u^2)
+    (tan(chi/2) = b90 / b).  So <delta^2> = n sigma_m u dt / 2 must equal the oracle's C_j / u^3 at
+    every u, to rounding; constants from scipy.constants (CODATA 2018, not the oracle's retyped ones).
+    Catches any factor of 2, pi, m vs m_r or eps0 power in C_j (the NRL relaxation pin only bounds
+    it to 5%)."""
+    import scipy.constants as sc
+    O = oracle_mod
+    N, w, V, lnL, dt = 2500, 3.7e9, 2e-6, 9.3, 7e-11
+    n = N * w / V
+    mr = sc.m_e / 2
+    Cj = O.cell_constant(N, w, V, lnL, dt, mass=sc.m_e, charge=sc.e, eps0=sc.epsilon_0)
+    for u in (1e4, 3.3e5, 2e6, 7.5e7):
+        b90 = sc.e ** 2 / (4 * np.pi * sc.epsilon_0 * mr * u ** 2)
+        sigma_m = 4 * np.pi * b90 ** 2 * lnL
+        delta2 = n * sigma_m * u * dt / 2
+        assert abs(Cj / u ** 3 - delta2) <= 1e-13 * delta2, (u, Cj / u ** 3, delta2)
