@@ -213,38 +213,51 @@ k_count(const int32_t* __restrict__ cell, int n, int M, int tile, int32_t* __res
     const int64_t end = min(start + tile, static_cast<int64_t>(n));
     const int lane = threadIdx.x & 31;
     int bad = 0, unsorted = 0;
-    // full 4-id groups (a tile starts at a multiple of 4: tile = W x sub, sub >= 256)
-    const int64_t vend = start + ((end - start) & ~static_cast<int64_t>(3));
-    const bool vec = (reinterpret_cast<uintptr_t>(cell) & 15u) == 0;
-    for (int64_t i0 = start; i0 < vend; i0 += 4 * static_cast<int64_t>(blockDim.x)) {
-        const int64_t i = i0 + 4 * static_cast<int64_t>(threadIdx.x);
+    // full 8-id groups (a tile starts at a multiple of 8: tile = W x sub, sub a multiple of 128):
+    // one 32-byte load per lane keeps twice the bytes of a 16-byte load in flight per warp
+    const int64_t vend = start + ((end - start) & ~static_cast<int64_t>(7));
+    const uintptr_t al = reinterpret_cast<uintptr_t>(cell);
+    for (int64_t i0 = start; i0 < vend; i0 += 8 * static_cast<int64_t>(blockDim.x)) {
+        const int64_t i = i0 + 8 * static_cast<int64_t>(threadIdx.x);
         const bool ok = i < vend;
         const unsigned act = __ballot_sync(0xFFFFFFFFu, ok);
         if (!ok) break;
-        int4 q;
-        if (vec) q = __ldg(reinterpret_cast<const int4*>(cell + i));
-        else q = make_int4(__ldg(cell + i), __ldg(cell + i + 1), __ldg(cell + i + 2), __ldg(cell + i + 3));
-        // an id is valid iff -1 <= c < M, i.e. (unsigned)(c + 1) <= M
-        bad |= (static_cast<uint32_t>(q.x + 1) > static_cast<uint32_t>(M)) |
-               (static_cast<uint32_t>(q.y + 1) > static_cast<uint32_t>(M)) |
-               (static_cast<uint32_t>(q.z + 1) > static_cast<uint32_t>(M)) |
-               (static_cast<uint32_t>(q.w + 1) > static_cast<uint32_t>(M));
-        const int32_t k0 = count_key(q.x, M), k1 = count_key(q.y, M), k2 = count_key(q.z, M),
-                      k3 = count_key(q.w, M);
-        int32_t prev = __shfl_up_sync(act, k3, 1);
+        int32_t c[8];
+        if ((al & 31u) == 0) {
+            unsigned long long a, b, d, e;
+            asm("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];" : "=l"(a), "=l"(b), "=l"(d), "=l"(e) : "l"(cell + i));
+            c[0] = static_cast<int32_t>(a); c[1] = static_cast<int32_t>(a >> 32);
+            c[2] = static_cast<int32_t>(b); c[3] = static_cast<int32_t>(b >> 32);
+            c[4] = static_cast<int32_t>(d); c[5] = static_cast<int32_t>(d >> 32);
+            c[6] = static_cast<int32_t>(e); c[7] = static_cast<int32_t>(e >> 32);
+        } else {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) c[u] = __ldg(cell + i + u);
+        }
+        int32_t k[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            // an id is valid iff -1 <= c < M, i.e. (unsigned)(c + 1) <= M
+            bad |= static_cast<uint32_t>(c[u] + 1) > static_cast<uint32_t>(M);
+            k[u] = count_key(c[u], M);
+        }
+        int32_t prev = __shfl_up_sync(act, k[7], 1);
         if (lane == 0) prev = (i > 0) ? count_key(__ldg(cell + i - 1), M) : 0;
-        unsorted |= (k0 < prev) | (k1 < k0) | (k2 < k1) | (k3 < k2);
-        const int32_t kl = __shfl_sync(act, k0, 0);
-        if (__all_sync(act, (k0 == kl) & (k1 == kl) & (k2 == kl) & (k3 == kl))) {
-            if (lane == 0) atomicAdd(&hist[kl], 4 * __popc(act));
+        unsorted |= k[0] < prev;
+#pragma unroll
+        for (int u = 1; u < 8; ++u) unsorted |= k[u] < k[u - 1];
+        const int32_t kl = __shfl_sync(act, k[0], 0);
+        bool same = true;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) same = same && (k[u] == kl);
+        if (__all_sync(act, same)) {
+            if (lane == 0) atomicAdd(&hist[kl], 8 * __popc(act));
             continue;
         }
-        atomicAdd(&hist[k0], 1);
-        atomicAdd(&hist[k1], 1);
-        atomicAdd(&hist[k2], 1);
-        atomicAdd(&hist[k3], 1);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) atomicAdd(&hist[k[u]], 1);
     }
-    for (int64_t i = vend + threadIdx.x; i < end; i += blockDim.x) {     // tail (< 4 ids)
+    for (int64_t i = vend + threadIdx.x; i < end; i += blockDim.x) {     // tail (< 8 ids)
         const int32_t c = __ldg(cell + i);
         bad |= static_cast<uint32_t>(c + 1) > static_cast<uint32_t>(M);
         const int32_t k = count_key(c, M);
