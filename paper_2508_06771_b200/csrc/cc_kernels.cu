@@ -528,12 +528,30 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
     uint32_t* my = wcnt + w * MW;
     const uint32_t lt = (1u << lane) - 1u;
 
-    // pass A: per-warp counts of the sub-range (loads batched, branch-free); the next batch's ids
-    // are loaded before this batch is counted (CC_SCATTER_PREFETCH)
+    // pass A: per-warp counts of the sub-range (loads batched, branch-free); counting is order-free,
+    // so lane l takes the kScatterUnrollA consecutive ids [i0 + l UA, ...) with 32-byte loads and
+    // "row" u of the match is the u-th id of every lane; the next batch's ids are loaded before
+    // this batch is counted (CC_SCATTER_PREFETCH)
+    static_assert(kScatterUnrollA % 8 == 0, "pass A loads 8 ids per 32-byte load");
+    const bool vec32 = (reinterpret_cast<uintptr_t>(cell) & 31u) == 0;
     int32_t cN[kScatterUnrollA];
     auto fetchA = [&](int64_t i0) {
+        const int64_t b = i0 + static_cast<int64_t>(kScatterUnrollA) * lane;
+        if (vec32 && b + kScatterUnrollA <= s1) {
 #pragma unroll
-        for (int u = 0; u < kScatterUnrollA; ++u) cN[u] = __ldg(cell + min(i0 + 32 * u + lane, s1 - 1));
+            for (int h = 0; h < kScatterUnrollA / 8; ++h) {
+                unsigned long long a0, a1, a2, a3;
+                asm("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
+                    : "=l"(a0), "=l"(a1), "=l"(a2), "=l"(a3) : "l"(cell + b + 8 * h));
+                cN[8 * h + 0] = static_cast<int32_t>(a0); cN[8 * h + 1] = static_cast<int32_t>(a0 >> 32);
+                cN[8 * h + 2] = static_cast<int32_t>(a1); cN[8 * h + 3] = static_cast<int32_t>(a1 >> 32);
+                cN[8 * h + 4] = static_cast<int32_t>(a2); cN[8 * h + 5] = static_cast<int32_t>(a2 >> 32);
+                cN[8 * h + 6] = static_cast<int32_t>(a3); cN[8 * h + 7] = static_cast<int32_t>(a3 >> 32);
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < kScatterUnrollA; ++u) cN[u] = __ldg(cell + min(b + u, s1 - 1));
+        }
     };
     if (kScatterPrefetch && s0 < s1) fetchA(s0);
     for (int64_t i0 = s0; i0 < s1; i0 += 32 * kScatterUnrollA) {
@@ -541,7 +559,7 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
         if (!kScatterPrefetch) fetchA(i0);
 #pragma unroll
         for (int u = 0; u < kScatterUnrollA; ++u) {
-            const int64_t i = i0 + 32 * u + lane;
+            const int64_t i = i0 + static_cast<int64_t>(kScatterUnrollA) * lane + u;
             const int32_t c = cN[u];
             key[u] = (i >= s1) ? -1 - lane : ((c >= 0 && c < M) ? c : M);
         }
