@@ -153,7 +153,7 @@ Layout make_layout(int64_t n, int32_t M)
     L.o_ref = o;      o = align256(o + static_cast<size_t>(M) * 4 * sizeof(double));
     L.o_trec = o;     o = align256(o + static_cast<size_t>(M) * kRec * sizeof(double));
     L.o_tilesum = o;  o = align256(o + static_cast<size_t>(L.T > 0 ? L.T : 1) * kTileSum * sizeof(double));
-    L.o_chunkcell = o; o = align256(o + static_cast<size_t>(L.max_chunks) * sizeof(int32_t));
+    L.o_chunkcell = o; o = align256(o + static_cast<size_t>(L.max_chunks) * sizeof(int4));
     L.o_perm = o;     o = align256(o + static_cast<size_t>(n > 0 ? n : 1) * sizeof(int32_t));   // CC_PRESERVE_ORDER
     L.o_wsv = o;      o = align256(o + static_cast<size_t>(n > 0 ? n : 1) * 4 * sizeof(double));
     L.total = o;
@@ -398,9 +398,9 @@ k_scan_cells(const int32_t* __restrict__ cnt, int M, int32_t* __restrict__ off, 
 // k_collide_large written by the whole warp (coalesced).
 __global__ void __launch_bounds__(256)
 k_cell_setup(const int32_t* __restrict__ cnt, const int32_t* __restrict__ chunk_off, int M,
-             int32_t* __restrict__ chunk_cell, double* __restrict__ Cj, cc::U4* __restrict__ keys,
+             int4* __restrict__ chunk_cell, double* __restrict__ Cj, cc::U4* __restrict__ keys,
              CellConst cc_, uint32_t cell_base, uint32_t step, uint32_t s0, uint32_t s1,
-             const uint32_t* __restrict__ step_dev)
+             const uint32_t* __restrict__ step_dev, const int32_t* __restrict__ off, int chunk)
 {
     const int j = blockIdx.x * 8 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
@@ -415,7 +415,9 @@ k_cell_setup(const int32_t* __restrict__ cnt, const int32_t* __restrict__ chunk_
         keys[j] = cc::philox4x32_10(cc::U4{0u, cell_base + static_cast<uint32_t>(j), step, 1u}, s0, s1);
     }
     const int32_t c1 = chunk_off[j + 1];
-    for (int32_t c = chunk_off[j] + lane; c < c1; c += 32) chunk_cell[c] = j;
+    // per chunk {cell, cell's first slot, N, first item}: k_collide_large starts from one load
+    const int32_t Nj = cnt[j], oj = off[j], c0 = chunk_off[j];
+    for (int32_t c = c0 + lane; c < c1; c += 32) chunk_cell[c] = make_int4(j, oj, Nj, (c - c0) * chunk);
 }
 
 // ------------------------------------------------------------------ CCS3: stable scatter
@@ -680,7 +682,7 @@ struct CollideArgs {
     const int32_t* cnt;
     const int32_t* off;
     const int32_t* chunk_off;
-    const int32_t* chunk_cell;  // [max_chunks] cell of each chunk (valid below chunk_off[M])
+    const int4* chunk_cell;     // [max_chunks] {cell, cell's first slot, N, first item} (valid below chunk_off[M])
     const double* Cj;
     const cc::U4* keys;
     double* v_out;
@@ -973,12 +975,13 @@ k_collide_large(CollideArgs A)
     __shared__ double aq[NANBU ? kCollideThreads / 32 : 1][NANBU ? kWarpItems : 1];  // Nanbu A per item
     __shared__ double red[kCollideThreads / 32][6];
     const int c = blockIdx.x;
-    if (c >= A.chunk_off[A.M]) return;      // grid is an upper bound on the chunk count
-    const int j = A.chunk_cell[c];
-    const int32_t N = A.cnt[j], o = A.off[j];
+    if (c >= __ldg(A.chunk_off + A.M)) return;      // grid is an upper bound on the chunk count
+    const int4 cm = __ldg(A.chunk_cell + c);
+    const int j = cm.x;
+    const int32_t N = cm.z, o = cm.y;
     const uint32_t step = eff_step(A);
     const uint32_t items = static_cast<uint32_t>(N + 1) / 2;
-    const uint32_t i0 = static_cast<uint32_t>(c - A.chunk_off[j]) * static_cast<uint32_t>(A.chunk);
+    const uint32_t i0 = static_cast<uint32_t>(cm.w);
     const uint32_t i1 = min(i0 + static_cast<uint32_t>(A.chunk), items);
     const bool triplet = (A.model & cc::kOddTriplet) && (N & 1);   // N > 64 here
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1845,9 +1848,9 @@ int run_binning(const double* v_in, int64_t ldv, const int32_t* cell_in, int n, 
     mark(ev, 1, st);
     k_scan_tiles<<<(M1 + 31) / 32, dim3(32, kScanRows), 0, st>>>(tcount, L.T, M1, cnt);
     k_scan_cells<<<1, 1024, 0, st>>>(cnt, M, off, chunk_off, L.chunk);
-    k_cell_setup<<<(M + 7) / 8, 256, 0, st>>>(cnt, chunk_off, M, at<int32_t>(ws, L.o_chunkcell), Cj, keys, k,
+    k_cell_setup<<<(M + 7) / 8, 256, 0, st>>>(cnt, chunk_off, M, at<int4>(ws, L.o_chunkcell), Cj, keys, k,
                                                    cell_base, step, static_cast<uint32_t>(seed),
-                                                   static_cast<uint32_t>(seed >> 32), step_dev);
+                                                   static_cast<uint32_t>(seed >> 32), step_dev, off, L.chunk);
     mark(ev, 2, st);
     if (v_in)
         k_scatter<true><<<L.T, 32 * L.W, smem, st>>>(v_in, ldv, cell_in, n, M, L.W, L.sub, tcount, off, wsv, skip,
@@ -1989,7 +1992,7 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     A.cnt = at<int32_t>(workspace, L.o_cnt);
     A.off = at<int32_t>(workspace, L.o_off);
     A.chunk_off = at<int32_t>(workspace, L.o_chunk);
-    A.chunk_cell = at<int32_t>(workspace, L.o_chunkcell);
+    A.chunk_cell = at<int4>(workspace, L.o_chunkcell);
     A.Cj = at<double>(workspace, L.o_C);
     A.keys = at<cc::U4>(workspace, L.o_keys);
     A.v_out = v_out;
