@@ -61,6 +61,8 @@ def lib():
         L.or_feistel_pi.restype = C.c_int64
         L.or_cell_perm.argtypes = [C.c_int64, C.c_uint32, C.c_uint32, C.c_uint64, C.c_void_p]
         L.or_cell_perm.restype = None
+        L.or_cell_perm_uniform.argtypes = [C.c_int64, C.c_uint32, C.c_uint32, C.c_uint64, C.c_void_p]
+        L.or_cell_perm_uniform.restype = None
         L.or_cell_keys.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, u32p]
         L.or_cell_keys.restype = None
         L.or_pair_uniforms.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
@@ -155,12 +157,20 @@ def feistel_pi(i: int, N: int, keys) -> int:
     return lib().or_feistel_pi(i, N, np.ascontiguousarray(keys, dtype=np.uint32))
 
 
-def cell_perm(N: int, G: int, step: int, seed: int) -> np.ndarray:
-    """pi_j as a table: pi[q] = stable slot at pair-order position q (R1)."""
+def cell_perm(N: int, G: int, step: int, seed: int, uniform: bool = False) -> np.ndarray:
+    """pi_j as a table: pi[q] = stable slot at pair-order position q.  Default: the
+    blocked pairing R1b; uniform=True: R1 over the whole cell
+    (CC_CELL_UNIFORM).  The two agree for N <= BLOCK."""
     out = np.zeros(max(N, 0), np.int64)
     if N > 0:
-        lib().or_cell_perm(N, G, step, seed, _ptr(out))
+        (lib().or_cell_perm_uniform if uniform else lib().or_cell_perm)(N, G, step, seed, _ptr(out))
     return out
+
+
+# R1b constants (DESIGN.md §3): segment length, segments per block, block size
+SEG = 32
+BLOCK_SEGS = 12
+BLOCK = SEG * BLOCK_SEGS
 
 
 def pair_uniforms(k: int, G: int, step: int, seed: int):
@@ -228,6 +238,7 @@ class OracleResult:
 ODD_TRIPLET = 1
 NANBU = 2
 PRESERVE_ORDER = 4
+CELL_UNIFORM = 8
 
 
 def nanbu_A(s: float) -> float:

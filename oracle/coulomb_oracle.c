@@ -247,29 +247,100 @@ int64_t or_feistel_pi(int64_t i, int64_t N, const uint32_t k[4])
 
 void or_cell_keys(uint32_t G, uint32_t step, uint64_t seed, uint32_t k[4]);
 
-/* pi_j as a full table: pi[q] = stable slot (0..N-1) at pair-order position q. */
-void or_cell_perm(int64_t N, uint32_t G, uint32_t step, uint64_t seed, int64_t *pi)
+/* The R1 construction over n items with a chosen key stream (used for the
+ * whole cell in R1, and for the segment order sigma and the block
+ * permutations tau_b of R1b below):
+ *   n <= 64: item s draws word (s mod 4) of Philox(ctr = (sort_base + s div 4,
+ *            G, step, sort_purpose)); pi lists the items by increasing (key, s);
+ *   n > 64:  the 8-round keyed Feistel above with k = Philox(ctr = (feistel_ctr,
+ *            G, step, feistel_purpose)).
+ * R1 itself is sort_base = 0, sort_purpose = 2, feistel_ctr = 0, feistel_purpose = 1. */
+static void or_r1_perm(int64_t n, uint32_t G, uint32_t step, uint64_t seed,
+                       uint32_t sort_base, uint32_t sort_purpose,
+                       uint32_t feistel_ctr, uint32_t feistel_purpose, int64_t *pi)
 {
-    if (N <= 0) return;
-    if (N <= OR_SMALL_CELL) {
-        uint32_t key[2] = { (uint32_t)seed, (uint32_t)(seed >> 32) };
+    uint32_t key[2] = { (uint32_t)seed, (uint32_t)(seed >> 32) };
+    if (n <= 0) return;
+    if (n <= OR_SMALL_CELL) {
         uint32_t r[OR_SMALL_CELL];
-        for (int64_t s = 0; s < N; ++s) {
-            uint32_t ctr[4] = { (uint32_t)(s / 4), G, step, 2u }, w[4];
+        for (int64_t s = 0; s < n; ++s) {
+            uint32_t ctr[4] = { sort_base + (uint32_t)(s / 4), G, step, sort_purpose }, w[4];
             or_philox4x32_10(ctr, key, w);
             r[s] = w[s % 4];
         }
-        for (int64_t s = 0; s < N; ++s) {           /* rank of slot s */
+        for (int64_t s = 0; s < n; ++s) {           /* rank of item s */
             int64_t rank = 0;
-            for (int64_t t = 0; t < N; ++t)
+            for (int64_t t = 0; t < n; ++t)
                 if (r[t] < r[s] || (r[t] == r[s] && t < s)) ++rank;
             pi[rank] = s;
         }
         return;
     }
-    uint32_t k[4];
-    or_cell_keys(G, step, seed, k);
-    for (int64_t q = 0; q < N; ++q) pi[q] = or_feistel_pi(q, N, k);
+    uint32_t ctr[4] = { feistel_ctr, G, step, feistel_purpose }, k[4];
+    or_philox4x32_10(ctr, key, k);
+    for (int64_t q = 0; q < n; ++q) pi[q] = or_feistel_pi(q, n, k);
+}
+
+/* R1 (CC_CELL_UNIFORM): pi_j over the whole cell, pi[q] = stable slot (0..N-1)
+ * at pair-order position q. */
+void or_cell_perm_uniform(int64_t N, uint32_t G, uint32_t step, uint64_t seed, int64_t *pi)
+{
+    or_r1_perm(N, G, step, seed, 0u, 2u, 0u, 1u, pi);
+}
+
+/* R1b (the default pairing): blocked random pairing.  Cells of N <= OR_BLOCK
+ * slots are one block and get R1 unchanged.  A larger cell's stable slots are
+ * cut into S_f = floor(N / L) segments of L consecutive slots
+ * [s L, s L + L) plus, if N mod L > 0, a tail segment [S_f L, N).  The full
+ * segments are put in a random order sigma (the R1 construction over S_f items
+ * with sort purpose 6 / Feistel purpose 5); the tail goes last.  Consecutive
+ * groups of OR_BLOCK_SEGS segments of that sequence form the blocks
+ * b = 0 .. ceil(S / OR_BLOCK_SEGS) - 1 (S = number of segments, tail included);
+ * block b's slots, listed segment by segment in sequence order, are its
+ * "block slots" u = 0 .. n_b - 1 (n_b = OR_BLOCK except for the last block).
+ * Inside block b the R1 construction over n_b items with sort counters
+ * (b OR_BLOCK / 4 + u div 4, purpose 2) and Feistel counter (b, purpose 1)
+ * gives tau_b, and pair-order position q = b OR_BLOCK + r holds the slot of
+ * block slot tau_b(r).  Pairs never straddle blocks (OR_BLOCK is even); an odd
+ * cell's last block is odd and its last position N - 1 sits out (R2).
+ * Every block is a uniformly random set of whole segments, so every step mixes
+ * the cell across its blocks; a block fits one CTA's shared memory on the GPU
+ * (R1b gives the reasons and the uniformity evidence).              */
+#define OR_SEG 32
+#define OR_BLOCK_SEGS 12
+#define OR_BLOCK (OR_SEG * OR_BLOCK_SEGS)
+
+void or_cell_perm(int64_t N, uint32_t G, uint32_t step, uint64_t seed, int64_t *pi)
+{
+    if (N <= 0) return;
+    if (N <= OR_BLOCK) {
+        or_cell_perm_uniform(N, G, step, seed, pi);
+        return;
+    }
+    int64_t Sf = N / OR_SEG, tail = N - Sf * OR_SEG;
+    int64_t S = Sf + (tail > 0 ? 1 : 0);
+    int64_t *sigma = (int64_t *)malloc(sizeof(int64_t) * (size_t)Sf);
+    or_r1_perm(Sf, G, step, seed, 0u, 6u, 0u, 5u, sigma);
+    /* seq_start[p] = first stable slot of the segment at sequence position p */
+    int64_t *seq_start = (int64_t *)malloc(sizeof(int64_t) * (size_t)S);
+    for (int64_t p = 0; p < Sf; ++p) seq_start[p] = sigma[p] * OR_SEG;
+    if (tail > 0) seq_start[Sf] = Sf * OR_SEG;
+    int64_t nblocks = (S + OR_BLOCK_SEGS - 1) / OR_BLOCK_SEGS;
+    int64_t *slot = (int64_t *)malloc(sizeof(int64_t) * OR_BLOCK);
+    int64_t *tau = (int64_t *)malloc(sizeof(int64_t) * OR_BLOCK);
+    for (int64_t b = 0; b < nblocks; ++b) {
+        int64_t nb = 0;                                  /* block slots of block b */
+        for (int64_t p = b * OR_BLOCK_SEGS; p < S && p < (b + 1) * OR_BLOCK_SEGS; ++p) {
+            int64_t len = (p == Sf) ? tail : OR_SEG;
+            for (int64_t i = 0; i < len; ++i) slot[nb++] = seq_start[p] + i;
+        }
+        or_r1_perm(nb, G, step, seed, (uint32_t)(b * (OR_BLOCK / 4)), 2u, (uint32_t)b, 1u, tau);
+        for (int64_t r = 0; r < nb; ++r) pi[b * OR_BLOCK + r] = slot[tau[r]];
+    }
+    free(tau);
+    free(slot);
+    free(seq_start);
+    free(sigma);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -474,6 +545,7 @@ void or_nanbu_pair(double va[3], double vb[3], double C, double u1, double u2)
 #define OR_ODD_TRIPLET 1u
 #define OR_NANBU 2u
 #define OR_PRESERVE_ORDER 4u
+#define OR_CELL_UNIFORM 8u     /* R1 over the whole cell instead of R1b's blocks */
 
 /* one binary collision of the selected model */
 void or_collide_pair(double va[3], double vb[3], double C, double u1, double u2, uint32_t flags)
@@ -602,7 +674,8 @@ int or_coulomb_collide(const double *v_in, int64_t ldv, const int32_t *cell_in,
         if (N == 0) continue;
         uint32_t G = cell_base + (uint32_t)j;
         int64_t *pi = (int64_t *)malloc(sizeof(int64_t) * (size_t)N);
-        or_cell_perm(N, G, (uint32_t)step, seed, pi);
+        if (flags & OR_CELL_UNIFORM) or_cell_perm_uniform(N, G, (uint32_t)step, seed, pi);
+        else or_cell_perm(N, G, (uint32_t)step, seed, pi);
         double C = or_cell_constant(N, weight, volume_arr ? volume_arr[j] : volume,
                                     lnL_arr ? lnL_arr[j] : lnL, dt, mass, charge, eps0);
         int triplet = (flags & OR_ODD_TRIPLET) && N >= 3 && (N % 2 == 1);

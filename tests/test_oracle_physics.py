@@ -133,3 +133,36 @@ def test_cold_beams_relax_toward_maxwellian(oracle_mod):
         kurt.append(np.mean(x ** 4) - 3.0)
     assert abs(np.sum(v ** 2) - e0) < 1e-10 * e0
     assert max(abs(k) for k in kurt) < 0.35, kurt
+
+
+def test_blocked_pairing_relaxes_like_uniform_pairing_on_energy_sorted_input(oracle_mod):
+    """R1b's worst case: every cell's input is sorted by kinetic energy, so each 32-slot segment
+    holds particles of nearly equal speed.  Hot/cold equilibration (hot half 4 eV, cold half 1 eV,
+    tracked through perm_out over 10 steps at the configs' dt, 4 data/collision seeds) must
+    proceed at the rate of R1's whole-cell uniform pairing (itself pinned to the NRL law above)
+    within 2% on the mean (one seed's 10-step energy transfer scatters by ~1%)."""
+    O = oracle_mod
+    ncell, per, steps = 4, 100_000, 10
+    w = W.weight_for(per)
+    half = per // 2
+    drop = {0: [], O.CELL_UNIFORM: []}
+    for seed in range(4):
+        rng = np.random.default_rng(100 + seed)
+        v = np.concatenate([rng.normal(0, W.sigma_v(4.0), (3, ncell, half)),
+                            rng.normal(0, W.sigma_v(1.0), (3, ncell, half))], axis=2)
+        hot0 = np.concatenate([np.ones((ncell, half), bool), np.zeros((ncell, half), bool)], axis=1)
+        order = np.argsort((v ** 2).sum(axis=0), axis=1, kind="stable")   # energy-sorted in every cell
+        v = np.take_along_axis(v, order[None], axis=2).reshape(3, -1)
+        hot0 = np.take_along_axis(hot0, order, axis=1).reshape(-1)
+        cell0 = np.repeat(np.arange(ncell, dtype=np.int32), per)
+        for flags in drop:
+            vv, cc, hot = v, cell0, hot0
+            eh0 = (vv[:, hot] ** 2).sum()
+            for s in range(steps):
+                r = O.coulomb_collide(vv, cc, ncell, dt=W.DT, weight=w, cell_volume=W.CELL_VOLUME,
+                                      ln_lambda=W.LN_LAMBDA, seed=42 + seed, step=s, want_pairs=False,
+                                      flags=flags)
+                vv, cc, hot = r.v_out, r.cell_out, hot[r.perm_out]
+            drop[flags].append(eh0 - (vv[:, hot] ** 2).sum())
+    ratio = np.mean(drop[0]) / np.mean(drop[O.CELL_UNIFORM])
+    assert min(drop[0]) > 0 and abs(ratio - 1.0) < 0.02, (ratio, drop)
