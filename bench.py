@@ -720,6 +720,12 @@ def run_ours(args):
         if fl == _lib.CC_PRESERVE_ORDER:
             variants[name]["what"] = ("outputs in input order: the chain keeps the C4 input's random order "
                                       "(a cold-order step plus the scattered output stores)")
+    # R1 over the whole cell (CC_CELL_UNIFORM: gathered records, no index modes) in all three orders
+    model["flags"] = _lib.CC_CELL_UNIFORM
+    for mode in ("steady", "warm", "cold"):
+        r = run_mode(mode, max(3, K // 4), W, 500_000 + 1000 * len(mode))
+        variants["cell_uniform_" + mode] = {"flags": _lib.CC_CELL_UNIFORM, "ms_per_step": r["ms"],
+                                            "stages_ms": r["stages"], "value": r["pairs"] / (r["ms"] * 1e-3)}
     model["flags"] = 0
 
     # ---- end to end through the host-buffer entry coulomb_collide_host (cold input): every step

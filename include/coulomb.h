@@ -65,6 +65,15 @@ extern "C" {
  *                     16-byte stores).  Lets a caller keep its own particle order (and
  *                     skip copying cell_out / perm_out back, see coulomb_collide_host).  */
 #define CC_PRESERVE_ORDER 4u
+/* In-cell pairing (readings R1 / R1b; P:313-314 pairs adjacent entries of an
+ * atomically built index list and draws no permutation):
+ *  default           R1b, blocked pairing: a cell of N <= 384 slots is permuted as a whole
+ *                    (R1); a larger cell's stable slots are cut into 32-slot segments, the
+ *                    full segments are put in a keyed random order (the tail segment last),
+ *                    every 12 consecutive segments of that order form a block of <= 384
+ *                    slots, and R1 is applied inside each block; pairs never straddle blocks.
+ *  CC_CELL_UNIFORM   R1 over the whole cell (one keyed permutation of all N_j slots).      */
+#define CC_CELL_UNIFORM 8u
 
 #define CC_MAX_CELLS 32768  /* binning keeps per-warp cell counters in shared memory */
 #define CC_DIAG_LEN 16
@@ -212,12 +221,14 @@ int cc_bin(const int32_t *cell_in, int64_t n, int32_t cells,
            int32_t *perm_out, int32_t *off_out,
            void *workspace, size_t workspace_bytes, void *stream);
 
-/* Reading R1: for every pair of every cell, the two STABLE slots
+/* Readings R1b / R1: for every pair of every cell, the two STABLE slots
  * (off_j + pi_j(2k), off_j + pi_j(2k+1)), cell-major, k-minor, written to
  * pair_slots_out[2*g], [2*g+1]; g runs over sum_j floor(N_j/2) pairs, at most
- * max_pairs are written.  off: DEVICE [cells+1] as produced by cc_bin.       */
+ * max_pairs are written.  off: DEVICE [cells+1] as produced by cc_bin.  flags: 0
+ * (the default blocked pairing R1b) or CC_CELL_UNIFORM (R1); anything else is
+ * CC_EINVAL.  pi_j is computed from its definition slot by slot (a test hook).   */
 int cc_pairs(const int32_t *off, int32_t cells, uint32_t cell_base,
-             uint64_t seed, uint64_t step,
+             uint64_t seed, uint64_t step, uint32_t flags,
              int32_t *pair_slots_out, int64_t max_pairs, void *stream);
 
 /* R3: Philox4x32-10 of m counters ctr4 [m][4] with key (seed lo, seed hi). */

@@ -27,6 +27,7 @@ CC_ODD_TRIPLET = 1
 CC_NANBU = 2
 CC_NCCL_ID_BYTES = 128
 CC_PRESERVE_ORDER = 4
+CC_CELL_UNIFORM = 8
 STAGE_NAMES = ("count", "scan", "scatter", "collide", "finalize")
 
 # every symbol include/coulomb.h declares
@@ -93,7 +94,7 @@ def load():
     L.cc_strerror.restype = C.c_char_p
     L.cc_bin.argtypes = [vp, i64, i32, vp, vp, vp, sz, vp]
     L.cc_bin.restype = C.c_int
-    L.cc_pairs.argtypes = [vp, i32, u32, u64, u64, vp, i64, vp]
+    L.cc_pairs.argtypes = [vp, i32, u32, u64, u64, u32, vp, i64, vp]
     L.cc_pairs.restype = C.c_int
     L.cc_philox.argtypes = [vp, u64, vp, i64, vp]
     L.cc_philox.restype = C.c_int

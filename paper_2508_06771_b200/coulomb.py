@@ -208,13 +208,13 @@ def cc_bin(cell: torch.Tensor, cells: int, workspace: Optional[torch.Tensor] = N
     return perm, off
 
 
-def cc_pairs(off: torch.Tensor, cells: int, *, cell_base=0, seed=42, step=0) -> torch.Tensor:
+def cc_pairs(off: torch.Tensor, cells: int, *, cell_base=0, seed=42, step=0, flags=0) -> torch.Tensor:
     dev = off.device
     _need(off, "off", torch.int32, dev)
     cnt = (off[1:] - off[:-1]).to(torch.int64)
     npairs = int((cnt // 2).sum().item())
     out = torch.empty((max(npairs, 1), 2), dtype=torch.int32, device=dev)
-    rc = _lib.load().cc_pairs(_ptr(off), cells, cell_base, seed, step, _ptr(out), npairs,
+    rc = _lib.load().cc_pairs(_ptr(off), cells, cell_base, seed, step, flags, _ptr(out), npairs,
                               C.c_void_p(_stream(dev)))
     check(rc, "cc_pairs")
     return out[:npairs]

@@ -14,6 +14,11 @@
 namespace cc {
 
 constexpr int kSmallCell = 64;          // R1: N <= 64 uses the sort-by-key form
+// R1b (blocked pairing): segments of kSeg consecutive stable slots,
+// blocks of kBlockSegs segments = kBlock slots (one k_collide_large CTA each)
+constexpr int kSeg = 32;
+constexpr int kBlockSegs = 12;
+constexpr int kBlock = kSeg * kBlockSegs;
 
 // ---------------------------------------------------------------- Philox4x32-10
 struct U4 { uint32_t x, y, z, w; };
@@ -217,25 +222,48 @@ __device__ __forceinline__ uint32_t feistel_pi(const Feistel& f, uint32_t i)
     return x;
 }
 
-// Sort key of stable slot s in a small cell: word (s mod 4) of
-// Philox(ctr = (s div 4, G, step, 2), key = seed).
+// Sort key of item s of an R1 sort-by-key permutation: word (s mod 4) of
+// Philox(ctr = (base + s div 4, G, step, purpose), key = seed).  R1's small cell:
+// base 0, purpose 2; R1b's block b: base 96 b, purpose 2; R1b's segment order: purpose 6.
 __device__ __forceinline__ uint32_t small_key(uint32_t s, uint32_t G, uint32_t step,
-                                              uint32_t k0, uint32_t k1)
+                                              uint32_t k0, uint32_t k1, uint32_t base = 0u,
+                                              uint32_t purpose = 2u)
 {
-    const U4 w = philox4x32_10(U4{s >> 2, G, step, 2u}, k0, k1);
+    const U4 w = philox4x32_10(U4{base + (s >> 2), G, step, purpose}, k0, k1);
     const uint32_t q = s & 3u;
     return q == 0 ? w.x : q == 1 ? w.y : q == 2 ? w.z : w.w;
+}
+
+// One thread: the item at position r of the sort-by-key permutation of n <= 64 items
+// (used off the hot path: k_triplets, the cc_pairs test hook).
+__device__ __noinline__ uint32_t small_select(uint32_t n, uint32_t r, uint32_t G, uint32_t step,
+                                              uint32_t k0, uint32_t k1, uint32_t base, uint32_t purpose)
+{
+    uint32_t key[kSmallCell];
+    for (uint32_t s = 0; s < n; s += 4) {
+        const U4 w = philox4x32_10(U4{base + (s >> 2), G, step, purpose}, k0, k1);
+        key[s] = w.x;
+        if (s + 1 < n) key[s + 1] = w.y;
+        if (s + 2 < n) key[s + 2] = w.z;
+        if (s + 3 < n) key[s + 3] = w.w;
+    }
+    for (uint32_t s = 0; s < n; ++s) {
+        uint32_t rank = 0;
+        for (uint32_t t = 0; t < n; ++t) rank += (key[t] < key[s] || (key[t] == key[s] && t < s)) ? 1u : 0u;
+        if (rank == r) return s;
+    }
+    return 0u;
 }
 
 // Warp-cooperative pi table of a small cell (N <= 64): pi_sm[q] = slot at
 // pair-order position q.  All 32 lanes must call it; the warp must be converged.
 __device__ __forceinline__ void small_cell_perm(uint32_t N, uint32_t G, uint32_t step,
                                                 uint32_t k0, uint32_t k1, int lane,
-                                                int32_t* pi_sm)
+                                                int32_t* pi_sm, uint32_t base = 0u, uint32_t purpose = 2u)
 {
     const uint32_t s0 = static_cast<uint32_t>(lane), s1 = s0 + 32u;
-    const uint32_t r0 = (s0 < N) ? small_key(s0, G, step, k0, k1) : 0xFFFFFFFFu;
-    const uint32_t r1 = (s1 < N) ? small_key(s1, G, step, k0, k1) : 0xFFFFFFFFu;
+    const uint32_t r0 = (s0 < N) ? small_key(s0, G, step, k0, k1, base, purpose) : 0xFFFFFFFFu;
+    const uint32_t r1 = (s1 < N) ? small_key(s1, G, step, k0, k1, base, purpose) : 0xFFFFFFFFu;
     uint32_t rank0 = 0, rank1 = 0;
     for (uint32_t t = 0; t < N; ++t) {
         const uint32_t src = (t < 32u) ? r0 : r1;

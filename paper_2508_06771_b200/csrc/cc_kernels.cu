@@ -30,7 +30,7 @@
 
 // Ablation switch for performance studies only (tools/ablate.sh); 0 in every
 // build of the product: bit 0 skips the TA math, bit 1 pairs slots 2k, 2k+1
-// (no Feistel), bit 2 skips CCS4 (Philox + AS241).
+// (no Feistel), bit 2 skips CCS4 (Philox + AS241), bit 3 skips the index modes' stage copies.
 #ifndef CC_ABLATE
 #define CC_ABLATE 0
 #endif
@@ -84,10 +84,9 @@ constexpr int kScatterUnrollB = CC_SCATTER_UB;   // (cell, v) loads in flight pe
 constexpr int kP1Unroll = CC_P1_UNROLL, kP2BUnroll = CC_P2B_UNROLL;
 constexpr int kCollideThreads = CC_COLLIDE_THREADS;
 constexpr int kChunk = CC_CHUNK;         // items (pairs or sitter) per k_collide_large CTA
-constexpr int kRec = 8;                  // chunk moment record: S1' (3), S2' (3), pad
-constexpr int kSmallRec = 12;            // small-cell record: S1', S2' about the exact mean, the mean (3), pad
-constexpr int kCellSum = 4;              // per-cell raw post-collision sums: v (3), |v|^2
-constexpr int kTileSum = 4;              // per-tile raw pre-collision sums of live particles: v (3), |v|^2
+constexpr int kRec = 12;                 // chunk record: S1' (3), S2' (3) post-collision; raw pre-collision v (3), |v|^2; pad
+constexpr int kSmallRec = 16;            // small-cell record: S1', S2' about the exact mean, the mean (3), pad, pre (12..15)
+constexpr int kCellSum = 8;              // per-cell raw sums: post-collision v (3), |v|^2; pre-collision v (3), |v|^2
 constexpr int kScatterSmemBudget = CC_SCATTER_BUDGET_KB * 1024;   // per-warp counters of one CTA
 #ifndef CC_SCATTER_MAXW
 #define CC_SCATTER_MAXW 12
@@ -101,7 +100,7 @@ struct Layout {
     int chunk = kChunk;                  // pairs per k_collide_large CTA (multiple of kCollideThreads)
     int64_t max_chunks = 0;
     size_t o_err = 0, o_tcount = 0, o_cnt = 0, o_off = 0, o_chunk = 0, o_C = 0, o_keys = 0;
-    size_t o_perm = 0, o_small = 0, o_recs = 0, o_cellsum = 0, o_ref = 0, o_tilesum = 0, o_chunkcell = 0, o_trec = 0, o_wsv = 0, total = 0;
+    size_t o_seg = 0, o_perm = 0, o_small = 0, o_recs = 0, o_cellsum = 0, o_ref = 0, o_chunkcell = 0, o_trec = 0, o_wsv = 0, total = 0;
 };
 
 size_t align256(size_t x) { return (x + 255u) & ~static_cast<size_t>(255u); }
@@ -152,8 +151,8 @@ Layout make_layout(int64_t n, int32_t M)
     L.o_cellsum = o;  o = align256(o + static_cast<size_t>(M) * kCellSum * sizeof(double));
     L.o_ref = o;      o = align256(o + static_cast<size_t>(M) * 4 * sizeof(double));
     L.o_trec = o;     o = align256(o + static_cast<size_t>(M) * kRec * sizeof(double));
-    L.o_tilesum = o;  o = align256(o + static_cast<size_t>(L.T > 0 ? L.T : 1) * kTileSum * sizeof(double));
     L.o_chunkcell = o; o = align256(o + static_cast<size_t>(L.max_chunks) * sizeof(int4));
+    L.o_seg = o;      o = align256(o + static_cast<size_t>(L.max_chunks) * cc::kBlockSegs * sizeof(int32_t));  // R1b
     L.o_perm = o;     o = align256(o + static_cast<size_t>(n > 0 ? n : 1) * sizeof(int32_t));   // CC_PRESERVE_ORDER
     L.o_wsv = o;      o = align256(o + static_cast<size_t>(n > 0 ? n : 1) * 4 * sizeof(double));
     L.total = o;
@@ -188,8 +187,9 @@ __device__ __forceinline__ int32_t unpack_perm(double w)
 }
 
 // ------------------------------------------------------------------ CCS1: count
-// flags[0]: sticky invalid-id flag; flags[1]: "input not cell-sorted" (cleared
-// by the host before each call).  Sorted means live ids non-decreasing in input
+// flags[0]: sticky invalid-id flag; flags[1]: "input not cell-sorted"; flags[2]: the
+// number of descents (positions whose cell key is below the previous one's), which
+// selects the binning mode (bin_mode); flags[1..2] are cleared before each call.  Sorted means live ids non-decreasing in input
 // order with every dead/invalid particle after the last live one; then the
 // stable order is the identity and k_scatter packs the records in place.
 // Each thread takes 4 consecutive ids (one 16-byte load when the array is
@@ -202,6 +202,31 @@ __device__ __forceinline__ int32_t count_key(int32_t c, int M)
     return static_cast<uint32_t>(c) < static_cast<uint32_t>(M) ? c : M;
 }
 
+// Binning mode of a call, decided on the device from k_count's flags:
+//  kModeSorted  input already cell-sorted (dead last): the stable order is the identity,
+//               nothing is moved; the collide reads v_in at the stable slot itself;
+//  kModePerm    nearly sorted (descents <= n / kPermModeDiv, the steady state of a PIC loop
+//               that feeds the operator its own output): the scatter writes only the input
+//               index of each stable slot (4 bytes, the paper's "track and sort particle
+//               indices"); the collide reads v_in through it — mostly contiguous runs;
+//  kModeRec     otherwise (randomly ordered input): the scatter moves each particle as a
+//               32-byte record {vx, vy, vz, perm} and the collide reads the records.
+// Index modes are used only with R1b (index_modes != 0); R1 always takes kModeRec.
+constexpr int kModeRec = 0, kModePerm = 1, kModeSorted = 2;
+#ifndef CC_PERM_MODE_DIV
+#define CC_PERM_MODE_DIV 16
+#endif
+constexpr int kPermModeDiv = CC_PERM_MODE_DIV;   // (design studies: 0 = kModePerm for every unsorted input)
+__device__ __forceinline__ int bin_mode(const int32_t* flags, int n, int index_modes)
+{
+    if (!index_modes) return kModeRec;
+    if (__ldg(flags + 1) == 0) return kModeSorted;
+#ifdef CC_STUDY_NOREC
+    return kModePerm;                    // design study only: the R1b collide without its record path
+#endif
+    return static_cast<int64_t>(__ldg(flags + 2)) * kPermModeDiv <= n ? kModePerm : kModeRec;
+}
+
 __global__ void __launch_bounds__(kCountThreads)
 k_count(const int32_t* __restrict__ cell, int n, int M, int tile, int32_t* __restrict__ tcount,
         int32_t* __restrict__ flags)
@@ -212,7 +237,7 @@ k_count(const int32_t* __restrict__ cell, int n, int M, int tile, int32_t* __res
     const int64_t start = static_cast<int64_t>(blockIdx.x) * tile;
     const int64_t end = min(start + tile, static_cast<int64_t>(n));
     const int lane = threadIdx.x & 31;
-    int bad = 0, unsorted = 0;
+    int bad = 0, unsorted = 0;          // unsorted: this thread's descents (k[i] < k[i-1])
     // full 8-id groups (a tile starts at a multiple of 8: tile = W x sub, sub a multiple of 128):
     // one 32-byte load per lane keeps twice the bytes of a 16-byte load in flight per warp
     const int64_t vend = start + ((end - start) & ~static_cast<int64_t>(7));
@@ -243,9 +268,9 @@ k_count(const int32_t* __restrict__ cell, int n, int M, int tile, int32_t* __res
         }
         int32_t prev = __shfl_up_sync(act, k[7], 1);
         if (lane == 0) prev = (i > 0) ? count_key(__ldg(cell + i - 1), M) : 0;
-        unsorted |= k[0] < prev;
+        unsorted += k[0] < prev;
 #pragma unroll
-        for (int u = 1; u < 8; ++u) unsorted |= k[u] < k[u - 1];
+        for (int u = 1; u < 8; ++u) unsorted += k[u] < k[u - 1];
         const int32_t kl = __shfl_sync(act, k[0], 0);
         bool same = true;
 #pragma unroll
@@ -261,14 +286,18 @@ k_count(const int32_t* __restrict__ cell, int n, int M, int tile, int32_t* __res
         const int32_t c = __ldg(cell + i);
         bad |= static_cast<uint32_t>(c + 1) > static_cast<uint32_t>(M);
         const int32_t k = count_key(c, M);
-        if (i > 0) unsorted |= k < count_key(__ldg(cell + i - 1), M);
+        if (i > 0) unsorted += k < count_key(__ldg(cell + i - 1), M);
         atomicAdd(&hist[k], 1);
     }
+    __shared__ int32_t desc_sm;
+    if (threadIdx.x == 0) desc_sm = 0;
     const int any_bad = __syncthreads_or(bad);
-    const int any_unsorted = __syncthreads_or(unsorted);
+    const int wdesc = __reduce_add_sync(0xFFFFFFFFu, unsorted);
+    if (lane == 0 && wdesc) atomicAdd(&desc_sm, wdesc);
+    __syncthreads();
     if (threadIdx.x == 0) {
         if (any_bad) atomicOr(flags, 1);
-        if (any_unsorted) atomicOr(flags + 1, 1);
+        if (desc_sm) { atomicOr(flags + 1, 1); atomicAdd(flags + 2, desc_sm); }
     }
     int32_t* row = tcount + static_cast<int64_t>(blockIdx.x) * (M + 1);
     for (int i = threadIdx.x; i <= M; i += blockDim.x) row[i] = hist[i];
@@ -395,29 +424,54 @@ k_scan_cells(const int32_t* __restrict__ cnt, int M, int32_t* __restrict__ off, 
 
 // Per-cell constants (warp per cell, 8 cells per CTA): TA constant C_j (R5-R7),
 // Feistel keys (R1, R3) from lane 0, and the chunk -> cell table of
-// k_collide_large written by the whole warp (coalesced).
+// k_collide_large written by the whole warp (coalesced).  R1b (seg != NULL, chunk =
+// kBlock / 2): a cell of N > kBlock slots also gets its segment order sigma, written
+// as each block's kBlockSegs first stable slots (absolute: the cell offset included) in
+// seg[chunk * kBlockSegs + g]; the tail segment, if any, is the last entry.  Cells of
+// 64 < N <= kBlock (one block) get their consecutive segments, so the collide reads one table.
 __global__ void __launch_bounds__(256)
 k_cell_setup(const int32_t* __restrict__ cnt, const int32_t* __restrict__ chunk_off, int M,
              int4* __restrict__ chunk_cell, double* __restrict__ Cj, cc::U4* __restrict__ keys,
              CellConst cc_, uint32_t cell_base, uint32_t step, uint32_t s0, uint32_t s1,
-             const uint32_t* __restrict__ step_dev, const int32_t* __restrict__ off, int chunk)
+             const uint32_t* __restrict__ step_dev, const int32_t* __restrict__ off, int chunk,
+             int32_t* __restrict__ seg)
 {
+    __shared__ int32_t sig_sm[8][cc::kSmallCell];
     const int j = blockIdx.x * 8 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (j >= M) return;
+    if (step_dev) step += *step_dev;              // graph replay: effective step read on the device
+    const uint32_t G = cell_base + static_cast<uint32_t>(j);
     if (lane == 0) {
         const int32_t N = cnt[j];
         const double V = cc_.volume_arr ? cc_.volume_arr[j] : cc_.volume;
         const double lnL = cc_.ln_lambda_arr ? cc_.ln_lambda_arr[j] : cc_.ln_lambda;
         const double nj = static_cast<double>(N) * cc_.weight / V;
         Cj[j] = fmax(cc_.K * nj * lnL, 0.0);
-        if (step_dev) step += *step_dev;          // graph replay: effective step read on the device
-        keys[j] = cc::philox4x32_10(cc::U4{0u, cell_base + static_cast<uint32_t>(j), step, 1u}, s0, s1);
+        keys[j] = cc::philox4x32_10(cc::U4{0u, G, step, 1u}, s0, s1);
     }
     const int32_t c1 = chunk_off[j + 1];
     // per chunk {cell, cell's first slot, N, first item}: k_collide_large starts from one load
     const int32_t Nj = cnt[j], oj = off[j], c0 = chunk_off[j];
     for (int32_t c = c0 + lane; c < c1; c += 32) chunk_cell[c] = make_int4(j, oj, Nj, (c - c0) * chunk);
+    if (seg && Nj > cc::kSmallCell) {
+        int32_t* out = seg + static_cast<int64_t>(c0) * cc::kBlockSegs;
+        if (Nj > cc::kBlock) {
+            // R1b segment order sigma: the R1 construction over the S_f full segments with
+            // sort purpose 6 (S_f <= 64) / Feistel purpose 5; the tail segment goes last
+            const uint32_t Sf = static_cast<uint32_t>(Nj) / cc::kSeg;
+            if (Sf <= static_cast<uint32_t>(cc::kSmallCell)) {
+                cc::small_cell_perm(Sf, G, step, s0, s1, lane, sig_sm[threadIdx.x >> 5], 0u, 6u);
+                for (uint32_t p = lane; p < Sf; p += 32) out[p] = oj + sig_sm[threadIdx.x >> 5][p] * cc::kSeg;
+            } else {
+                const cc::Feistel f = cc::make_feistel(Sf, cc::philox4x32_10(cc::U4{0u, G, step, 5u}, s0, s1));
+                for (uint32_t p = lane; p < Sf; p += 32) out[p] = oj + static_cast<int32_t>(cc::feistel_pi(f, p)) * cc::kSeg;
+            }
+            if (lane == 0 && Sf * cc::kSeg < static_cast<uint32_t>(Nj)) out[Sf] = oj + static_cast<int32_t>(Sf) * cc::kSeg;
+        } else if (lane < cc::kBlockSegs) {
+            out[lane] = oj + lane * cc::kSeg;          // one block: the stable slots in order
+        }
+    }
 }
 
 // ------------------------------------------------------------------ CCS3: stable scatter
@@ -446,32 +500,6 @@ __device__ __forceinline__ void red_add_if(bool pred, uint32_t* addr, uint32_t v
                  :: "r"(a), "r"(static_cast<unsigned>(pred)), "r"(val) : "memory");
 }
 
-__device__ __forceinline__ void tile_pre_add(double (&pre)[kTileSum], double x, double y, double z)
-{
-    pre[0] += x; pre[1] += y; pre[2] += z;
-    pre[3] = fma(x, x, fma(y, y, fma(z, z, pre[3])));
-}
-
-// fixed-order block reduction of the per-thread pre-collision sums -> tilesum[tile]
-__device__ __forceinline__ void tile_pre_store(double (&pre)[kTileSum], double* tilesum, int W)
-{
-    __shared__ double red[kMaxScatterWarps][kTileSum];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-    for (int q = 0; q < kTileSum; ++q)
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) pre[q] += __shfl_down_sync(0xFFFFFFFFu, pre[q], d);
-    if (lane == 0)
-#pragma unroll
-        for (int q = 0; q < kTileSum; ++q) red[w][q] = pre[q];
-    __syncthreads();
-    if (threadIdx.x < kTileSum) {
-        double a = 0.0;
-        for (int ww = 0; ww < W; ++ww) a += red[ww][threadIdx.x];
-        if (tilesum) tilesum[static_cast<int64_t>(blockIdx.x) * kTileSum + threadIdx.x] = a;
-    }
-}
-
 template <bool HAS_V>
 __device__ __forceinline__ void load_batch(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__ cell,
                                            int64_t i, double& x, double& y, double& z, int32_t& c)
@@ -485,11 +513,15 @@ template <bool HAS_V>
 __global__ void __launch_bounds__(32 * kMaxScatterWarps, CC_SCATTER_CTAS)
 k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__ cell, int n, int M,
           int W, int sub, const int32_t* __restrict__ tbase, const int32_t* __restrict__ off,
-          double* __restrict__ wsv, const int32_t* __restrict__ flags, double* __restrict__ tilesum)
+          double* __restrict__ wsv, const int32_t* __restrict__ flags, int index_modes)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    double pre[kTileSum] = {0.0, 0.0, 0.0, 0.0};      // pre-collision sums of the tile's live particles
+    // binning mode (bin_mode): sorted -> nothing to move; perm -> 4-byte input indices only
+    const int mode = flags ? bin_mode(flags, n, index_modes) : kModeRec;
+    if (mode == kModeSorted) return;
+    const bool recs = mode == kModeRec;
+    int32_t* __restrict__ sperm = reinterpret_cast<int32_t*>(wsv);   // kModePerm: input index per stable slot
     if (flags && flags[1] == 0) {
         // input already cell-sorted: the stable order is the identity, so the
         // records are written in place (a streaming SoA -> 32-byte-record pack)
@@ -506,13 +538,9 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
             for (int u = 0; u < kScatterUnrollB; ++u) {
                 const int64_t i = i0 + 32 * u + lane;
                 const bool live = c[u] >= 0 && c[u] < M;
-                if (i < t1) {
-                    st256(wsv + 4 * i, x[u], y[u], z[u], pack_pc(static_cast<int32_t>(i), live ? c[u] : -1));
-                    if (live) tile_pre_add(pre, x[u], y[u], z[u]);
-                }
+                if (i < t1) st256(wsv + 4 * i, x[u], y[u], z[u], pack_pc(static_cast<int32_t>(i), live ? c[u] : -1));
             }
         }
-        tile_pre_store(pre, tilesum, W);
         return;
     }
     const int M1 = M + 1;
@@ -608,7 +636,7 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
         for (int u = 0; u < kScatterUnrollB; ++u) {
             const int64_t i = i0 + 32 * u + lane;
             const int64_t ic = min(i, s1 - 1);
-            if (HAS_V) { x[u] = __ldg(v + ic); y[u] = __ldg(v + ldv + ic); z[u] = __ldg(v + 2 * ldv + ic); }
+            if (HAS_V && recs) { x[u] = __ldg(v + ic); y[u] = __ldg(v + ldv + ic); z[u] = __ldg(v + 2 * ldv + ic); }
             else { x[u] = y[u] = z[u] = 0.0; }
             const int32_t c = cB[u];
             key[u] = (i >= s1) ? -1 - lane : ((c >= 0 && c < M) ? c : M);
@@ -631,13 +659,14 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
             if (b >= 0) {
                 const int32_t dest = base[b] + static_cast<int32_t>(o) + __popc(peers[u] & lt);
                 const int64_t i = i0 + 32 * u + lane;
-                st256(wsv + 4 * static_cast<int64_t>(dest), x[u], y[u], z[u],
-                      pack_pc(static_cast<int32_t>(i), b < M ? b : -1));
-                if (b < M) tile_pre_add(pre, x[u], y[u], z[u]);
+                if (recs)
+                    st256(wsv + 4 * static_cast<int64_t>(dest), x[u], y[u], z[u],
+                          pack_pc(static_cast<int32_t>(i), b < M ? b : -1));
+                else
+                    sperm[dest] = static_cast<int32_t>(i);
             }
         }
     }
-    tile_pre_store(pre, tilesum, W);
 }
 
 // ------------------------------------------------------------------ CCS4 + CCS5 items
@@ -698,6 +727,14 @@ struct CollideArgs {
     uint32_t cell_base, step, s0, s1;
     const uint32_t* step_dev;   // NULL, or DEVICE offset added to `step` (cc_params.step_dev)
     int chunk;                  // pairs per k_collide_large CTA (<= kChunk, multiple of kCollideThreads)
+    int blocked;                // R1b pairing (default); 0: R1 over the whole cell (CC_CELL_UNIFORM)
+    int index_modes;            // bin_mode may pick kModeSorted / kModePerm (R1b calls)
+    const int32_t* flags;       // k_count's flags (bin_mode)
+    int n;
+    const double* v_in;         // the caller's SoA input (read directly in the index modes)
+    int64_t ldvi;
+    int vec16;                  // v_in 16-byte aligned and ldvi even (16-byte copies of aligned runs)
+    const int32_t* seg;         // R1b: [chunks][kBlockSegs] first stable slot of each block segment
     // fused S2b + S2c push of the outputs (cc_params.push; NEXT f2): x_in is read at the
     // particle's input index, x_out / v_out / cell_out written at the output slot
     int push;
@@ -744,6 +781,29 @@ __device__ __forceinline__ Rec load_slot(const CollideArgs& A, int64_t s)
     Rec r;
     ld256(A.wsv + 4 * s, r.x, r.y, r.z, r.w);
     return r;
+}
+
+__device__ __forceinline__ int call_mode(const CollideArgs& A) { return bin_mode(A.flags, A.n, A.index_modes); }
+
+// Stable slot s in any binning mode: the record (kModeRec), or v_in at the slot's input
+// index (kModeSorted: the slot itself; kModePerm: the index k_scatter wrote).
+__device__ __forceinline__ Rec load_slot_m(const CollideArgs& A, int mode, int64_t s)
+{
+    if (mode == kModeRec) return load_slot(A, s);
+    const int64_t i = (mode == kModeSorted) ? s : static_cast<int64_t>(__ldg(reinterpret_cast<const int32_t*>(A.wsv) + s));
+    Rec r;
+    r.x = __ldg(A.v_in + i);
+    r.y = __ldg(A.v_in + A.ldvi + i);
+    r.z = __ldg(A.v_in + 2 * A.ldvi + i);
+    r.w = pack_pc(static_cast<int32_t>(i), 0);
+    return r;
+}
+
+// raw pre-collision sums v (3), |v|^2 (the diagnostics' "before" terms)
+__device__ __forceinline__ void pre_add(double (&pre)[4], double x, double y, double z)
+{
+    pre[0] += x; pre[1] += y; pre[2] += z;
+    pre[3] = fma(x, x, fma(y, y, fma(z, z, pre[3])));
 }
 
 // Fused push of one particle (cell j = its LOCAL collision cell, -1 dead): kick v (if E),
@@ -876,6 +936,8 @@ k_collide_small(CollideArgs A)
     const int32_t o = A.off[j];
     const uint32_t G = A.cell_base + static_cast<uint32_t>(j);
     const uint32_t step = eff_step(A);
+    const int mode = call_mode(A);
+    double pre[4] = {0.0, 0.0, 0.0, 0.0};
     cc::small_cell_perm(static_cast<uint32_t>(N), G, step, A.s0, A.s1, lane, pi_sm[w]);
     const double C = A.Cj[j];
     Acc acc;
@@ -888,17 +950,22 @@ k_collide_small(CollideArgs A)
     if (triplet && k == items - 2) {
         // R19: the last three of the pair order collide as a TA77 triplet
 #pragma unroll
-        for (int q = 0; q < 3; ++q) mine[q] = load_slot(A, o + pi_sm[w][N - 3 + q]);
+        for (int q = 0; q < 3; ++q) {
+            mine[q] = load_slot_m(A, mode, o + pi_sm[w][N - 3 + q]);
+            pre_add(pre, mine[q].x, mine[q].y, mine[q].z);
+        }
         triplet_update(A, G, C, step, mine);
 #pragma unroll
         for (int q = 0; q < 3; ++q) write_out_any(A, o + N - 3 + q, j, mine[q]);
         nmine = 3;
     } else if (k < items && !(triplet && k == items - 1)) {
         const int32_t pa = o + 2 * static_cast<int32_t>(k);
-        mine[0] = load_slot(A, o + pi_sm[w][2 * k]);
+        mine[0] = load_slot_m(A, mode, o + pi_sm[w][2 * k]);
+        pre_add(pre, mine[0].x, mine[0].y, mine[0].z);
         nmine = 1;
         if (2 * k + 1 < static_cast<uint32_t>(N)) {
-            mine[1] = load_slot(A, o + pi_sm[w][2 * k + 1]);
+            mine[1] = load_slot_m(A, mode, o + pi_sm[w][2 * k + 1]);
+            pre_add(pre, mine[1].x, mine[1].y, mine[1].z);
             double u1, u2;
             pair_uniforms(A, j, k, step, u1, u2);
             cc::collide_model(mine[0].x, mine[0].y, mine[0].z, mine[1].x, mine[1].y, mine[1].z, C, u1, u2, A.model);
@@ -923,12 +990,15 @@ k_collide_small(CollideArgs A)
     for (int t = 0; t < 3; ++t)
         if (t < nmine) q.post(mine[t].x, mine[t].y, mine[t].z, mx, my, mz);
     warp_reduce(q.a);
+    warp_reduce(pre);
     if (lane == 0) {
         double* r = A.small_recs + static_cast<int64_t>(j) * kSmallRec;
 #pragma unroll
         for (int c = 0; c < 6; ++c) r[c] = q.a[c];
         r[6] = mx; r[7] = my; r[8] = mz;
         r[9] = r[10] = r[11] = 0.0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) r[12 + c] = pre[c];
     }
 }
 
@@ -936,6 +1006,12 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
 {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem_src) : "memory");
+}
+
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src)
+{
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem_src) : "memory");
 }
 
 __device__ __forceinline__ void cp_async_wait_all()
@@ -951,6 +1027,18 @@ __device__ __forceinline__ void stage_slot(const CollideArgs& A, int64_t s, doub
     cp_async16(dst + 2, g + 2);
 }
 
+// A staged particle: interleaved 32-byte records (kModeRec) or, in the index modes, the
+// planar stage x[kBlock], y[kBlock], z[kBlock], input index (int32)[kBlock].
+__device__ __forceinline__ Rec stage_rec(const double* stage, bool planar, uint32_t u)
+{
+    if (planar)
+        return Rec{stage[u], stage[cc::kBlock + u], stage[2 * cc::kBlock + u],
+                   pack_pc(reinterpret_cast<const int32_t*>(stage + 3 * cc::kBlock)[u], 0)};
+    const double2 a01 = *reinterpret_cast<const double2*>(stage + 4 * u);
+    const double2 a23 = *reinterpret_cast<const double2*>(stage + 4 * u + 2);
+    return Rec{a01.x, a01.y, a23.x, a23.y};
+}
+
 // N_j > 64: one CTA per cell-aligned chunk of kChunk items, two phases:
 //  1. every thread computes pi_j(2k), pi_j(2k+1) (keyed Feistel, R1) for its
 //     items and issues cp.async gathers of both records into shared memory —
@@ -964,16 +1052,29 @@ constexpr int kWarpItems = 32 * kItemsPerThread;            // items of one warp
 constexpr size_t kCollideSmem = 2ull * kChunk * 4 * sizeof(double);
 static_assert(kChunk % kCollideThreads == 0, "chunk must be a whole number of thread items");
 
-template <bool NANBU, bool PUSH>
-__global__ void __launch_bounds__(kCollideThreads, CC_COLLIDE_CTAS)
+static_assert(kChunk >= cc::kBlock / 2, "one k_collide_large CTA holds an R1b block (stage and thread items)");
+
+// BLOCKED (R1b, the default pairing): the CTA owns block b = i0 / (kBlock/2) of its cell.
+// Phase 1 copies the block's segments (whole 32-record runs of the cell-sorted records,
+// in the block's segment order; cells of N <= kBlock are one block of consecutive slots)
+// into the stage with contiguous 16-byte cp.async — a warp instruction moves 512
+// consecutive bytes — and computes tau_b of each item's two block slots; phase 2 reads
+// the pair's records from the stage at those slots.  No random global access.
+#ifndef CC_BLOCKED_CTAS
+#define CC_BLOCKED_CTAS 10
+#endif
+template <bool NANBU, bool PUSH, bool BLOCKED>
+__global__ void __launch_bounds__(kCollideThreads, BLOCKED ? CC_BLOCKED_CTAS : CC_COLLIDE_CTAS)
 k_collide_large(CollideArgs A)
 {
-    extern __shared__ __align__(16) double stage[];       // [2][kChunk][4]
+    extern __shared__ __align__(16) double stage[];       // R1: [2][kChunk][4]; R1b: [kBlock][4]
+    __shared__ int32_t pi_small[BLOCKED ? cc::kSmallCell : 1];
+    __shared__ __align__(16) double ref_sm[4];             // R1b: the cell's first stable slot (moment shift)
     __shared__ double zq[kCollideThreads / 32][kWarpItems];  // normal variate z = Phi^-1(u1) per item
     __shared__ double u2q[kCollideThreads / 32][kWarpItems]; // u2 per item
     __shared__ int16_t tq[kCollideThreads / 32][kWarpItems]; // compacted AS241-tail (Nanbu: Newton) items
     __shared__ double aq[NANBU ? kCollideThreads / 32 : 1][NANBU ? kWarpItems : 1];  // Nanbu A per item
-    __shared__ double red[kCollideThreads / 32][6];
+    __shared__ double red[kCollideThreads / 32][10];
     const int c = blockIdx.x;
     if (c >= __ldg(A.chunk_off + A.M)) return;      // grid is an upper bound on the chunk count
     const int4 cm = __ldg(A.chunk_cell + c);
@@ -985,9 +1086,127 @@ k_collide_large(CollideArgs A)
     const uint32_t i1 = min(i0 + static_cast<uint32_t>(A.chunk), items);
     const bool triplet = (A.model & cc::kOddTriplet) && (N & 1);   // N > 64 here
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    // phase 1: pi_j (keyed Feistel, R1) of each item's two slots in lock step
+    const int mode = BLOCKED ? call_mode(A) : kModeRec;
+    int32_t nb = 0;                                        // R1b: slots of this CTA's block
+    uint32_t xs[kItemsPerThread][2];                      // R1b: block slots of each item's pair
+    if (BLOCKED) {
+        const uint32_t b = i0 / static_cast<uint32_t>(cc::kBlock / 2);
+        nb = min(N - static_cast<int32_t>(b) * cc::kBlock, cc::kBlock);
+        const int nseg = (nb + cc::kSeg - 1) / cc::kSeg;
+        int32_t sg[cc::kBlockSegs];                       // absolute first stable slot of each segment
+        {
+            const int4* sp = reinterpret_cast<const int4*>(A.seg + static_cast<int64_t>(c) * cc::kBlockSegs);
+#pragma unroll
+            for (int g4 = 0; g4 < cc::kBlockSegs / 4; ++g4) {
+                const int4 q = __ldg(sp + g4);
+                sg[4 * g4] = q.x; sg[4 * g4 + 1] = q.y; sg[4 * g4 + 2] = q.z; sg[4 * g4 + 3] = q.w;
+            }
+        }
+        if (mode == kModeRec) {
+            // 16-byte pieces: segment g = pieces [64 g, 64 g + 64), record (piece mod 64) / 2
+#pragma unroll
+            for (int g = 0; g < cc::kBlockSegs; ++g) {
+                if (g < nseg) {
+                    for (int p = threadIdx.x; p < 2 * cc::kSeg; p += kCollideThreads) {
+                        const int r = p >> 1, h = p & 1;
+                        if (g * cc::kSeg + r < nb)
+                            cp_async16(stage + 4 * (g * cc::kSeg + r) + 2 * h,
+                                       A.wsv + 4 * (static_cast<int64_t>(sg[g]) + r) + 2 * h);
+                    }
+                }
+            }
+            if (threadIdx.x < 2) cp_async16(ref_sm + 2 * threadIdx.x, A.wsv + 4 * static_cast<int64_t>(o) + 2 * threadIdx.x);
+        }
+        // index modes: the input indices are loaded first and the copies issued after tau_b,
+        // so the index loads' latency hides behind the Feistel rounds
+        static_assert(kCollideThreads % cc::kSeg == 0, "a warp covers whole segments");
+        constexpr int kPer = cc::kBlock / kCollideThreads;
+        int32_t idx[kPer];
+        int32_t iref = o;                                  // input index of the cell's first stable slot
+        if (mode != kModeRec) {
+            if (mode == kModePerm && threadIdx.x < 3) iref = __ldg(reinterpret_cast<const int32_t*>(A.wsv) + o);
+            // index modes: block slot u = stable slot o + sg[u / 32] + u % 32 = input index
+            // (kModeSorted) or the index k_scatter wrote (kModePerm); its three velocity
+            // components are copied from the SoA input (a warp reads 32 mostly consecutive
+            // indices: three coalesced 256-byte runs), w = the input index
+#pragma unroll
+            for (int q = 0; q < kPer; ++q) {
+                const int u = static_cast<int>(threadIdx.x) + q * kCollideThreads;
+                // segment of u: q * (kCollideThreads / 32) + w, selected without dynamic indexing
+                int32_t st0 = 0;
+#pragma unroll
+                for (int ww = 0; ww < kCollideThreads / cc::kSeg; ++ww)
+                    if (ww == w) st0 = sg[q * (kCollideThreads / cc::kSeg) + ww];
+                const int64_t sl = static_cast<int64_t>(st0) + lane;
+                idx[q] = (u < nb) ? (mode == kModeSorted ? static_cast<int32_t>(sl)
+                                                         : __ldg(reinterpret_cast<const int32_t*>(A.wsv) + sl))
+                                  : -1;
+            }
+        }
+        const uint32_t G = A.cell_base + static_cast<uint32_t>(j);
+        if (nb > cc::kSmallCell) {
+            const cc::Feistel f = cc::make_feistel(static_cast<uint32_t>(nb), cc::philox4x32_10(cc::U4{b, G, step, 1u}, A.s0, A.s1));
+#pragma unroll
+            for (int q = 0; q < kItemsPerThread; ++q) {
+                const uint32_t e = threadIdx.x + q * kCollideThreads;
+                uint32_t x[2] = {2 * e, 2 * e + 1};
+                if (i0 + e < i1 && !(CC_ABLATE & 2)) {
+                    cc::feistel_E_multi(f, x);
+                    while (x[0] >= f.N) x[0] = cc::feistel_E(f, x[0]);
+                    if (2 * e + 1 < static_cast<uint32_t>(nb))
+                        while (x[1] >= f.N) x[1] = cc::feistel_E(f, x[1]);
+                }
+                xs[q][0] = x[0];
+                xs[q][1] = x[1];
+            }
+        } else {
+            // the last block of a large cell holds <= 64 slots: R1's sort-by-key form
+            if (w == 0) cc::small_cell_perm(static_cast<uint32_t>(nb), G, step, A.s0, A.s1, lane, pi_small,
+                                           b * static_cast<uint32_t>(cc::kBlock / 4), 2u);
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < kItemsPerThread; ++q) {
+                const uint32_t e = threadIdx.x + q * kCollideThreads;
+                xs[q][0] = (2 * e < static_cast<uint32_t>(nb)) ? pi_small[2 * e] : 0u;
+                xs[q][1] = (2 * e + 1 < static_cast<uint32_t>(nb)) ? pi_small[2 * e + 1] : 0u;
+            }
+        }
+        if (mode != kModeRec) {
+            // planar stage (consecutive lanes -> consecutive 8-byte words: no bank conflicts)
+            int32_t* pw = reinterpret_cast<int32_t*>(stage + 3 * cc::kBlock);
+#pragma unroll
+            for (int q = 0; q < kPer; ++q) {
+                const int u = static_cast<int>(threadIdx.x) + q * kCollideThreads;
+                // a warp's 32 slots are one segment; when their input indices are one even-aligned
+                // run (always for sorted input in an even-offset cell; about half the segments of
+                // steady input) the three 256-byte rows move as 16-byte copies
+                const int32_t i0w = __shfl_sync(0xFFFFFFFFu, idx[q], 0);
+                const bool run = A.vec16 && __all_sync(0xFFFFFFFFu, idx[q] == i0w + lane) && (i0w & 1) == 0;
+                if (CC_ABLATE & 8) {
+                } else if (run) {
+                    const int seg0 = u - lane;                   // planar position of the segment
+#pragma unroll
+                    for (int r = 0; r < 2; ++r) {
+                        const int pc = lane + 32 * r;            // 48 pieces: row pc / 16, pair pc % 16
+                        if (pc < 48) {
+                            const int row = pc >> 4, h = pc & 15;
+                            cp_async16(stage + row * cc::kBlock + seg0 + 2 * h, A.v_in + row * A.ldvi + i0w + 2 * h);
+                        }
+                    }
+                } else if (idx[q] >= 0) {
+                    const double* src = A.v_in + idx[q];
+                    cp_async8(stage + u, src);
+                    cp_async8(stage + cc::kBlock + u, src + A.ldvi);
+                    cp_async8(stage + 2 * cc::kBlock + u, src + 2 * A.ldvi);
+                }
+                if (idx[q] >= 0) pw[u] = idx[q];
+            }
+            if (threadIdx.x < 3) cp_async8(ref_sm + threadIdx.x, A.v_in + iref + threadIdx.x * A.ldvi);
+        }
+    }
+    // phase 1 (R1): pi_j (keyed Feistel) of each item's two slots in lock step
     // (rare cycle walks afterwards), gathers issued item by item
-    {
+    if (!BLOCKED) {
         const cc::Feistel f = cc::make_feistel(static_cast<uint32_t>(N), A.keys[j]);
 #pragma unroll kP1Unroll
         for (int q = 0; q < kItemsPerThread; ++q) {
@@ -1036,14 +1255,23 @@ k_collide_large(CollideArgs A)
         }
     }
     // shift for the moment partials: pre-collision v of the cell's first stable slot
-    const Rec ref = load_slot(A, o);
+    Rec ref;
+    if (!BLOCKED) ref = load_slot(A, o);
+    const double C = A.Cj[j];
+    cp_async_wait_all();
+    __syncthreads();
+    if (BLOCKED) ref = Rec{ref_sm[0], ref_sm[1], ref_sm[2], 0.0};
     if (i0 == 0 && threadIdx.x == 0) {
         double* cr = A.cellref + 4 * static_cast<int64_t>(j);
         cr[0] = ref.x; cr[1] = ref.y; cr[2] = ref.z; cr[3] = 0.0;
     }
-    const double C = A.Cj[j];
-    cp_async_wait_all();
-    __syncthreads();
+    // raw pre-collision sums of the particles this thread updates (diagnostics)
+    double pre[4] = {0.0, 0.0, 0.0, 0.0};
+#ifdef CC_STUDY_NOREC
+    const bool planar = BLOCKED;
+#else
+    const bool planar = mode != kModeRec;
+#endif
 
     // phase 2b: CCS5 TA update out of shared memory, pair-ordered coalesced output
     if (NANBU) {
@@ -1060,12 +1288,10 @@ k_collide_large(CollideArgs A)
             const int slot = t * 32 + lane;
             bool newton = false;
             if (k < i1 && !(triplet && k + 2 >= items) && 2 * k + 1 < static_cast<uint32_t>(N)) {
-                const double2 a01 = *reinterpret_cast<const double2*>(stage + 4 * e);
-                const double az = stage[4 * e + 2];
-                const double2 b01 = *reinterpret_cast<const double2*>(stage + 4 * (kChunk + e));
-                const double bz = stage[4 * (kChunk + e) + 2];
+                const uint32_t ia = BLOCKED ? xs[t][0] : e, ib = BLOCKED ? xs[t][1] : kChunk + e;
+                const Rec a = stage_rec(stage, planar, ia), b = stage_rec(stage, planar, ib);
                 double Av, x;
-                newton = !cc::nanbu_A_direct(cc::nanbu_s(a01.x, a01.y, az, b01.x, b01.y, bz, C), Av, x);
+                newton = !cc::nanbu_A_direct(cc::nanbu_s(a.x, a.y, a.z, b.x, b.y, b.z, C), Av, x);
                 aq[w][slot] = newton ? x : Av;
             }
             const uint32_t nm = __ballot_sync(0xFFFFFFFFu, newton);
@@ -1090,13 +1316,12 @@ k_collide_large(CollideArgs A)
         if (k < i1 && !(triplet && k + 2 >= items)) {     // the triplet's two items: k_triplets
             const uint32_t e = k - i0;
             const int32_t pa = o + 2 * static_cast<int32_t>(k);
-            const double2 a01 = *reinterpret_cast<const double2*>(stage + 4 * e);
-            const double2 a23 = *reinterpret_cast<const double2*>(stage + 4 * e + 2);
-            Rec a{a01.x, a01.y, a23.x, a23.y};
+            const uint32_t ia = BLOCKED ? xs[t][0] : e, ib = BLOCKED ? xs[t][1] : kChunk + e;
+            Rec a = stage_rec(stage, planar, ia);
+            pre_add(pre, a.x, a.y, a.z);
             if (2 * k + 1 < static_cast<uint32_t>(N)) {
-                const double2 b01 = *reinterpret_cast<const double2*>(stage + 4 * (kChunk + e));
-                const double2 b23 = *reinterpret_cast<const double2*>(stage + 4 * (kChunk + e) + 2);
-                Rec b{b01.x, b01.y, b23.x, b23.y};
+                Rec b = stage_rec(stage, planar, ib);
+                pre_add(pre, b.x, b.y, b.z);
                 if (PUSH) {                                // the push's position gathers, in flight
                     prefetch_x(A, unpack_perm(a.w));       // during the collision arithmetic
                     prefetch_x(A, unpack_perm(b.w));
@@ -1115,17 +1340,39 @@ k_collide_large(CollideArgs A)
         }
     }
     warp_reduce(acc.a);
-    if (lane == 0)
+    warp_reduce(pre);
+    if (lane == 0) {
 #pragma unroll
         for (int q = 0; q < 6; ++q) red[w][q] = acc.a[q];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) red[w][6 + q] = pre[q];
+    }
     __syncthreads();
     if (threadIdx.x < kRec) {
         double sum = 0.0;
-        if (threadIdx.x < 6)
+        if (threadIdx.x < 10)
 #pragma unroll
             for (int ww = 0; ww < kCollideThreads / 32; ++ww) sum += red[ww][threadIdx.x];
         A.recs[static_cast<int64_t>(c) * kRec + threadIdx.x] = sum;
     }
+}
+
+// R1b: the stable slot (relative to the cell) at pair-order position q of a cell of
+// N > kBlock slots, from the segment table k_cell_setup wrote (one thread, off the hot path)
+__device__ __noinline__ uint32_t blocked_slot(const CollideArgs& A, int j, int32_t N, uint32_t q)
+{
+    const uint32_t b = q / cc::kBlock, r = q % cc::kBlock;
+    const uint32_t nb = static_cast<uint32_t>(min(N - static_cast<int32_t>(b) * cc::kBlock, cc::kBlock));
+    const uint32_t G = A.cell_base + static_cast<uint32_t>(j), step = eff_step(A);
+    uint32_t u;
+    if (nb > static_cast<uint32_t>(cc::kSmallCell)) {
+        const cc::Feistel f = cc::make_feistel(nb, cc::philox4x32_10(cc::U4{b, G, step, 1u}, A.s0, A.s1));
+        u = cc::feistel_pi(f, r);
+    } else {
+        u = cc::small_select(nb, r, G, step, A.s0, A.s1, b * (cc::kBlock / 4), 2u);
+    }
+    const int32_t c = A.chunk_off[j] + static_cast<int32_t>(b);
+    return static_cast<uint32_t>(A.seg[static_cast<int64_t>(c) * cc::kBlockSegs + u / cc::kSeg] - A.off[j]) + u % cc::kSeg;
 }
 
 // Triplet mode, N_j > 64 and odd: thread per cell runs R19 on the last three
@@ -1140,12 +1387,21 @@ __global__ void k_triplets(CollideArgs A)
     double* tr = A.trec + static_cast<int64_t>(j) * kRec;
     Acc acc;
     acc.zero();
+    double pre[4] = {0.0, 0.0, 0.0, 0.0};
     if (N & 1) {
         const int32_t o = A.off[j];
-        const cc::Feistel f = cc::make_feistel(static_cast<uint32_t>(N), A.keys[j]);
         Rec r[3];
+        if (A.blocked && N > cc::kBlock) {
+#pragma unroll 1
+            for (int q = 0; q < 3; ++q)
+                r[q] = load_slot_m(A, call_mode(A), o + static_cast<int64_t>(blocked_slot(A, j, N, static_cast<uint32_t>(N - 3 + q))));
+        } else {
+            const cc::Feistel f = cc::make_feistel(static_cast<uint32_t>(N), A.keys[j]);
 #pragma unroll
-        for (int q = 0; q < 3; ++q) r[q] = load_slot(A, o + static_cast<int64_t>(cc::feistel_pi(f, N - 3 + q)));
+            for (int q = 0; q < 3; ++q) r[q] = load_slot(A, o + static_cast<int64_t>(cc::feistel_pi(f, N - 3 + q)));
+        }
+#pragma unroll
+        for (int q = 0; q < 3; ++q) pre_add(pre, r[q].x, r[q].y, r[q].z);
         triplet_update(A, A.cell_base + static_cast<uint32_t>(j), A.Cj[j], eff_step(A), r);
         const double* cr = A.cellref + 4 * static_cast<int64_t>(j);
 #pragma unroll
@@ -1156,7 +1412,9 @@ __global__ void k_triplets(CollideArgs A)
     }
 #pragma unroll
     for (int q = 0; q < 6; ++q) tr[q] = acc.a[q];
-    tr[6] = tr[7] = 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tr[6 + q] = pre[q];
+    tr[10] = tr[11] = 0.0;
 }
 
 // CC_PRESERVE_ORDER, pass 1: output position p -> a 32-byte record {v, cell} at the
@@ -1191,9 +1449,10 @@ __global__ void k_unpack(const double* __restrict__ wsv, int64_t n, double* __re
 __global__ void k_copy_dead(CollideArgs A, int n)
 {
     const int32_t L = A.off[A.M];
+    const int mode = call_mode(A);
     for (int64_t p = L + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < n;
          p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const Rec r = load_slot(A, p);
+        const Rec r = load_slot_m(A, mode, p);
         write_out_any(A, static_cast<int32_t>(p), -1, r);
     }
 }
@@ -1231,14 +1490,14 @@ __global__ void k_finalize_cells(const int32_t* __restrict__ cnt, const int32_t*
     const int lane = threadIdx.x & 31;
     if (j >= M) return;
     const int32_t N = cnt[j];
-    double s[6] = {0, 0, 0, 0, 0, 0};
+    double s[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};    // post S1', S2' (6), raw pre (4)
     double rx = 0, ry = 0, rz = 0;
     if (N > cc::kSmallCell) {
         for (int32_t c = chunk_off[j] + lane; c < chunk_off[j + 1]; c += 32)
 #pragma unroll
-            for (int q = 0; q < 6; ++q) s[q] += recs[static_cast<int64_t>(c) * kRec + q];
+            for (int q = 0; q < 10; ++q) s[q] += recs[static_cast<int64_t>(c) * kRec + q];
 #pragma unroll
-        for (int q = 0; q < 6; ++q)
+        for (int q = 0; q < 10; ++q)
 #pragma unroll
             for (int d = 16; d > 0; d >>= 1) s[q] += __shfl_down_sync(0xFFFFFFFFu, s[q], d);
     }
@@ -1248,13 +1507,15 @@ __global__ void k_finalize_cells(const int32_t* __restrict__ cnt, const int32_t*
             const double* r = small_recs + static_cast<int64_t>(j) * kSmallRec;
 #pragma unroll
             for (int q = 0; q < 6; ++q) s[q] = r[q];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) s[6 + q] = r[12 + q];
             rx = r[6]; ry = r[7]; rz = r[8];
         } else {
             const double* cr = cellref + 4 * static_cast<int64_t>(j);
             rx = cr[0]; ry = cr[1]; rz = cr[2];
             if (trec)
 #pragma unroll
-                for (int q = 0; q < 6; ++q) s[q] += trec[static_cast<int64_t>(j) * kRec + q];
+                for (int q = 0; q < 10; ++q) s[q] += trec[static_cast<int64_t>(j) * kRec + q];
         }
     }
     if (moments_out) {
@@ -1278,12 +1539,14 @@ __global__ void k_finalize_cells(const int32_t* __restrict__ cnt, const int32_t*
         e += s[3 + q] + 2.0 * r[q] * s[q] + Nd * r[q] * r[q];
     }
     cs[3] = e;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) cs[4 + q] = s[6 + q];
 }
 
 // single CTA of 1024 threads: fixed-order reductions over cells and tiles
 __global__ void __launch_bounds__(1024)
 k_finalize_diag(const int32_t* __restrict__ cnt, const double* __restrict__ cellsum, int M,
-                const double* __restrict__ tilesum, int T, double* __restrict__ diag)
+                double* __restrict__ diag)
 {
     __shared__ double red[32][12];
     double s[12];
@@ -1297,12 +1560,11 @@ k_finalize_diag(const int32_t* __restrict__ cnt, const double* __restrict__ cell
         s[1] += N / 2;
         s[2] += N & 1;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) s[7 + q] += cellsum[static_cast<int64_t>(j) * kCellSum + q];
+        for (int q = 0; q < 4; ++q) {
+            s[7 + q] += cellsum[static_cast<int64_t>(j) * kCellSum + q];
+            s[3 + q] += cellsum[static_cast<int64_t>(j) * kCellSum + 4 + q];
+        }
     }
-#pragma unroll 4
-    for (int t = threadIdx.x; t < T; t += blockDim.x)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) s[3 + q] += tilesum[static_cast<int64_t>(t) * kTileSum + q];
     if (threadIdx.x == 0) s[11] = cnt[M];
 #pragma unroll
     for (int q = 0; q < 12; ++q)
@@ -1341,7 +1603,7 @@ __global__ void k_extract_perm(const double* __restrict__ wsv, int n, int32_t* _
 // one CTA per cell; pair base = sum_{i<j} floor(N_i/2) computed in-block (test hook only)
 __global__ void __launch_bounds__(256)
 k_pairs(const int32_t* __restrict__ off, int M, uint32_t cell_base, uint32_t step, uint32_t s0,
-        uint32_t s1, int32_t* __restrict__ out, int64_t max_pairs)
+        uint32_t s1, int32_t* __restrict__ out, int64_t max_pairs, int blocked)
 {
     __shared__ int64_t red[8];
     __shared__ int32_t pi_sm[cc::kSmallCell];
@@ -1366,6 +1628,32 @@ k_pairs(const int32_t* __restrict__ off, int M, uint32_t cell_base, uint32_t ste
                     out[2 * g] = o + pi_sm[2 * k];
                     out[2 * g + 1] = o + pi_sm[2 * k + 1];
                 }
+            }
+        }
+        return;
+    }
+    if (blocked && N > cc::kBlock) {
+        // R1b computed from its definition pair by pair (test hook: no segment table)
+        const uint32_t Sf = static_cast<uint32_t>(N) / cc::kSeg;
+        const cc::Feistel fs = cc::make_feistel(Sf > 1 ? Sf : 2u, cc::philox4x32_10(cc::U4{0u, G, step, 5u}, s0, s1));
+        for (int k = threadIdx.x; k < N / 2; k += blockDim.x) {
+            const int64_t g = pb + k;
+            if (g >= max_pairs) continue;
+#pragma unroll 1
+            for (int m = 0; m < 2; ++m) {
+                const uint32_t q = 2u * k + m, b = q / cc::kBlock, r = q % cc::kBlock;
+                const uint32_t nb = min(static_cast<uint32_t>(N) - b * cc::kBlock, static_cast<uint32_t>(cc::kBlock));
+                uint32_t u;
+                if (nb > static_cast<uint32_t>(cc::kSmallCell))
+                    u = cc::feistel_pi(cc::make_feistel(nb, cc::philox4x32_10(cc::U4{b, G, step, 1u}, s0, s1)), r);
+                else
+                    u = cc::small_select(nb, r, G, step, s0, s1, b * (cc::kBlock / 4), 2u);
+                const uint32_t p = b * cc::kBlockSegs + u / cc::kSeg;     // position in the segment sequence
+                uint32_t seg0;
+                if (p >= Sf) seg0 = Sf * cc::kSeg;                          // the tail segment
+                else if (Sf <= static_cast<uint32_t>(cc::kSmallCell)) seg0 = cc::small_select(Sf, p, G, step, s0, s1, 0u, 6u) * cc::kSeg;
+                else seg0 = cc::feistel_pi(fs, p) * cc::kSeg;
+                out[2 * g + m] = o + static_cast<int32_t>(seg0 + u % cc::kSeg);
             }
         }
         return;
@@ -1825,11 +2113,14 @@ void mark(void* const* ev, int i, cudaStream_t st)
 
 int run_binning(const double* v_in, int64_t ldv, const int32_t* cell_in, int n, int M, const Layout& L,
                 void* ws, const CellConst& k, uint32_t cell_base, uint32_t step, uint64_t seed,
-                cudaStream_t st, void* const* ev, bool allow_sorted_skip, const uint32_t* step_dev = nullptr)
+                cudaStream_t st, void* const* ev, bool allow_sorted_skip, const uint32_t* step_dev = nullptr,
+                bool blocked = false)
 {
+    // R1b: one k_collide_large CTA per block of kBlock slots (kBlock / 2 pair items); R1: L.chunk
+    const int chunk = blocked ? cc::kBlock / 2 : L.chunk;
     int32_t* err = at<int32_t>(ws, L.o_err);
     mark(ev, 0, st);                     // the timed region starts before the flag reset
-    if (cudaMemsetAsync(err + 1, 0, sizeof(int32_t), st) != cudaSuccess) return CC_ECUDA;   // "unsorted" flag
+    if (cudaMemsetAsync(err + 1, 0, 2 * sizeof(int32_t), st) != cudaSuccess) return CC_ECUDA;   // unsorted flag, descents
     int32_t* tcount = at<int32_t>(ws, L.o_tcount);
     int32_t* cnt = at<int32_t>(ws, L.o_cnt);
     int32_t* off = at<int32_t>(ws, L.o_off);
@@ -1844,20 +2135,22 @@ int run_binning(const double* v_in, int64_t ldv, const int32_t* cell_in, int n, 
     if (!rc) rc = want_smem(k_scatter<false>, smem);
     if (rc) return rc;
     const int32_t* skip = allow_sorted_skip ? err : nullptr;
+    const int index_modes = (allow_sorted_skip && blocked) ? 1 : 0;
     k_count<<<L.T, kCountThreads, sizeof(int32_t) * M1, st>>>(cell_in, n, M, L.tile, tcount, err);
     mark(ev, 1, st);
     k_scan_tiles<<<(M1 + 31) / 32, dim3(32, kScanRows), 0, st>>>(tcount, L.T, M1, cnt);
-    k_scan_cells<<<1, 1024, 0, st>>>(cnt, M, off, chunk_off, L.chunk);
+    k_scan_cells<<<1, 1024, 0, st>>>(cnt, M, off, chunk_off, chunk);
     k_cell_setup<<<(M + 7) / 8, 256, 0, st>>>(cnt, chunk_off, M, at<int4>(ws, L.o_chunkcell), Cj, keys, k,
                                                    cell_base, step, static_cast<uint32_t>(seed),
-                                                   static_cast<uint32_t>(seed >> 32), step_dev, off, L.chunk);
+                                                   static_cast<uint32_t>(seed >> 32), step_dev, off, chunk,
+                                                   blocked ? at<int32_t>(ws, L.o_seg) : nullptr);
     mark(ev, 2, st);
     if (v_in)
         k_scatter<true><<<L.T, 32 * L.W, smem, st>>>(v_in, ldv, cell_in, n, M, L.W, L.sub, tcount, off, wsv, skip,
-                                                     at<double>(ws, L.o_tilesum));
+                                                     index_modes);
     else
         k_scatter<false><<<L.T, 32 * L.W, smem, st>>>(nullptr, 0, cell_in, n, M, L.W, L.sub, tcount, off, wsv, skip,
-                                                      nullptr);
+                                                      0);
     return launch_ok();
 }
 
@@ -1875,6 +2168,24 @@ CellConst cell_const(const cc_params& p, double dt)
     return k;
 }
 
+template <bool BLOCKED>
+int launch_collide_large(const CollideArgs& A, unsigned grid, bool nanbu, bool push, cudaStream_t st)
+{
+    int rc = want_smem(k_collide_large<false, false, BLOCKED>, kCollideSmem);
+    if (!rc) rc = want_smem(k_collide_large<true, false, BLOCKED>, kCollideSmem);
+    if (!rc) rc = want_smem(k_collide_large<false, true, BLOCKED>, kCollideSmem);
+    if (!rc) rc = want_smem(k_collide_large<true, true, BLOCKED>, kCollideSmem);
+    if (rc) return rc;
+    if (push) {
+        if (nanbu) k_collide_large<true, true, BLOCKED><<<grid, kCollideThreads, kCollideSmem, st>>>(A);
+        else k_collide_large<false, true, BLOCKED><<<grid, kCollideThreads, kCollideSmem, st>>>(A);
+    } else {
+        if (nanbu) k_collide_large<true, false, BLOCKED><<<grid, kCollideThreads, kCollideSmem, st>>>(A);
+        else k_collide_large<false, false, BLOCKED><<<grid, kCollideThreads, kCollideSmem, st>>>(A);
+    }
+    return CC_OK;
+}
+
 bool finite_pos(double x) { return std::isfinite(x) && x > 0.0; }
 
 // Host-side argument checks of coulomb_collide (scalars and cc_params), shared with the
@@ -1886,7 +2197,7 @@ int check_call(const cc_params& p, int64_t n, int32_t cells, int64_t ldv, double
     if (!finite_pos(p.mass) || !finite_pos(p.charge) || !finite_pos(p.eps0) || !std::isfinite(p.weight) ||
         p.weight < 0.0 || (!p.cell_volume_arr && !finite_pos(p.cell_volume)) ||
         (!p.ln_lambda_arr && !std::isfinite(p.ln_lambda)) ||
-        (p.flags & ~(CC_ODD_TRIPLET | CC_NANBU | CC_PRESERVE_ORDER)) != 0)
+        (p.flags & ~(CC_ODD_TRIPLET | CC_NANBU | CC_PRESERVE_ORDER | CC_CELL_UNIFORM)) != 0)
         return CC_EINVAL;
     if (p.push) {                            // fused push (NEXT f2): same checks as cc_push
         const cc_push_params& q = *p.push;
@@ -1982,8 +2293,9 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     const CellConst k = cell_const(p, dt);
     const int nn = static_cast<int>(n);
     void* const* ev = p.stage_events;
+    const bool blocked = (p.flags & CC_CELL_UNIFORM) == 0;     // R1b (default) or R1
     int rc = run_binning(v_in, ldv, cell_in, nn, M, L, workspace, k, cell_base, static_cast<uint32_t>(step), seed,
-                         st, ev, true, p.step_dev);
+                         st, ev, true, p.step_dev, blocked);
     if (rc) return rc;
 
     CollideArgs A;
@@ -2010,7 +2322,15 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     A.cell_base = cell_base;
     A.step = static_cast<uint32_t>(step);
     A.step_dev = p.step_dev;
-    A.chunk = L.chunk;
+    A.chunk = blocked ? cc::kBlock / 2 : L.chunk;
+    A.blocked = blocked ? 1 : 0;
+    A.index_modes = blocked ? 1 : 0;
+    A.flags = at<int32_t>(workspace, L.o_err);
+    A.n = nn;
+    A.v_in = v_in;
+    A.ldvi = ldv;
+    A.vec16 = aligned(v_in, 16) && (ldv % 2 == 0);
+    A.seg = at<int32_t>(workspace, L.o_seg);
     A.push = 0;
     A.E = nullptr; A.x_in = nullptr; A.x_out = nullptr;
     A.ldE = A.ldxi = A.ldxo = 0;
@@ -2038,22 +2358,13 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
     A.pair_vec = aligned(v_out, 16) && (ldv % 2 == 0) && aligned(cell_out, 8) && (!perm_out || aligned(perm_out, 8));
 
     mark(ev, 3, st);
-    rc = want_smem(k_collide_large<false, false>, kCollideSmem);
-    if (!rc) rc = want_smem(k_collide_large<true, false>, kCollideSmem);
-    if (!rc) rc = want_smem(k_collide_large<false, true>, kCollideSmem);
-    if (!rc) rc = want_smem(k_collide_large<true, true>, kCollideSmem);
-    if (rc) return rc;
     k_collide_small<<<(M + 7) / 8, 256, 0, st>>>(A);
     {
         const unsigned grid = static_cast<unsigned>(L.max_chunks);
         const bool nb = (A.model & CC_NANBU) != 0;
-        if (A.push) {
-            if (nb) k_collide_large<true, true><<<grid, kCollideThreads, kCollideSmem, st>>>(A);
-            else k_collide_large<false, true><<<grid, kCollideThreads, kCollideSmem, st>>>(A);
-        } else {
-            if (nb) k_collide_large<true, false><<<grid, kCollideThreads, kCollideSmem, st>>>(A);
-            else k_collide_large<false, false><<<grid, kCollideThreads, kCollideSmem, st>>>(A);
-        }
+        if (blocked) rc = launch_collide_large<true>(A, grid, nb, A.push != 0, st);
+        else rc = launch_collide_large<false>(A, grid, nb, A.push != 0, st);
+        if (rc) return rc;
     }
     if (A.model & CC_ODD_TRIPLET) k_triplets<<<(M + 255) / 256, 256, 0, st>>>(A);
     k_copy_dead<<<148 * 4, 256, 0, st>>>(A, nn);
@@ -2070,7 +2381,7 @@ int coulomb_collide(const double* v_in, int64_t ldv, const int32_t* cell_in, dou
                                                       (A.model & CC_ODD_TRIPLET) ? A.trec : nullptr, M, mc,
                                                       moments_out, cellsum);
     if (diag_out)
-        k_finalize_diag<<<1, 1024, 0, st>>>(A.cnt, cellsum, M, at<double>(workspace, L.o_tilesum), L.T, diag_out);
+        k_finalize_diag<<<1, 1024, 0, st>>>(A.cnt, cellsum, M, diag_out);
     mark(ev, 5, st);
     return launch_ok();
 }
@@ -2215,14 +2526,15 @@ int cc_bin(const int32_t* cell_in, int64_t n, int32_t cells, int32_t* perm_out, 
 }
 
 int cc_pairs(const int32_t* off, int32_t cells, uint32_t cell_base, uint64_t seed, uint64_t step,
-             int32_t* pair_slots_out, int64_t max_pairs, void* stream)
+             uint32_t flags, int32_t* pair_slots_out, int64_t max_pairs, void* stream)
 {
     cudaGetLastError();   // launch errors below are ours, not a stale earlier one
-    if (!off || cells < 1 || step >= (1ull << 32) || max_pairs < 0) return CC_EINVAL;
+    if (!off || cells < 1 || step >= (1ull << 32) || max_pairs < 0 || (flags & ~CC_CELL_UNIFORM)) return CC_EINVAL;
     if (max_pairs > 0 && !pair_slots_out) return CC_EINVAL;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     k_pairs<<<cells, 256, 0, st>>>(off, cells, cell_base, static_cast<uint32_t>(step), static_cast<uint32_t>(seed),
-                                   static_cast<uint32_t>(seed >> 32), pair_slots_out, max_pairs);
+                                   static_cast<uint32_t>(seed >> 32), pair_slots_out, max_pairs,
+                                   (flags & CC_CELL_UNIFORM) ? 0 : 1);
     return launch_ok();
 }
 

@@ -40,11 +40,11 @@ def vel_err(v_gpu, v_ref, floor):
     return np.max(np.abs(v_gpu - v_ref) / scale) if v_ref.size else 0.0
 
 
-def check_collide(O, w, step=0, moments=True):
+def check_collide(O, w, step=0, moments=True, flags=0):
     p = w.params()
-    out = cc.coulomb_collide(to_dev(w.v), to_dev(w.cell), w.cells, step=step, **p)
+    out = cc.coulomb_collide(to_dev(w.v), to_dev(w.cell), w.cells, step=step, flags=flags, **p)
     torch.cuda.synchronize()
-    ref = O.coulomb_collide(w.v, w.cell, w.cells, step=step, want_pairs=False, **p)
+    ref = O.coulomb_collide(w.v, w.cell, w.cells, step=step, want_pairs=False, flags=flags, **p)
     assert np.array_equal(out.perm_out.cpu().numpy(), ref.perm_out)
     assert np.array_equal(out.cell_out.cpu().numpy(), ref.cell_out)
     err = vel_err(out.v_out.cpu().numpy(), ref.v_out, 1e-3 * W.sigma_v(2.0))
@@ -148,15 +148,42 @@ def test_bin_bit_exact(O, n, M, dead):
     assert np.array_equal(perm.cpu().numpy(), rp)
 
 
-@pytest.mark.parametrize("n,M", [(1000, 1), (5000, 3), (20_000, 500), (100_000, 13), (3000, 3000)])
-def test_pairs_bit_exact(O, n, M):
+@pytest.mark.parametrize("flags", [0, 8])
+@pytest.mark.parametrize("n,M", [(1000, 1), (5000, 3), (20_000, 500), (100_000, 13), (3000, 3000),
+                                 (2113, 1), (4097, 1)])
+def test_pairs_bit_exact(O, n, M, flags):
+    """flags 0: the blocked pairing R1b (segment orders by sort-by-key for <= 64 segments and by
+    Feistel above; last blocks of <= 64 slots); 8 = CC_CELL_UNIFORM: R1 over the whole cell."""
     w = W.random_cells(n, M, seed=7 * n + M, skew=True)
     _, off = cc.cc_bin(to_dev(w.cell), M)
     for step in (0, 5):
-        pairs = cc.cc_pairs(off, M, cell_base=11, seed=99, step=step).cpu().numpy()
-        ref = O.coulomb_collide(w.v, w.cell, M, cell_base=11, seed=99, step=step,
+        pairs = cc.cc_pairs(off, M, cell_base=11, seed=99, step=step, flags=flags).cpu().numpy()
+        ref = O.coulomb_collide(w.v, w.cell, M, cell_base=11, seed=99, step=step, flags=flags,
                                 dt=w.dt, weight=w.weight, cell_volume=w.cell_volume)
         assert np.array_equal(pairs, ref.pair_slots)
+
+
+# cell sizes at R1b's edges: one block (384), last blocks of 1-3 slots (385-387: the triplet
+# straddles two blocks), whole segments only (768), tails (767, 769, 800), the segment order by
+# sort-by-key (2047: 63 segments) vs Feistel (2080: 65, 2113), a 10-slot last block (3850)
+R1B_SIZES = [384, 385, 386, 387, 767, 768, 769, 800, 2047, 2080, 2113, 3850, 4097]
+
+
+@pytest.mark.parametrize("flags", [0, 1, 2])
+def test_blocked_pairing_edges(O, flags):
+    """Whole operator on single cells of R1b's edge sizes (flags: TA77, odd triplet — whose three
+    members straddle blocks when the last block holds 1-2 slots — and Nanbu)."""
+    for N in R1B_SIZES:
+        w = W.random_cells(N, 1, seed=N + 5 * flags)
+        check_collide(O, w, step=3 + N % 7, flags=flags)
+
+
+@pytest.mark.parametrize("n,M,skew", [(120_007, 64, True), (9000, 2, False), (100_000, 1, False)])
+def test_collide_parity_uniform_r1(O, n, M, skew):
+    """CC_CELL_UNIFORM keeps R1 (whole-cell permutation, gathered records)."""
+    w = W.random_cells(n, M, seed=n + 7 * M, dead_frac=0.02, skew=skew)
+    check_collide(O, w, step=11, flags=8)
+    check_collide(O, w, step=11, flags=8 | 1)
 
 
 # ------------------------------------------------------------------ whole operator
@@ -174,19 +201,23 @@ def test_collide_parity(O, n, M, dead, skew):
 
 @pytest.mark.parametrize("n,M,dead", [(50_000, 64, 0.0), (80_000, 300, 0.05), (10_000, 5000, 0.1)])
 def test_sorted_input_fast_path(O, n, M, dead):
-    """Cell-sorted input (dead last): k_count flags it sorted, k_scatter packs the records in
-    place (the identity order, no ranking pass); results must equal the oracle's."""
+    """Cell-sorted input (dead last): k_count flags it sorted, so (R1b, the default) k_scatter
+    moves nothing and the collide copies each block's segments straight from the caller's SoA
+    input (kModeSorted); under CC_CELL_UNIFORM k_scatter packs the records in place.  Results
+    must equal the oracle's either way."""
     w = W.random_cells(n, M, seed=n + M + 1, dead_frac=dead, skew=True)
     key = np.where(w.cell < 0, M, w.cell)
     order = np.argsort(key, kind="stable")
     w.v = np.ascontiguousarray(w.v[:, order])
     w.cell = np.ascontiguousarray(w.cell[order])
-    check_collide(O, w, step=4)
-    # one element out of order: the full binning path runs instead
+    for flags in (0, 8):
+        check_collide(O, w, step=4, flags=flags)
+    # one element out of order: the full binning path runs instead (kModePerm: few descents)
     if n > 10:
         w.cell = w.cell.copy()
         w.cell[[1, n // 2]] = w.cell[[n // 2, 1]]
-        check_collide(O, w, step=4)
+        for flags in (0, 8):
+            check_collide(O, w, step=4, flags=flags)
 
 
 @pytest.mark.parametrize("frac", [0.0, 0.02, 0.1, 0.3, 1.0])

@@ -32,9 +32,11 @@ def rk4(y, n, lnL, dt):
     return y + dt / 6 * (k1 + 2 * k2 + 2 * k3 + k4)
 
 
-def run_chain(w, flags, steps, dt):
+def run_chain(w, flags, steps, dt, seed=None):
     p = w.params()
     p["dt"] = dt
+    if seed is not None:
+        p["seed"] = seed
     v, cell = torch.from_numpy(w.v).to(DEV), torch.from_numpy(w.cell).to(DEV)
     col = cc.Collider(w.n, 1, DEV, **{k: p[k] for k in ("dt", "weight", "cell_volume", "ln_lambda", "seed")})
     hist = [cc.cc_p2c_moments(cc.cc_p2c(v, cell, 1), weight=w.weight, cell_volume=w.cell_volume)[0].cpu().numpy()]
@@ -61,11 +63,17 @@ def test_c2_isotropisation_matches_nrl(flags, Tperp, Tpar):
     w = W.c2(T_perp=Tperp, T_par=Tpar)
     n_e = w.n * w.weight / w.cell_volume
     # (1) the rate: at dt/10 (where TA's finite-dt sampler has converged to the Fokker-Planck
-    #     limit, DESIGN R5) over the first 20 steps, while the distribution is still bi-Maxwellian
-    tperp, tpar = run_chain(w, flags, 20, w.dt / 10)
-    ref = nrl_traj(tperp[0], tpar[0], n_e, w.ln_lambda, w.dt / 10, 20)
-    ratio = ((tperp[-1] - tpar[-1]) - (tperp[0] - tpar[0])) / ((ref[-1, 0] - ref[-1, 1]) - (ref[0, 0] - ref[0, 1]))
-    assert abs(ratio - 1.0) < 0.05, ratio
+    #     limit, DESIGN R5) over the first 20 steps, while the distribution is still bi-Maxwellian.
+    #     One chain's ratio scatters by ~6% (1e5 samples, 2% relaxation: measured with the oracle
+    #     for R1 and R1b alike), so the rate is the mean over 8 collision seeds (sigma ~2%)
+    ratios = []
+    for seed in range(42, 50):
+        tperp, tpar = run_chain(w, flags, 20, w.dt / 10, seed=seed)
+        ref = nrl_traj(tperp[0], tpar[0], n_e, w.ln_lambda, w.dt / 10, 20)
+        ratios.append(((tperp[-1] - tpar[-1]) - (tperp[0] - tpar[0])) /
+                      ((ref[-1, 0] - ref[-1, 1]) - (ref[0, 0] - ref[0, 1])))
+    ratio = float(np.mean(ratios))
+    assert abs(ratio - 1.0) < 0.05, ratios
     # (2) config 2 as stated: 500 chained steps at the nominal dt — energy 2 T_perp + T_par
     #     conserved, the anisotropy decays at the NRL rate within the finite-dt and
     #     non-bi-Maxwellian margin, and reaches the noise floor
