@@ -64,6 +64,10 @@ constexpr int kSub = CC_SUB;             // elements per warp sub-range in k_sca
 constexpr bool kScatterPrefetch = CC_SCATTER_PREFETCH != 0;   // next batch's cell ids loaded one batch ahead
 constexpr int kScatterUnrollA = CC_SCATTER_UA;   // cell loads in flight per lane, counting pass
 constexpr int kScatterUnrollB = CC_SCATTER_UB;   // (cell, v) loads in flight per lane, scatter pass
+#ifndef CC_SCATTER_UP
+#define CC_SCATTER_UP 4
+#endif
+constexpr int kScatterUnrollP = CC_SCATTER_UP;   // ids per lane per batch, index-only scatter pass (kModePerm)
 // k_collide_large shape (tools/collide_shape.sh overrides them for design studies)
 #ifndef CC_COLLIDE_THREADS
 #define CC_COLLIDE_THREADS 64
@@ -509,6 +513,63 @@ __device__ __forceinline__ void load_batch(const double* __restrict__ v, int64_t
     else { x = y = z = 0.0; }
 }
 
+// k_scatter pass B over one warp's sub-range [s0, s1): each id's rank among equal-cell
+// predecessors, its destination slot, and the move: the 32-byte record (RECS) or the input
+// index alone (kModePerm, no velocity loads, so more ids per batch).  The next batch's ids
+// are loaded before this batch is ranked, its velocities at the top of its own iteration.
+template <int UB, bool RECS, bool HAS_V>
+__device__ __forceinline__ void scatter_pass_b(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__ cell,
+                                               int64_t s0, int64_t s1, int M, uint32_t* my, const int32_t* base,
+                                               int lane, double* __restrict__ wsv, int32_t* __restrict__ sperm)
+{
+    const uint32_t lt = (1u << lane) - 1u;
+    int32_t cB[UB];
+    auto fetchB = [&](int64_t i0) {
+#pragma unroll
+        for (int u = 0; u < UB; ++u) cB[u] = __ldg(cell + min(i0 + 32 * u + lane, s1 - 1));
+    };
+    if (kScatterPrefetch && s0 < s1) fetchB(s0);
+    for (int64_t i0 = s0; i0 < s1; i0 += 32 * UB) {
+        int32_t key[UB];
+        double x[UB], y[UB], z[UB];
+        if (!kScatterPrefetch) fetchB(i0);
+#pragma unroll
+        for (int u = 0; u < UB; ++u) {
+            const int64_t i = i0 + 32 * u + lane;
+            const int64_t ic = min(i, s1 - 1);
+            if (HAS_V && RECS) { x[u] = __ldg(v + ic); y[u] = __ldg(v + ldv + ic); z[u] = __ldg(v + 2 * ldv + ic); }
+            else { x[u] = y[u] = z[u] = 0.0; }
+            const int32_t c = cB[u];
+            key[u] = (i >= s1) ? -1 - lane : ((c >= 0 && c < M) ? c : M);
+        }
+        if (kScatterPrefetch && i0 + 32 * UB < s1) fetchB(i0 + 32 * UB);
+        uint32_t peers[UB], old[UB];
+#pragma unroll
+        for (int u = 0; u < UB; ++u) peers[u] = __match_any_sync(0xFFFFFFFFu, key[u]);
+#pragma unroll
+        for (int u = 0; u < UB; ++u) {
+            const int32_t b = max(key[u], 0);
+            old[u] = atom_add_if(key[u] >= 0 && lane == __ffs(peers[u]) - 1, my + (b >> 1),
+                                 static_cast<uint32_t>(__popc(peers[u])) << ((b & 1) << 4));
+        }
+#pragma unroll
+        for (int u = 0; u < UB; ++u) {
+            const int32_t b = key[u];
+            const uint32_t o = __shfl_sync(0xFFFFFFFFu, (old[u] >> ((max(b, 0) & 1) << 4)) & 0xFFFFu,
+                                           __ffs(peers[u]) - 1);
+            if (b >= 0) {
+                const int32_t dest = base[b] + static_cast<int32_t>(o) + __popc(peers[u] & lt);
+                const int64_t i = i0 + 32 * u + lane;
+                if (RECS)
+                    st256(wsv + 4 * static_cast<int64_t>(dest), x[u], y[u], z[u],
+                          pack_pc(static_cast<int32_t>(i), b < M ? b : -1));
+                else
+                    sperm[dest] = static_cast<int32_t>(i);
+            }
+        }
+    }
+}
+
 template <bool HAS_V>
 __global__ void __launch_bounds__(32 * kMaxScatterWarps, CC_SCATTER_CTAS)
 k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__ cell, int n, int M,
@@ -620,53 +681,9 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
     }
     __syncthreads();
 
-    // pass B: ranks, destinations, 32-byte records (loads batched, branch-free); the next batch's
-    // ids are loaded before this batch is ranked, its velocities at the top of its own iteration
-    int32_t cB[kScatterUnrollB];
-    auto fetchB = [&](int64_t i0) {
-#pragma unroll
-        for (int u = 0; u < kScatterUnrollB; ++u) cB[u] = __ldg(cell + min(i0 + 32 * u + lane, s1 - 1));
-    };
-    if (kScatterPrefetch && s0 < s1) fetchB(s0);
-    for (int64_t i0 = s0; i0 < s1; i0 += 32 * kScatterUnrollB) {
-        int32_t key[kScatterUnrollB];
-        double x[kScatterUnrollB], y[kScatterUnrollB], z[kScatterUnrollB];
-        if (!kScatterPrefetch) fetchB(i0);
-#pragma unroll
-        for (int u = 0; u < kScatterUnrollB; ++u) {
-            const int64_t i = i0 + 32 * u + lane;
-            const int64_t ic = min(i, s1 - 1);
-            if (HAS_V && recs) { x[u] = __ldg(v + ic); y[u] = __ldg(v + ldv + ic); z[u] = __ldg(v + 2 * ldv + ic); }
-            else { x[u] = y[u] = z[u] = 0.0; }
-            const int32_t c = cB[u];
-            key[u] = (i >= s1) ? -1 - lane : ((c >= 0 && c < M) ? c : M);
-        }
-        if (kScatterPrefetch && i0 + 32 * kScatterUnrollB < s1) fetchB(i0 + 32 * kScatterUnrollB);
-        uint32_t peers[kScatterUnrollB], old[kScatterUnrollB];
-#pragma unroll
-        for (int u = 0; u < kScatterUnrollB; ++u) peers[u] = __match_any_sync(0xFFFFFFFFu, key[u]);
-#pragma unroll
-        for (int u = 0; u < kScatterUnrollB; ++u) {
-            const int32_t b = max(key[u], 0);
-            old[u] = atom_add_if(key[u] >= 0 && lane == __ffs(peers[u]) - 1, my + (b >> 1),
-                                 static_cast<uint32_t>(__popc(peers[u])) << ((b & 1) << 4));
-        }
-#pragma unroll
-        for (int u = 0; u < kScatterUnrollB; ++u) {
-            const int32_t b = key[u];
-            const uint32_t o = __shfl_sync(0xFFFFFFFFu, (old[u] >> ((max(b, 0) & 1) << 4)) & 0xFFFFu,
-                                           __ffs(peers[u]) - 1);
-            if (b >= 0) {
-                const int32_t dest = base[b] + static_cast<int32_t>(o) + __popc(peers[u] & lt);
-                const int64_t i = i0 + 32 * u + lane;
-                if (recs)
-                    st256(wsv + 4 * static_cast<int64_t>(dest), x[u], y[u], z[u],
-                          pack_pc(static_cast<int32_t>(i), b < M ? b : -1));
-                else
-                    sperm[dest] = static_cast<int32_t>(i);
-            }
-        }
-    }
+    // pass B: ranks, destinations, 32-byte records or 4-byte indices (loads batched, branch-free)
+    if (recs) scatter_pass_b<kScatterUnrollB, true, HAS_V>(v, ldv, cell, s0, s1, M, my, base, lane, wsv, sperm);
+    else scatter_pass_b<kScatterUnrollP, false, false>(v, ldv, cell, s0, s1, M, my, base, lane, wsv, sperm);
 }
 
 // ------------------------------------------------------------------ CCS4 + CCS5 items
