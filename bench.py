@@ -53,8 +53,17 @@ UNIT = "pair-collisions/s"
 ALGO_BYTES = 52
 # SURVEY §8(d) design traffic per particle: cold (unsorted input) and warm (cell-sorted input)
 DESIGN_BYTES = {"cold": 112, "warm": 56}
-# what each kernel's own contract moves once per particle (informative, not the roofline)
-STAGE_CONTRACT_BYTES = {"count": 4, "scatter": 4 + 24 + 32, "collide": 28 + 32}
+# the binning mode the device picks for each bench workload (k_count's descents) and
+# what each kernel's own contract moves once per particle in it (informative, not the roofline):
+#   steady -> index mode: scatter reads the cell id twice and writes a 4-byte index; the collide
+#             reads the index and v (24) and writes v, cell, perm (32)
+#   cold   -> record mode: scatter reads cell twice + v, writes a 32-byte record; collide reads it back
+#   warm   -> sorted mode: no scatter; the collide reads v straight from the input
+BIN_MODE = {"steady": "index", "steady_nomig": "index", "cold": "record", "warm": "sorted"}
+STAGE_CONTRACT_BYTES = {"index": {"count": 4, "scatter": 12, "collide": 4 + 24 + 32},
+                        "record": {"count": 4, "scatter": 8 + 24 + 32, "collide": 32 + 32},
+                        "sorted": {"count": 4, "scatter": 0, "collide": 24 + 32}}
+PIPELINE_BYTES = {m: sum(b.values()) for m, b in STAGE_CONTRACT_BYTES.items()}   # 76 / 132 / 60
 KERNEL_SOURCES = ("paper_2508_06771_b200/csrc/cc_kernels.cu", "paper_2508_06771_b200/csrc/cc_device.cuh",
                   "include/coulomb.h")
 
@@ -797,9 +806,10 @@ def run_ours(args):
         traffic_note = "no profiles/traffic.json"
     kernel_of = {"count": "k_count", "scatter": "k_scatter", "collide": "k_collide_large"}
 
-    def roofline(r, with_traffic=False):
+    def roofline(r, mode, with_traffic=False):
         """ALGO_BYTES per particle x n over the dominant kernel's event-timed duration."""
         st = r["stages"]
+        contract = STAGE_CONTRACT_BYTES[BIN_MODE[mode]]
         dom = max(("count", "scatter", "collide"), key=lambda k: st[k])
         achieved = ALGO_BYTES * n_live / (st[dom] * 1e-3) / 1e9
         tr = traffic.get(kernel_of[dom], {}).get("dram_bytes_per_launch") if (world == 1 and with_traffic) else None
@@ -809,8 +819,9 @@ def run_ours(args):
                 "traffic_source": ("profiles/traffic.json (ncu --set full, same kernel sources, steady call)"
                                    if tr else traffic_note),
                 "algorithmic_bytes_per_particle": ALGO_BYTES, "algorithmic_bytes_per_launch": ALGO_BYTES * n_live,
-                "kernel_contract_bytes_per_particle": STAGE_CONTRACT_BYTES[dom],
-                "kernel_contract_frac": STAGE_CONTRACT_BYTES[dom] * n_live / (st[dom] * 1e-3) / 1e9 / hbm_peak,
+                "binning_mode": BIN_MODE[mode],
+                "kernel_contract_bytes_per_particle": contract[dom],
+                "kernel_contract_frac": contract[dom] * n_live / (st[dom] * 1e-3) / 1e9 / hbm_peak,
                 "kernel_ms": st[dom], "peak_source": peak_src}
 
     STEP_KERNELS = ("k_count", "k_scan_tiles", "k_scan_cells", "k_cell_setup", "k_scatter", "k_collide_small",
@@ -819,10 +830,11 @@ def run_ours(args):
     def step_hbm(ms):
         """Whole step: algorithmic 52 B/particle over the step time (SURVEY §8(d) reading 2) and the DRAM
         bytes ncu measured for every kernel of one steady call (reading 1), with SURVEY §8(d)'s
-        1.15 x design-traffic guard against its cold (112 B) and warm (56 B) designs."""
+        1.15 x design-traffic guard against its cold (112 B) and warm (56 B) designs and against this
+        pipeline's own index-mode design (76 B)."""
         out = {"algorithmic_bytes_per_particle": ALGO_BYTES,
                "frac": ALGO_BYTES * n_live / (ms * 1e-3) / 1e9 / hbm_peak,
-               "design_bytes_per_particle": DESIGN_BYTES}
+               "design_bytes_per_particle": DESIGN_BYTES, "pipeline_design_bytes_per_particle": PIPELINE_BYTES}
         if world != 1 or not all(k in traffic for k in STEP_KERNELS):
             out["achieved_dram_frac"] = None
             out["traffic_note"] = traffic_note
@@ -834,6 +846,7 @@ def run_ours(args):
                     "achieved_dram_frac": b / (ms * 1e-3) / 1e9 / hbm_peak,
                     "guard_1.15x_cold_design": b / n_live <= 1.15 * DESIGN_BYTES["cold"],
                     "guard_1.15x_warm_design": b / n_live <= 1.15 * DESIGN_BYTES["warm"],
+                    "guard_1.15x_index_mode_design": b / n_live <= 1.15 * PIPELINE_BYTES["index"],
                     "source": "profiles/traffic.json (ncu dram__bytes_read/write.sum per kernel, one steady call, "
                               "same kernel sources)"})
         return out
@@ -841,9 +854,9 @@ def run_ours(args):
     def timing(r):
         return {"ms_mean": r["ms"], "ms_median": r["ms_median"], "ms_min": r["ms_min"], "ms_max": r["ms_max"]}
 
-    def summary(r):
+    def summary(r, mode):
         return {"value": r["pairs"] / (r["ms"] * 1e-3), "ms_per_step": r["ms"], "wall_ms_per_step": r["wall_ms"],
-                "timing": timing(r), "stages_ms": r["stages"], "roofline": roofline(r),
+                "timing": timing(r), "stages_ms": r["stages"], "roofline": roofline(r, mode),
                 "step_hbm_frac": ALGO_BYTES * n_live / (r["ms"] * 1e-3) / 1e9 / hbm_peak}
 
     head = res["steady"]
@@ -862,12 +875,12 @@ def run_ours(args):
                    "timing": "CUDA events around each operator call (drift excluded); value = mean of K, "
                              "median/min/max in timing",
                    "parallelism": f"cell-range shards x{world}" if world > 1 else "1 GPU"},
-        "roofline": roofline(head, with_traffic=True),
+        "roofline": roofline(head, "steady", with_traffic=True),
         "timing": timing(head),
         "stages_ms": head["stages"],
         "step_hbm": step_hbm(head["ms"]),
-        "cold": dict(summary(res["cold"]), what="every step bins the same randomly ordered input"),
-        "warm": dict(summary(res["warm"]), what="chained steps, no drift (input already cell-sorted)"),
+        "cold": dict(summary(res["cold"], "cold"), what="every step bins the same randomly ordered input"),
+        "warm": dict(summary(res["warm"], "warm"), what="chained steps, no drift (input already cell-sorted)"),
         "e2e": {"value": res["cold"]["pairs"] / (e2e_ms * 1e-3), "unit": UNIT,
                 "h2d_bytes_per_step": int(v_host.numel() * 8 + c_host.numel() * 4),
                 "d2h_bytes_per_step": int(n_live * 24), "ms_per_step": e2e_ms,
@@ -882,7 +895,7 @@ def run_ours(args):
     }
     if world > 1:
         line["multi_gpu"] = {
-            "steady_without_migration": dict(summary(res["steady_nomig"]),
+            "steady_without_migration": dict(summary(res["steady_nomig"], "steady_nomig"),
                                              what="drift inside the shard only, no migration step"),
             "migration": {"peers": mig.peers, "cap_per_peer": mig.cap, "slot_bytes": mig.slot,
                           "status": mig_status, "ms_per_step": res["steady"]["stages"].get("migrate"),

@@ -361,6 +361,27 @@ __device__ __forceinline__ void ta_update_z(double& ax, double& ay, double& az,
     rotate_pair(ax, ay, az, bx, by, bz, ux, uy, uz, u, sinT, omc, u2);
 }
 
+// The same update with sqrt(<delta^2>) = sqrt(C) |u|^-3/2 = sqrtC * (1/|u|) * rsqrt(|u|): the
+// per-cell sqrt(C) is taken once per CTA, so no IEEE sqrt per pair (a few ulp of delta, far
+// inside the 1e-12 parity bar).
+__device__ __forceinline__ void ta_update_zs(double& ax, double& ay, double& az,
+                                             double& bx, double& by, double& bz,
+                                             double sqrtC, double z, double u2)
+{
+    const double ux = ax - bx, uy = ay - by, uz = az - bz;
+    if (ux == 0.0 && uy == 0.0 && uz == 0.0) return;
+    const double usq = fma(ux, ux, fma(uy, uy, uz * uz));
+    const double rs = rsqrt_nr(usq);                 // 1/|u|
+    const double u = usq * rs;
+    const double delta = (sqrtC * rs) * rsqrt_nr(u) * z;
+    const double dd = fmin(fabs(delta), 1e150);
+    const double d2 = dd * dd;
+    const double inv = rcp_nr(1.0 + d2);
+    const double sinT = 2.0 * copysign(dd, delta) * inv;
+    const double omc = 2.0 * d2 * inv;
+    rotate_pair(ax, ay, az, bx, by, bz, ux, uy, uz, u, sinT, omc, u2);
+}
+
 __device__ __forceinline__ void ta_update(double& ax, double& ay, double& az,
                                           double& bx, double& by, double& bz,
                                           double C, double u1, double u2)

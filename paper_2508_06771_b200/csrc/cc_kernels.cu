@@ -1275,6 +1275,7 @@ k_collide_large(CollideArgs A)
     Rec ref;
     if (!BLOCKED) ref = load_slot(A, o);
     const double C = A.Cj[j];
+    const double sqC = sqrt(C);
     cp_async_wait_all();
     __syncthreads();
     if (BLOCKED) ref = Rec{ref_sm[0], ref_sm[1], ref_sm[2], 0.0};
@@ -1347,7 +1348,7 @@ k_collide_large(CollideArgs A)
                 if (NANBU)
                     cc::nanbu_apply(a.x, a.y, a.z, b.x, b.y, b.z, aq[w][slot], zq[w][slot], u2q[w][slot]);
                 else if (!(CC_ABLATE & 1))
-                    cc::ta_update_z(a.x, a.y, a.z, b.x, b.y, b.z, C, zq[w][slot], u2q[w][slot]);
+                    cc::ta_update_zs(a.x, a.y, a.z, b.x, b.y, b.z, sqC, zq[w][slot], u2q[w][slot]);
                 write_pair_out<PUSH>(A, pa, j, a, b);
                 acc.post(b.x, b.y, b.z, ref.x, ref.y, ref.z);
             } else {
