@@ -6,7 +6,7 @@
  *
  * One call of coulomb_collide() = one step of S1 on a set of electrons binned
  * in cells:  CCS1 count -> CCS2 prefix sum -> CCS3 stable bin -> random
- * in-cell pairing (reading R1) -> CCS4 two randoms per pair ->
+ * in-cell pairing (readings R1b / R1) -> CCS4 two randoms per pair ->
  * CCS5 Takizuka–Abe binary collision -> per-cell moments
  * (the P2C block reduction of §4.5) and global diagnostics.
  * Everything runs in fp64 ("All runs are in double precision").
@@ -156,7 +156,12 @@ size_t cc_workspace_bytes(int64_t n, int32_t cells);
  *  Output order (reading R14): cell-major; inside cell j (slots
  *  [off_j, off_j + N_j)) the particles are in PAIR order — slots off_j+2k and
  *  off_j+2k+1 hold pair k's first and second member, and for odd N_j slot
- *  off_j+N_j-1 holds the particle that sat out (R2).  Dead particles follow at
+ *  off_j+N_j-1 holds the particle that sat out (R2).  With the default R1b
+ *  pairing, pairs k in [192 b, 192 b + 192) are the pairs of block b.
+ *  Binning: the call picks its binning mode on the device from
+ *  the input's order — sorted input is read in place, nearly sorted input is
+ *  binned by 4-byte indices (then read through them), randomly ordered input is
+ *  moved as 32-byte records; the results do not depend on the mode.  Dead particles follow at
  *  [L, n) in input order (L = number of live particles).  v_out/cell_out/
  *  perm_out must not alias the inputs.
  *  cells     number of LOCAL cells M (1 <= M <= CC_MAX_CELLS).
@@ -171,6 +176,8 @@ size_t cc_workspace_bytes(int64_t n, int32_t cells);
  *            4-6 sum v before, 7 sum |v|^2 before, 8-10 sum v after,
  *            11 sum |v|^2 after, 12-15 zero.  Sums are deterministic (fixed
  *            reduction order): two calls with equal inputs give equal bytes.
+ *  flags (params): CC_ODD_TRIPLET, CC_NANBU, CC_PRESERVE_ORDER, CC_CELL_UNIFORM;
+ *            any other bit is CC_EINVAL.
  *  workspace >= cc_workspace_bytes(n, cells) bytes, 256-byte aligned.        */
 int coulomb_collide(const double *v_in, int64_t ldv, const int32_t *cell_in,
                     double *v_out, int32_t *cell_out, int32_t *perm_out,

@@ -426,55 +426,56 @@ k_scan_cells(const int32_t* __restrict__ cnt, int M, int32_t* __restrict__ off, 
     if (tid == nt - 1) { off[M] = ra; chunk_off[M] = rb; }
 }
 
-// Per-cell constants (warp per cell, 8 cells per CTA): TA constant C_j (R5-R7),
-// Feistel keys (R1, R3) from lane 0, and the chunk -> cell table of
-// k_collide_large written by the whole warp (coalesced).  R1b (seg != NULL, chunk =
-// kBlock / 2): a cell of N > kBlock slots also gets its segment order sigma, written
-// as each block's kBlockSegs first stable slots (absolute: the cell offset included) in
-// seg[chunk * kBlockSegs + g]; the tail segment, if any, is the last entry.  Cells of
+// Per-cell constants (one CTA of kSetupThreads per cell): TA constant C_j (R5-R7) and the
+// Feistel keys (R1, R3) from thread 0, and the chunk -> cell table of k_collide_large
+// written by the CTA (coalesced).  R1b (seg != NULL, chunk = kBlock / 2): a cell of
+// N > kBlock slots also gets its segment order sigma, written as each block's kBlockSegs
+// first stable slots (absolute: the cell offset included) in seg[chunk * kBlockSegs + g];
+// the tail segment, if any, is the last entry.  Sigma's Feistel form is a pure function of
+// the position, so the CTA's threads share a C4 cell's 781 positions (6 each).  Cells of
 // 64 < N <= kBlock (one block) get their consecutive segments, so the collide reads one table.
-__global__ void __launch_bounds__(256)
+constexpr int kSetupThreads = 128;
+__global__ void __launch_bounds__(kSetupThreads)
 k_cell_setup(const int32_t* __restrict__ cnt, const int32_t* __restrict__ chunk_off, int M,
              int4* __restrict__ chunk_cell, double* __restrict__ Cj, cc::U4* __restrict__ keys,
              CellConst cc_, uint32_t cell_base, uint32_t step, uint32_t s0, uint32_t s1,
              const uint32_t* __restrict__ step_dev, const int32_t* __restrict__ off, int chunk,
              int32_t* __restrict__ seg)
 {
-    __shared__ int32_t sig_sm[8][cc::kSmallCell];
-    const int j = blockIdx.x * 8 + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (j >= M) return;
+    __shared__ int32_t sig_sm[cc::kSmallCell];
+    const int j = blockIdx.x;
+    const int t = threadIdx.x, lane = t & 31;
     if (step_dev) step += *step_dev;              // graph replay: effective step read on the device
     const uint32_t G = cell_base + static_cast<uint32_t>(j);
-    if (lane == 0) {
-        const int32_t N = cnt[j];
+    const int32_t Nj = cnt[j], oj = off[j], c0 = chunk_off[j], c1 = chunk_off[j + 1];
+    if (t == 0) {
         const double V = cc_.volume_arr ? cc_.volume_arr[j] : cc_.volume;
         const double lnL = cc_.ln_lambda_arr ? cc_.ln_lambda_arr[j] : cc_.ln_lambda;
-        const double nj = static_cast<double>(N) * cc_.weight / V;
+        const double nj = static_cast<double>(Nj) * cc_.weight / V;
         Cj[j] = fmax(cc_.K * nj * lnL, 0.0);
         keys[j] = cc::philox4x32_10(cc::U4{0u, G, step, 1u}, s0, s1);
     }
-    const int32_t c1 = chunk_off[j + 1];
     // per chunk {cell, cell's first slot, N, first item}: k_collide_large starts from one load
-    const int32_t Nj = cnt[j], oj = off[j], c0 = chunk_off[j];
-    for (int32_t c = c0 + lane; c < c1; c += 32) chunk_cell[c] = make_int4(j, oj, Nj, (c - c0) * chunk);
+    for (int32_t c = c0 + t; c < c1; c += kSetupThreads) chunk_cell[c] = make_int4(j, oj, Nj, (c - c0) * chunk);
     if (seg && Nj > cc::kSmallCell) {
         int32_t* out = seg + static_cast<int64_t>(c0) * cc::kBlockSegs;
-        if (Nj > cc::kBlock) {
-            // R1b segment order sigma: the R1 construction over the S_f full segments with
-            // sort purpose 6 (S_f <= 64) / Feistel purpose 5; the tail segment goes last
-            const uint32_t Sf = static_cast<uint32_t>(Nj) / cc::kSeg;
-            if (Sf <= static_cast<uint32_t>(cc::kSmallCell)) {
-                cc::small_cell_perm(Sf, G, step, s0, s1, lane, sig_sm[threadIdx.x >> 5], 0u, 6u);
-                for (uint32_t p = lane; p < Sf; p += 32) out[p] = oj + sig_sm[threadIdx.x >> 5][p] * cc::kSeg;
-            } else {
-                const cc::Feistel f = cc::make_feistel(Sf, cc::philox4x32_10(cc::U4{0u, G, step, 5u}, s0, s1));
-                for (uint32_t p = lane; p < Sf; p += 32) out[p] = oj + static_cast<int32_t>(cc::feistel_pi(f, p)) * cc::kSeg;
-            }
-            if (lane == 0 && Sf * cc::kSeg < static_cast<uint32_t>(Nj)) out[Sf] = oj + static_cast<int32_t>(Sf) * cc::kSeg;
-        } else if (lane < cc::kBlockSegs) {
-            out[lane] = oj + lane * cc::kSeg;          // one block: the stable slots in order
+        const uint32_t Sf = static_cast<uint32_t>(Nj) / cc::kSeg;
+        if (Nj <= cc::kBlock) {
+            if (t < cc::kBlockSegs) out[t] = oj + t * cc::kSeg;     // one block: the stable slots in order
+            return;
         }
+        // R1b segment order sigma: R1's construction over the S_f full segments (sort purpose 6
+        // for S_f <= 64, Feistel purpose 5 above); the tail segment goes last
+        if (Sf <= static_cast<uint32_t>(cc::kSmallCell)) {
+            if (t < 32) {
+                cc::small_cell_perm(Sf, G, step, s0, s1, lane, sig_sm, 0u, 6u);
+                for (uint32_t p = lane; p < Sf; p += 32) out[p] = oj + sig_sm[p] * cc::kSeg;
+            }
+        } else {
+            const cc::Feistel f = cc::make_feistel(Sf, cc::philox4x32_10(cc::U4{0u, G, step, 5u}, s0, s1));
+            for (uint32_t p = t; p < Sf; p += kSetupThreads) out[p] = oj + static_cast<int32_t>(cc::feistel_pi(f, p)) * cc::kSeg;
+        }
+        if (t == 0 && Sf * cc::kSeg < static_cast<uint32_t>(Nj)) out[Sf] = oj + static_cast<int32_t>(Sf) * cc::kSeg;
     }
 }
 
@@ -2158,7 +2159,7 @@ int run_binning(const double* v_in, int64_t ldv, const int32_t* cell_in, int n, 
     mark(ev, 1, st);
     k_scan_tiles<<<(M1 + 31) / 32, dim3(32, kScanRows), 0, st>>>(tcount, L.T, M1, cnt);
     k_scan_cells<<<1, 1024, 0, st>>>(cnt, M, off, chunk_off, chunk);
-    k_cell_setup<<<(M + 7) / 8, 256, 0, st>>>(cnt, chunk_off, M, at<int4>(ws, L.o_chunkcell), Cj, keys, k,
+    k_cell_setup<<<M, kSetupThreads, 0, st>>>(cnt, chunk_off, M, at<int4>(ws, L.o_chunkcell), Cj, keys, k,
                                                    cell_base, step, static_cast<uint32_t>(seed),
                                                    static_cast<uint32_t>(seed >> 32), step_dev, off, chunk,
                                                    blocked ? at<int32_t>(ws, L.o_seg) : nullptr);

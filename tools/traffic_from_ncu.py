@@ -9,6 +9,7 @@ import subprocess
 import sys
 
 UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+TIME_MS = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
 
 
 def main():
@@ -22,7 +23,8 @@ def main():
         for r in rows[2:]:
             name = r[ik].split("(")[0].split("::")[-1].split("<")[0].strip()
             b = float(r[ir]) * UNIT[units[ir]] + float(r[iw]) * UNIT[units[iw]]
-            out[name] = {"dram_bytes_per_launch": b, "ncu_ms": float(r[it]), "report": os.path.basename(rep)}
+            out[name] = {"dram_bytes_per_launch": b, "ncu_ms": float(r[it]) * TIME_MS.get(units[it], 1.0),
+                         "report": os.path.basename(rep)}
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
     import bench
