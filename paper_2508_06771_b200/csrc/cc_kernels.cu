@@ -35,6 +35,16 @@
 #define CC_ABLATE 0
 #endif
 
+// Bounds-asserting build (-DCC_DEBUG_BOUNDS, tools/debug_bounds.sh) for the index and segment
+// arithmetic of R1b and the binning modes (compute-sanitizer is unavailable on the GPU pool);
+// compiled out of the product.
+#ifdef CC_DEBUG_BOUNDS
+#include <cassert>
+#define CC_DBG_ASSERT(c) assert(c)
+#else
+#define CC_DBG_ASSERT(c) ((void)0)
+#endif
+
 namespace {
 
 #ifndef CC_COUNT_THREADS
@@ -521,7 +531,7 @@ __device__ __forceinline__ void load_batch(const double* __restrict__ v, int64_t
 template <int UB, bool RECS, bool HAS_V>
 __device__ __forceinline__ void scatter_pass_b(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__ cell,
                                                int64_t s0, int64_t s1, int M, uint32_t* my, const int32_t* base,
-                                               int lane, double* __restrict__ wsv, int32_t* __restrict__ sperm)
+                                               int lane, double* __restrict__ wsv, int32_t* __restrict__ sperm, int n)
 {
     const uint32_t lt = (1u << lane) - 1u;
     int32_t cB[UB];
@@ -566,6 +576,7 @@ __device__ __forceinline__ void scatter_pass_b(const double* __restrict__ v, int
                           pack_pc(static_cast<int32_t>(i), b < M ? b : -1));
                 else
                     sperm[dest] = static_cast<int32_t>(i);
+                CC_DBG_ASSERT(dest >= 0 && dest < n && i < s1);
             }
         }
     }
@@ -683,8 +694,8 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
     __syncthreads();
 
     // pass B: ranks, destinations, 32-byte records or 4-byte indices (loads batched, branch-free)
-    if (recs) scatter_pass_b<kScatterUnrollB, true, HAS_V>(v, ldv, cell, s0, s1, M, my, base, lane, wsv, sperm);
-    else scatter_pass_b<kScatterUnrollP, false, false>(v, ldv, cell, s0, s1, M, my, base, lane, wsv, sperm);
+    if (recs) scatter_pass_b<kScatterUnrollB, true, HAS_V>(v, ldv, cell, s0, s1, M, my, base, lane, wsv, sperm, n);
+    else scatter_pass_b<kScatterUnrollP, false, false>(v, ldv, cell, s0, s1, M, my, base, lane, wsv, sperm, n);
 }
 
 // ------------------------------------------------------------------ CCS4 + CCS5 items
@@ -1120,6 +1131,12 @@ k_collide_large(CollideArgs A)
                 sg[4 * g4] = q.x; sg[4 * g4 + 1] = q.y; sg[4 * g4 + 2] = q.z; sg[4 * g4 + 3] = q.w;
             }
         }
+#ifdef CC_DEBUG_BOUNDS
+        for (int g = 0; g < nseg; ++g) {
+            const int32_t len = min(cc::kSeg, nb - g * cc::kSeg);
+            CC_DBG_ASSERT(sg[g] >= o && sg[g] + len <= o + N && (sg[g] - o) % cc::kSeg == 0);
+        }
+#endif
         if (mode == kModeRec) {
             // 16-byte pieces: segment g = pieces [64 g, 64 g + 64), record (piece mod 64) / 2
 #pragma unroll
@@ -1159,6 +1176,7 @@ k_collide_large(CollideArgs A)
                 idx[q] = (u < nb) ? (mode == kModeSorted ? static_cast<int32_t>(sl)
                                                          : __ldg(reinterpret_cast<const int32_t*>(A.wsv) + sl))
                                   : -1;
+                CC_DBG_ASSERT(idx[q] >= -1 && idx[q] < A.n && (u >= nb || idx[q] >= 0));
             }
         }
         const uint32_t G = A.cell_base + static_cast<uint32_t>(j);
@@ -1176,6 +1194,8 @@ k_collide_large(CollideArgs A)
                 }
                 xs[q][0] = x[0];
                 xs[q][1] = x[1];
+                CC_DBG_ASSERT(i0 + e >= i1 || (x[0] < static_cast<uint32_t>(nb) &&
+                                               (2 * e + 1 >= static_cast<uint32_t>(nb) || x[1] < static_cast<uint32_t>(nb))));
             }
         } else {
             // the last block of a large cell holds <= 64 slots: R1's sort-by-key form
@@ -1391,7 +1411,9 @@ __device__ __noinline__ uint32_t blocked_slot(const CollideArgs& A, int j, int32
         u = cc::small_select(nb, r, G, step, A.s0, A.s1, b * (cc::kBlock / 4), 2u);
     }
     const int32_t c = A.chunk_off[j] + static_cast<int32_t>(b);
-    return static_cast<uint32_t>(A.seg[static_cast<int64_t>(c) * cc::kBlockSegs + u / cc::kSeg] - A.off[j]) + u % cc::kSeg;
+    const uint32_t slot = static_cast<uint32_t>(A.seg[static_cast<int64_t>(c) * cc::kBlockSegs + u / cc::kSeg] - A.off[j]) + u % cc::kSeg;
+    CC_DBG_ASSERT(u < nb && slot < static_cast<uint32_t>(N));
+    return slot;
 }
 
 // Triplet mode, N_j > 64 and odd: thread per cell runs R19 on the last three
