@@ -219,7 +219,8 @@ __device__ __forceinline__ int32_t count_key(int32_t c, int M)
 // Binning mode of a call, decided on the device from k_count's flags:
 //  kModeSorted  input already cell-sorted (dead last): the stable order is the identity,
 //               nothing is moved; the collide reads v_in at the stable slot itself;
-//  kModePerm    nearly sorted (descents <= n / kPermModeDiv, the steady state of a PIC loop
+//  kModePerm    nearly sorted (descents at most 1/kPermModeDiv of a random order's expected
+//               n (M - 1) / (2 M) — i.e. up to ~25% for many cells; the steady state of a PIC loop
 //               that feeds the operator its own output): the scatter writes only the input
 //               index of each stable slot (4 bytes, the paper's "track and sort particle
 //               indices"); the collide reads v_in through it — mostly contiguous runs;
@@ -228,17 +229,21 @@ __device__ __forceinline__ int32_t count_key(int32_t c, int M)
 // Index modes are used only with R1b (index_modes != 0); R1 always takes kModeRec.
 constexpr int kModeRec = 0, kModePerm = 1, kModeSorted = 2;
 #ifndef CC_PERM_MODE_DIV
-#define CC_PERM_MODE_DIV 16
+#define CC_PERM_MODE_DIV 2
 #endif
-constexpr int kPermModeDiv = CC_PERM_MODE_DIV;   // (design studies: 0 = kModePerm for every unsorted input)
-__device__ __forceinline__ int bin_mode(const int32_t* flags, int n, int index_modes)
+// (design studies: 0 = kModePerm for every unsorted input).  Measured at C4: the
+// index mode beats the record mode at 2-20% movers (2.50-2.79 vs 3.17-3.19 ms/step at 10-20%).
+constexpr int kPermModeDiv = CC_PERM_MODE_DIV;
+__device__ __forceinline__ int bin_mode(const int32_t* flags, int n, int M, int index_modes)
 {
     if (!index_modes) return kModeRec;
     if (__ldg(flags + 1) == 0) return kModeSorted;
 #ifdef CC_STUDY_NOREC
     return kModePerm;                    // design study only: the R1b collide without its record path
 #endif
-    return static_cast<int64_t>(__ldg(flags + 2)) * kPermModeDiv <= n ? kModePerm : kModeRec;
+    // descents <= (n (M-1) / (2M)) / kPermModeDiv, in integers
+    return static_cast<int64_t>(__ldg(flags + 2)) * 2 * M * kPermModeDiv <= static_cast<int64_t>(n) * (M - 1) ? kModePerm
+                                                                                                      : kModeRec;
 }
 
 __global__ void __launch_bounds__(kCountThreads)
@@ -591,7 +596,7 @@ k_scatter(const double* __restrict__ v, int64_t ldv, const int32_t* __restrict__
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     // binning mode (bin_mode): sorted -> nothing to move; perm -> 4-byte input indices only
-    const int mode = flags ? bin_mode(flags, n, index_modes) : kModeRec;
+    const int mode = flags ? bin_mode(flags, n, M, index_modes) : kModeRec;
     if (mode == kModeSorted) return;
     const bool recs = mode == kModeRec;
     int32_t* __restrict__ sperm = reinterpret_cast<int32_t*>(wsv);   // kModePerm: input index per stable slot
@@ -812,7 +817,7 @@ __device__ __forceinline__ Rec load_slot(const CollideArgs& A, int64_t s)
     return r;
 }
 
-__device__ __forceinline__ int call_mode(const CollideArgs& A) { return bin_mode(A.flags, A.n, A.index_modes); }
+__device__ __forceinline__ int call_mode(const CollideArgs& A) { return bin_mode(A.flags, A.n, A.M, A.index_modes); }
 
 // Stable slot s in any binning mode: the record (kModeRec), or v_in at the slot's input
 // index (kModeSorted: the slot itself; kModePerm: the index k_scatter wrote).
