@@ -13,8 +13,11 @@ the steady state of a PIC loop: each step consumes the previous step's
 electrons to a neighbour cell; the first step starts from a random particle
 order (the paper stores particles unsorted).  "cold" (the same randomly
 ordered input every step) and "warm" (sorted input, no drift) are reported
-beside it.  Inputs are 2.87 GB, far larger than the 126 MB L2, so no flush is
-needed between steps.  For N > 1 (torchrun) each rank owns a C5 shard: global
+beside it.  The operator picks its binning mode on the device from the input's
+order: steady -> index mode (4-byte indices), cold -> record mode
+(32-byte records), warm -> sorted mode (nothing moved); the R1 whole-cell pairing
+(CC_CELL_UNIFORM) is timed as a variant.  Inputs are 2.87 GB, far larger than the
+126 MB L2, so no flush is needed between steps.  For N > 1 (torchrun) each rank owns a C5 shard: global
 cells [4096 r, 4096 (r+1)) of a 64 x 64N grid, its own data seed; the stand-in
 drift of SURVEY §8(e) moves particles of the shard's first and last cell rows
 across the shard boundary (p = 0.1), and the step includes their migration to
