@@ -116,3 +116,24 @@ def test_oracle_never_imports_product():
             txt = open(os.path.join(ROOT, "oracle", f)).read()
             assert not re.search(r"^\s*(import|from)\s+paper_2508_06771_b200", txt, flags=re.M), f
             assert "#include" not in txt or "cc_device" not in txt, f
+
+
+def test_flag_constants_agree_across_header_binding_and_oracle():
+    """The cc_params.flags bits (include/coulomb.h) equal the binding's and the oracle's, and an
+    unknown bit is rejected on the host before any launch."""
+    from paper_2508_06771_b200 import _lib
+    import ctypes as C
+    import oracle
+    src = open(os.path.join(ROOT, "include", "coulomb.h")).read()
+    hdr = {k: int(v) for k, v in re.findall(r"#define (CC_[A-Z_]+) (\d+)u", src)}
+    for name in ("CC_ODD_TRIPLET", "CC_NANBU", "CC_PRESERVE_ORDER", "CC_CELL_UNIFORM"):
+        assert getattr(_lib, name) == hdr[name], name
+        assert getattr(oracle, name[3:]) == hdr[name], name
+    L = _lib.load()
+    p = _lib.CCParams()
+    L.cc_default_params(C.byref(p))
+    p.flags = 16
+    null = None
+    rc = L.coulomb_collide(null, 10, null, null, null, null, 10, 4, 0, 1e-10, C.byref(p), 1, 0,
+                           null, null, null, 0, null)
+    assert rc == _lib.CC_EINVAL
