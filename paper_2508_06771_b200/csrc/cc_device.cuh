@@ -5,8 +5,10 @@
 //   philox4x32_10   CCS4 randoms, reading R3
 //   u01             two 32-bit words -> uniform on (0,1), R3
 //   ppnd16          AS241 inverse normal CDF (Wichura 1988), R4
-//   pairing (R1)    keyed in-cell permutation pi_j: sort-by-Philox-key for
-//                   N <= 64, 8-round keyed Feistel + cycle walking above
+//   pairing (R1)    keyed permutation of n items: sort-by-Philox-key for
+//                   n <= 64, 8-round keyed Feistel + cycle walking above — over
+//                   the whole cell (R1), or (R1b) over a cell's full segments
+//                   (the segment order) and over each block's slots (tau_b)
 //   ta_update       CCS5 Takizuka–Abe pair collision, R5/R8/R9
 #pragma once
 #include <cstdint>

@@ -2,18 +2,25 @@
 // operator (arXiv 2508.06771 step S1; Table 5).
 //
 // Pipeline of one coulomb_collide() call (all on the caller's stream):
-//   k_count        CCS1: per-tile cell histograms  -> tcount[T][M+1]
+//   k_count        CCS1: per-tile cell histograms  -> tcount[T][M+1],
+//                  invalid-id flag, descent count (picks the binning mode)
 //   k_scan_tiles   CCS2, part 1: per cell, exclusive scan over tiles
-//   k_scan_cells   CCS2, part 2: off[] (cell offsets), chunk_off[], per-cell
-//                  TA constant C_j (R5/R6/R7) and Feistel keys (R1, R3)
+//   k_scan_cells   CCS2, part 2: off[] (cell offsets), chunk_off[]
+//   k_cell_setup   per cell: TA constant C_j (R5/R6/R7), Feistel keys (R1, R3),
+//                  the chunk table and the R1b segment order (absolute segment
+//                  starts of every block)
 //   k_scatter      CCS3 as a STABLE counting sort: per-warp
-//                  sub-ranges, match.any ranks, no global atomics; writes the
-//                  particle as one 32-byte record {vx, vy, vz, (perm, cell)}
-//                  into the cell-sorted workspace array ws_v
+//                  sub-ranges, match.any ranks, no global atomics; by binning
+//                  mode: nothing (sorted input), the input index of each stable
+//                  slot (nearly sorted), or the particle as one 32-byte record
+//                  {vx, vy, vz, (perm, cell)} (random order) into ws_v
 //   k_collide_small  N_j <= 64: one warp per cell; pi_j by sort-by-key (R1)
-//   k_collide_large  N_j > 64: cell-aligned chunks of pairs; pi_j by keyed
-//                  Feistel (R1); CCS4 Philox per pair; CCS5 TA update; output
-//                  in pair order, SoA; fused per-chunk moment partials
+//   k_collide_large  N_j > 64: R1b (default) one CTA per block of whole
+//                  segments, copied into shared memory and paired there by
+//                  tau_b; R1 (CC_CELL_UNIFORM) cell-aligned chunks of pairs
+//                  gathered by the whole-cell Feistel pi_j; CCS4 Philox per
+//                  pair; CCS5 TA update; output in pair order, SoA; fused
+//                  per-chunk moment partials (post- and pre-collision)
 //   k_copy_dead    dead particles after the live ones, input order
 //   k_finalize_cells / k_finalize_diag   deterministic reductions of the
 //                  partials -> moments_out [M][7], diag_out [16]
@@ -1074,9 +1081,9 @@ __device__ __forceinline__ Rec stage_rec(const double* stage, bool planar, uint3
 }
 
 // N_j > 64: one CTA per cell-aligned chunk of kChunk items, two phases:
-//  1. every thread computes pi_j(2k), pi_j(2k+1) (keyed Feistel, R1) for its
+//  1. (R1) every thread computes pi_j(2k), pi_j(2k+1) (keyed Feistel) for its
 //     items and issues cp.async gathers of both records into shared memory —
-//     the whole chunk's 64 KB of gathers are in flight at once;
+//     the whole chunk's gathers are in flight at once; (R1b) see BLOCKED below;
 //  2. items are processed two per thread per round: Philox (CCS4), the central
 //     AS241 branch in place and the tail branch (~15% of draws) compacted
 //     across the warp and evaluated once per 32 tails, then TA (CCS5), and the
